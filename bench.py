@@ -1,0 +1,340 @@
+"""Benchmark: cell-updates/s of the full second-order Lagrange-flux step on B200.
+
+Workload (BASELINE.json configs[3]/[4]): the seeded smooth-perturbation flow,
+periodic, fp64, 16384 x 16384 cells per GPU -- config 4 at N = 1 and the weak
+scaling of config 5 (16384 x 16384 N on [0,1] x [0,N], one y-slab per rank) at
+N > 1.  A step is one LagfluxSolver::heun_step (both stages + dt, solver.cpp:489-546);
+one cell-update advances one interior cell by one step (bench.cpp:104,107).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+ours:       value = cells x K / device time of K device-resident steps (CUDA events on
+            the launching stream, barrier + synchronize around, max over ranks).
+            e2e   = the same through the public API with HOST buffers: upload of the
+            initial state from pinned memory, K steps, download of the final state,
+            all inside the timed region.
+reference:  the reference's own LagfluxSolver (oracle/_ref, compiled from its sources)
+            on all host cores, on a bounded strip of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+BYTES_PER_CELL_UPDATE = 160  # read U^n, write U*, read U^n + U*, write U^{n+1}
+FALLBACK_HBM_GBS = 6650.0    # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+METRIC = "cell-updates/sec (fp64, full 2nd-order step)"
+UNIT = "cell-updates/s"
+CPU_SAMPLE_ROWS = 512        # reference / oracle CPU sample: 16384 x 512 strip of config 4
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the fused kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows
+                                                         if r[2].replace(".", "").isdigit())}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return torch, dist, world, rank, local
+
+
+def cpu_sample_case(cases, rows=CPU_SAMPLE_ROWS, n=16384):
+    """A bounded strip of the config-4 workload: 16384 x rows cells, same dx = dy, periodic."""
+    return cases.smooth(n, 1, ny=rows, y_extent=rows / n)
+
+
+def time_reference_cpu(case, steps, warmup, threads):
+    """The reference's LagfluxSolver::heun_step on host cores (bench.cpp:70-76 timing)."""
+    from oracle import oracle as O
+    from paper_1607_08710_b200 import cases as CS
+    f0 = CS.initial_field(case)
+    r = O.RefSolver(case.grid, case.bc, case.gamma, case.params, threads=threads)
+    r.set_state(f0)
+    if warmup:
+        r.heun_steps(warmup, case.cfl, case.t_final)
+    t0 = time.perf_counter()
+    r.heun_steps(steps, case.cfl, case.t_final)
+    wall = time.perf_counter() - t0
+    return case.cells * steps / wall, wall
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU implementation on this box's host cores."""
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return 0
+    from paper_1607_08710_b200 import cases as CS
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PLACES", "cores")
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_lagflux.so not built"}))
+        return 0
+    case = cpu_sample_case(CS)
+    steps = max(1, min(args.steps, 10))
+    value, wall = time_reference_cpu(case, steps, min(args.warmup, 1), threads)
+    sample = (f"{case.grid.nx}x{case.grid.ny} periodic strip of the config-4 generator "
+              f"(seed {case.seed}), {steps} timed heun_step calls after "
+              f"{min(args.warmup, 1)} warm-up, OpenMP {threads} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": wall / steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config4-smooth-16384^2 (bounded CPU strip)",
+                       "nx": case.grid.nx, "ny": case.grid.ny, "boundary": "periodic"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    torch, dist, world, rank, local = dist_setup(args)
+    from paper_1607_08710_b200 import cases as CS
+    from paper_1607_08710_b200 import grid as G
+    from paper_1607_08710_b200.solver import LagfluxSolver, nccl_unique_id
+
+    n = args.n
+    case = CS.smooth(n, args.steps) if world == 1 else CS.smooth_weak(world, n, args.steps)
+    g = case.grid
+    dist_arg = None
+    if world > 1:
+        nid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        dist_arg = (rank, world, local, nid[0])
+    solver = LagfluxSolver(g, case.bc, case.gamma, case.params, devices=(local,), path=args.path,
+                           dist=dist_arg)
+    stream = torch.cuda.current_stream()
+    solver.set_stream(stream.cuda_stream)
+    state = G.SolverState(field=np.zeros((4, 1, 1)))  # device-resident; host copy not needed
+    solver.init_fourier(state, case.seed)
+    controls = G.TimeControls(case.cfl, case.t_final, G.INT64_MAX)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    solver.advance(state, controls, args.warmup)
+    barrier()
+    launches0 = solver.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        taken = solver.advance(state, controls, args.steps)
+        ev1.record(stream)
+        barrier()
+    launches = solver.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    cells_total = g.nx * g.ny
+    value = cells_total * taken / (ms_max / 1e3)
+    clock_summary = clocks.summary()
+
+    # dominant kernel: per-launch CUDA events around the fused step kernel
+    try:
+        kernel_ms, loop_ms, k_launches = solver.time_steps(max(5, min(args.steps, 20)), case.cfl)
+        kernel_name = "fused Heun step (lfb::k_fused_step)"
+    except ValueError:  # stage-wise path: no single dominant kernel, use the whole step
+        kernel_ms, loop_ms, k_launches = ms_max, ms_max, max(taken, 1)
+        kernel_name = "whole stage-wise step (no fused kernel on this path)"
+    per_launch_ms = kernel_ms / max(k_launches, 1)
+    cells_local = g.nx * solver.local_rows()[1]
+    hbm, hbm_src = measured_hbm()
+    achieved = BYTES_PER_CELL_UPDATE * cells_local / (per_launch_ms / 1e3) / 1e9
+    traffic = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": hbm_src,
+                "algorithmic_bytes_per_cell_update": BYTES_PER_CELL_UPDATE,
+                "kernel": kernel_name,
+                "kernel_ms_per_launch": per_launch_ms,
+                "kernel_share_of_step": kernel_ms / loop_ms if loop_ms > 0 else None,
+                "frac_of_nominal_8TBs": achieved / 8000.0,
+                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "traffic_source": traffic.get("source") if traffic else None}
+
+    # e2e through the public API with host buffers (rank-local slab)
+    e2e = None
+    if not args.no_e2e:
+        row0, rows = solver.local_rows()
+        host = torch.empty((4, g.nyt, g.nxt), dtype=torch.float64, pin_memory=True)
+        hf = host.numpy()
+        solver.download(hf)  # the current state as this step's input (untimed)
+        barrier()
+        with_state = G.SolverState(field=hf)
+        t0 = time.perf_counter()
+        ev0.record(stream)
+        solver.attach(with_state)                  # H2D from pinned host memory
+        k2 = solver.advance(with_state, controls, args.steps)
+        solver.sync_to_host(with_state)            # D2H of the result
+        ev1.record(stream)
+        barrier()
+        wall = time.perf_counter() - t0
+        e_ms = ev0.elapsed_time(ev1)
+        t = torch.tensor([max(e_ms, wall * 1e3)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        state_bytes = 4 * 8 * g.nx * rows
+        e2e = {"value": cells_total * k2 / (float(t.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": state_bytes / max(k2, 1),
+               "d2h_bytes_per_step": (state_bytes + 48 * k2) / max(k2, 1),
+               "what": f"upload of the state from pinned host memory, {k2} steps "
+                       f"(dt/diagnostics back to the host), download of the final state"}
+        del host
+
+    cpu_baseline = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        from oracle import oracle as O
+        if O.ref_available():
+            threads = os.cpu_count() or 1
+            cs = cpu_sample_case(CS)
+            steps = 3
+            v, wall = time_reference_cpu(cs, steps, 1, threads)
+            cpu_baseline = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                            "sample": f"{cs.grid.nx}x{cs.grid.ny} periodic strip of the config-4 "
+                                      f"generator, {steps} heun_step calls after 1 warm-up "
+                                      f"({wall:.1f} s), OpenMP {threads} threads"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": taken, "warmup": args.warmup, "ms_per_step": ms_max / max(taken, 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded 8-mode Fourier flow, BASELINE config 4/5)",
+                "config": {"workload": f"config{4 if world == 1 else 5}-smooth "
+                                       f"{g.nx}x{g.ny} periodic, y-slabs={world}",
+                           "nx": g.nx, "ny": g.ny, "cfl": case.cfl, "seed": case.seed,
+                           "parallelism": f"y-slab x{world}", "path": args.path,
+                           "l2": "inputs larger than L2 (state %.1f GB per GPU)" % (
+                               4 * 8 * g.nx * solver.local_rows()[1] / 1e9)},
+                "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clock_summary}
+        print(json.dumps(line))
+    solver.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=16384, help="cells per side per GPU")
+    ap.add_argument("--path", choices=["auto", "fused", "staged"], default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

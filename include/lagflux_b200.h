@@ -1,0 +1,153 @@
+/*
+ * lagflux_b200.h -- C ABI of the B200-native Lagrange-flux time step.
+ *
+ * Drop-in boundary for lagflux::LagfluxSolver (reference
+ * /root/reference/proj/include/lagflux/solver.hpp:78-131).  A handle owns the
+ * device copy of one SolverState::field plus all scratch; the field stays
+ * resident on the GPU between steps (upload once, download for dumps).  Plain
+ * pointers and sizes only; errors are returned as an int status plus a record
+ * (the reference's exceptions, error.hpp:9-64).  One host thread per handle,
+ * like the reference object (not thread-safe, mutable scratch).
+ *
+ * Entry point                      replaces (reference file:line)
+ *   lf_create / lf_destroy         LagfluxSolver::LagfluxSolver  solver.cpp:61-88
+ *   lf_create_dist                 (new) one y-slab per rank, NCCL halos + dt max
+ *   lf_upload / lf_download        SolverState::field host <-> device (CellField,
+ *                                  grid.hpp:73-92; ghosted row-major, ld = nxt)
+ *   lf_compute_dt                  LagfluxSolver::compute_dt     solver.cpp:434-480
+ *   lf_euler_stage                 LagfluxSolver::euler_stage    solver.cpp:482-487
+ *   lf_heun_step                   LagfluxSolver::heun_step      solver.cpp:489-546
+ *   lf_advance                     the run.cpp:180-210 step loop with the dt /
+ *                                  time / diagnostics kept on the device
+ *   lf_init_fourier                (new) on-device seeded smooth-flow IC (BASELINE 4-5)
+ *   lf_last_error                  the exception object (what(), PositivityError fields)
+ */
+#ifndef LAGFLUX_B200_H
+#define LAGFLUX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LF_ABI_VERSION 1
+
+/* BcKind (grid.hpp:51) */
+enum { LF_TRANSMISSIVE = 0, LF_REFLECTIVE = 1, LF_PERIODIC = 2 };
+
+/* status / error kinds */
+enum {
+  LF_OK = 0,
+  LF_ERR_CONFIG = 1,       /* ConfigError */
+  LF_ERR_DT_STATE = 2,     /* InvalidStateError in compute_dt (solver.cpp:471-475) */
+  LF_ERR_DT_NONPOS = 3,    /* Error "non-positive time step" (solver.cpp:478) */
+  LF_ERR_PRIMITIVE = 4,    /* InvalidStateError in build_primitives (solver.cpp:164-170) */
+  LF_ERR_TRACE = 5,        /* InvalidStateError in compute_fluxes (solver.cpp:245-255) */
+  LF_ERR_POSITIVITY = 6,   /* PositivityError in apply_update (solver.cpp:310-326) */
+  LF_ERR_DEVICE = 7,       /* CUDA / NCCL failure (no reference counterpart) */
+  LF_ERR_ARGUMENT = 8      /* invalid argument to this ABI */
+};
+
+/* Path selection for lf_heun_step / lf_advance. */
+enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2 };
+
+typedef struct lf_desc {
+  int dim;              /* 1 or 2 (CartesianGrid::dim) */
+  int nx, ny;           /* global interior cells (ny = 1 in 1D) */
+  double dx, dy;        /* CartesianGrid::dx, dy (pass them; do not recompute) */
+  double x0, y0;
+  double gamma;         /* PerfectGasEos::gamma */
+  double beta;          /* LimiterParams::beta */
+  int spatial_order;    /* SchemeParams::spatial_order (1 or 2) */
+  int time_order;       /* SchemeParams::time_order (1 or 2) */
+  int bc[4];            /* x_low, x_high, y_low, y_high */
+} lf_desc;
+
+typedef struct lf_error {
+  int kind;
+  int axis;             /* LF_ERR_TRACE: 0 x-face, 1 y-face */
+  int64_t i, j;         /* cell / face indices exactly as the reference reports them */
+  int64_t step;
+  double dt;
+  double value;         /* offending density / pressure (LF_ERR_PRIMITIVE), rho (POSITIVITY) */
+  double value2;        /* internal energy density (POSITIVITY) */
+  char message[320];    /* the reference's what() text */
+} lf_error;
+
+typedef struct lf_step_out {
+  double dt;
+  int hits_limit;
+  double time;          /* SolverState::time after the step */
+  int64_t step;         /* SolverState::step after the step */
+  double min_rho;       /* StepDiagnostics::min_rho */
+  double min_p;         /* StepDiagnostics::min_p */
+} lf_step_out;
+
+typedef struct lf_handle lf_handle;
+
+int lf_abi_version(void);
+
+/* Single process.  ndev == 1: one GPU.  ndev > 1: the grid is split into ndev
+ * y-slabs driven from this process (devices may repeat: several slabs on one
+ * GPU run the identical slab code path, which is how the decomposition is
+ * checked on a 1-GPU machine). */
+int lf_create(const lf_desc* desc, const int* devices, int ndev, lf_handle** out);
+
+/* One rank of an nranks-way y-slab decomposition (one process per GPU).
+ * nccl_id: 128 bytes from lf_nccl_unique_id() on rank 0, broadcast by the caller. */
+int lf_nccl_unique_id(void* id128);
+int lf_create_dist(const lf_desc* desc, int device, int rank, int nranks, const void* nccl_id,
+                   lf_handle** out);
+
+void lf_destroy(lf_handle* h);
+
+/* Rows [row0, row0 + nrows) of this handle's slab, as global rows. */
+int lf_local_rows(lf_handle* h, int* row0, int* nrows);
+
+/* Host <-> device field transfer in the reference's ghosted layout:
+ * component c of cell (i, j) (total indices, ghosts included) at field[c][j*ld + i],
+ * ld >= nx + 4.  Distributed handles transfer their own slab rows only, at the
+ * same global positions.  Download writes interior cells; fill_ghosts != 0
+ * additionally applies the boundary conditions to the host ghosts
+ * (apply_boundary, grid.cpp:116-121). */
+int lf_upload(lf_handle* h, double* const field[4], int64_t ld);
+int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghosts);
+
+/* Seeded smooth-perturbation initial state (BASELINE configs 4-5), generated on the device. */
+int lf_init_fourier(lf_handle* h, uint64_t seed);
+
+int lf_compute_dt(lf_handle* h, double cfl, double time, double limit_time, double* dt);
+/* state <- euler_stage(state, dt) (the reference writes `out`; the C++ adapter
+ * uploads `in` and downloads into `out`) */
+int lf_euler_stage(lf_handle* h, double dt, int64_t step);
+/* boundary_outflow: SolverState::boundary_outflow, updated in place (may be NULL). */
+int lf_heun_step(lf_handle* h, double cfl, double time, double limit_time, int64_t step,
+                 double* boundary_outflow, lf_step_out* out);
+/* Up to nsteps Heun steps while time < t_final (run.cpp:180), dt/time on the
+ * device and no host synchronisation until the end.  per_step: nsteps records
+ * (may be NULL).  *taken receives the steps executed. */
+int lf_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* time,
+               int64_t* step, double* boundary_outflow, lf_step_out* per_step, int* taken);
+
+int lf_last_error(lf_handle* h, lf_error* err);
+
+/* ---- measurement / tuning hooks (used by bench.py; no reference counterpart) ---- */
+int lf_set_stream(lf_handle* h, void* cuda_stream);   /* NULL: the handle's own stream */
+int lf_set_path(lf_handle* h, int path);               /* LF_PATH_* */
+/* Time n device-resident steps with CUDA events around each launch of the
+ * dominant kernel.  kernel_ms: summed kernel time; step_ms: whole-loop time. */
+int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
+                  int* kernel_launches);
+int lf_device_bytes(lf_handle* h, int64_t* bytes);
+/* Kernels launched by this library in this process so far (all handles). */
+int lf_launch_count(lf_handle* h, int64_t* launches);
+/* One scalar per interior cell: the CFL rate field is not kept; this returns the
+ * max rate of the current state (diagnostic for tests). */
+int lf_max_rate(lf_handle* h, double* rate);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAGFLUX_B200_H */

@@ -1,0 +1,685 @@
+/*
+ * lagflux_oracle.c -- CPU restatement of the reference Lagrange-flux step.
+ * TEST INFRASTRUCTURE ONLY (see lagflux_oracle.h).  Compiled with
+ * -O2 -ffp-contract=off so every expression rounds exactly as the shipped
+ * reference build does (no FMA, SSE2 scalar).
+ *
+ * Every function names the reference file:line it restates.  Parenthesised
+ * expressions keep the C++ left-to-right evaluation order of the reference.
+ */
+#include "lagflux_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+struct lfo_solver {
+  lfo_grid g;
+  lfo_scheme s;
+  int64_t cells;           /* nxt*nyt */
+  double* prim[2][4];      /* solver.hpp:125 prim_ */
+  double* fx[2][4];        /* FluxSet::x   (nx+1)*ny  (flux1_, flux2_) */
+  double* fy[2][4];        /* FluxSet::y   nx*(ny+1) */
+  double* ustar_x[2];
+  double* ustar_y[2];
+  double* pred[4];         /* predictor_ */
+};
+
+static int nxt_of(const lfo_grid* g) { return g->nx + 2 * g->gx; }
+static int nyt_of(const lfo_grid* g) { return g->ny + 2 * g->gy; }
+static int64_t idx_of(const lfo_grid* g, int i, int j) { return (int64_t)j * nxt_of(g) + i; }
+
+/* std::to_string(double) is "%f" (libstdc++). */
+static void fmt_f(char* buf, size_t n, double v) { snprintf(buf, n, "%f", v); }
+
+static void set_err(lfo_error* e, int kind) {
+  if (!e) return;
+  memset(e, 0, sizeof *e);
+  e->kind = kind;
+  e->i = e->j = e->step = -1;
+}
+
+/* grid.cpp:23-56 */
+int lfo_make_grid_1d(int nx, double x_min, double x_max, lfo_grid* g) {
+  if (nx < 1 || !(x_max > x_min)) return LFO_ERR_CONFIG;
+  memset(g, 0, sizeof *g);
+  g->dim = 1; g->nx = nx; g->ny = 1;
+  g->dx = (x_max - x_min) / nx; g->dy = 1.0;
+  g->x0 = x_min; g->y0 = 0.0; g->gx = 2; g->gy = 0;
+  return 0;
+}
+
+int lfo_make_grid_2d(int nx, int ny, double x_min, double x_max, double y_min, double y_max,
+                     lfo_grid* g) {
+  if (nx < 1 || ny < 1 || !(x_max > x_min) || !(y_max > y_min)) return LFO_ERR_CONFIG;
+  memset(g, 0, sizeof *g);
+  g->dim = 2; g->nx = nx; g->ny = ny;
+  g->dx = (x_max - x_min) / nx; g->dy = (y_max - y_min) / ny;
+  g->x0 = x_min; g->y0 = y_min; g->gx = 2; g->gy = 2;
+  return 0;
+}
+
+/* grid.cpp:72-114: x sides over interior rows first, then y sides over every
+ * column so the corners pick up the fresh x ghosts.  parity 0 even, 1 flip_x,
+ * 2 flip_y (GhostParity, grid.hpp:60). */
+void lfo_fill_ghosts(const lfo_grid* g, const int bc[4], int parity, double* f) {
+  const int nxt = nxt_of(g);
+  const double sx = parity == 1 ? -1.0 : 1.0;
+  const double sy = parity == 2 ? -1.0 : 1.0;
+#define AT(i, j) f[(int64_t)(j) * nxt + (i)]
+  for (int j = g->gy; j < g->gy + g->ny; ++j) {
+    for (int l = 1; l <= g->gx; ++l) {
+      const int lo = g->gx - l;
+      const int hi = g->gx + g->nx - 1 + l;
+      switch (bc[0]) {
+        case LFO_TRANSMISSIVE: AT(lo, j) = AT(g->gx, j); break;
+        case LFO_REFLECTIVE: AT(lo, j) = sx * AT(g->gx + l - 1, j); break;
+        default: AT(lo, j) = AT(g->gx + ((g->nx - l) % g->nx + g->nx) % g->nx, j); break;
+      }
+      switch (bc[1]) {
+        case LFO_TRANSMISSIVE: AT(hi, j) = AT(g->gx + g->nx - 1, j); break;
+        case LFO_REFLECTIVE: AT(hi, j) = sx * AT(g->gx + g->nx - l, j); break;
+        default: AT(hi, j) = AT(g->gx + (l - 1) % g->nx, j); break;
+      }
+    }
+  }
+  if (g->gy == 0) return;
+  for (int i = 0; i < nxt; ++i) {
+    for (int l = 1; l <= g->gy; ++l) {
+      const int lo = g->gy - l;
+      const int hi = g->gy + g->ny - 1 + l;
+      switch (bc[2]) {
+        case LFO_TRANSMISSIVE: AT(i, lo) = AT(i, g->gy); break;
+        case LFO_REFLECTIVE: AT(i, lo) = sy * AT(i, g->gy + l - 1); break;
+        default: AT(i, lo) = AT(i, g->gy + ((g->ny - l) % g->ny + g->ny) % g->ny); break;
+      }
+      switch (bc[3]) {
+        case LFO_TRANSMISSIVE: AT(i, hi) = AT(i, g->gy + g->ny - 1); break;
+        case LFO_REFLECTIVE: AT(i, hi) = sy * AT(i, g->gy + g->ny - l); break;
+        default: AT(i, hi) = AT(i, g->gy + (l - 1) % g->ny); break;
+      }
+    }
+  }
+#undef AT
+}
+
+/* grid.cpp:116-121 */
+void lfo_apply_boundary(const lfo_grid* g, const int bc[4], double* const field[4]) {
+  lfo_fill_ghosts(g, bc, 0, field[0]);
+  lfo_fill_ghosts(g, bc, 1, field[1]);
+  lfo_fill_ghosts(g, bc, 2, field[2]);
+  lfo_fill_ghosts(g, bc, 0, field[3]);
+}
+
+/* grid.cpp:123-134 */
+void lfo_interior_totals(const lfo_grid* g, double* const field[4], double tot[4]) {
+  const double vol = g->dim == 2 ? g->dx * g->dy : g->dx;
+  for (int c = 0; c < 4; ++c) {
+    double sum = 0.0;
+    for (int j = g->gy; j < g->gy + g->ny; ++j)
+      for (int i = g->gx; i < g->gx + g->nx; ++i) sum += field[c][idx_of(g, i, j)];
+    tot[c] = sum * vol;
+  }
+}
+
+/* libstdc++ std::min/std::max tie semantics. */
+static inline double smin(double a, double b) { return (b < a) ? b : a; }
+static inline double smax(double a, double b) { return (a < b) ? b : a; }
+
+/* reconstruct.hpp:24-30 */
+double lfo_sweby(double a, double b, double beta) {
+  if (!(a * b > 0.0)) return 0.0;
+  const double aa = fabs(a);
+  const double ab = fabs(b);
+  const double m = smax(smin(aa, beta * ab), smin(beta * aa, ab));
+  return a > 0.0 ? m : -m;
+}
+
+/* reconstruct.hpp:33-35, 44-49 */
+static inline void face_trace(double q0, double q1, double q2, double q3, double beta,
+                              double* minus, double* plus) {
+  const double s1 = lfo_sweby(q2 - q1, q1 - q0, beta);
+  const double s2 = lfo_sweby(q3 - q2, q2 - q1, beta);
+  *minus = q1 + 0.5 * s1;
+  *plus = q2 - 0.5 * s2;
+}
+
+/* riemann_hll.hpp:27-40 with sound_speed euler.hpp:99-104 */
+void lfo_lagrangian_hll(const double wl[4], const double wr[4], double nx, double ny,
+                        double gamma_l, double gamma_r, double* p_star, double* u_star) {
+  const double ul = wl[1] * nx + wl[2] * ny;
+  const double ur = wr[1] * nx + wr[2] * ny;
+  const double cl = sqrt(gamma_l * wl[3] / wl[0]);
+  const double cr = sqrt(gamma_r * wr[3] / wr[0]);
+  const double cmax = smax(cl, cr);
+  const double rho_sum = wl[0] + wr[0];
+  *p_star = (wr[0] * wl[3] + wl[0] * wr[3]) / rho_sum -
+            (wl[0] * wr[0] / rho_sum) * cmax * (ur - ul);
+  *u_star = (wl[0] * ul + wr[0] * ur) / rho_sum - (wr[3] - wl[3]) / (cmax * rho_sum);
+}
+
+/* euler.hpp:87-97 (the positivity guard is the caller's, solver.cpp:222) */
+static inline void cons_from_prim(const double w[4], double gamma, double u[4]) {
+  u[0] = w[0];
+  u[1] = w[0] * w[1];
+  u[2] = w[0] * w[2];
+  u[3] = w[3] / (gamma - 1.0) + 0.5 * w[0] * (w[1] * w[1] + w[2] * w[2]);
+}
+
+/* solver.cpp:26-43 */
+static inline void contact_flux(const double um[4], const double up[4], double nx, double ny,
+                                double p_star, double u_star, double f[4]) {
+  double ua[4];
+  if (u_star > 0.0) {
+    memcpy(ua, um, sizeof ua);
+  } else if (u_star < 0.0) {
+    memcpy(ua, up, sizeof ua);
+  } else {
+    for (int c = 0; c < 4; ++c) ua[c] = 0.5 * (um[c] + up[c]);
+  }
+  f[0] = ua[0] * u_star;
+  f[1] = ua[1] * u_star + p_star * nx;
+  f[2] = ua[2] * u_star + p_star * ny;
+  f[3] = ua[3] * u_star + p_star * u_star;
+}
+
+/* solver.cpp:47-53 */
+void lfo_edge_flux(const double wm[4], const double wp[4], double nx, double ny, double gamma,
+                   double f[4]) {
+  double ps, us, um[4], up[4];
+  lfo_lagrangian_hll(wm, wp, nx, ny, gamma, gamma, &ps, &us);
+  cons_from_prim(wm, gamma, um);
+  cons_from_prim(wp, gamma, up);
+  contact_flux(um, up, nx, ny, ps, us, f);
+}
+
+/* solver.cpp:61-88 */
+lfo_solver* lfo_create(const lfo_grid* g, const lfo_scheme* s, lfo_error* err) {
+  set_err(err, 0);
+  if (g->nx < 1 || g->ny < 1) {
+    set_err(err, LFO_ERR_CONFIG);
+    if (err) snprintf(err->message, sizeof err->message, "grid has no interior cells");
+    return NULL;
+  }
+  if (g->gx < 2 || (g->dim == 2 && g->gy < 2)) {
+    set_err(err, LFO_ERR_CONFIG);
+    if (err) snprintf(err->message, sizeof err->message, "MUSCL stencils need at least two ghost layers");
+    return NULL;
+  }
+  /* validate_boundary, grid.cpp:65-70 */
+  if ((s->bc[0] == LFO_PERIODIC) != (s->bc[1] == LFO_PERIODIC)) {
+    set_err(err, LFO_ERR_CONFIG);
+    if (err) snprintf(err->message, sizeof err->message, "periodic boundary in x must be set on both sides");
+    return NULL;
+  }
+  if (g->dim == 2 && (s->bc[2] == LFO_PERIODIC) != (s->bc[3] == LFO_PERIODIC)) {
+    set_err(err, LFO_ERR_CONFIG);
+    if (err) snprintf(err->message, sizeof err->message, "periodic boundary in y must be set on both sides");
+    return NULL;
+  }
+  lfo_solver* so = (lfo_solver*)calloc(1, sizeof *so);
+  so->g = *g;
+  so->s = *s;
+  so->cells = (int64_t)nxt_of(g) * nyt_of(g);
+  const size_t nex = (size_t)(g->nx + 1) * g->ny;
+  const size_t ney = g->dim == 2 ? (size_t)g->nx * (g->ny + 1) : 0;
+  for (int k = 0; k < 2; ++k) {
+    for (int c = 0; c < 4; ++c) {
+      so->prim[k][c] = (double*)calloc((size_t)so->cells, sizeof(double));
+      so->fx[k][c] = (double*)calloc(nex ? nex : 1, sizeof(double));
+      so->fy[k][c] = (double*)calloc(ney ? ney : 1, sizeof(double));
+    }
+    so->ustar_x[k] = (double*)calloc(nex ? nex : 1, sizeof(double));
+    so->ustar_y[k] = (double*)calloc(ney ? ney : 1, sizeof(double));
+  }
+  for (int c = 0; c < 4; ++c) so->pred[c] = (double*)calloc((size_t)so->cells, sizeof(double));
+  return so;
+}
+
+void lfo_destroy(lfo_solver* so) {
+  if (!so) return;
+  for (int k = 0; k < 2; ++k) {
+    for (int c = 0; c < 4; ++c) {
+      free(so->prim[k][c]);
+      free(so->fx[k][c]);
+      free(so->fy[k][c]);
+    }
+    free(so->ustar_x[k]);
+    free(so->ustar_y[k]);
+  }
+  for (int c = 0; c < 4; ++c) free(so->pred[c]);
+  free(so);
+}
+
+/* solver.cpp:434-480 */
+int lfo_compute_dt(lfo_solver* so, double* const field[4], double cfl, double time,
+                   double limit_time, double* dt_out, lfo_error* err) {
+  const lfo_grid* g = &so->g;
+  const double gamma = so->s.gamma;
+  const int nx = g->nx, ny = g->ny;
+  const int dim2 = g->dim == 2;
+  const int64_t n_cells = (int64_t)nx * ny;
+  int64_t fail = INT64_MAX;
+  double rate = 0.0;
+  set_err(err, 0);
+  for (int64_t cc = 0; cc < n_cells; ++cc) {
+    const int64_t cell = idx_of(g, g->gx + (int)(cc % nx), g->gy + (int)(cc / nx));
+    const double r = field[0][cell];
+    if (!(r > 0.0)) {
+      if (cc < fail) fail = cc;
+      continue;
+    }
+    const double inv = 1.0 / r;
+    const double u = field[1][cell] * inv;
+    const double v = field[2][cell] * inv;
+    const double p = (gamma - 1.0) *
+                     (field[3][cell] -
+                      0.5 * (field[1][cell] * field[1][cell] + field[2][cell] * field[2][cell]) *
+                          inv);
+    if (!(p > 0.0)) {
+      if (cc < fail) fail = cc;
+      continue;
+    }
+    const double c = sqrt(gamma * p * inv);
+    double rr = (fabs(u) + c) / g->dx;
+    if (dim2) rr += (fabs(v) + c) / g->dy;
+    rate = smax(rate, rr);
+  }
+  if (fail != INT64_MAX) {
+    set_err(err, LFO_ERR_DT_STATE);
+    err->i = fail % nx;
+    err->j = fail / nx;
+    snprintf(err->message, sizeof err->message,
+             "non-physical state while computing the time step at cell (%lld,%lld)",
+             (long long)err->i, (long long)err->j);
+    return LFO_ERR_DT_STATE;
+  }
+  double dt = cfl / rate;
+  if (time + dt > limit_time) dt = limit_time - time;
+  if (!(dt > 0.0)) {
+    set_err(err, LFO_ERR_DT_NONPOS);
+    err->dt = dt;
+    snprintf(err->message, sizeof err->message,
+             "non-positive time step (time limit already reached?)");
+    return LFO_ERR_DT_NONPOS;
+  }
+  *dt_out = dt;
+  return 0;
+}
+
+/* solver.cpp:131-171 */
+static int build_primitives(lfo_solver* so, double* const field[4], int slot, int64_t step,
+                            lfo_error* err) {
+  const lfo_grid* g = &so->g;
+  const double g0 = so->s.gamma;
+  double* rho = so->prim[slot][0];
+  double* u = so->prim[slot][1];
+  double* v = so->prim[slot][2];
+  double* p = so->prim[slot][3];
+  const double* rin = field[0];
+  const double* mx = field[1];
+  const double* my = field[2];
+  const double* re = field[3];
+  int64_t fail = INT64_MAX;
+  for (int64_t c = 0; c < so->cells; ++c) {
+    const double r = rin[c];
+    if (!(r > 0.0)) {
+      if (c < fail) fail = c;
+      rho[c] = u[c] = v[c] = p[c] = 0.0;
+      continue;
+    }
+    const double inv = 1.0 / r;
+    const double uu = mx[c] * inv;
+    const double vv = my[c] * inv;
+    const double pp = (g0 - 1.0) * (re[c] - 0.5 * (mx[c] * mx[c] + my[c] * my[c]) * inv);
+    rho[c] = r;
+    u[c] = uu;
+    v[c] = vv;
+    p[c] = pp;
+    if (!(pp > 0.0)) {
+      if (c < fail) fail = c;
+    }
+  }
+  if (fail == INT64_MAX) return 0;
+  /* primitive_from_conserved with CellContext (euler.hpp:73-85, 56-66) */
+  const int64_t c = fail;
+  set_err(err, LFO_ERR_PRIMITIVE);
+  err->i = c % nxt_of(g) - g->gx;
+  err->j = c / nxt_of(g) - g->gy;
+  err->step = step;
+  char num[64], suffix[96];
+  const char* what;
+  if (!(rin[c] > 0.0)) {
+    what = "non-positive density";
+    err->value = rin[c];
+  } else {
+    const double inv = 1.0 / rin[c];
+    err->value = (g0 - 1.0) * (re[c] - 0.5 * (mx[c] * mx[c] + my[c] * my[c]) * inv);
+    what = "non-positive pressure";
+  }
+  fmt_f(num, sizeof num, err->value);
+  if (step >= 0)
+    snprintf(suffix, sizeof suffix, " at cell (%lld,%lld) step %lld", (long long)err->i,
+             (long long)err->j, (long long)step);
+  else
+    snprintf(suffix, sizeof suffix, " at cell (%lld,%lld)", (long long)err->i, (long long)err->j);
+  snprintf(err->message, sizeof err->message, "%s = %s%s", what, num, suffix);
+  return LFO_ERR_PRIMITIVE;
+}
+
+/* solver.cpp:173-256 */
+static int compute_fluxes(lfo_solver* so, int fs, int slot, int64_t step, lfo_error* err) {
+  const lfo_grid* g = &so->g;
+  const double* rho = so->prim[slot][0];
+  const double* u = so->prim[slot][1];
+  const double* v = so->prim[slot][2];
+  const double* p = so->prim[slot][3];
+  const double gamma = so->s.gamma;
+  const double beta = so->s.beta;
+  const int muscl = so->s.spatial_order >= 2;
+  const int nx = g->nx, ny = g->ny, nxt = nxt_of(g);
+  const int64_t nex = (int64_t)(nx + 1) * ny;
+  int64_t fail = INT64_MAX;
+
+  for (int axis = 0; axis < (g->dim == 2 ? 2 : 1); ++axis) {
+    const int is_x = axis == 0;
+    const int64_t n_edges = is_x ? nex : (int64_t)nx * (ny + 1);
+    const int64_t stride = is_x ? 1 : nxt;
+    const int along = is_x ? nx + 1 : nx;
+    const double nrm_x = is_x ? 1.0 : 0.0;
+    const double nrm_y = is_x ? 0.0 : 1.0;
+    double* const* out = is_x ? so->fx[fs] : so->fy[fs];
+    double* ustar = is_x ? so->ustar_x[fs] : so->ustar_y[fs];
+    for (int64_t e = 0; e < n_edges; ++e) {
+      const int a = (int)(e % along);
+      const int b = (int)(e / along);
+      const int64_t chigh = idx_of(g, g->gx + a, g->gy + b);
+      const int64_t clow = chigh - stride;
+      double wm[4], wp[4];
+      if (muscl) {
+        face_trace(rho[clow - stride], rho[clow], rho[chigh], rho[chigh + stride], beta, &wm[0], &wp[0]);
+        face_trace(u[clow - stride], u[clow], u[chigh], u[chigh + stride], beta, &wm[1], &wp[1]);
+        face_trace(v[clow - stride], v[clow], v[chigh], v[chigh + stride], beta, &wm[2], &wp[2]);
+        face_trace(p[clow - stride], p[clow], p[chigh], p[chigh + stride], beta, &wm[3], &wp[3]);
+      } else {
+        wm[0] = rho[clow]; wm[1] = u[clow]; wm[2] = v[clow]; wm[3] = p[clow];
+        wp[0] = rho[chigh]; wp[1] = u[chigh]; wp[2] = v[chigh]; wp[3] = p[chigh];
+      }
+      if (!(wm[0] > 0.0) || !(wm[3] > 0.0) || !(wp[0] > 0.0) || !(wp[3] > 0.0)) {
+        const int64_t code = (is_x ? 0 : nex) + e;
+        if (code < fail) fail = code;
+        ustar[e] = 0.0;
+        for (int c = 0; c < 4; ++c) out[c][e] = 0.0;
+        continue;
+      }
+      double ps, us, um[4], up[4], f[4];
+      lfo_lagrangian_hll(wm, wp, nrm_x, nrm_y, gamma, gamma, &ps, &us);
+      ustar[e] = us;
+      cons_from_prim(wm, gamma, um);
+      cons_from_prim(wp, gamma, up);
+      contact_flux(um, up, nrm_x, nrm_y, ps, us, f);
+      for (int c = 0; c < 4; ++c) out[c][e] = f[c];
+    }
+  }
+  if (fail == INT64_MAX) return 0;
+  const int is_x = fail < nex;
+  const int64_t e = is_x ? fail : fail - nex;
+  const int along = is_x ? nx + 1 : nx;
+  set_err(err, LFO_ERR_TRACE);
+  err->axis = is_x ? 0 : 1;
+  err->i = e % along;
+  err->j = e / along;
+  err->step = step;
+  snprintf(err->message, sizeof err->message,
+           "non-physical reconstructed trace at %s-face (%lld,%lld) step %lld", is_x ? "x" : "y",
+           (long long)err->i, (long long)err->j, (long long)step);
+  return LFO_ERR_TRACE;
+}
+
+/* solver.cpp:258-329.  fa/fb are flux-set indices (fb < 0: single stage). */
+static int apply_update(lfo_solver* so, double* const base[4], int fa, int fb, double dt,
+                        double* const out[4], int64_t step, double* min_rho, double* min_p,
+                        lfo_error* err) {
+  const lfo_grid* g = &so->g;
+  const int nx = g->nx, ny = g->ny;
+  const double lam_x = dt / g->dx;
+  const double lam_y = dt / g->dy;
+  const int two = fb >= 0;
+  const int dim2 = g->dim == 2;
+  const int64_t n_cells = (int64_t)nx * ny;
+  int64_t fail = INT64_MAX;
+  double mr = INFINITY, me = INFINITY;
+  for (int64_t cc = 0; cc < n_cells; ++cc) {
+    const int i = (int)(cc % nx);
+    const int j = (int)(cc / nx);
+    const int64_t cell = idx_of(g, g->gx + i, g->gy + j);
+    const size_t exl = (size_t)j * (nx + 1) + i;
+    const size_t exr = exl + 1;
+    const size_t eyb = (size_t)j * nx + i;
+    const size_t eyt = eyb + (size_t)nx;
+    double vals[4];
+    for (int c = 0; c < 4; ++c) {
+      const double* ax = so->fx[fa][c];
+      const double fxl = two ? 0.5 * (ax[exl] + so->fx[fb][c][exl]) : ax[exl];
+      const double fxr = two ? 0.5 * (ax[exr] + so->fx[fb][c][exr]) : ax[exr];
+      double val = base[c][cell] - lam_x * (fxr - fxl);
+      if (dim2) {
+        const double* ay = so->fy[fa][c];
+        const double fyb = two ? 0.5 * (ay[eyb] + so->fy[fb][c][eyb]) : ay[eyb];
+        const double fyt = two ? 0.5 * (ay[eyt] + so->fy[fb][c][eyt]) : ay[eyt];
+        val -= lam_y * (fyt - fyb);
+      }
+      vals[c] = val;
+    }
+    out[0][cell] = vals[0];
+    out[1][cell] = vals[1];
+    out[2][cell] = vals[2];
+    out[3][cell] = vals[3];
+    const double eint = vals[3] - 0.5 * (vals[1] * vals[1] + vals[2] * vals[2]) / vals[0];
+    if (!(vals[0] > 0.0) || !(eint > 0.0)) {
+      if (cc < fail) fail = cc;
+    } else {
+      mr = smin(mr, vals[0]);
+      me = smin(me, eint);
+    }
+  }
+  if (fail != INT64_MAX) {
+    const int64_t i = fail % nx, j = fail / nx;
+    const int64_t cell = idx_of(g, (int)(g->gx + i), (int)(g->gy + j));
+    const double r = out[0][cell];
+    const double eint =
+        out[3][cell] - 0.5 * (out[1][cell] * out[1][cell] + out[2][cell] * out[2][cell]) / r;
+    char rs[64], es[64], ds[64];
+    fmt_f(rs, sizeof rs, r);
+    fmt_f(es, sizeof es, eint);
+    fmt_f(ds, sizeof ds, dt);
+    set_err(err, LFO_ERR_POSITIVITY);
+    err->i = i;
+    err->j = j;
+    err->step = step;
+    err->dt = dt;
+    err->value = r;
+    err->value2 = eint;
+    snprintf(err->message, sizeof err->message,
+             "update lost positivity at cell (%lld,%lld): rho = %s, internal energy density = %s, "
+             "step %lld, dt %s",
+             (long long)i, (long long)j, rs, es, (long long)step, ds);
+    return LFO_ERR_POSITIVITY;
+  }
+  if (min_rho) *min_rho = mr;
+  if (min_p) *min_p = me;
+  return 0;
+}
+
+/* solver.cpp:406-432 */
+static void accumulate_boundary_outflow(lfo_solver* so, int fa, int fb, double dt, double acc[4]) {
+  const lfo_grid* g = &so->g;
+  const int nx = g->nx, ny = g->ny;
+  const double ax = dt * (g->dim == 1 ? 1.0 : g->dy);
+  for (int c = 0; c < 4; ++c) {
+    const double* a = so->fx[fa][c];
+    const double* b = fb >= 0 ? so->fx[fb][c] : a;
+    double s = 0.0;
+    for (int j = 0; j < ny; ++j) {
+      const size_t row = (size_t)j * (nx + 1);
+      const double r = fb >= 0 ? 0.5 * (a[row + nx] + b[row + nx]) : a[row + nx];
+      const double l = fb >= 0 ? 0.5 * (a[row] + b[row]) : a[row];
+      s += r - l;
+    }
+    acc[c] += ax * s;
+  }
+  if (g->dim == 2) {
+    const double ay = dt * g->dx;
+    for (int c = 0; c < 4; ++c) {
+      const double* a = so->fy[fa][c];
+      const double* b = fb >= 0 ? so->fy[fb][c] : a;
+      double s = 0.0;
+      for (int i = 0; i < nx; ++i) {
+        const size_t t = (size_t)ny * nx + i;
+        const double tv = fb >= 0 ? 0.5 * (a[t] + b[t]) : a[t];
+        const double bv = fb >= 0 ? 0.5 * (a[i] + b[i]) : a[i];
+        s += tv - bv;
+      }
+      acc[c] += ay * s;
+    }
+  }
+}
+
+/* solver.cpp:482-487 */
+int lfo_euler_stage(lfo_solver* so, double* const in[4], double dt, double* const out[4],
+                    int64_t step, lfo_error* err) {
+  set_err(err, 0);
+  lfo_apply_boundary(&so->g, so->s.bc, in);
+  int rc = build_primitives(so, in, 0, step, err);
+  if (rc) return rc;
+  rc = compute_fluxes(so, 0, 0, step, err);
+  if (rc) return rc;
+  return apply_update(so, in, 0, -1, dt, out, step, NULL, NULL, err);
+}
+
+/* solver.cpp:489-546 (single material) */
+int lfo_heun_step(lfo_solver* so, double* const field[4], double cfl, double limit_time,
+                  double* time, int64_t* step, double* boundary_outflow, lfo_step_out* out,
+                  lfo_error* err) {
+  set_err(err, 0);
+  lfo_apply_boundary(&so->g, so->s.bc, field);
+  double dt = 0.0;
+  int rc = lfo_compute_dt(so, field, cfl, *time, limit_time, &dt, err);
+  if (rc) return rc;
+  const int hits_limit = *time + dt >= limit_time;
+
+  rc = build_primitives(so, field, 0, *step, err);
+  if (rc) return rc;
+  rc = compute_fluxes(so, 0, 0, *step, err);
+  if (rc) return rc;
+  double min_rho = 0.0, min_eint = 0.0;
+  rc = apply_update(so, field, 0, -1, dt, so->pred, *step, &min_rho, &min_eint, err);
+  if (rc) return rc;
+
+  if (so->s.time_order >= 2) {
+    lfo_apply_boundary(&so->g, so->s.bc, so->pred);
+    rc = build_primitives(so, so->pred, 1, *step, err);
+    if (rc) return rc;
+    rc = compute_fluxes(so, 1, 1, *step, err);
+    if (rc) return rc;
+    rc = apply_update(so, field, 0, 1, dt, field, *step, &min_rho, &min_eint, err);
+    if (rc) return rc;
+    accumulate_boundary_outflow(so, 0, 1, dt, boundary_outflow);
+  } else {
+    /* std::swap(state.field.comp, predictor_.comp): copy the predictor out. */
+    for (int c = 0; c < 4; ++c) {
+      double* t = field[c];
+      memcpy(t, so->pred[c], (size_t)so->cells * sizeof(double));
+    }
+    accumulate_boundary_outflow(so, 0, -1, dt, boundary_outflow);
+  }
+  const double min_p = (so->s.gamma - 1.0) * min_eint;
+  *time = hits_limit ? limit_time : *time + dt;
+  *step += 1;
+  if (out) {
+    out->dt = dt;
+    out->hits_limit = hits_limit;
+    out->time = *time;
+    out->step = *step;
+    out->min_rho = min_rho;
+    out->min_p = min_p;
+    for (int c = 0; c < 4; ++c) out->boundary_outflow[c] = boundary_outflow[c];
+  }
+  return 0;
+}
+
+/* ---- Seeded smooth-perturbation generator ----
+ * std::mt19937_64 restated (seed_seq-free integer seeding).  Each field k and
+ * mode m draws, in order, kx, ky (1 + raw % 8), amplitude a = (raw>>11)*2^-53
+ * and phase phi = 2*pi*((raw>>11)*2^-53).  The mode is
+ *   a * sin(2 pi (kx x + ky y) + phi)
+ *     = a * (sin(2 pi kx x + phi) cos(2 pi ky y) + cos(2 pi kx x + phi) sin(2 pi ky y)),
+ * and the generator is DEFINED by the separable right-hand side evaluated from
+ * 1D tables, so host and device produce identical bits. */
+typedef struct { uint64_t mt[312]; int mti; } mt64;
+
+static void mt64_seed(mt64* s, uint64_t seed) {
+  s->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    s->mt[i] = 6364136223846793005ULL * (s->mt[i - 1] ^ (s->mt[i - 1] >> 62)) + (uint64_t)i;
+  s->mti = 312;
+}
+
+static uint64_t mt64_next(mt64* s) {
+  static const uint64_t mag01[2] = {0ULL, 0xB5026F5AA96619E9ULL};
+  const uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
+  if (s->mti >= 312) {
+    int i;
+    for (i = 0; i < 312 - 156; ++i) {
+      uint64_t x = (s->mt[i] & UM) | (s->mt[i + 1] & LM);
+      s->mt[i] = s->mt[i + 156] ^ (x >> 1) ^ mag01[(int)(x & 1ULL)];
+    }
+    for (; i < 311; ++i) {
+      uint64_t x = (s->mt[i] & UM) | (s->mt[i + 1] & LM);
+      s->mt[i] = s->mt[i + (156 - 312)] ^ (x >> 1) ^ mag01[(int)(x & 1ULL)];
+    }
+    uint64_t x = (s->mt[311] & UM) | (s->mt[0] & LM);
+    s->mt[311] = s->mt[155] ^ (x >> 1) ^ mag01[(int)(x & 1ULL)];
+    s->mti = 0;
+  }
+  uint64_t x = s->mt[s->mti++];
+  x ^= (x >> 29) & 0x5555555555555555ULL;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+  x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+  x ^= (x >> 43);
+  return x;
+}
+
+void lfo_fourier_tables(uint64_t seed, int nx, int ny, double x0, double y0, double dx,
+                        double dy, double* tx, double* ty, double* amp) {
+  const double two_pi = 6.283185307179586476925286766559;
+  mt64 rng;
+  mt64_seed(&rng, seed);
+  for (int k = 0; k < 4; ++k) {
+    for (int m = 0; m < 8; ++m) {
+      const int kx = 1 + (int)(mt64_next(&rng) % 8ULL);
+      const int ky = 1 + (int)(mt64_next(&rng) % 8ULL);
+      const double a = (double)(mt64_next(&rng) >> 11) * 0x1.0p-53;
+      const double phi = two_pi * ((double)(mt64_next(&rng) >> 11) * 0x1.0p-53);
+      amp[k * 8 + m] = a;
+      double* sx = tx + ((size_t)(k * 8 + m) * 2) * nx;
+      double* cx = sx + nx;
+      for (int i = 0; i < nx; ++i) {
+        const double x = x0 + (i + 0.5) * dx;
+        const double arg = two_pi * (kx * x) + phi;
+        sx[i] = sin(arg);
+        cx[i] = cos(arg);
+      }
+      double* sy = ty + ((size_t)(k * 8 + m) * 2) * ny;
+      double* cy = sy + ny;
+      for (int j = 0; j < ny; ++j) {
+        const double y = y0 + (j + 0.5) * dy;
+        const double arg = two_pi * (ky * y);
+        sy[j] = sin(arg);
+        cy[j] = cos(arg);
+      }
+    }
+  }
+}

@@ -1,0 +1,254 @@
+// ref_shim.cpp -- C entry points over the UNMODIFIED reference solver.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together with
+// the reference's own sources (/root/reference/proj/src/solver.cpp, grid.cpp)
+// into oracle/_ref/libref_lagflux.so.  It is the "reference" CPU arm of
+// bench.py and the pin for the C restatement (oracle/lagflux_oracle.c).
+// Nothing in this file restates the algorithm: it only marshals arrays into a
+// lagflux::SolverState and calls lagflux::LagfluxSolver (solver.hpp:78-131).
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "lagflux/error.hpp"
+#include "lagflux/solver.hpp"
+#include "lagflux_oracle.h"
+
+using namespace lagflux;
+
+struct lfr_solver {
+  CartesianGrid g;
+  BoundaryCondition bc;
+  PerfectGasEos eos;
+  SchemeParams params;
+  LagfluxSolver* solver = nullptr;
+  SolverState state;
+  CellField scratch;  // euler_stage output
+};
+
+namespace {
+
+BcKind bc_kind(int k) {
+  return k == LFO_REFLECTIVE ? BcKind::reflective
+                             : (k == LFO_PERIODIC ? BcKind::periodic : BcKind::transmissive);
+}
+
+void clear(lfo_error* e) {
+  if (!e) return;
+  std::memset(e, 0, sizeof *e);
+  e->i = e->j = e->step = -1;
+}
+
+int map_exception(lfo_error* e, int default_kind) {
+  clear(e);
+  int kind = default_kind;
+  try {
+    throw;
+  } catch (const PositivityError& x) {
+    kind = LFO_ERR_POSITIVITY;
+    if (e) {
+      e->i = x.cell_i;
+      e->j = x.cell_j;
+      e->step = x.step;
+      e->dt = x.dt;
+      std::snprintf(e->message, sizeof e->message, "%s", x.what());
+    }
+  } catch (const ConfigError& x) {
+    kind = LFO_ERR_CONFIG;
+    if (e) std::snprintf(e->message, sizeof e->message, "%s", x.what());
+  } catch (const InvalidStateError& x) {
+    const std::string w = x.what();
+    if (w.rfind("non-physical state while computing the time step", 0) == 0)
+      kind = LFO_ERR_DT_STATE;
+    else if (w.rfind("non-physical reconstructed trace", 0) == 0)
+      kind = LFO_ERR_TRACE;
+    else
+      kind = LFO_ERR_PRIMITIVE;
+    if (e) std::snprintf(e->message, sizeof e->message, "%s", x.what());
+  } catch (const Error& x) {
+    kind = LFO_ERR_DT_NONPOS;
+    if (e) std::snprintf(e->message, sizeof e->message, "%s", x.what());
+  } catch (const std::exception& x) {
+    if (e) std::snprintf(e->message, sizeof e->message, "%s", x.what());
+  }
+  if (e) e->kind = kind;
+  return kind;
+}
+
+CartesianGrid to_grid(const lfo_grid* g) {
+  CartesianGrid c;
+  c.dim = g->dim;
+  c.nx = g->nx;
+  c.ny = g->ny;
+  c.dx = g->dx;
+  c.dy = g->dy;
+  c.x0 = g->x0;
+  c.y0 = g->y0;
+  c.gx = g->gx;
+  c.gy = g->gy;
+  return c;
+}
+
+void copy_in(CellField& f, double* const src[4]) {
+  for (int c = 0; c < 4; ++c)
+    std::memcpy(f.comp[c].data(), src[c], f.comp[c].size() * sizeof(double));
+}
+
+void copy_out(const CellField& f, double* const dst[4]) {
+  for (int c = 0; c < 4; ++c)
+    std::memcpy(dst[c], f.comp[c].data(), f.comp[c].size() * sizeof(double));
+}
+
+}  // namespace
+
+extern "C" {
+
+lfr_solver* lfr_create(const lfo_grid* g, const lfo_scheme* s, int threads, lfo_error* err) {
+  clear(err);
+  auto* r = new lfr_solver;
+  try {
+    r->g = to_grid(g);
+    r->bc = {bc_kind(s->bc[0]), bc_kind(s->bc[1]), bc_kind(s->bc[2]), bc_kind(s->bc[3])};
+    r->eos = PerfectGasEos{s->gamma};
+    r->params.limiter = LimiterParams{s->beta};
+    r->params.spatial_order = s->spatial_order;
+    r->params.time_order = s->time_order;
+    r->solver = new LagfluxSolver(r->g, r->bc, r->eos, r->params, threads);
+    r->state.field = CellField(r->g);
+    r->scratch = CellField(r->g);
+  } catch (...) {
+    map_exception(err, LFO_ERR_CONFIG);
+    delete r->solver;
+    delete r;
+    return nullptr;
+  }
+  return r;
+}
+
+void lfr_destroy(lfr_solver* r) {
+  if (!r) return;
+  delete r->solver;
+  delete r;
+}
+
+// Replace the solver state (field, time, step, outflow; diagnostics cleared).
+void lfr_set_state(lfr_solver* r, double* const field[4], double time, int64_t step) {
+  copy_in(r->state.field, field);
+  r->state.time = time;
+  r->state.step = step;
+  r->state.diagnostics.clear();
+  for (double& b : r->state.boundary_outflow) b = 0.0;
+}
+
+void lfr_get_state(lfr_solver* r, double* const field[4], double* time, int64_t* step,
+                   double* outflow) {
+  copy_out(r->state.field, field);
+  if (time) *time = r->state.time;
+  if (step) *step = r->state.step;
+  if (outflow)
+    for (int c = 0; c < 4; ++c) outflow[c] = r->state.boundary_outflow[size_t(c)];
+}
+
+// n calls of LagfluxSolver::heun_step on the internal state (bench.cpp:70-75).
+// dts/diag (optional, n entries / n*5 doubles) receive the per-step record
+// {dt, time, min_rho, min_p, step}.  Returns 0 or the error kind; *done = steps taken.
+int lfr_heun_steps(lfr_solver* r, int n, double cfl, double limit_time, double* dts,
+                   double* diag, int* done, lfo_error* err) {
+  clear(err);
+  TimeControls controls{cfl, limit_time, INT64_MAX};
+  int k = 0;
+  try {
+    for (; k < n; ++k) {
+      const double dt = r->solver->heun_step(r->state, controls, limit_time, nullptr);
+      if (dts) dts[k] = dt;
+      if (diag) {
+        const StepDiagnostics& d = r->state.diagnostics.back();
+        diag[5 * k + 0] = d.dt;
+        diag[5 * k + 1] = d.time;
+        diag[5 * k + 2] = d.min_rho;
+        diag[5 * k + 3] = d.min_p;
+        diag[5 * k + 4] = double(d.step);
+      }
+    }
+  } catch (...) {
+    if (done) *done = k;
+    return map_exception(err, LFO_ERR_PRIMITIVE);
+  }
+  if (done) *done = k;
+  return 0;
+}
+
+// LagfluxSolver::compute_dt on the internal state field.
+int lfr_compute_dt(lfr_solver* r, double cfl, double time, double limit_time, double* dt,
+                   lfo_error* err) {
+  clear(err);
+  try {
+    apply_boundary(r->g, r->bc, r->state.field);
+    TimeControls controls{cfl, limit_time, INT64_MAX};
+    *dt = r->solver->compute_dt(r->state.field, controls, time, limit_time);
+  } catch (...) {
+    return map_exception(err, LFO_ERR_DT_STATE);
+  }
+  return 0;
+}
+
+// LagfluxSolver::euler_stage(state.field, dt, out): out is returned in `out`
+// (ghosts as the reference leaves them: zero-initialised scratch).
+int lfr_euler_stage(lfr_solver* r, double dt, int64_t step, double* const out[4],
+                    lfo_error* err) {
+  clear(err);
+  try {
+    for (auto& c : r->scratch.comp) std::fill(c.begin(), c.end(), 0.0);
+    r->solver->euler_stage(r->state.field, dt, r->scratch, step);
+  } catch (...) {
+    return map_exception(err, LFO_ERR_PRIMITIVE);
+  }
+  copy_out(r->scratch, out);
+  return 0;
+}
+
+// Element functions for known-answer tests.
+void lfr_fill_ghosts(const lfo_grid* g, const int bc[4], int parity, double* f) {
+  const CartesianGrid cg = to_grid(g);
+  const BoundaryCondition b{bc_kind(bc[0]), bc_kind(bc[1]), bc_kind(bc[2]), bc_kind(bc[3])};
+  fill_ghosts(cg, b, parity == 1 ? GhostParity::flip_x
+                                 : (parity == 2 ? GhostParity::flip_y : GhostParity::even),
+              f);
+}
+
+double lfr_sweby(double a, double b, double beta) { return sweby_limiter(a, b, LimiterParams{beta}); }
+
+void lfr_lagrangian_hll(const double wl[4], const double wr[4], double nx, double ny,
+                        double gamma, double* p_star, double* u_star) {
+  const ContactSolution s = lagrangian_hll({wl[0], wl[1], wl[2], wl[3]},
+                                           {wr[0], wr[1], wr[2], wr[3]}, Vec2{nx, ny},
+                                           PerfectGasEos{gamma});
+  *p_star = s.p_star;
+  *u_star = s.u_star;
+}
+
+void lfr_edge_flux(const double wm[4], const double wp[4], double nx, double ny, double gamma,
+                   double f[4]) {
+  const EdgeFlux e = edge_flux({wm[0], wm[1], wm[2], wm[3]}, {wp[0], wp[1], wp[2], wp[3]},
+                               Vec2{nx, ny}, PerfectGasEos{gamma});
+  f[0] = e.mass;
+  f[1] = e.mom_x;
+  f[2] = e.mom_y;
+  f[3] = e.energy;
+}
+
+int lfr_omp_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+}  // extern "C"

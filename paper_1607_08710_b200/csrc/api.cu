@@ -1,0 +1,842 @@
+// api.cu -- the C ABI (include/lagflux_b200.h) over the device kernels.
+//
+// Host orchestration of LagfluxSolver::heun_step (solver.cpp:489-546):
+//   fill ghosts -> (halo exchange between y-slabs) -> CFL rate -> predictor ->
+//   fill ghosts of U* -> corrector -> diagnostics and boundary outflow,
+// reporting failures with the reference's exception kinds, indices and text.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cinttypes>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "fused.h"
+#include "handle.h"
+#include "host_util.h"
+#include "nccl_comm.h"
+
+using namespace lfb;
+
+namespace {
+
+struct DeviceFail {
+  std::string what;
+};
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      throw DeviceFail{std::string(#x) + ": " + cudaGetErrorString(e_)};             \
+  } while (0)
+
+void clear_err(lf_error* e) {
+  std::memset(e, 0, sizeof *e);
+  e->i = e->j = e->step = -1;
+}
+
+int set_err(lf_handle* h, int kind, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+int set_err(lf_handle* h, int kind, const char* fmt, ...) {
+  clear_err(&h->err);
+  h->err.kind = kind;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(h->err.message, sizeof h->err.message, fmt, ap);
+  va_end(ap);
+  return kind;
+}
+
+std::string fmt_f(double v) {  // std::to_string(double) == "%f"
+  char b[64];
+  snprintf(b, sizeof b, "%f", v);
+  return b;
+}
+
+double bits_to_double(unsigned long long b) {
+  double d;
+  std::memcpy(&d, &b, sizeof d);
+  return d;
+}
+
+// ---------------------------------------------------------------- allocation
+void alloc_state(SlabState& s) {
+  CK(cudaSetDevice(s.device));
+  const size_t bytes = (size_t)s.L.alloc * sizeof(double);
+  CK(cudaMalloc(&s.U, bytes));
+  CK(cudaMalloc(&s.U2, bytes));
+  CK(cudaMemsetAsync(s.U, 0, bytes, s.stream));
+  CK(cudaMemsetAsync(s.U2, 0, bytes, s.stream));
+  CK(cudaMalloc(&s.scal, 4 * sizeof(Scalars)));
+  CK(cudaHostAlloc(&s.scal_host, 4 * sizeof(Scalars), cudaHostAllocDefault));
+  CK(cudaMalloc(&s.aux, 8 * sizeof(unsigned long long)));
+  CK(cudaEventCreate(&s.ev_a));
+  CK(cudaEventCreate(&s.ev_b));
+}
+
+void alloc_staged(SlabState& s) {
+  if (s.Us) return;
+  CK(cudaSetDevice(s.device));
+  const size_t bytes = (size_t)s.L.alloc * sizeof(double);
+  CK(cudaMalloc(&s.Us, bytes));
+  CK(cudaMalloc(&s.W, bytes));
+  CK(cudaMemsetAsync(s.Us, 0, bytes, s.stream));
+  CK(cudaMemsetAsync(s.W, 0, bytes, s.stream));
+  s.fx_stride = s.L.pitch * (int64_t)s.L.ny;
+  s.fy_stride = s.L.pitch * (int64_t)(s.L.ny + 1);
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaMalloc(&s.FX[k], 4 * s.fx_stride * sizeof(double)));
+    CK(cudaMalloc(&s.FY[k], 4 * s.fy_stride * sizeof(double)));
+  }
+  const size_t nb = 2 * 4 * (size_t)(2 * s.L.ny + 2 * s.L.nx);
+  CK(cudaMalloc(&s.bnd, nb * sizeof(double)));
+  CK(cudaHostAlloc(&s.bnd_host, nb * sizeof(double), cudaHostAllocDefault));
+}
+
+void free_slab(SlabState& s) {
+  cudaSetDevice(s.device);
+  cudaFree(s.U);
+  cudaFree(s.U2);
+  cudaFree(s.Us);
+  cudaFree(s.W);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(s.FX[k]);
+    cudaFree(s.FY[k]);
+  }
+  cudaFree(s.bnd);
+  cudaFreeHost(s.bnd_host);
+  cudaFree(s.scal);
+  cudaFreeHost(s.scal_host);
+  cudaFree(s.aux);
+  if (s.ev_a) cudaEventDestroy(s.ev_a);
+  if (s.ev_b) cudaEventDestroy(s.ev_b);
+  if (s.own_stream) cudaStreamDestroy(s.own_stream);
+}
+
+// ---------------------------------------------------------------- validation
+int validate_desc(lf_handle* h, const lf_desc* d) {
+  if (d->dim != 1 && d->dim != 2) return set_err(h, LF_ERR_CONFIG, "dimension must be 1 or 2");
+  if (d->nx < 1 || d->ny < 1) return set_err(h, LF_ERR_CONFIG, "grid has no interior cells");
+  if (d->dim == 1 && d->ny != 1) return set_err(h, LF_ERR_CONFIG, "a 1D grid has ny = 1");
+  for (int b = 0; b < 4; ++b)
+    if (d->bc[b] < 0 || d->bc[b] > 2) return set_err(h, LF_ERR_CONFIG, "unknown boundary kind");
+  // validate_boundary, grid.cpp:65-70
+  if ((d->bc[0] == LF_PERIODIC) != (d->bc[1] == LF_PERIODIC))
+    return set_err(h, LF_ERR_CONFIG, "periodic boundary in x must be set on both sides");
+  if (d->dim == 2 && (d->bc[2] == LF_PERIODIC) != (d->bc[3] == LF_PERIODIC))
+    return set_err(h, LF_ERR_CONFIG, "periodic boundary in y must be set on both sides");
+  if (d->spatial_order != 1 && d->spatial_order != 2)
+    return set_err(h, LF_ERR_CONFIG, "spatial_order must be 1 or 2");
+  if (d->time_order != 1 && d->time_order != 2)
+    return set_err(h, LF_ERR_CONFIG, "time_order must be 1 or 2");
+  return 0;
+}
+
+void init_common(lf_handle* h, const lf_desc* d) {
+  h->d = *d;
+  h->dim2 = d->dim == 2;
+  h->k.gamma = d->gamma;
+  h->k.gm1 = d->gamma - 1.0;
+  h->k.beta = d->beta;
+  h->k.dx = d->dx;
+  h->k.dy = d->dy;
+}
+
+// Split ny rows into n slabs (first slabs take the remainder).
+void slab_rows(int ny, int n, int s, int* y0, int* rows) {
+  const int base = ny / n, rem = ny % n;
+  *rows = base + (s < rem ? 1 : 0);
+  *y0 = s * base + std::min(s, rem);
+}
+
+// ---------------------------------------------------------------- halos
+// Copy the NG boundary rows (full padded width, x ghosts included, so corners
+// wrap as in grid.cpp:98-113) between neighbouring in-process slabs.
+void exchange_local(lf_handle* h, double* SlabState::*buf) {
+  const int n = (int)h->slabs.size();
+  if (n == 1) return;
+  const bool periodic = h->d.bc[2] == LF_PERIODIC;
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    CK(cudaEventRecord(s.ev_a, s.stream));
+  }
+  for (int t = 0; t < n; ++t) {
+    SlabState& dst = h->slabs[t];
+    CK(cudaSetDevice(dst.device));
+    for (int side = 0; side < 2; ++side) {
+      int src_i = side == 0 ? t - 1 : t + 1;
+      if (src_i < 0 || src_i >= n) {
+        if (!periodic) continue;
+        src_i = (src_i + n) % n;
+      }
+      SlabState& src = h->slabs[src_i];
+      CK(cudaStreamWaitEvent(dst.stream, src.ev_a, 0));
+      const int src_row = side == 0 ? src.L.ny - NG : 0;
+      const int dst_row = side == 0 ? -NG : dst.L.ny;
+      for (int c = 0; c < 4; ++c) {
+        const double* sp = (src.*buf) + src.L.origin() + c * src.L.fstride +
+                           (int64_t)src_row * src.L.pitch - NG;
+        double* dp = (dst.*buf) + dst.L.origin() + c * dst.L.fstride +
+                     (int64_t)dst_row * dst.L.pitch - NG;
+        CK(cudaMemcpy2DAsync(dp, dst.L.pitch * sizeof(double), sp, src.L.pitch * sizeof(double),
+                             (size_t)(dst.L.nx + 2 * NG) * sizeof(double), NG,
+                             cudaMemcpyDefault, dst.stream));
+      }
+    }
+  }
+  // the copies read the neighbours' rows: nobody may overwrite them before done
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    CK(cudaEventRecord(s.ev_b, s.stream));
+  }
+  for (auto& s : h->slabs)
+    for (auto& o : h->slabs) {
+      if (&o == &s) continue;
+      CK(cudaSetDevice(s.device));
+      CK(cudaStreamWaitEvent(s.stream, o.ev_b, 0));
+    }
+}
+
+// Ghost cells of `buf` on every slab: x sides, halo rows, then y sides at the
+// domain edges (grid.cpp:79-113 order).
+void fill_all(lf_handle* h, double* SlabState::*buf) {
+  const int xbc[4] = {h->d.bc[0], h->d.bc[1], h->d.bc[2], h->d.bc[3]};
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    launch_fill_x(s.field(s.*buf), s.L, xbc, s.stream);
+  }
+  if (h->nccl)
+    nccl_exchange_halos(h, buf);
+  else
+    exchange_local(h, buf);
+  for (auto& s : h->slabs) {
+    if (!h->dim2 || !(s.sl.fill_lo || s.sl.fill_hi)) continue;
+    CK(cudaSetDevice(s.device));
+    launch_fill_y_only(s.field(s.*buf), s.L, xbc, s.sl, s.stream);
+  }
+  CK(cudaGetLastError());
+}
+
+void sync_all(lf_handle* h) {
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    CK(cudaStreamSynchronize(s.stream));
+  }
+}
+
+// Read back scalars slot `slot` of every slab and combine them (max rate, min
+// everything else) -- across ranks with one NCCL all-reduce.
+Scalars combined_scalars(lf_handle* h, int slot) {
+  Scalars r{};
+  bool first = true;
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    CK(cudaMemcpyAsync(&s.scal_host[slot], &s.scal[slot], sizeof(Scalars),
+                       cudaMemcpyDeviceToHost, s.stream));
+  }
+  sync_all(h);
+  for (auto& s : h->slabs) {
+    const Scalars& x = s.scal_host[slot];
+    if (first) {
+      r = x;
+      first = false;
+      continue;
+    }
+    r.rate_bits = std::max(r.rate_bits, x.rate_bits);
+    r.fail_dt = std::min(r.fail_dt, x.fail_dt);
+    r.fail_prim = std::min(r.fail_prim, x.fail_prim);
+    r.fail_trace = std::min(r.fail_trace, x.fail_trace);
+    r.fail_update = std::min(r.fail_update, x.fail_update);
+    r.min_rho_bits = std::min(r.min_rho_bits, x.min_rho_bits);
+    r.min_eint_bits = std::min(r.min_eint_bits, x.min_eint_bits);
+  }
+  if (h->nccl) nccl_combine_scalars(h, &r);
+  return r;
+}
+
+// Fetch the 4 components of local cell (i, j) of `buf` on the slab owning global row jg.
+bool fetch_cell(lf_handle* h, double* SlabState::*buf, int i, int jg, double v[4]) {
+  for (auto& s : h->slabs) {
+    int jl = jg - s.sl.y0;
+    const bool inside = jl >= 0 && jl < s.L.ny;
+    const bool ghost_lo = s.sl.fill_lo && jl >= -2 && jl < 0;
+    const bool ghost_hi = s.sl.fill_hi && jl >= s.L.ny && jl < s.L.ny + 2;
+    if (!(inside || ghost_lo || ghost_hi)) continue;
+    CK(cudaSetDevice(s.device));
+    for (int c = 0; c < 4; ++c)
+      CK(cudaMemcpy(&v[c], (s.*buf) + s.L.origin() + c * s.L.fstride + (int64_t)jl * s.L.pitch + i,
+                    sizeof(double), cudaMemcpyDeviceToHost));
+    return true;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------- error records
+int report_prim(lf_handle* h, double* SlabState::*buf, long long c, int64_t step) {
+  const int gy = h->dim2 ? 2 : 0;
+  const long long nxt = h->d.nx + 4;
+  const long long ii = c % nxt - 2, jj = c / nxt - gy;
+  double v[4] = {0, 0, 0, 0};
+  fetch_cell(h, buf, (int)ii, (int)jj, v);
+  // primitive_from_conserved with CellContext (euler.hpp:73-85)
+  const char* what;
+  double value;
+  if (!(v[0] > 0.0)) {
+    what = "non-positive density";
+    value = v[0];
+  } else {
+    const double inv = 1.0 / v[0];
+    const double kinetic = 0.5 * (v[1] * v[1] + v[2] * v[2]) * inv;
+    value = (h->d.gamma - 1.0) * (v[3] - kinetic);
+    what = "non-positive pressure";
+  }
+  char suffix[96];
+  if (step >= 0)
+    snprintf(suffix, sizeof suffix, " at cell (%lld,%lld) step %lld", ii, jj, (long long)step);
+  else
+    snprintf(suffix, sizeof suffix, " at cell (%lld,%lld)", ii, jj);
+  set_err(h, LF_ERR_PRIMITIVE, "%s = %s%s", what, fmt_f(value).c_str(), suffix);
+  h->err.i = ii;
+  h->err.j = jj;
+  h->err.step = step;
+  h->err.value = value;
+  return LF_ERR_PRIMITIVE;
+}
+
+int report_trace(lf_handle* h, long long code, int64_t step) {
+  const long long nx = h->d.nx;
+  const long long nex = (nx + 1) * h->d.ny;
+  const bool is_x = code < nex;
+  const long long e = is_x ? code : code - nex;
+  const long long along = is_x ? nx + 1 : nx;
+  set_err(h, LF_ERR_TRACE, "non-physical reconstructed trace at %s-face (%lld,%lld) step %lld",
+          is_x ? "x" : "y", e % along, e / along, (long long)step);
+  h->err.axis = is_x ? 0 : 1;
+  h->err.i = e % along;
+  h->err.j = e / along;
+  h->err.step = step;
+  return LF_ERR_TRACE;
+}
+
+int report_update(lf_handle* h, double* SlabState::*out, long long cc, int64_t step, double dt) {
+  const long long nx = h->d.nx;
+  const long long i = cc % nx, j = cc / nx;
+  double v[4] = {0, 0, 0, 0};
+  fetch_cell(h, out, (int)i, (int)j, v);
+  const double r = v[0];
+  const double eint = v[3] - 0.5 * (v[1] * v[1] + v[2] * v[2]) / r;
+  set_err(h, LF_ERR_POSITIVITY,
+          "update lost positivity at cell (%lld,%lld): rho = %s, internal energy density = %s, "
+          "step %lld, dt %s",
+          i, j, fmt_f(r).c_str(), fmt_f(eint).c_str(), (long long)step, fmt_f(dt).c_str());
+  h->err.i = i;
+  h->err.j = j;
+  h->err.step = step;
+  h->err.dt = dt;
+  h->err.value = r;
+  h->err.value2 = eint;
+  return LF_ERR_POSITIVITY;
+}
+
+// dt from the combined rate (solver.cpp:471-479)
+int finish_dt(lf_handle* h, const Scalars& sc, double cfl, double time, double limit, double* dt) {
+  if (sc.fail_dt != LLONG_MAX) {
+    const long long nx = h->d.nx;
+    set_err(h, LF_ERR_DT_STATE,
+            "non-physical state while computing the time step at cell (%lld,%lld)",
+            sc.fail_dt % nx, sc.fail_dt / nx);
+    h->err.i = sc.fail_dt % nx;
+    h->err.j = sc.fail_dt / nx;
+    return LF_ERR_DT_STATE;
+  }
+  const double rate = bits_to_double(sc.rate_bits);
+  double d = cfl / rate;
+  if (time + d > limit) d = limit - time;
+  if (!(d > 0.0)) {
+    set_err(h, LF_ERR_DT_NONPOS, "non-positive time step (time limit already reached?)");
+    h->err.dt = d;
+    return LF_ERR_DT_NONPOS;
+  }
+  *dt = d;
+  return 0;
+}
+
+// CFL rate of `buf` (ghosts not needed) into scalars slot 0.
+void launch_rate_all(lf_handle* h, double* SlabState::*buf) {
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    reset_scalars(&s.scal[0], s.stream);
+    launch_rate(s.field(s.*buf), s.L, s.sl, h->k, h->dim2, &s.scal[0], s.stream);
+  }
+}
+
+// One stage on every slab: prims(in) -> fluxes(set k) -> update(base, ...) -> out.
+void staged_stage(lf_handle* h, double* SlabState::*in, double* SlabState::*base,
+                  double* SlabState::*out, int k, bool two, double dt, int slot) {
+  fill_all(h, in);
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    reset_scalars(&s.scal[slot], s.stream);
+    launch_prims(s.field(s.*in), s.field(s.W), s.L, s.sl, h->k.gm1, h->dim2, &s.scal[slot],
+                 s.stream);
+    const FluxArr fx = s.fluxx(k), fy = s.fluxy(k);
+    launch_fluxes(s.field(s.W), fx, fy, s.L, s.sl, h->k, h->d.spatial_order >= 2, h->dim2,
+                  &s.scal[slot], s.stream);
+    const FluxArr fx0 = s.fluxx(0), fy0 = s.fluxy(0);
+    launch_update(s.field(s.*base), fx0, fy0, two ? &fx : nullptr, two ? &fy : nullptr,
+                  s.field(s.*out), s.L, s.sl, dt, h->d.dx, h->d.dy, h->dim2, &s.scal[slot],
+                  s.stream);
+  }
+  CK(cudaGetLastError());
+}
+
+// accumulate_boundary_outflow (solver.cpp:406-432): ordered serial sums over
+// the domain-boundary faces, gathered from every slab in global order.
+void boundary_outflow(lf_handle* h, bool two, double dt, double* acc) {
+  const int nx = h->d.nx, nyg = h->d.ny;
+  std::vector<double> left(4 * (size_t)nyg), right(4 * (size_t)nyg), bot(4 * (size_t)nx),
+      top(4 * (size_t)nx);
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    launch_gather_boundary(s.fluxx(0), s.fluxy(0), two ? s.fluxx(1) : s.fluxx(0),
+                           two ? s.fluxy(1) : s.fluxy(0), s.L, two, s.bnd, s.stream);
+    const size_t nb = 4 * (size_t)(2 * s.L.ny + 2 * s.L.nx);
+    CK(cudaMemcpyAsync(s.bnd_host, s.bnd, nb * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+  }
+  sync_all(h);
+  for (auto& s : h->slabs) {
+    const int ny = s.L.ny;
+    const double* b = s.bnd_host;
+    for (int c = 0; c < 4; ++c)
+      for (int j = 0; j < ny; ++j) {
+        left[(size_t)c * nyg + s.sl.y0 + j] = b[(size_t)c * ny + j];
+        right[(size_t)c * nyg + s.sl.y0 + j] = b[4 * (size_t)ny + (size_t)c * ny + j];
+      }
+    if (s.sl.y0 == 0)
+      for (int c = 0; c < 4; ++c)
+        for (int i = 0; i < nx; ++i) bot[(size_t)c * nx + i] = b[8 * (size_t)ny + (size_t)c * nx + i];
+    if (s.sl.y0 + ny == nyg)
+      for (int c = 0; c < 4; ++c)
+        for (int i = 0; i < nx; ++i)
+          top[(size_t)c * nx + i] = b[8 * (size_t)ny + 4 * (size_t)nx + (size_t)c * nx + i];
+  }
+  if (h->nccl) nccl_gather_boundary(h, left.data(), right.data(), bot.data(), top.data());
+  const double ax = dt * (h->dim2 ? h->d.dy : 1.0);
+  for (int c = 0; c < 4; ++c) {
+    double sum = 0.0;
+    for (int j = 0; j < nyg; ++j) sum += right[(size_t)c * nyg + j] - left[(size_t)c * nyg + j];
+    acc[c] += ax * sum;
+  }
+  if (h->dim2) {
+    const double ay = dt * h->d.dx;
+    for (int c = 0; c < 4; ++c) {
+      double sum = 0.0;
+      for (int i = 0; i < nx; ++i) sum += top[(size_t)c * nx + i] - bot[(size_t)c * nx + i];
+      acc[c] += ay * sum;
+    }
+  }
+}
+
+void swap_state(lf_handle* h, double* SlabState::*a, double* SlabState::*b) {
+  for (auto& s : h->slabs) std::swap(s.*a, s.*b);
+}
+
+// Check the stage scalars in the reference's order.
+int check_stage(lf_handle* h, const Scalars& sc, double* SlabState::*in,
+                double* SlabState::*out, int64_t step, double dt) {
+  if (sc.fail_prim != LLONG_MAX) return report_prim(h, in, sc.fail_prim, step);
+  if (sc.fail_trace != LLONG_MAX) return report_trace(h, sc.fail_trace, step);
+  if (sc.fail_update != LLONG_MAX) return report_update(h, out, sc.fail_update, step, dt);
+  return 0;
+}
+
+int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t step,
+                double* outflow, lf_step_out* out) {
+  for (auto& s : h->slabs) alloc_staged(s);
+  fill_all(h, &SlabState::U);
+  launch_rate_all(h, &SlabState::U);
+  double dt = 0.0;
+  int rc = finish_dt(h, combined_scalars(h, 0), cfl, time, limit, &dt);
+  if (rc) return rc;
+  const bool hits = time + dt >= limit;
+
+  // predictor: U -> Us with flux set 0 (solver.cpp:496-500)
+  staged_stage(h, &SlabState::U, &SlabState::U, &SlabState::Us, 0, false, dt, 1);
+  const Scalars s1 = combined_scalars(h, 1);
+  rc = check_stage(h, s1, &SlabState::U, &SlabState::Us, step, dt);
+  if (rc) return rc;
+  double min_rho = bits_to_double(s1.min_rho_bits), min_eint = bits_to_double(s1.min_eint_bits);
+  double acc[4] = {0, 0, 0, 0};
+  if (outflow) std::memcpy(acc, outflow, sizeof acc);
+
+  if (h->d.time_order >= 2) {
+    // corrector: Us -> U2 from U^n with 0.5*(F1 + F2) (solver.cpp:503-509)
+    staged_stage(h, &SlabState::Us, &SlabState::U, &SlabState::U2, 1, true, dt, 2);
+    const Scalars s2 = combined_scalars(h, 2);
+    if (s2.fail_prim != LLONG_MAX) return report_prim(h, &SlabState::Us, s2.fail_prim, step);
+    if (s2.fail_trace != LLONG_MAX) return report_trace(h, s2.fail_trace, step);
+    // the reference writes the corrector in place before it throws
+    swap_state(h, &SlabState::U, &SlabState::U2);
+    if (s2.fail_update != LLONG_MAX) return report_update(h, &SlabState::U, s2.fail_update, step, dt);
+    min_rho = bits_to_double(s2.min_rho_bits);
+    min_eint = bits_to_double(s2.min_eint_bits);
+    boundary_outflow(h, true, dt, acc);
+  } else {
+    swap_state(h, &SlabState::U, &SlabState::Us);  // std::swap(state.field.comp, predictor_.comp)
+    boundary_outflow(h, false, dt, acc);
+  }
+  h->rate_valid = false;
+  if (outflow) std::memcpy(outflow, acc, sizeof acc);
+  if (out) {
+    out->dt = dt;
+    out->hits_limit = hits;
+    out->time = hits ? limit : time + dt;
+    out->step = step + 1;
+    out->min_rho = min_rho;
+    out->min_p = (h->d.gamma - 1.0) * min_eint;
+  }
+  return 0;
+}
+
+bool use_fused(lf_handle* h) {
+  if (h->path == LF_PATH_STAGED) return false;
+  return fused_supported(h);
+}
+
+template <class F>
+int guarded(lf_handle* h, F&& f) {
+  if (!h) return LF_ERR_ARGUMENT;
+  try {
+    return f();
+  } catch (const DeviceFail& e) {
+    return set_err(h, LF_ERR_DEVICE, "%s", e.what.c_str());
+  } catch (const std::bad_alloc&) {
+    return set_err(h, LF_ERR_DEVICE, "host allocation failed");
+  } catch (const std::exception& e) {
+    return set_err(h, LF_ERR_DEVICE, "%s", e.what());
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int lf_abi_version(void) { return LF_ABI_VERSION; }
+
+int lf_create(const lf_desc* desc, const int* devices, int ndev, lf_handle** out) {
+  if (!desc || !out || ndev < 1) return LF_ERR_ARGUMENT;
+  *out = nullptr;
+  auto* h = new lf_handle;
+  clear_err(&h->err);
+  int rc = validate_desc(h, desc);
+  if (rc) {
+    *out = h;  // keep the handle so lf_last_error can report
+    return rc;
+  }
+  init_common(h, desc);
+  rc = guarded(h, [&] {
+    if (ndev > 1 && !h->dim2) return set_err(h, LF_ERR_CONFIG, "y-slabs need a 2D grid");
+    h->slabs.resize((size_t)ndev);
+    const bool periodic = desc->bc[2] == LF_PERIODIC;
+    for (int s = 0; s < ndev; ++s) {
+      SlabState& sl = h->slabs[(size_t)s];
+      sl.device = devices ? devices[s] : 0;
+      int y0, rows;
+      slab_rows(desc->ny, ndev, s, &y0, &rows);
+      if (ndev > 1 && rows < NG)
+        return set_err(h, LF_ERR_CONFIG, "each y-slab needs at least %d rows", NG);
+      sl.L = Layout::make(desc->nx, rows);
+      sl.sl.y0 = y0;
+      sl.sl.ny_global = desc->ny;
+      sl.sl.fill_lo = ndev == 1 || (!periodic && s == 0);
+      sl.sl.fill_hi = ndev == 1 || (!periodic && s == ndev - 1);
+      CK(cudaSetDevice(sl.device));
+      CK(cudaStreamCreateWithFlags(&sl.own_stream, cudaStreamNonBlocking));
+      sl.stream = sl.own_stream;
+      alloc_state(sl);
+    }
+    // enable peer access between distinct devices (in-process multi-GPU)
+    for (auto& a : h->slabs)
+      for (auto& b : h->slabs)
+        if (a.device != b.device) {
+          int can = 0;
+          cudaDeviceCanAccessPeer(&can, a.device, b.device);
+          if (can) {
+            cudaSetDevice(a.device);
+            cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          }
+        }
+    sync_all(h);
+    return 0;
+  });
+  *out = h;
+  return rc;
+}
+
+int lf_nccl_unique_id(void* id128) { return nccl_unique_id(id128); }
+
+int lf_create_dist(const lf_desc* desc, int device, int rank, int nranks, const void* nccl_id,
+                   lf_handle** out) {
+  if (!desc || !out || nranks < 1 || rank < 0 || rank >= nranks) return LF_ERR_ARGUMENT;
+  *out = nullptr;
+  auto* h = new lf_handle;
+  clear_err(&h->err);
+  int rc = validate_desc(h, desc);
+  if (rc) {
+    *out = h;
+    return rc;
+  }
+  init_common(h, desc);
+  rc = guarded(h, [&] {
+    if (nranks > 1 && !h->dim2) return set_err(h, LF_ERR_CONFIG, "y-slabs need a 2D grid");
+    h->rank = rank;
+    h->nranks = nranks;
+    h->slabs.resize(1);
+    SlabState& sl = h->slabs[0];
+    sl.device = device;
+    int y0, rows;
+    slab_rows(desc->ny, nranks, rank, &y0, &rows);
+    if (nranks > 1 && rows < NG)
+      return set_err(h, LF_ERR_CONFIG, "each y-slab needs at least %d rows", NG);
+    const bool periodic = desc->bc[2] == LF_PERIODIC;
+    sl.L = Layout::make(desc->nx, rows);
+    sl.sl.y0 = y0;
+    sl.sl.ny_global = desc->ny;
+    sl.sl.fill_lo = nranks == 1 || (!periodic && rank == 0);
+    sl.sl.fill_hi = nranks == 1 || (!periodic && rank == nranks - 1);
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&sl.own_stream, cudaStreamNonBlocking));
+    sl.stream = sl.own_stream;
+    alloc_state(sl);
+    if (nranks > 1) {
+      int e = nccl_init(h, nccl_id);
+      if (e) return e;
+    }
+    sync_all(h);
+    return 0;
+  });
+  *out = h;
+  return rc;
+}
+
+void lf_destroy(lf_handle* h) {
+  if (!h) return;
+  for (auto& s : h->slabs) {
+    if (s.device >= 0) cudaSetDevice(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+  }
+  nccl_destroy(h);
+  fused_release(h);
+  for (auto& s : h->slabs) free_slab(s);
+  delete h;
+}
+
+int lf_local_rows(lf_handle* h, int* row0, int* nrows) {
+  if (!h || h->slabs.empty()) return LF_ERR_ARGUMENT;
+  *row0 = h->slabs.front().sl.y0;
+  *nrows = h->slabs.back().sl.y0 + h->slabs.back().L.ny - *row0;
+  return 0;
+}
+
+int lf_upload(lf_handle* h, double* const field[4], int64_t ld) {
+  return guarded(h, [&] {
+    if (!field || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad field or ld");
+    const int gy = h->dim2 ? 2 : 0;
+    for (auto& s : h->slabs) {
+      CK(cudaSetDevice(s.device));
+      for (int c = 0; c < 4; ++c) {
+        const double* src = field[c] + (int64_t)(s.sl.y0 + gy) * ld + 2;
+        double* dst = s.U + s.L.origin() + c * s.L.fstride;
+        CK(cudaMemcpy2DAsync(dst, s.L.pitch * sizeof(double), src, ld * sizeof(double),
+                             (size_t)s.L.nx * sizeof(double), (size_t)s.L.ny, cudaMemcpyDefault,
+                             s.stream));
+      }
+    }
+    sync_all(h);
+    h->rate_valid = false;
+    return 0;
+  });
+}
+
+int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghosts) {
+  return guarded(h, [&] {
+    if (!field || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad field or ld");
+    const int gy = h->dim2 ? 2 : 0;
+    for (auto& s : h->slabs) {
+      CK(cudaSetDevice(s.device));
+      for (int c = 0; c < 4; ++c) {
+        double* dst = field[c] + (int64_t)(s.sl.y0 + gy) * ld + 2;
+        const double* src = s.U + s.L.origin() + c * s.L.fstride;
+        CK(cudaMemcpy2DAsync(dst, ld * sizeof(double), src, s.L.pitch * sizeof(double),
+                             (size_t)s.L.nx * sizeof(double), (size_t)s.L.ny, cudaMemcpyDefault,
+                             s.stream));
+      }
+    }
+    sync_all(h);
+    if (fill_ghosts) host_apply_boundary(h->d, field, ld);
+    return 0;
+  });
+}
+
+int lf_init_fourier(lf_handle* h, uint64_t seed) {
+  return guarded(h, [&] {
+    if (!h->dim2) return set_err(h, LF_ERR_CONFIG, "the Fourier initial state is 2D");
+    std::vector<double> tx, ty, amp;
+    fourier_tables(seed, h->d, tx, ty, amp);  // whole-grid tables (host, libm)
+    // global maxima need every slab's raw values first
+    std::vector<double*> dtx(h->slabs.size()), dty(h->slabs.size()), damp(h->slabs.size());
+    for (size_t k = 0; k < h->slabs.size(); ++k) {
+      SlabState& s = h->slabs[k];
+      CK(cudaSetDevice(s.device));
+      CK(cudaMalloc(&dtx[k], tx.size() * sizeof(double)));
+      CK(cudaMalloc(&dty[k], 64 * (size_t)s.L.ny * sizeof(double)));
+      CK(cudaMalloc(&damp[k], 32 * sizeof(double)));
+      CK(cudaMemcpy(dtx[k], tx.data(), tx.size() * sizeof(double), cudaMemcpyHostToDevice));
+      // this slab's rows of every y table
+      std::vector<double> tyl(64 * (size_t)s.L.ny);
+      for (int t = 0; t < 64; ++t)
+        std::memcpy(&tyl[(size_t)t * s.L.ny], &ty[(size_t)t * h->d.ny + s.sl.y0],
+                    (size_t)s.L.ny * sizeof(double));
+      CK(cudaMemcpy(dty[k], tyl.data(), tyl.size() * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(damp[k], amp.data(), 32 * sizeof(double), cudaMemcpyHostToDevice));
+      CK(cudaMemsetAsync(s.aux, 0, 4 * sizeof(unsigned long long), s.stream));
+      launch_fourier_raw(s.field(s.U), s.L, dtx[k], dty[k], damp[k], s.stream);
+      launch_absmax(s.field(s.U), s.L, s.aux, s.stream);
+    }
+    unsigned long long mx[4] = {0, 0, 0, 0};
+    for (auto& s : h->slabs) {
+      unsigned long long m[4];
+      CK(cudaSetDevice(s.device));
+      CK(cudaMemcpyAsync(m, s.aux, sizeof m, cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      for (int c = 0; c < 4; ++c) mx[c] = std::max(mx[c], m[c]);
+    }
+    if (h->nccl) nccl_max_u64(h, mx, 4);
+    for (size_t k = 0; k < h->slabs.size(); ++k) {
+      SlabState& s = h->slabs[k];
+      CK(cudaSetDevice(s.device));
+      CK(cudaMemcpyAsync(s.aux, mx, sizeof mx, cudaMemcpyHostToDevice, s.stream));
+      launch_fourier_finish(s.field(s.U), s.L, s.aux, h->d.gamma, s.stream);
+      CK(cudaStreamSynchronize(s.stream));
+      cudaFree(dtx[k]);
+      cudaFree(dty[k]);
+      cudaFree(damp[k]);
+    }
+    CK(cudaGetLastError());
+    h->rate_valid = false;
+    return 0;
+  });
+}
+
+int lf_compute_dt(lf_handle* h, double cfl, double time, double limit_time, double* dt) {
+  return guarded(h, [&] {
+    launch_rate_all(h, &SlabState::U);
+    return finish_dt(h, combined_scalars(h, 0), cfl, time, limit_time, dt);
+  });
+}
+
+int lf_max_rate(lf_handle* h, double* rate) {
+  return guarded(h, [&] {
+    launch_rate_all(h, &SlabState::U);
+    *rate = bits_to_double(combined_scalars(h, 0).rate_bits);
+    return 0;
+  });
+}
+
+int lf_euler_stage(lf_handle* h, double dt, int64_t step) {
+  return guarded(h, [&] {
+    for (auto& s : h->slabs) alloc_staged(s);
+    staged_stage(h, &SlabState::U, &SlabState::U, &SlabState::Us, 0, false, dt, 1);
+    const Scalars s1 = combined_scalars(h, 1);
+    int rc = check_stage(h, s1, &SlabState::U, &SlabState::Us, step, dt);
+    if (rc) return rc;
+    swap_state(h, &SlabState::U, &SlabState::Us);
+    h->rate_valid = false;
+    return 0;
+  });
+}
+
+int lf_heun_step(lf_handle* h, double cfl, double time, double limit_time, int64_t step,
+                 double* boundary_outflow, lf_step_out* out) {
+  return guarded(h, [&] {
+    if (h->d.time_order >= 2 && use_fused(h))
+      return fused_heun(h, cfl, time, limit_time, step, boundary_outflow, out);
+    return staged_heun(h, cfl, time, limit_time, step, boundary_outflow, out);
+  });
+}
+
+int lf_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* time,
+               int64_t* step, double* outflow, lf_step_out* per_step, int* taken) {
+  return guarded(h, [&] {
+    if (h->d.time_order >= 2 && use_fused(h))
+      return fused_advance(h, nsteps, cfl, t_final, time, step, outflow, per_step, taken);
+    // stage-wise fallback keeps the run.cpp loop on the host
+    int k = 0;
+    if (taken) *taken = 0;
+    while (k < nsteps && *time < t_final) {
+      lf_step_out o;
+      int rc = staged_heun(h, cfl, *time, t_final, *step, outflow, &o);
+      if (rc) return rc;
+      *time = o.time;
+      *step = o.step;
+      if (per_step) per_step[k] = o;
+      ++k;
+      if (taken) *taken = k;
+    }
+    return 0;
+  });
+}
+
+int lf_last_error(lf_handle* h, lf_error* err) {
+  if (!h || !err) return LF_ERR_ARGUMENT;
+  *err = h->err;
+  return 0;
+}
+
+int lf_set_stream(lf_handle* h, void* stream) {
+  if (!h) return LF_ERR_ARGUMENT;
+  for (auto& s : h->slabs) s.stream = stream ? (cudaStream_t)stream : s.own_stream;
+  return 0;
+}
+
+int lf_set_path(lf_handle* h, int path) {
+  if (!h || path < LF_PATH_AUTO || path > LF_PATH_STAGED) return LF_ERR_ARGUMENT;
+  h->path = path;
+  return 0;
+}
+
+int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
+                  int* kernel_launches) {
+  return guarded(h, [&] {
+    if (!use_fused(h) || h->d.time_order < 2)
+      return set_err(h, LF_ERR_ARGUMENT, "lf_time_steps times the fused Heun path");
+    return fused_time_steps(h, nsteps, cfl, kernel_ms, step_ms, kernel_launches);
+  });
+}
+
+int lf_device_bytes(lf_handle* h, int64_t* bytes) {
+  if (!h || !bytes) return LF_ERR_ARGUMENT;
+  int64_t b = 0;
+  for (auto& s : h->slabs) {
+    b += 2 * s.L.alloc * 8;
+    if (s.Us) b += 2 * s.L.alloc * 8 + 2 * 4 * (s.fx_stride + s.fy_stride) * 8;
+  }
+  *bytes = b + fused_bytes(h);
+  return 0;
+}
+
+}  // extern "C"
+
+extern "C" int lf_launch_count(lf_handle* h, int64_t* launches) {
+  if (!h || !launches) return LF_ERR_ARGUMENT;
+  *launches = lfb::launch_count();
+  return 0;
+}

@@ -1,0 +1,18 @@
+// fused.h -- the fused Heun step (fused_step.cu): one kernel per time step.
+#pragma once
+
+#include "handle.h"
+
+namespace lfb {
+
+bool fused_supported(lf_handle* h);
+int fused_heun(lf_handle* h, double cfl, double time, double limit, int64_t step,
+               double* outflow, lf_step_out* out);
+int fused_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* time,
+                  int64_t* step, double* outflow, lf_step_out* per_step, int* taken);
+int fused_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
+                     int* launches);
+void fused_release(lf_handle* h);
+int64_t fused_bytes(lf_handle* h);
+
+}  // namespace lfb

@@ -1,0 +1,58 @@
+// handle.h -- the object behind lf_handle (internal to the .so).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/lagflux_b200.h"
+#include "kernels.h"
+
+namespace lfb {
+
+// One y-slab of the grid, resident on one GPU.
+struct SlabState {
+  int device = 0;
+  Layout L;
+  Slab sl;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;     // own_stream or a caller stream (lf_set_stream)
+  double* U = nullptr;               // current state U^n (4 components, Layout)
+  double* U2 = nullptr;              // next state (fused output / corrector output)
+  // staged-path scratch (allocated on first use)
+  double* Us = nullptr;              // predictor U*
+  double* W = nullptr;               // primitives
+  double* FX[2] = {nullptr, nullptr};
+  double* FY[2] = {nullptr, nullptr};
+  int64_t fx_stride = 0, fy_stride = 0;
+  // boundary-face gather for the outflow diagnostic
+  double* bnd = nullptr;             // device, 2 sets x 4 comps x (2 ny + 2 nx)
+  double* bnd_host = nullptr;        // pinned mirror
+  Scalars* scal = nullptr;           // device: [0] step scalars, [1] stage-2 scalars, [2..] spare
+  Scalars* scal_host = nullptr;      // pinned mirror
+  unsigned long long* aux = nullptr; // device scratch (Fourier maxima)
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+
+  Field field(double* p) const { return Field{p + L.origin(), L.pitch, L.fstride}; }
+  FluxArr fluxx(int k) const { return FluxArr{FX[k], L.pitch, fx_stride}; }
+  FluxArr fluxy(int k) const { return FluxArr{FY[k], L.pitch, fy_stride}; }
+};
+
+struct Nccl;  // nccl.cpp
+
+}  // namespace lfb
+
+struct lf_handle {
+  lf_desc d{};
+  lfb::Consts k{};
+  int dim2 = 1;
+  int path = LF_PATH_AUTO;
+  std::vector<lfb::SlabState> slabs;
+  // distributed (one slab per process)
+  int rank = 0, nranks = 1;
+  lfb::Nccl* nccl = nullptr;
+  bool rate_valid = false;           // scal[0].rate_bits holds the rate of the current U
+  lf_error err{};
+};

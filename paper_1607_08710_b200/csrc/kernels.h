@@ -1,0 +1,88 @@
+// kernels.h -- host-side launchers for the device kernels (internal to the .so).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lagflux_device.cuh"
+#include "layout.cuh"
+
+namespace lfb {
+
+// Per-step device scalars.  Mins/maxes are kept as order-preserving 64-bit keys
+// so the reductions are exact atomics (max/min are order independent, exactly
+// like the reference's OpenMP reduction(max/min), solver.cpp:272,449).
+struct Scalars {
+  unsigned long long rate_bits;      // max CFL rate over interior cells (double bits, >= 0)
+  long long fail_dt;                 // smallest failing interior index in compute_dt
+  long long fail_prim;               // smallest failing ghosted index in build_primitives
+  long long fail_trace;              // smallest failing face code in compute_fluxes
+  long long fail_update;             // smallest failing interior index in apply_update
+  unsigned long long min_rho_bits;   // min rho over updated cells
+  unsigned long long min_eint_bits;  // min internal energy density over updated cells
+  double dt;                         // step dt (device-resident runs)
+  double time;                       // state time after the step (device-resident runs)
+  int hits;                          // time + dt >= limit
+  int status;                        // 0 ok, else an LF_ERR_* kind detected in this step
+  double pad[2];
+};
+
+// Slab geometry: local rows [0, ny) are global rows [y0, y0+ny) of ny_global.
+struct Slab {
+  int y0 = 0;
+  int ny_global = 0;
+  int fill_lo = 1;   // apply the y_low BC locally (else the halo came from a neighbour)
+  int fill_hi = 1;
+};
+
+// Face flux storage (reference FluxSet, solver.hpp:100-105): x faces (nx+1) x ny,
+// y faces nx x (ny+1), 4 components each, pitched rows.
+struct FluxArr {
+  double* p;
+  int64_t pitch;
+  int64_t fstride;
+};
+
+// Process-wide count of kernels launched by this library (lf_launch_count).
+void count_launch(int n = 1);
+long long launch_count();
+
+void reset_scalars(Scalars* s, cudaStream_t st);
+
+// ghost fill (grid.cpp:72-114), 4 layers: x sides over interior rows, then
+// (after any halo exchange) y sides over every column at the domain edges.
+void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_t st);
+void launch_fill_y_only(const Field& f, const Layout& L, const int bc[4], const Slab& sl,
+                        cudaStream_t st);
+
+// Boundary-face fluxes for accumulate_boundary_outflow (solver.cpp:406-432):
+// out = [left 4 x ny | right 4 x ny | bottom 4 x nx | top 4 x nx], Heun-averaged when two.
+void launch_gather_boundary(const FluxArr& fxa, const FluxArr& fya, const FluxArr& fxb,
+                            const FluxArr& fyb, const Layout& L, bool two, double* out,
+                            cudaStream_t st);
+
+void launch_rate(const Field& u, const Layout& L, const Slab& sl, const Consts& k, int dim2,
+                 Scalars* s, cudaStream_t st);
+
+void launch_prims(const Field& u, const Field& w, const Layout& L, const Slab& sl, double gm1,
+                  int dim2, Scalars* s, cudaStream_t st);
+
+void launch_fluxes(const Field& w, const FluxArr& fx, const FluxArr& fy, const Layout& L,
+                   const Slab& sl, const Consts& k, int muscl, int dim2, Scalars* s,
+                   cudaStream_t st);
+
+// out = base - lam*(dF); fb == nullptr: single stage; else F = 0.5*(Fa+Fb)
+void launch_update(const Field& base, const FluxArr& fxa, const FluxArr& fya,
+                   const FluxArr* fxb, const FluxArr* fyb, const Field& out, const Layout& L,
+                   const Slab& sl, double dt, double dx, double dy, int dim2, Scalars* s,
+                   cudaStream_t st);
+
+// Fourier initial condition (cases.py fourier_*): raw sums then normalisation.
+void launch_fourier_raw(const Field& f, const Layout& L, const double* tx, const double* ty,
+                        const double* amp, cudaStream_t st);
+void launch_absmax(const Field& f, const Layout& L, unsigned long long* out4, cudaStream_t st);
+void launch_fourier_finish(const Field& f, const Layout& L, const unsigned long long* max4,
+                           double gamma, cudaStream_t st);
+
+}  // namespace lfb

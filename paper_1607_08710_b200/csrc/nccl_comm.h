@@ -1,0 +1,23 @@
+// nccl_comm.h -- inter-rank exchange for one-process-per-GPU y-slabs.
+//
+// NCCL is loaded with dlopen on first use (the torch-bundled libnccl.so.2 when
+// torch is already in the process), so single-GPU use has no NCCL dependency.
+// Per stage: NG halo rows to/from each y-neighbour (grouped send/recv, ring
+// when y is periodic); per step: one all-reduce(min) over the packed scalars
+// (the CFL rate max travels as ~bits, so max and min share one collective).
+#pragma once
+
+#include "handle.h"
+
+namespace lfb {
+
+int nccl_unique_id(void* id128);
+int nccl_init(lf_handle* h, const void* id128);
+void nccl_destroy(lf_handle* h);
+void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf);
+void nccl_combine_scalars(lf_handle* h, Scalars* s);
+void nccl_max_u64(lf_handle* h, unsigned long long* v, int n);
+// sum-combine the boundary-face arrays (each rank owns disjoint entries)
+void nccl_gather_boundary(lf_handle* h, double* left, double* right, double* bot, double* top);
+
+}  // namespace lfb

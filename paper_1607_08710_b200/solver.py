@@ -1,0 +1,244 @@
+"""LagfluxSolver: the reference's solver interface over the CUDA C ABI.
+
+Mirrors lagflux::LagfluxSolver (/root/reference/proj/include/lagflux/solver.hpp:78-131)
+-- same method names, argument meaning and exception types -- so the parity
+tests read like the reference's own (proj/tests/test_solver.cpp).  The field
+lives on the GPU between steps: a SolverState is uploaded on its first step
+and ``sync_to_host(state)`` copies it back (dumps, end of run), the one-line
+addition a run.cpp-style driver needs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import grid as G
+from . import native as N
+
+
+def _raise(e: N.lf_error):
+    msg = e.message.decode(errors="replace")
+    if e.kind == N.LF_ERR_POSITIVITY:
+        raise G.PositivityError(msg, e.i, e.j, e.step, e.dt)
+    if e.kind == N.LF_ERR_CONFIG:
+        raise G.ConfigError(msg)
+    if e.kind in (N.LF_ERR_DT_STATE, N.LF_ERR_PRIMITIVE, N.LF_ERR_TRACE):
+        raise G.InvalidStateError(msg)
+    if e.kind == N.LF_ERR_DT_NONPOS:
+        raise G.Error(msg)
+    if e.kind == N.LF_ERR_ARGUMENT:
+        raise ValueError(msg)
+    raise G.DeviceError(msg or f"lagflux_b200 error kind {e.kind}")
+
+
+def make_desc(g: G.CartesianGrid, bc: G.BoundaryCondition, gamma: float,
+              params: G.SchemeParams) -> N.lf_desc:
+    return N.lf_desc(g.dim, g.nx, g.ny, g.dx, g.dy, g.x0, g.y0, gamma, params.beta,
+                     params.spatial_order, params.time_order, (C.c_int * 4)(*bc.as_list()))
+
+
+class LagfluxSolver:
+    """CUDA-backed drop-in for lagflux::LagfluxSolver.
+
+    devices: one entry per y-slab driven from this process (repeats allowed).
+    dist:    (rank, nranks, device, nccl_id_bytes) for one-process-per-GPU slabs.
+    path:    "auto" | "fused" | "staged" (Heun step implementation)."""
+
+    def __init__(self, g: G.CartesianGrid, bc: G.BoundaryCondition, gamma: float = 1.4,
+                 params: G.SchemeParams = G.SchemeParams(), threads: int = 1,
+                 devices: Sequence[int] = (0,), path: str = "auto", dist=None):
+        # constructor checks of solver.cpp:66-69
+        if g.nx < 1 or g.ny < 1:
+            raise G.ConfigError("grid has no interior cells")
+        if g.gx < 2 or (g.dim == 2 and g.gy < 2):
+            raise G.ConfigError("MUSCL stencils need at least two ghost layers")
+        G.validate_boundary(bc, g.dim)
+        self._lib = N.lib()
+        self._grid, self.bc, self.gamma, self.params = g, bc, gamma, params
+        self._threads = max(1, threads)
+        self._desc = make_desc(g, bc, gamma, params)
+        h = C.c_void_p()
+        if dist is None:
+            devs = (C.c_int * len(devices))(*devices)
+            rc = self._lib.lf_create(C.byref(self._desc), devs, len(devices), C.byref(h))
+        else:
+            rank, nranks, device, nccl_id = dist
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            rc = self._lib.lf_create_dist(C.byref(self._desc), device, rank, nranks, idbuf,
+                                          C.byref(h))
+        self._h = h
+        if rc:
+            err = self._error()
+            self.close()
+            _raise(err)
+        self.set_path(path)
+        self._resident = None  # SolverState whose field is on the device
+
+    # ------------------------------------------------------------ plumbing
+    def _error(self) -> N.lf_error:
+        e = N.lf_error()
+        if self._h:
+            self._lib.lf_last_error(self._h, C.byref(e))
+        return e
+
+    def _check(self, rc: int):
+        if rc:
+            _raise(self._error())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.lf_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def grid(self) -> G.CartesianGrid:
+        return self._grid
+
+    def threads(self) -> int:
+        return self._threads
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_path(self, path: str):
+        code = {"auto": N.LF_PATH_AUTO, "fused": N.LF_PATH_FUSED, "staged": N.LF_PATH_STAGED}[path]
+        self._check(self._lib.lf_set_path(self._h, code))
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        self._check(self._lib.lf_set_stream(self._h, stream_ptr))
+
+    def local_rows(self):
+        r0, n = C.c_int(), C.c_int()
+        self._check(self._lib.lf_local_rows(self._h, C.byref(r0), C.byref(n)))
+        return r0.value, n.value
+
+    def device_bytes(self) -> int:
+        b = C.c_int64()
+        self._check(self._lib.lf_device_bytes(self._h, C.byref(b)))
+        return b.value
+
+    # ------------------------------------------------------------ state transfer
+    def upload(self, field: np.ndarray):
+        self._check(self._lib.lf_upload(self._h, N.field_ptrs(field), self._grid.nxt))
+        self._resident = None
+
+    def download(self, field: np.ndarray, fill_ghosts: bool = False):
+        self._check(self._lib.lf_download(self._h, N.field_ptrs(field), self._grid.nxt,
+                                          1 if fill_ghosts else 0))
+
+    def attach(self, state: G.SolverState):
+        """Make `state` the device-resident state (uploads its field)."""
+        self.upload(state.field)
+        self._resident = state
+
+    def sync_to_host(self, state: G.SolverState, fill_ghosts: bool = False):
+        if self._resident is not state:
+            raise G.Error("state is not resident on this solver")
+        self.download(state.field, fill_ghosts)
+
+    def init_fourier(self, state: G.SolverState, seed: int):
+        """Device-side seeded smooth-flow initial state (cases.fourier_*)."""
+        self._check(self._lib.lf_init_fourier(self._h, seed))
+        self._resident = state
+
+    # ------------------------------------------------------------ the reference API
+    def compute_dt(self, field: np.ndarray, controls: G.TimeControls, time: float,
+                   limit_time: float) -> float:
+        """LagfluxSolver::compute_dt (solver.cpp:434-480) of a host field."""
+        self.upload(field)
+        dt = C.c_double()
+        self._check(self._lib.lf_compute_dt(self._h, controls.cfl, time, limit_time, C.byref(dt)))
+        return dt.value
+
+    def euler_stage(self, field_in: np.ndarray, dt: float, field_out: np.ndarray,
+                    step: int = -1) -> None:
+        """LagfluxSolver::euler_stage (solver.cpp:482-487): out's interior receives the stage."""
+        self.upload(field_in)
+        self._check(self._lib.lf_euler_stage(self._h, dt, step))
+        self.download(field_out)
+
+    def heun_step(self, state: G.SolverState, controls: G.TimeControls,
+                  limit_time: float) -> float:
+        """LagfluxSolver::heun_step (solver.cpp:489-546) on the device-resident state."""
+        if self._resident is not state:
+            self.attach(state)
+        out = N.lf_step_out()
+        acc = (C.c_double * 4)(*state.boundary_outflow)
+        rc = self._lib.lf_heun_step(self._h, controls.cfl, state.time, limit_time, state.step,
+                                    C.cast(acc, N.DP), C.byref(out))
+        if rc:
+            # on a corrector PositivityError the device state already holds the
+            # corrector output, as state.field does in the reference
+            _raise(self._error())
+        state.boundary_outflow = list(acc)
+        state.time, state.step = out.time, out.step
+        state.diagnostics.append(G.StepDiagnostics(out.step, out.time, out.dt, out.min_rho,
+                                                   out.min_p))
+        return out.dt
+
+    def advance(self, state: G.SolverState, controls: G.TimeControls, nsteps: int) -> int:
+        """Up to nsteps heun_steps while time < t_final, with dt on the device (run.cpp:180-210)."""
+        if self._resident is not state:
+            self.attach(state)
+        n = int(min(nsteps, max(0, controls.max_steps - state.step)))
+        if n <= 0:
+            return 0
+        rec = (N.lf_step_out * n)()
+        t, s = C.c_double(state.time), C.c_int64(state.step)
+        acc = (C.c_double * 4)(*state.boundary_outflow)
+        taken = C.c_int()
+        rc = self._lib.lf_advance(self._h, n, controls.cfl, controls.t_final, C.byref(t),
+                                  C.byref(s), C.cast(acc, N.DP), rec, C.byref(taken))
+        for k in range(taken.value):
+            o = rec[k]
+            state.diagnostics.append(G.StepDiagnostics(o.step, o.time, o.dt, o.min_rho, o.min_p))
+        state.time, state.step = t.value, s.value
+        state.boundary_outflow = list(acc)
+        if rc:
+            _raise(self._error())
+        return taken.value
+
+    def time_steps(self, nsteps: int, cfl: float):
+        """Device-timed steps: (summed kernel ms, loop ms, kernel launches)."""
+        k, s, n = C.c_double(), C.c_double(), C.c_int()
+        self._check(self._lib.lf_time_steps(self._h, nsteps, cfl, C.byref(k), C.byref(s),
+                                            C.byref(n)))
+        return k.value, s.value, n.value
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        self._check(self._lib.lf_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def max_rate(self) -> float:
+        r = C.c_double()
+        self._check(self._lib.lf_max_rate(self._h, C.byref(r)))
+        return r.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = N.lib().lf_nccl_unique_id(buf)
+    if rc:
+        raise G.DeviceError("ncclGetUniqueId failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+def run_case(case, solver: Optional[LagfluxSolver] = None, field: Optional[np.ndarray] = None,
+             batch: int = 64, **kw) -> G.SolverState:
+    """run_hydro_case's step loop (run.cpp:178-210) without dumps: to t_final or max_steps."""
+    from . import cases as CS
+    s = solver or LagfluxSolver(case.grid, case.bc, case.gamma, case.params, **kw)
+    state = G.SolverState(field=CS.initial_field(case) if field is None else field)
+    controls = G.TimeControls(case.cfl, case.t_final, case.max_steps)
+    s.attach(state)
+    while state.time < case.t_final and state.step < case.max_steps:
+        if s.advance(state, controls, batch) == 0:
+            break
+    s.sync_to_host(state)
+    return state

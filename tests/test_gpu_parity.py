@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle and the golden vectors.
+
+Bar (north star): bit equality per element (==) with the reference CPU build;
+the tolerance the north star allows (relative L1 <= 1e-10, dt to 1e-12) is
+asserted as well, but every case here is expected -- and required -- to be exact.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1607_08710_b200 import cases as CS
+from paper_1607_08710_b200 import grid as G
+from paper_1607_08710_b200.solver import LagfluxSolver
+from helpers import (assert_fields_equal, diag_array, golden_cases, load_golden, rel_l1,
+                     run_oracle)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = list(golden_cases().items())
+PATHS = ["staged", "auto"]
+
+
+def run_gpu(case, steps, path="auto", devices=(0,), field=None, use_advance=False):
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, devices=devices, path=path)
+    state = G.SolverState(field=CS.initial_field(case) if field is None else np.array(field))
+    controls = G.TimeControls(case.cfl, case.t_final, steps)
+    if use_advance:
+        s.attach(state)
+        while state.step < steps and state.time < case.t_final:
+            if s.advance(state, controls, steps) == 0:
+                break
+    else:
+        while state.step < steps and state.time < case.t_final:
+            s.heun_step(state, controls, case.t_final)
+    s.sync_to_host(state)
+    s.close()
+    return state
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("name,spec", GOLDEN, ids=[n for n, _ in GOLDEN])
+def test_golden_bitwise(cuda, name, spec, path):
+    case, steps = spec
+    gold = load_golden(name)
+    state = run_gpu(case, steps, path)
+    got = case.grid.interior(state.field)
+    assert_fields_equal(got, gold["final"], f"{name}/{path}")
+    d = diag_array(state)
+    assert np.array_equal(d[:, :4], gold["diag"][:, :4]), "dt / time / min_rho / min_p"
+    assert np.array_equal(np.array(state.boundary_outflow), gold["outflow"])
+    assert rel_l1(got, gold["final"]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["quadrant_32", "smooth_32", "sod_400x4", "mixed_40x24"])
+def test_device_resident_advance(cuda, name):
+    """lf_advance (dt/time kept on the device, no per-step sync) == golden."""
+    case, steps = dict(GOLDEN)[name]
+    gold = load_golden(name)
+    state = run_gpu(case, steps, "auto", use_advance=True)
+    assert_fields_equal(case.grid.interior(state.field), gold["final"], name)
+    assert np.array_equal(diag_array(state)[:, :4], gold["diag"][:, :4])
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("cfg", ["quadrant", "sedov", "smooth"])
+def test_larger_grids_vs_oracle(cuda, cfg, path):
+    case = {"quadrant": CS.quadrant(256, 30), "sedov": CS.sedov(192, 30),
+            "smooth": CS.smooth(200, 30, ny=136, y_extent=0.68)}[cfg]
+    ref, rdiag = run_oracle(case, case.max_steps)
+    state = run_gpu(case, case.max_steps, path)
+    assert_fields_equal(case.grid.interior(state.field), case.grid.interior(ref.field), cfg)
+    assert np.array_equal(diag_array(state)[:, :4], rdiag[:, :4])
+    assert np.array_equal(np.array(state.boundary_outflow), np.array(ref.boundary_outflow))
+
+
+@pytest.mark.parametrize("nslabs", [2, 3, 5])
+@pytest.mark.parametrize("cfg", ["smooth", "sedov", "quadrant"])
+def test_in_process_slabs_equal_single(cuda, cfg, nslabs):
+    """y-slab decomposition (halo rows + combined dt) is bit-identical to one slab."""
+    case = {"quadrant": CS.quadrant(64, 20), "sedov": CS.sedov(64, 20),
+            "smooth": CS.smooth(64, 20, ny=45, y_extent=45 / 64)}[cfg]
+    one = run_gpu(case, 20, "auto")
+    many = run_gpu(case, 20, "auto", devices=[0] * nslabs)
+    assert_fields_equal(case.grid.interior(many.field), case.grid.interior(one.field), cfg)
+    assert np.array_equal(diag_array(many), diag_array(one))
+    assert np.array_equal(np.array(many.boundary_outflow), np.array(one.boundary_outflow))
+
+
+def test_euler_stage_golden(cuda):
+    gold = load_golden("euler_stage_sod50")
+    g = G.make_grid_1d(50, 0.0, 1.0)
+    case = CS.Case("s", g, G.BoundaryCondition(), 1.4, G.SchemeParams(), 0.5, 0.2, G.INT64_MAX,
+                   "riemann_x")
+    for beta in (1.0, 1.5):
+        s = LagfluxSolver(g, case.bc, 1.4, G.SchemeParams(beta=beta))
+        out = G.new_field(g)
+        s.euler_stage(CS.initial_field(case), 8e-4, out)
+        assert_fields_equal(g.interior(out), gold[f"beta_{beta}"], f"beta {beta}")
+
+
+def test_compute_dt_known_answers(cuda):
+    """test_solver.cpp:161-180."""
+    import math
+    g = G.make_grid_1d(100, 0.0, 1.0)
+    f = G.new_field(g)
+    r, mx, my, e = G.conserved_from_primitive(np.ones(100), np.zeros(100), np.zeros(100), np.ones(100), 1.4)
+    g.interior(f)[:] = np.stack([r, mx, my, e])[:, None, :]
+    s = LagfluxSolver(g, G.BoundaryCondition())
+    dt = s.compute_dt(f, G.TimeControls(0.25, 10.0, 1000), 0.0, 10.0)
+    assert dt == pytest.approx(0.25 * 0.01 / math.sqrt(1.4), rel=1e-15)
+    assert dt == O.OracleSolver(g, G.BoundaryCondition()).compute_dt(f, 0.25, 0.0, 10.0)
+    assert s.compute_dt(f, G.TimeControls(0.25, 10.0, 1000), 9.9999, 10.0) == 10.0 - 9.9999
+    with pytest.raises(G.Error, match="non-positive time step"):
+        s.compute_dt(f, G.TimeControls(0.25, 10.0, 1000), 10.0, 10.0)
+
+
+def _sod1d(n=50):
+    g = G.make_grid_1d(n, 0.0, 1.0)
+    return g, CS.initial_field(CS.Case("s", g, G.BoundaryCondition(), 1.4, G.SchemeParams(), 0.5,
+                                       0.2, G.INT64_MAX, "riemann_x"))
+
+
+def test_errors_match_oracle_text(cuda):
+    """PositivityError / InvalidStateError carry the reference's text and fields."""
+    g, f = _sod1d()
+    o = O.OracleSolver(g, G.BoundaryCondition())
+    s = LagfluxSolver(g, G.BoundaryCondition())
+    with pytest.raises(G.PositivityError) as eo:
+        o.euler_stage(f.copy(), 10.0, G.new_field(g), 7)
+    with pytest.raises(G.PositivityError) as eg:
+        s.euler_stage(f.copy(), 10.0, G.new_field(g), 7)
+    assert str(eg.value) == str(eo.value)
+    assert (eg.value.cell_i, eg.value.cell_j, eg.value.step, eg.value.dt) == \
+        (eo.value.cell_i, eo.value.cell_j, eo.value.step, eo.value.dt)
+    bad = f.copy()
+    bad[3, 0, 2 + 13] = -1.0
+    with pytest.raises(G.InvalidStateError) as eo2:
+        o.euler_stage(bad.copy(), 1e-4, G.new_field(g), 3)
+    with pytest.raises(G.InvalidStateError) as eg2:
+        s.euler_stage(bad.copy(), 1e-4, G.new_field(g), 3)
+    assert str(eg2.value) == str(eo2.value)
+    # compute_dt sees the bad cell first in a full step
+    state = G.SolverState(field=bad.copy())
+    with pytest.raises(G.InvalidStateError) as eg3:
+        s.heun_step(state, G.TimeControls(0.5, 1.0), 1.0)
+    ostate = G.SolverState(field=bad.copy())
+    with pytest.raises(G.InvalidStateError) as eo3:
+        o.heun_step(ostate, 0.5, 1.0)
+    assert str(eg3.value) == str(eo3.value)
+
+
+def test_trace_failure_text(cuda):
+    from test_oracle_cpu import trace_failure_case
+    g, f, params = trace_failure_case()
+    o = O.OracleSolver(g, G.BoundaryCondition(), params=params)
+    s = LagfluxSolver(g, G.BoundaryCondition(), params=params)
+    with pytest.raises(G.InvalidStateError) as eo:
+        o.euler_stage(f.copy(), 1e-4, G.new_field(g), 5)
+    with pytest.raises(G.InvalidStateError) as eg:
+        s.euler_stage(f.copy(), 1e-4, G.new_field(g), 5)
+    assert str(eg.value) == str(eo.value)
+    for path in PATHS:
+        state = G.SolverState(field=f.copy())
+        s2 = LagfluxSolver(g, G.BoundaryCondition(), params=params, path=path)
+        with pytest.raises(G.InvalidStateError) as eg2:
+            s2.heun_step(state, G.TimeControls(0.5, 1.0), 1.0)
+        ostate = G.SolverState(field=f.copy())
+        with pytest.raises(G.InvalidStateError) as eo2:
+            o.heun_step(ostate, 0.5, 1.0)
+        assert str(eg2.value) == str(eo2.value)
+
+
+def test_corrector_positivity_failure_matches(cuda):
+    """A step whose corrector loses positivity: same error, same (in-place) state."""
+    g = G.make_grid_2d(24, 16, 0.0, 1.0, 0.0, 1.0)
+    case = CS.Case("q", g, G.BoundaryCondition.uniform(G.TRANSMISSIVE), 1.4, G.SchemeParams(),
+                   4.0, CS.STEP_DRIVEN_LIMIT, 5, "quadrant")   # CFL far beyond stability
+    f0 = CS.initial_field(case)
+    o = O.OracleSolver(g, case.bc)
+    ostate = G.SolverState(field=f0.copy())
+    with pytest.raises(G.Error) as eo:
+        for _ in range(5):
+            o.heun_step(ostate, case.cfl, case.t_final)
+    for path in PATHS:
+        s = LagfluxSolver(g, case.bc, path=path)
+        state = G.SolverState(field=f0.copy())
+        with pytest.raises(G.Error) as eg:
+            for _ in range(5):
+                s.heun_step(state, G.TimeControls(case.cfl, case.t_final), case.t_final)
+        assert type(eg.value) is type(eo.value)
+        assert str(eg.value) == str(eo.value)
+        s.sync_to_host(state)
+        assert_fields_equal(g.interior(state.field), g.interior(ostate.field), path)
+
+
+def test_fourier_device_init_equals_host(cuda):
+    case = CS.smooth(96, ny=80, y_extent=80 / 96)
+    host = CS.initial_field(case)
+    for devices in ((0,), (0, 0, 0)):
+        s = LagfluxSolver(case.grid, case.bc, devices=devices)
+        state = G.SolverState(field=G.new_field(case.grid))
+        s.init_fourier(state, case.seed)
+        s.sync_to_host(state)
+        assert_fields_equal(case.grid.interior(state.field), case.grid.interior(host), str(devices))
+
+
+def test_download_fill_ghosts_matches_reference_fill(cuda):
+    case = CS.smooth(20, ny=12, y_extent=0.6)
+    g = case.grid
+    f = CS.initial_field(case)
+    for bcs in ((0, 0, 0, 0), (1, 1, 1, 1), (2, 2, 2, 2), (2, 2, 1, 0)):
+        bc = G.BoundaryCondition(*bcs)
+        s = LagfluxSolver(g, bc)
+        s.upload(f)
+        out = G.new_field(g)
+        s.download(out, fill_ghosts=True)
+        ref = f.copy()
+        lib = O.oracle_lib()
+        for c, parity in enumerate((0, 1, 2, 0)):
+            arr = np.ascontiguousarray(ref[c])
+            lib.lfo_fill_ghosts(O.C.byref(O._cgrid(g)), (O.C.c_int * 4)(*bcs), parity,
+                                arr.ctypes.data_as(O.DP))
+            ref[c] = arr
+        assert_fields_equal(out, ref, str(bcs))
