@@ -492,6 +492,7 @@ int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t ste
     boundary_outflow(h, false, dt, acc);
   }
   h->rate_valid = false;
+  fused_invalidate(h);
   if (outflow) std::memcpy(outflow, acc, sizeof acc);
   if (out) {
     out->dt = dt;
@@ -524,6 +525,18 @@ int guarded(lf_handle* h, F&& f) {
 }
 
 }  // namespace
+
+namespace lfb {
+void fill_all_public(lf_handle* h, double* SlabState::*buf) { fill_all(h, buf); }
+Scalars rate_of_current(lf_handle* h) {
+  launch_rate_all(h, &SlabState::U);
+  return combined_scalars(h, 0);
+}
+int staged_heun_public(lf_handle* h, double cfl, double time, double limit, int64_t step,
+                       double* outflow, lf_step_out* out) {
+  return staged_heun(h, cfl, time, limit, step, outflow, out);
+}
+}  // namespace lfb
 
 // ====================================================================== C ABI
 extern "C" {
@@ -558,8 +571,13 @@ int lf_create(const lf_desc* desc, const int* devices, int ndev, lf_handle** out
       sl.sl.fill_lo = ndev == 1 || (!periodic && s == 0);
       sl.sl.fill_hi = ndev == 1 || (!periodic && s == ndev - 1);
       CK(cudaSetDevice(sl.device));
-      CK(cudaStreamCreateWithFlags(&sl.own_stream, cudaStreamNonBlocking));
-      sl.stream = sl.own_stream;
+      // slabs sharing a device share one stream: stream order is the schedule
+      if (s > 0 && sl.device == h->slabs[0].device) {
+        sl.stream = h->slabs[0].stream;
+      } else {
+        CK(cudaStreamCreateWithFlags(&sl.own_stream, cudaStreamNonBlocking));
+        sl.stream = sl.own_stream;
+      }
       alloc_state(sl);
     }
     // enable peer access between distinct devices (in-process multi-GPU)
@@ -662,6 +680,7 @@ int lf_upload(lf_handle* h, double* const field[4], int64_t ld) {
     }
     sync_all(h);
     h->rate_valid = false;
+    fused_invalidate(h);
     return 0;
   });
 }
@@ -732,6 +751,7 @@ int lf_init_fourier(lf_handle* h, uint64_t seed) {
     }
     CK(cudaGetLastError());
     h->rate_valid = false;
+    fused_invalidate(h);
     return 0;
   });
 }
@@ -760,6 +780,7 @@ int lf_euler_stage(lf_handle* h, double dt, int64_t step) {
     if (rc) return rc;
     swap_state(h, &SlabState::U, &SlabState::Us);
     h->rate_valid = false;
+    fused_invalidate(h);
     return 0;
   });
 }
@@ -803,7 +824,9 @@ int lf_last_error(lf_handle* h, lf_error* err) {
 
 int lf_set_stream(lf_handle* h, void* stream) {
   if (!h) return LF_ERR_ARGUMENT;
-  for (auto& s : h->slabs) s.stream = stream ? (cudaStream_t)stream : s.own_stream;
+  for (auto& s : h->slabs)
+    s.stream = stream ? (cudaStream_t)stream
+                      : (s.own_stream ? s.own_stream : h->slabs[0].own_stream);
   return 0;
 }
 

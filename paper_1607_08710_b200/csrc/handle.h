@@ -54,5 +54,15 @@ struct lf_handle {
   int rank = 0, nranks = 1;
   lfb::Nccl* nccl = nullptr;
   bool rate_valid = false;           // scal[0].rate_bits holds the rate of the current U
+  void* fused = nullptr;             // lfb::FusedState (fused_step.cu)
   lf_error err{};
 };
+
+namespace lfb {
+// api.cu services used by the fused path
+void fill_all_public(lf_handle* h, double* SlabState::*buf);
+Scalars rate_of_current(lf_handle* h);
+int staged_heun_public(lf_handle* h, double cfl, double time, double limit, int64_t step,
+                       double* outflow, lf_step_out* out);
+void fused_invalidate(lf_handle* h);
+}  // namespace lfb

@@ -206,3 +206,17 @@ void nccl_gather_boundary(lf_handle* h, double* left, double* right, double* bot
 }
 
 }  // namespace lfb
+
+namespace lfb {
+
+void nccl_reduce_step(lf_handle* h, void* acc_u64, int n, double* bnd, size_t nbnd) {
+  SlabState& s = h->slabs[0];
+  nck(g_api.GroupStart(), "ncclGroupStart");
+  nck(g_api.AllReduce(acc_u64, acc_u64, (size_t)n, ncclUint64, ncclMax, h->nccl->comm, s.stream),
+      "ncclAllReduce(step)");
+  nck(g_api.AllReduce(bnd, bnd, nbnd, ncclFloat64, ncclSum, h->nccl->comm, s.stream),
+      "ncclAllReduce(boundary)");
+  nck(g_api.GroupEnd(), "ncclGroupEnd");
+}
+
+}  // namespace lfb

@@ -17,6 +17,9 @@ void nccl_destroy(lf_handle* h);
 void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf);
 void nccl_combine_scalars(lf_handle* h, Scalars* s);
 void nccl_max_u64(lf_handle* h, unsigned long long* v, int n);
+// fused step: max-reduce n u64 step accumulators and sum-reduce the boundary
+// faces (nbnd doubles, each rank owns disjoint entries, zero elsewhere) in place
+void nccl_reduce_step(lf_handle* h, void* acc_u64, int n, double* bnd, size_t nbnd);
 // sum-combine the boundary-face arrays (each rank owns disjoint entries)
 void nccl_gather_boundary(lf_handle* h, double* left, double* right, double* bot, double* top);
 
