@@ -1,0 +1,70 @@
+// fused_common.cuh -- types shared by the fused-step kernels and their host driver.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lfb {
+
+constexpr int FUSED_NC = 128;                 // columns per strip (threads per warp group)
+constexpr int FUSED_TXO = FUSED_NC - 8;       // output columns per strip
+constexpr int FUSED_THREADS = 2 * FUSED_NC;   // predictor group + corrector group
+constexpr unsigned long long NINF_KEY = ~0x7ff0000000000000ull;  // ~bits(+inf)
+
+// Per-step control record, written by the host (first step) or k_finalize.
+struct StepCtl {
+  double time;                    // SolverState::time at the start of the step
+  unsigned long long rate_bits;   // CFL rate of the state at the start of the step
+  int done;                       // 1: skip (limit reached or an earlier step failed)
+  int dtfail;                     // the rate check of this step's input failed
+};
+
+// Per-step accumulators: every field reduces with max (min via ~bits), so one
+// atomicMax per warp and one NCCL max across ranks combine them exactly.
+struct StepAcc {
+  unsigned long long rate_next;   // CFL rate of U^{n+1}
+  unsigned long long fail;        // any failure flag in this step
+  unsigned long long nmin_rho;    // ~bits(min rho of U^{n+1})
+  unsigned long long nmin_eint;   // ~bits(min e_int of U^{n+1})
+  unsigned long long dtfail_next; // rate check of U^{n+1} failed
+  unsigned long long pad[3];
+};
+constexpr int STEP_ACC_WORDS = 5;
+
+// Per-step record handed back to the host.
+struct StepRec {
+  double dt;
+  double time;       // time after the step
+  double min_rho;
+  double min_eint;
+  int hits;
+  int status;        // 0 ok, 1 failure flag (host diagnoses), 2 skipped (done)
+};
+
+struct FusedArgs {
+  const double* __restrict__ u;   // U^n, component 0 at (0, 0)
+  double* __restrict__ un;        // U^{n+1}
+  int64_t pitch, fstride;
+  int nx, ny;                     // local interior
+  int y0g;                        // global row of local row 0
+  int nyg;                        // global rows
+  int rows_per_chunk;
+  double gamma, gm1, beta, dx, dy;
+  double cfl, limit;
+  int bc_xlo, bc_xhi, bc_ylo, bc_yhi;
+  int bottom_edge, top_edge;      // non-periodic domain edge at this slab's bottom / top
+  const StepCtl* ctl;
+  StepAcc* acc;
+  double* bnd;                    // [left 4*nyg | right 4*nyg | bottom 4*nx | top 4*nx]
+};
+
+size_t fused_smem_bytes();
+void fused_configure();
+void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st);
+void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* rec,
+                     const double* bnd, double* outflow, int nx, int nyg, double dx, double dy,
+                     double cfl, double limit, double t_final, cudaStream_t st);
+void launch_acc_init(StepAcc* acc, cudaStream_t st);
+
+}  // namespace lfb

@@ -1,0 +1,723 @@
+// fused_kernel.cu -- one kernel per Heun time step (LagfluxSolver::heun_step, solver.cpp:489-546).
+//
+// Design:
+//  * A block owns a strip of NC = 128 columns (TXO = 120 output columns plus a
+//    4-column halo each side) and marches down a chunk of rows.  The whole step
+//    -- primitives, MUSCL traces, Lagrangian HLL, upwind fluxes, predictor U*,
+//    corrector U^{n+1}, positivity checks, min rho / min e_int and the CFL rate
+//    of U^{n+1} for the next dt -- happens in one pass: U^n is read from HBM
+//    about once (plus ~7% halo re-reads, mostly L2 hits) and U^{n+1} written once,
+//    64 B/cell-update of compulsory traffic instead of the stage-wise 288 B.
+//  * Warp specialisation: warps 0-3 ("P") run stage 1 on input row r (U^n ->
+//    F^n faces -> U*(r-2)); warps 4-7 ("C") run stage 2 three rows behind
+//    (U*(a) -> F* faces -> U^{n+1}(a-2)).  P and C exchange rows through small
+//    shared-memory rings; each group synchronises internally on its own named
+//    barrier and both meet once per row iteration.
+//  * y-direction stencil data of a column lives in the registers of the thread
+//    owning that column (rolling 3-row window, slopes shared between the two
+//    faces of a cell); x-direction neighbours go through shared memory.  Each
+//    thread solves its x-face and its y-face Riemann problems in one straight
+//    line of code, so the two dependency chains overlap.
+//  * fp64 arithmetic keeps the reference's evaluation order (--fmad=false);
+//    divisions and square roots use fastmath.cuh (the compiler's own IEEE fast
+//    path with shared reciprocals and one deferred range check per face), so
+//    results are bit-identical to the reference.
+//  * Failure checks are detection only: any flag makes the host re-run that
+//    step with the stage-wise kernels, which reproduce the reference's exact
+//    error (kind, smallest index, text) and state semantics.
+#include <cuda_runtime.h>
+
+#include "../../include/lagflux_b200.h"
+#include "fastmath.cuh"
+#include "fused_common.cuh"
+#include "kernels.h"
+#include "lagflux_device.cuh"
+
+// Build-time tuning knobs (tools/variants.py sweeps them):
+//   LF_PAIR       1: solve the x- and y-face Riemann problems of a thread in one
+//                 straight line (ILP); 0: one after the other (fewer registers)
+//   LF_MINBLOCKS  resident blocks per SM requested from ptxas (register budget)
+#ifndef LF_PAIR
+#define LF_PAIR 1
+#endif
+
+namespace lfb {
+
+namespace {
+
+constexpr int NC = FUSED_NC;
+constexpr int TXO = FUSED_TXO;
+constexpr unsigned FULL = 0xffffffffu;
+
+struct FK {
+  double gamma, gm1, beta;
+  Recip rgm1, rdx, rdy;  // shared reciprocals of the constant divisors
+  Consts k;              // for the IEEE fallbacks
+};
+
+__device__ __forceinline__ void bar_named(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NC) : "memory");
+}
+
+__device__ __forceinline__ double key_to_double(unsigned long long b) {
+  return __longlong_as_double((long long)b);
+}
+
+// The reference-order IEEE face flux, out of line: taken only when a range
+// check of the fast path fails or u* is not strictly signed (the mean state).
+template <int AXIS>
+__device__ __noinline__ void face_ref(double m0, double m1, double m2, double m3, double p0,
+                                      double p1, double p2, double p3, Consts k, double* f) {
+  face_flux<AXIS>(m0, m1, m2, m3, p0, p1, p2, p3, k, f);
+}
+
+// Lagrange-flux face flux (riemann_hll.hpp:29-39, solver.cpp:26-43) on the fast
+// paths.  ok &= every range check, and is cleared when u* is 0 or NaN.
+template <int AXIS>
+__device__ __forceinline__ void face_fast(double m0, double m1, double m2, double m3, double p0,
+                                          double p1, double p2, double p3, const FK& c,
+                                          double f[4], bool& ok) {
+  const double ul = AXIS == 0 ? m1 : m2;
+  const double ur = AXIS == 0 ? p1 : p2;
+  const double cl = sqrt_fast(div1_fast(c.gamma * m3, m0, ok), ok);
+  const double cr = sqrt_fast(div1_fast(c.gamma * p3, p0, ok), ok);
+  const double cmax = pmax(cl, cr);
+  const double rho_sum = m0 + p0;
+  const Recip rs = recip_of(rho_sum);
+  const double ps = div_fast(p0 * m3 + m0 * p3, rs, ok) - div_fast(m0 * p0, rs, ok) * cmax * (ur - ul);
+  const double us = div_fast(m0 * ul + p0 * ur, rs, ok) - div1_fast(p3 - m3, cmax * rho_sum, ok);
+  const bool pos = us > 0.0;
+  ok = ok && (pos || us < 0.0);
+  const double s0 = pos ? m0 : p0, s1 = pos ? m1 : p1, s2 = pos ? m2 : p2, s3 = pos ? m3 : p3;
+  const double a1 = s0 * s1, a2 = s0 * s2;
+  const double a3 = div_fast(s3, c.rgm1, ok) + 0.5 * s0 * (s1 * s1 + s2 * s2);
+  f[0] = s0 * us;
+  f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
+  f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
+  f[3] = a3 * us + ps * us;
+}
+
+// Cell traces (reconstruct.hpp:33-49): lo = q - 0.5 s (plus side of the face
+// below/left), hi = q + 0.5 s (minus side of the face above/right).
+template <bool MUSCL>
+__device__ __forceinline__ void cell_traces(double qm, double q0, double qp, double beta,
+                                            double& lo, double& hi) {
+  if (MUSCL) {
+    const double hs = 0.5 * sweby_fast(qp - q0, q0 - qm, beta);
+    lo = q0 - hs;
+    hi = q0 + hs;
+  } else {
+    lo = q0;
+    hi = q0;
+  }
+}
+
+// Primitives (solver.cpp:153-157) with the fast reciprocal; IEEE fallback.
+__device__ __forceinline__ void prim_fast(double r, double mx, double my, double e, double gm1,
+                                          double w[4]) {
+  bool ok = true;
+  const double inv = div1_fast(1.0, r, ok);
+  w[0] = r;
+  if (ok) {
+    w[1] = mx * inv;
+    w[2] = my * inv;
+    w[3] = gm1 * (e - (0.5 * (mx * mx + my * my)) * inv);
+  } else {
+    primitive(r, mx, my, e, gm1, w[1], w[2], w[3]);
+  }
+}
+
+// ---------------------------------------------------------------- TMA / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LF_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LF_WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// one contiguous row segment global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes,
+                                        unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+constexpr int URING = 8;   // U^n rows resident in shared memory (r-5 .. r+2)
+constexpr int PREFETCH = 2;
+
+#ifndef LF_MINBLOCKS
+#define LF_MINBLOCKS 2
+#endif
+template <bool MUSCL>
+__global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(FusedArgs a) {
+  extern __shared__ __align__(128) double smem[];
+  double* sU = smem;                   // [URING][4][NC] U^n rows (TMA destination)
+  double* sWx = sU + URING * 4 * NC;   // [4][NC]     P: W(r-2) for x slopes
+  double* sTx = sWx + 4 * NC;          // [4][NC]     P: x hi-traces
+  double* sFnx = sTx + 4 * NC;         // [4][4][NC]  ring: F^n x-faces of a row
+  double* sFny = sFnx + 16 * NC;       // [4][4][NC]  ring: F^n y-faces
+  double* sWs = sFny + 16 * NC;        // [2][4][NC]  W* rows (P -> C)
+  double* sWc = sWs + 8 * NC;          // [4][NC]     C: W*(j) for x slopes
+  double* sTc = sWc + 4 * NC;          // [4][NC]     C: x hi-traces
+  double* sFc = sTc + 4 * NC;          // [4][NC]     C: 0.5 (F^n + F*) x-faces
+  double* sStash = sFc + 4 * NC;       // [4][NC]     C: top-edge ghost image
+  unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sStash + 4 * NC);  // [URING]
+
+  const StepCtl ctl = *a.ctl;
+  if (ctl.done) return;
+  if (ctl.dtfail) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) atomicMax(&a.acc->fail, 1ull);
+    return;
+  }
+  // dt exactly as compute_dt (solver.cpp:476-477) and apply_update (:262-263)
+  const double rate = key_to_double(ctl.rate_bits);
+  double dt = a.cfl / rate;
+  if (ctl.time + dt > a.limit) dt = a.limit - ctl.time;
+  if (!(dt > 0.0)) {
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) atomicMax(&a.acc->fail, 1ull);
+    return;
+  }
+  const double lam_x = dt / a.dx;
+  const double lam_y = dt / a.dy;
+
+  FK C;
+  C.gamma = a.gamma;
+  C.gm1 = a.gm1;
+  C.beta = a.beta;
+  C.rgm1 = recip_of(a.gm1);
+  C.rdx = recip_of(a.dx);
+  C.rdy = recip_of(a.dy);
+  C.k.gamma = a.gamma;
+  C.k.gm1 = a.gm1;
+  C.k.beta = a.beta;
+  C.k.dx = a.dx;
+  C.k.dy = a.dy;
+
+  const int t = threadIdx.x & (NC - 1);
+  const bool is_p = threadIdx.x < NC;
+  const int x0 = blockIdx.x * TXO;
+  const int c = x0 - 4 + t;                      // this thread's column
+  const int y0 = blockIdx.y * a.rows_per_chunk;  // chunk output rows [y0, y1)
+  const int y1 = min(y0 + a.rows_per_chunk, a.ny);
+  const int nit = (y1 - y0) + 9;
+  const int klastp = (y1 - y0) + 7;              // last P iteration (input row y1+3)
+  const bool col_in_mem = c >= -NG && c < a.nx + NG;
+  const bool col_interior = c >= 0 && c < a.nx;
+  const bool bottom_edge = a.bottom_edge && y0 == 0;
+  const bool top_edge = a.top_edge && y1 == a.ny;
+  // row rho (relative to y0-4) of component q starts at src_row(rho) + q*fstride
+  const double* src0 = a.u + (int64_t)(y0 - 4) * a.pitch + (x0 - 4);
+  const uint32_t row_bytes = NC * sizeof(double);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < URING; ++s) mbar_init(&mbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < PREFETCH; ++k) {
+      mbar_expect_tx(&mbar[k], 4 * row_bytes);
+      for (int q = 0; q < 4; ++q)
+        tma_row(sU + (k * 4 + q) * NC, src0 + (int64_t)k * a.pitch + q * a.fstride, row_bytes, &mbar[k]);
+    }
+  }
+  __syncthreads();
+
+  unsigned fail = 0;
+
+  if (is_p) {
+    // ================================================================ stage 1 (P)
+    double wm2[4] = {1.0, 0.0, 0.0, 1.0}, wm1[4] = {1.0, 0.0, 0.0, 1.0};
+    double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fyprev[4] = {0.0, 0.0, 0.0, 0.0};
+    // this thread owns x-face (t-1 | t), needed for U* up to column nx+1
+    const bool dox = t >= 2 && t <= NC - 2 && c <= a.nx + 2;
+    for (int k = 0; k < nit; ++k) {
+      const int r = y0 - 4 + k;
+      const bool p_active = k <= klastp;
+      if (threadIdx.x == 0 && k + PREFETCH <= klastp) {
+        // the slot's previous row (k+PREFETCH-URING) was last read before the
+        // previous iteration's __syncthreads
+        const int kn = k + PREFETCH, s = kn & (URING - 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[s], 4 * row_bytes);
+        for (int q = 0; q < 4; ++q)
+          tma_row(sU + (s * 4 + q) * NC, src0 + (int64_t)kn * a.pitch + q * a.fstride, row_bytes,
+                  &mbar[s]);
+      }
+      double w[4] = {1.0, 0.0, 0.0, 1.0};
+      double ylo[4] = {1.0, 0.0, 0.0, 1.0}, yhi[4] = {1.0, 0.0, 0.0, 1.0};
+      if (p_active) {
+        // -- U^n(r) -> W(r) (solver.cpp:145-163)
+        mbar_wait(&mbar[k & (URING - 1)], (k / URING) & 1);
+        if (col_in_mem) {
+          const double* u = sU + (k & (URING - 1)) * 4 * NC + t;
+          const double r0 = u[0], m1 = u[NC], m2 = u[2 * NC], e3 = u[3 * NC];
+          prim_fast(r0, m1, m2, e3, a.gm1, w);
+          if ((!(r0 > 0.0) || !(w[3] > 0.0)) && col_interior && r >= 0 && r < a.ny) fail = 1;
+        }
+        if (k >= 2) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            sWx[q * NC + t] = wm2[q];  // row r-2 for the x direction
+            cell_traces<MUSCL>(wm2[q], wm1[q], w[q], a.beta, ylo[q], yhi[q]);  // row r-1
+          }
+        }
+      }
+      bar_named(1);
+      double xlo[4] = {1.0, 0.0, 0.0, 1.0};
+      if (p_active && k >= 2 && t >= 1 && t <= NC - 2) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double hi;
+          cell_traces<MUSCL>(sWx[q * NC + t - 1], sWx[q * NC + t], sWx[q * NC + t + 1], a.beta,
+                             xlo[q], hi);
+          sTx[q * NC + t] = hi;
+        }
+      }
+      bar_named(1);
+      double fy[4] = {0.0, 0.0, 0.0, 0.0};
+      if (p_active && k >= 2) {
+        // x-face (t-1 | t) of row r-2 and y-face (r-2 | r-1)
+        const int tm = dox ? t - 1 : t;
+        double mx[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = dox ? sTx[q * NC + tm] : xlo[q];
+        double fx[4];
+        bool okx = true, oky = true;
+        face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
+#if !LF_PAIR
+        if (dox && !okx)
+          face_ref<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
+#endif
+        face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
+                     C, fy, oky);
+#if LF_PAIR
+        if (dox && !okx)
+          face_ref<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
+#endif
+        // (lanes whose face is never consumed -- halo lanes, columns past the
+        // grid -- must not take the fallback: their dummy states have u* = 0)
+        if (k >= 3 && !oky && t >= 2 && t <= NC - 3 && col_in_mem)
+          face_ref<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
+                      C.k, fy);
+        if (dox) {
+          if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && r - 2 >= 0 &&
+              r - 2 < a.ny)
+            fail = 1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sFnx[((k & 3) * 4 + q) * NC + t] = fx[q];
+        }
+        if (k >= 3) {
+          if (!traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && col_interior && r - 1 >= 0 &&
+              r - 1 <= a.ny)
+            fail = 1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sFny[((k & 3) * 4 + q) * NC + t] = fy[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) hiprev[q] = yhi[q];
+      }
+      bar_named(1);
+      // -- predictor U*(r-2) (solver.cpp:283-291 with one flux set), then its
+      //    primitives W*(r-2) (build_primitives of predictor_, solver.cpp:505)
+      if (p_active && k >= 4 && t >= 2 && t <= NC - 3 && col_in_mem) {
+        const int row = r - 2;
+        const double* ub = sU + ((k - 2) & (URING - 1)) * 4 * NC + t;
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double fxl = sFnx[((k & 3) * 4 + q) * NC + t];
+          const double fxr = sFnx[((k & 3) * 4 + q) * NC + t + 1];
+          double val = ub[q * NC] - lam_x * (fxr - fxl);
+          val -= lam_y * (fy[q] - fyprev[q]);
+          v[q] = val;
+        }
+        double ws[4];
+        prim_fast(v[0], v[1], v[2], v[3], a.gm1, ws);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sWs[((k & 1) * 4 + q) * NC + t] = ws[q];
+        if (col_interior && row >= 0 && row < a.ny) {
+          // e_int = v3 - (0.5 (v1^2 + v2^2)) / v0 > 0 (solver.cpp:300-302), tested
+          // without the division: v3 v0 > K (1 + 2^-48) implies it; else flag
+          // (conservative: the stage-wise re-run decides exactly)
+          const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
+          const double lhs = v[3] * v[0];
+          if (!(v[0] > 0.0) || !(lhs > kin * (1.0 + 0x1p-48)) || !(lhs >= 0x1p-960)) fail = 1;
+          if (!(ws[3] > 0.0)) fail = 1;
+        }
+      }
+      if (p_active && k >= 3) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fyprev[q] = fy[q];
+      }
+      if (p_active) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          wm2[q] = wm1[q];
+          wm1[q] = w[q];
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    // ================================================================ stage 2 (C)
+    double vm2[4] = {1.0, 0.0, 0.0, 1.0}, vm1[4] = {1.0, 0.0, 0.0, 1.0};
+    double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fcprev[4] = {0.0, 0.0, 0.0, 0.0};
+    unsigned long long rate_key = 0ull, nmin_r = NINF_KEY, nmin_e = NINF_KEY;
+    unsigned dtfail = 0;
+    // source column of this thread's W* value (ghost columns at non-periodic x edges)
+    int src_t = t;
+    bool flip_u = false;
+    if (c < 0 && a.bc_xlo != LF_PERIODIC) {
+      const int sc = a.bc_xlo == LF_REFLECTIVE ? -c - 1 : 0;
+      src_t = t + (sc - c);
+      flip_u = a.bc_xlo == LF_REFLECTIVE;
+    } else if (c >= a.nx && a.bc_xhi != LF_PERIODIC) {
+      const int sc = a.bc_xhi == LF_REFLECTIVE ? 2 * a.nx - 1 - c : a.nx - 1;
+      src_t = t + (sc - c);
+      flip_u = a.bc_xhi == LF_REFLECTIVE;
+    }
+    const bool has_ws = t >= 2 && t <= NC - 3 && src_t >= 2 && src_t <= NC - 3;
+    const bool dox = t >= 4 && t <= NC - 4 && c <= a.nx;  // x-faces of output cells
+    for (int k = 0; k < nit; ++k) {
+      const int aa = y0 - 7 + k;   // W* row consumed this iteration
+      const int j = aa - 2;        // U^{n+1} row finished this iteration
+      const bool c_active = k >= 5;
+      double w[4] = {1.0, 0.0, 0.0, 1.0};
+      double ylo[4] = {1.0, 0.0, 0.0, 1.0}, yhi[4] = {1.0, 0.0, 0.0, 1.0};
+      if (c_active) {
+        // -- W*(aa) with the boundary images of the reference's ghost fill of
+        //    predictor_ (grid.cpp:72-114); a reflective image negates the normal
+        //    velocity exactly as it negates the normal momentum
+        if (has_ws) {
+          const double* ws = sWs + ((k + 1) & 1) * 4 * NC + src_t;
+          w[0] = ws[0];
+          w[1] = ws[NC];
+          w[2] = ws[2 * NC];
+          w[3] = ws[3 * NC];
+          if (flip_u) w[1] = -w[1];
+        }
+        if (bottom_edge && aa == 0) {
+          // W*(-1) = image of W*(0)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) vm1[q] = w[q];
+          if (a.bc_ylo == LF_REFLECTIVE) vm1[2] = -vm1[2];
+        }
+        if (bottom_edge && aa == 1) {
+          // hi trace of ghost row -1 from W*(-2) = image(W*(1) or W*(0)), W*(-1), W*(0)
+          double g2[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) g2[q] = a.bc_ylo == LF_REFLECTIVE ? w[q] : vm1[q];
+          if (a.bc_ylo == LF_REFLECTIVE) g2[2] = -g2[2];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            double lo;
+            cell_traces<MUSCL>(g2[q], vm2[q], vm1[q], a.beta, lo, hiprev[q]);
+          }
+        }
+        if (top_edge && aa == a.ny) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            w[q] = vm1[q];
+            sStash[q * NC + t] = a.bc_yhi == LF_REFLECTIVE ? vm2[q] : vm1[q];
+          }
+          if (a.bc_yhi == LF_REFLECTIVE) {
+            w[2] = -w[2];
+            sStash[2 * NC + t] = -sStash[2 * NC + t];
+          }
+        } else if (top_edge && aa == a.ny + 1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w[q] = sStash[q * NC + t];
+        }
+        if (k >= 7) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            sWc[q * NC + t] = vm2[q];  // row j = aa-2 for the x direction
+            cell_traces<MUSCL>(vm2[q], vm1[q], w[q], a.beta, ylo[q], yhi[q]);  // row aa-1
+          }
+        }
+      }
+      bar_named(2);
+      double xlo[4] = {1.0, 0.0, 0.0, 1.0};
+      if (c_active && k >= 9 && t >= 3 && t <= NC - 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double hi;
+          cell_traces<MUSCL>(sWc[q * NC + t - 1], sWc[q * NC + t], sWc[q * NC + t + 1], a.beta,
+                             xlo[q], hi);
+          sTc[q * NC + t] = hi;
+        }
+      }
+      bar_named(2);
+      double fc[4] = {0.0, 0.0, 0.0, 0.0};
+      if (c_active && k >= 7) {
+        const bool dx_ = dox && k >= 9;
+        const int tm = dx_ ? t - 1 : t;
+        double mx[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = dx_ ? sTc[q * NC + tm] : xlo[q];
+        double fx[4], fs[4];
+        bool okx = true, oky = true;
+        face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
+#if !LF_PAIR
+        if (dx_ && !okx)
+          face_ref<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
+#endif
+        face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
+                     C, fs, oky);
+#if LF_PAIR
+        if (dx_ && !okx)
+          face_ref<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
+#endif
+        if (k >= 8 && !oky && t >= 4 && t <= NC - 5 && col_interior)
+          face_ref<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
+                      C.k, fs);
+        if (dx_) {
+          if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && j >= 0 &&
+              j < a.ny)
+            fail = 1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            sFc[q * NC + t] = 0.5 * (sFnx[(((k + 1) & 3) * 4 + q) * NC + t] + fx[q]);
+        }
+        if (k >= 8) {
+          if (!traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && col_interior && aa - 1 >= 0 &&
+              aa - 1 <= a.ny)
+            fail = 1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) fc[q] = 0.5 * (sFny[(((k + 1) & 3) * 4 + q) * NC + t] + fs[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) hiprev[q] = yhi[q];
+      }
+      bar_named(2);
+      // -- corrector U^{n+1}(j) (solver.cpp:283-291, two flux sets) + epilogue
+      if (c_active && k >= 9 && t >= 4 && t <= NC - 5 && col_interior) {
+        const double* ub = sU + ((k - 5) & (URING - 1)) * 4 * NC + t;
+        const int64_t o = (int64_t)j * a.pitch + c;
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double val = ub[q * NC] - lam_x * (sFc[q * NC + t + 1] - sFc[q * NC + t]);
+          val -= lam_y * (fc[q] - fcprev[q]);
+          v[q] = val;
+          a.un[q * a.fstride + o] = val;
+        }
+        // positivity (solver.cpp:300-307) and the diagnostics minima
+        bool ok = true;
+        const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
+        double eint = v[3] - div1_fast(kin, v[0], ok);
+        if (!ok) eint = internal_energy(v[0], v[1], v[2], v[3]);
+        if (!(v[0] > 0.0) || !(eint > 0.0)) {
+          fail = 1;
+        } else {
+          const unsigned long long kr = ~pos_bits(v[0]), ke = ~pos_bits(eint);
+          nmin_r = kr > nmin_r ? kr : nmin_r;
+          nmin_e = ke > nmin_e ? ke : nmin_e;
+        }
+        // CFL rate of U^{n+1} for the next step's dt (solver.cpp:457-469)
+        double rr = 0.0;
+        bool rok = false;
+        if (v[0] > 0.0) {
+          bool okr = true;
+          const double inv = div1_fast(1.0, v[0], okr);
+          const double uu = v[1] * inv, vv = v[2] * inv;
+          const double p = C.gm1 * (v[3] - 0.5 * (v[1] * v[1] + v[2] * v[2]) * inv);
+          if (p > 0.0) {
+            const double cs = sqrt_fast(C.gamma * p * inv, okr);
+            rr = div_fast(abs_bits(uu) + cs, C.rdx, okr);
+            rr += div_fast(abs_bits(vv) + cs, C.rdy, okr);
+            rok = true;
+          }
+          if (!okr) rok = cfl_rate<true>(v[0], v[1], v[2], v[3], C.k, rr);
+        }
+        if (rok) {
+          if (rr == rr) {
+            const unsigned long long b = pos_bits(rr);
+            rate_key = b > rate_key ? b : rate_key;
+          }
+        } else {
+          dtfail = 1;
+        }
+        // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
+        const int jg = j + a.y0g;
+        if (c == 0)
+          for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = sFc[q * NC + t];
+        if (c == a.nx - 1)
+          for (int q = 0; q < 4; ++q) a.bnd[4 * (int64_t)a.nyg + (int64_t)q * a.nyg + jg] = sFc[q * NC + t + 1];
+        if (jg == 0)
+          for (int q = 0; q < 4; ++q) a.bnd[8 * (int64_t)a.nyg + (int64_t)q * a.nx + c] = fcprev[q];
+        if (jg == a.nyg - 1)
+          for (int q = 0; q < 4; ++q)
+            a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fc[q];
+      }
+      if (c_active && k >= 8) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fcprev[q] = fc[q];
+      }
+      if (c_active) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          vm2[q] = vm1[q];
+          vm1[q] = w[q];
+        }
+      }
+      __syncthreads();
+    }
+    // block-level reductions (warp shuffles, then one atomic per warp)
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long r2 = __shfl_xor_sync(FULL, rate_key, o);
+      const unsigned long long a2 = __shfl_xor_sync(FULL, nmin_r, o);
+      const unsigned long long b2 = __shfl_xor_sync(FULL, nmin_e, o);
+      rate_key = r2 > rate_key ? r2 : rate_key;
+      nmin_r = a2 > nmin_r ? a2 : nmin_r;
+      nmin_e = b2 > nmin_e ? b2 : nmin_e;
+    }
+    dtfail = __any_sync(FULL, dtfail);
+    if ((threadIdx.x & 31) == 0) {
+      if (rate_key) atomicMax(&a.acc->rate_next, rate_key);
+      if (nmin_r != NINF_KEY) atomicMax(&a.acc->nmin_rho, nmin_r);
+      if (nmin_e != NINF_KEY) atomicMax(&a.acc->nmin_eint, nmin_e);
+      if (dtfail) atomicMax(&a.acc->dtfail_next, 1ull);
+    }
+  }
+  if (__any_sync(FULL, fail) && (threadIdx.x & 31) == 0) atomicMax(&a.acc->fail, 1ull);
+}
+
+// After the step's kernel (and the cross-rank all-reduce of acc): dt / time
+// bookkeeping (solver.cpp:494,542-544), the ordered boundary-outflow sums
+// (solver.cpp:406-432, one thread per component and direction) and the
+// control record of the next step.
+__global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCtl* nxt,
+                           StepRec* rec, const double* __restrict__ bnd, double* outflow,
+                           int nx, int nyg, double dx, double dy, double cfl, double limit,
+                           double t_final) {
+  __shared__ double sums[8];
+  const int tid = threadIdx.x;
+  const StepCtl c = *ctl;
+  const bool skip = c.done != 0;
+  double dt = 0.0;
+  if (!skip) {
+    const double rate = __longlong_as_double((long long)c.rate_bits);
+    dt = cfl / rate;
+    if (c.time + dt > limit) dt = limit - c.time;
+  }
+  const bool failed = !skip && (acc->fail != 0 || c.dtfail || !(dt > 0.0));
+  if (!skip && !failed && tid < 8) {
+    // solver.cpp:412-430: per component, right - left over rows in order; then top - bottom
+    const int q = tid & 3;
+    double s = 0.0;
+    if (tid < 4) {
+      const double* l = bnd + (int64_t)q * nyg;
+      const double* r = bnd + 4 * (int64_t)nyg + (int64_t)q * nyg;
+      for (int jj = 0; jj < nyg; ++jj) s += r[jj] - l[jj];
+    } else {
+      const double* b = bnd + 8 * (int64_t)nyg + (int64_t)q * nx;
+      const double* tp = bnd + 8 * (int64_t)nyg + 4 * (int64_t)nx + (int64_t)q * nx;
+      for (int ii = 0; ii < nx; ++ii) s += tp[ii] - b[ii];
+    }
+    sums[tid] = s;
+  }
+  __syncthreads();
+  if (tid != 0) return;
+  StepRec r;
+  r.dt = dt;
+  r.hits = 0;
+  r.time = c.time;
+  r.min_rho = 0.0;
+  r.min_eint = 0.0;
+  StepCtl n;
+  n.rate_bits = acc->rate_next;
+  n.dtfail = acc->dtfail_next != 0;
+  if (skip) {
+    r.status = 2;
+    n = c;
+    n.done = 1;
+  } else if (failed) {
+    r.status = 1;
+    n = c;
+    n.done = 1;
+  } else {
+    r.status = 0;
+    r.hits = c.time + dt >= limit;
+    r.time = r.hits ? limit : c.time + dt;
+    r.min_rho = __longlong_as_double((long long)~acc->nmin_rho);
+    r.min_eint = __longlong_as_double((long long)~acc->nmin_eint);
+    const double ax = dt * dy, ay = dt * dx;
+    for (int q = 0; q < 4; ++q) {
+      outflow[q] += ax * sums[q];
+      outflow[q] += ay * sums[4 + q];
+    }
+    n.time = r.time;
+    n.done = !(r.time < t_final);
+  }
+  *rec = r;
+  *nxt = n;
+  // reset this step's accumulators for the step after next
+  acc->rate_next = 0ull;
+  acc->fail = 0ull;
+  acc->nmin_rho = NINF_KEY;
+  acc->nmin_eint = NINF_KEY;
+  acc->dtfail_next = 0ull;
+}
+
+__global__ void k_acc_init(StepAcc* acc) {
+  for (int i = 0; i < 2; ++i) {
+    acc[i].rate_next = 0ull;
+    acc[i].fail = 0ull;
+    acc[i].nmin_rho = NINF_KEY;
+    acc[i].nmin_eint = NINF_KEY;
+    acc[i].dtfail_next = 0ull;
+  }
+}
+
+constexpr size_t SMEM_BYTES =
+    (size_t)(URING * 4 + 4 + 4 + 16 + 16 + 8 + 4 + 4 + 4 + 4) * NC * sizeof(double) +
+    URING * sizeof(unsigned long long);
+
+}  // namespace
+
+size_t fused_smem_bytes() { return SMEM_BYTES; }
+
+void fused_configure() {
+  cudaFuncSetAttribute(k_fused_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)SMEM_BYTES);
+  cudaFuncSetAttribute(k_fused_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)SMEM_BYTES);
+}
+
+void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st) {
+  count_launch();
+  if (muscl)
+    k_fused_step<true><<<grid, FUSED_THREADS, SMEM_BYTES, st>>>(a);
+  else
+    k_fused_step<false><<<grid, FUSED_THREADS, SMEM_BYTES, st>>>(a);
+}
+
+void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* rec,
+                     const double* bnd, double* outflow, int nx, int nyg, double dx, double dy,
+                     double cfl, double limit, double t_final, cudaStream_t st) {
+  count_launch();
+  k_finalize<<<1, 32, 0, st>>>(ctl, acc, nxt, rec, bnd, outflow, nx, nyg, dx, dy, cfl, limit,
+                               t_final);
+}
+
+void launch_acc_init(StepAcc* acc, cudaStream_t st) {
+  count_launch();
+  k_acc_init<<<1, 1, 0, st>>>(acc);
+}
+
+}  // namespace lfb

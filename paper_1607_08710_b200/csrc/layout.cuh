@@ -36,7 +36,9 @@ struct Layout {
     L.ny = ny;
     L.pitch = ((int64_t)XPAD + nx + NG + 15) / 16 * 16;
     L.fstride = L.pitch * (int64_t)(ny + 2 * NG);
-    L.alloc = 4 * L.fstride;
+    // one spare row: the fused step's row copies of the last column strip may
+    // run past the end of a row (the values are never used)
+    L.alloc = 4 * L.fstride + (L.pitch > 256 ? L.pitch : 256);
     return L;
   }
   __host__ __device__ int64_t origin() const { return (int64_t)NG * pitch + XPAD; }
