@@ -325,7 +325,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="cells per side per GPU")
-    ap.add_argument("--path", choices=["auto", "fused", "staged"], default="auto")
+    ap.add_argument("--path", choices=["auto", "twopass", "fused", "staged"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

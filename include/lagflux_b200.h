@@ -49,8 +49,13 @@ enum {
   LF_ERR_ARGUMENT = 8      /* invalid argument to this ABI */
 };
 
-/* Path selection for lf_heun_step / lf_advance. */
-enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2 };
+/* Heun-step implementation for lf_heun_step / lf_advance (all give identical results):
+ *   AUTO     the fastest available (TWOPASS)
+ *   FUSED    one kernel per step (U^n read once, U^{n+1} written once)
+ *   STAGED   the reference's phase structure, one kernel per loop (also the
+ *            exact diagnosis path for every failure)
+ *   TWOPASS  predictor and corrector as two warp-independent streaming kernels */
+enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2, LF_PATH_TWOPASS = 3 };
 
 typedef struct lf_desc {
   int dim;              /* 1 or 2 (CartesianGrid::dim) */

@@ -528,6 +528,9 @@ int guarded(lf_handle* h, F&& f) {
 
 namespace lfb {
 void fill_all_public(lf_handle* h, double* SlabState::*buf) { fill_all(h, buf); }
+void alloc_staged_public(lf_handle* h) {
+  for (auto& s : h->slabs) alloc_staged(s);
+}
 Scalars rate_of_current(lf_handle* h) {
   launch_rate_all(h, &SlabState::U);
   return combined_scalars(h, 0);
@@ -831,7 +834,7 @@ int lf_set_stream(lf_handle* h, void* stream) {
 }
 
 int lf_set_path(lf_handle* h, int path) {
-  if (!h || path < LF_PATH_AUTO || path > LF_PATH_STAGED) return LF_ERR_ARGUMENT;
+  if (!h || path < LF_PATH_AUTO || path > LF_PATH_TWOPASS) return LF_ERR_ARGUMENT;
   h->path = path;
   return 0;
 }

@@ -31,6 +31,7 @@
 #include "fastmath.cuh"
 #include "fused_common.cuh"
 #include "kernels.h"
+#include "face_fast.cuh"
 #include "lagflux_device.cuh"
 
 // Build-time tuning knobs (tools/variants.py sweeps them):
@@ -49,82 +50,12 @@ constexpr int NC = FUSED_NC;
 constexpr int TXO = FUSED_TXO;
 constexpr unsigned FULL = 0xffffffffu;
 
-struct FK {
-  double gamma, gm1, beta;
-  Recip rgm1, rdx, rdy;  // shared reciprocals of the constant divisors
-  Consts k;              // for the IEEE fallbacks
-};
-
 __device__ __forceinline__ void bar_named(int id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NC) : "memory");
 }
 
 __device__ __forceinline__ double key_to_double(unsigned long long b) {
   return __longlong_as_double((long long)b);
-}
-
-// The reference-order IEEE face flux, out of line: taken only when a range
-// check of the fast path fails or u* is not strictly signed (the mean state).
-template <int AXIS>
-__device__ __noinline__ void face_ref(double m0, double m1, double m2, double m3, double p0,
-                                      double p1, double p2, double p3, Consts k, double* f) {
-  face_flux<AXIS>(m0, m1, m2, m3, p0, p1, p2, p3, k, f);
-}
-
-// Lagrange-flux face flux (riemann_hll.hpp:29-39, solver.cpp:26-43) on the fast
-// paths.  ok &= every range check, and is cleared when u* is 0 or NaN.
-template <int AXIS>
-__device__ __forceinline__ void face_fast(double m0, double m1, double m2, double m3, double p0,
-                                          double p1, double p2, double p3, const FK& c,
-                                          double f[4], bool& ok) {
-  const double ul = AXIS == 0 ? m1 : m2;
-  const double ur = AXIS == 0 ? p1 : p2;
-  const double cl = sqrt_fast(div1_fast(c.gamma * m3, m0, ok), ok);
-  const double cr = sqrt_fast(div1_fast(c.gamma * p3, p0, ok), ok);
-  const double cmax = pmax(cl, cr);
-  const double rho_sum = m0 + p0;
-  const Recip rs = recip_of(rho_sum);
-  const double ps = div_fast(p0 * m3 + m0 * p3, rs, ok) - div_fast(m0 * p0, rs, ok) * cmax * (ur - ul);
-  const double us = div_fast(m0 * ul + p0 * ur, rs, ok) - div1_fast(p3 - m3, cmax * rho_sum, ok);
-  const bool pos = us > 0.0;
-  ok = ok && (pos || us < 0.0);
-  const double s0 = pos ? m0 : p0, s1 = pos ? m1 : p1, s2 = pos ? m2 : p2, s3 = pos ? m3 : p3;
-  const double a1 = s0 * s1, a2 = s0 * s2;
-  const double a3 = div_fast(s3, c.rgm1, ok) + 0.5 * s0 * (s1 * s1 + s2 * s2);
-  f[0] = s0 * us;
-  f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
-  f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
-  f[3] = a3 * us + ps * us;
-}
-
-// Cell traces (reconstruct.hpp:33-49): lo = q - 0.5 s (plus side of the face
-// below/left), hi = q + 0.5 s (minus side of the face above/right).
-template <bool MUSCL>
-__device__ __forceinline__ void cell_traces(double qm, double q0, double qp, double beta,
-                                            double& lo, double& hi) {
-  if (MUSCL) {
-    const double hs = 0.5 * sweby_fast(qp - q0, q0 - qm, beta);
-    lo = q0 - hs;
-    hi = q0 + hs;
-  } else {
-    lo = q0;
-    hi = q0;
-  }
-}
-
-// Primitives (solver.cpp:153-157) with the fast reciprocal; IEEE fallback.
-__device__ __forceinline__ void prim_fast(double r, double mx, double my, double e, double gm1,
-                                          double w[4]) {
-  bool ok = true;
-  const double inv = div1_fast(1.0, r, ok);
-  w[0] = r;
-  if (ok) {
-    w[1] = mx * inv;
-    w[2] = my * inv;
-    w[3] = gm1 * (e - (0.5 * (mx * mx + my * my)) * inv);
-  } else {
-    primitive(r, mx, my, e, gm1, w[1], w[2], w[3]);
-  }
 }
 
 // ---------------------------------------------------------------- TMA / mbarrier

@@ -17,6 +17,7 @@
 
 #include "fused.h"
 #include "fused_common.cuh"
+#include "twopass.h"
 #include "nccl_comm.h"
 
 namespace lfb {
@@ -48,7 +49,8 @@ struct FusedState {
   StepCtl* ctl_host = nullptr;     // pinned [2]
   int cur = 0;                     // ctl slot of the current state
   bool valid = false;              // ctl[cur].rate_bits is the rate of the current U
-  int rows_per_chunk = 0;
+  int rows_per_chunk = 0;          // fused kernel
+  int tp_rows = 0;                 // two-pass kernels
   cudaEvent_t e0 = nullptr, e1 = nullptr;
 };
 
@@ -70,6 +72,7 @@ static void fused_alloc(lf_handle* h, int steps) {
   FusedState* f = fstate(h);
   SlabState& s0 = h->slabs[0];
   FK(cudaSetDevice(s0.device));
+  if (h->path != LF_PATH_FUSED) alloc_staged_public(h);  // U*, F^n faces of the two passes
   if (!f) {
     f = new FusedState;
     h->fused = f;
@@ -93,6 +96,10 @@ static void fused_alloc(lf_handle* h, int steps) {
     const int target_blocks = 2 * sms * 6;
     const int chunks = std::max(1, (target_blocks + strips - 1) / strips);
     f->rows_per_chunk = std::max((ny_local + chunks - 1) / chunks, 64);
+    // two-pass: independent warps, ~3 waves of 16 resident warps per SM
+    const int tp_target = sms * 16 * 3;
+    const int tp_chunks = std::max(1, (tp_target + tp_strips(h->d.nx) - 1) / tp_strips(h->d.nx));
+    f->tp_rows = std::max((ny_local + tp_chunks - 1) / tp_chunks, 32);
   }
   if (steps > f->cap) {
     cudaFree(f->rec);
@@ -167,7 +174,45 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   double* bnd = f->bnd + (size_t)cur * bnd_words(h);
   if (h->nccl) FK(cudaMemsetAsync(bnd, 0, bnd_words(h) * sizeof(double), s0.stream));
   if (k0) FK(cudaEventRecord(k0, s0.stream));
+  if (h->path != LF_PATH_FUSED) {
+    // two passes: predictor U^n -> U*, F^n; ghosts / halos of U*; corrector
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) fill_all_public(h, &SlabState::Us);
+      for (auto& s : h->slabs) {
+        PassArgs a;
+        a.x = (pass == 0 ? s.U : s.Us) + s.L.origin();
+        a.base = s.U + s.L.origin();
+        a.out = (pass == 0 ? s.Us : s.U2) + s.L.origin();
+        a.fx = s.FX[0];
+        a.fy = s.FY[0];
+        a.fxo = s.FX[0];
+        a.fyo = s.FY[0];
+        a.pitch = s.L.pitch;
+        a.fstride = s.L.fstride;
+        a.fx_stride = s.fx_stride;
+        a.fy_stride = s.fy_stride;
+        a.nx = s.L.nx;
+        a.ny = s.L.ny;
+        a.y0g = s.sl.y0;
+        a.nyg = h->d.ny;
+        a.strips = tp_strips(s.L.nx);
+        a.rows_per_chunk = f->tp_rows;
+        a.gamma = h->k.gamma;
+        a.gm1 = h->k.gm1;
+        a.beta = h->k.beta;
+        a.dx = h->d.dx;
+        a.dy = h->d.dy;
+        a.cfl = cfl;
+        a.limit = limit;
+        a.ctl = f->ctl + cur;
+        a.acc = f->acc + cur;
+        a.bnd = bnd;
+        launch_pass(a, pass == 1, h->d.spatial_order >= 2, s.stream);
+      }
+    }
+  }
   for (auto& s : h->slabs) {
+    if (h->path != LF_PATH_FUSED) break;
     FusedArgs a;
     a.u = s.U + s.L.origin();
     a.un = s.U2 + s.L.origin();

@@ -61,6 +61,7 @@ struct lf_handle {
 namespace lfb {
 // api.cu services used by the fused path
 void fill_all_public(lf_handle* h, double* SlabState::*buf);
+void alloc_staged_public(lf_handle* h);
 Scalars rate_of_current(lf_handle* h);
 int staged_heun_public(lf_handle* h, double cfl, double time, double limit, int64_t step,
                        double* outflow, lf_step_out* out);

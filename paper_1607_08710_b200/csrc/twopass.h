@@ -1,0 +1,36 @@
+// twopass.h -- the two-pass (predictor / corrector) Heun step kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fused_common.cuh"
+
+namespace lfb {
+
+constexpr int TP_THREADS = 128;   // 4 independent warps per block
+
+struct PassArgs {
+  const double* x;      // stage input, ghost-filled: U^n (predictor) or U* (corrector)
+  const double* base;   // U^n (both passes update from U^n, solver.cpp:500,507)
+  double* out;          // U* (predictor) or U^{n+1} (corrector)
+  const double* fx;     // corrector: F^n x-faces  [4][ny][pitch]  face c = left face of column c
+  const double* fy;     // corrector: F^n y-faces  [4][ny+1][pitch] face j = bottom face of row j
+  double* fxo;          // predictor: F^n x-faces written
+  double* fyo;          // predictor: F^n y-faces written
+  int64_t pitch, fstride, fx_stride, fy_stride;
+  int nx, ny;           // local interior
+  int y0g, nyg;         // global row of local row 0, global rows
+  int strips, rows_per_chunk;
+  double gamma, gm1, beta, dx, dy;
+  double cfl, limit;
+  const StepCtl* ctl;
+  StepAcc* acc;
+  double* bnd;          // corrector: boundary faces [left 4*nyg | right 4*nyg | bottom 4*nx | top 4*nx]
+};
+
+int tp_strips(int nx);
+void launch_pass(const PassArgs& a, bool corr, bool muscl, cudaStream_t st);
+
+}  // namespace lfb

@@ -1,0 +1,296 @@
+// twopass_kernel.cu -- the Heun step as two warp-independent streaming passes.
+//
+//   predictor  U^n (ghost-filled) -> U*, F^n x-faces, F^n y-faces
+//   corrector  U*  (ghost-filled), U^n, F^n -> U^{n+1}, min rho / min e_int,
+//              CFL rate of U^{n+1}, boundary-face fluxes, failure flags
+//
+// This is the reference's own stage structure (solver.cpp:496-509: ghost fill,
+// build_primitives, compute_fluxes, apply_update, twice) with each stage fused
+// into one kernel.  Every warp owns a strip of 32 columns (28 output columns and
+// a 2-column halo each side) and marches down a chunk of rows on its own: the
+// y-direction stencil lives in a rolling 3-row register window of the lane that
+// owns the column (slopes shared by the two y-faces of a cell), x-neighbours
+// come from warp shuffles.  There is no block-level synchronisation at all, so
+// the scheduler is free to interleave warps; the U^n / U* row of the next
+// iteration is loaded one iteration ahead.
+//
+// Compared with the one-kernel step (fused_kernel.cu) this moves 288 B per
+// cell-update instead of 64 B, whose HBM ceiling (22.7 G cell-updates/s at the
+// measured 6.5 TB/s) is far above the fp64 issue rate either design achieves;
+// it wins because it keeps every SM issuing instead of waiting at barriers.
+#include <cuda_runtime.h>
+
+#include "../../include/lagflux_b200.h"
+#include "face_fast.cuh"
+#include "fused_common.cuh"
+#include "kernels.h"
+#include "twopass.h"
+
+namespace lfb {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int LANES = 32;
+constexpr int TXW = LANES - 4;  // output columns per warp strip
+
+__device__ __forceinline__ double key_to_double(unsigned long long b) {
+  return __longlong_as_double((long long)b);
+}
+
+template <int N>
+__device__ __forceinline__ void shfl_up4(const double (&v)[N], double (&o)[N], int d) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) o[q] = __shfl_up_sync(FULL, v[q], d);
+}
+template <int N>
+__device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N], int d) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) o[q] = __shfl_down_sync(FULL, v[q], d);
+}
+
+#ifndef LF_TP_MINBLOCKS
+#define LF_TP_MINBLOCKS 3
+#endif
+
+template <bool CORR, bool MUSCL>
+__global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a) {
+  const StepCtl ctl = *a.ctl;
+  if (ctl.done) return;
+  if (ctl.dtfail) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) atomicMax(&a.acc->fail, 1ull);
+    return;
+  }
+  // dt exactly as compute_dt (solver.cpp:476-477) and apply_update (:262-263)
+  const double rate = key_to_double(ctl.rate_bits);
+  double dt = a.cfl / rate;
+  if (ctl.time + dt > a.limit) dt = a.limit - ctl.time;
+  if (!(dt > 0.0)) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) atomicMax(&a.acc->fail, 1ull);
+    return;
+  }
+  const double lam_x = dt / a.dx;
+  const double lam_y = dt / a.dy;
+  const FK C = make_fk(a.gamma, a.gm1, a.beta, a.dx, a.dy);
+
+  const int lane = threadIdx.x & 31;
+  const int warp = blockIdx.x * (TP_THREADS / 32) + (threadIdx.x >> 5);
+  const int strip = warp % a.strips;
+  const int chunk = warp / a.strips;
+  const int y0 = chunk * a.rows_per_chunk;
+  if (y0 >= a.ny) return;  // whole warp
+  const int y1 = min(y0 + a.rows_per_chunk, a.ny);
+  const int x0 = strip * TXW;
+  const int c = x0 - 2 + lane;
+  const bool col_in_mem = c >= -NG && c < a.nx + NG;
+  const bool col_interior = c >= 0 && c < a.nx;
+  const bool upd = lane >= 2 && lane <= LANES - 3 && col_interior;   // owns an output cell
+  // x-face (lane-1 | lane) is stored by lanes 2..29 (faces x0 .. x0+27), plus
+  // the domain's last face nx by whichever lane holds column nx
+  const bool store_fx = (lane >= 2 && lane <= LANES - 3 && c <= a.nx) || (lane == LANES - 2 && c == a.nx);
+  const int nit = (y1 - y0) + 4;
+
+  unsigned fail = 0;
+  unsigned long long rate_key = 0ull, nmin_r = NINF_KEY, nmin_e = NINF_KEY;
+  unsigned dtfail = 0;
+
+  const double* xin = a.x + c;
+  double nxt[4] = {1.0, 0.0, 0.0, 1.0};
+  if (col_in_mem) {
+    const int64_t o = (int64_t)(y0 - 2) * a.pitch;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) nxt[q] = __ldg(xin + q * a.fstride + o);
+  }
+  double wm2[4] = {1.0, 0.0, 0.0, 1.0}, wm1[4] = {1.0, 0.0, 0.0, 1.0};
+  double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fyprev[4] = {0.0, 0.0, 0.0, 0.0};
+
+  for (int it = 0; it < nit; ++it) {
+    const int r = y0 - 2 + it;   // input row
+    const int row = r - 2;       // row updated this iteration (when it >= 4)
+    double cur[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+    if (it + 1 < nit && col_in_mem) {
+      const int64_t o = (int64_t)(r + 1) * a.pitch;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nxt[q] = __ldg(xin + q * a.fstride + o);
+    }
+    // operands of this iteration's update, issued early
+    double base[4] = {0.0, 0.0, 0.0, 0.0}, fnx[4] = {0.0, 0.0, 0.0, 0.0}, fny[4] = {0.0, 0.0, 0.0, 0.0};
+    if (it >= 4 && col_in_mem) {
+      const int64_t o = (int64_t)row * a.pitch + c;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) base[q] = __ldg(a.base + q * a.fstride + o);
+      if (CORR && c >= 0 && c <= a.nx) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fnx[q] = __ldg(a.fx + q * a.fx_stride + o);
+      }
+    }
+    if (CORR && it >= 3 && col_interior) {
+      // face (row | row+1); at it == 3 this is the chunk's first face (y0-1 | y0)
+      const int64_t o = (int64_t)(row + 1) * a.pitch + c;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) fny[q] = __ldg(a.fy + q * a.fy_stride + o);
+    }
+    // -- W(r) (solver.cpp:145-163)
+    double w[4] = {1.0, 0.0, 0.0, 1.0};
+    if (col_in_mem) {
+      prim_fast(cur[0], cur[1], cur[2], cur[3], a.gm1, w);
+      if ((!(cur[0] > 0.0) || !(w[3] > 0.0)) && col_interior && r >= 0 && r < a.ny) fail = 1;
+    }
+    // -- y: traces of row r-1, face (r-2 | r-1); x: traces of row r-2 (shuffles)
+    double ylo[4], yhi[4], xlo[4], xhi[4], xm[4], xp[4];
+    shfl_up4(wm2, xm, 1);
+    shfl_down4(wm2, xp, 1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cell_traces<MUSCL>(wm2[q], wm1[q], w[q], a.beta, ylo[q], yhi[q]);
+      cell_traces<MUSCL>(xm[q], wm2[q], xp[q], a.beta, xlo[q], xhi[q]);
+    }
+    double xmh[4];
+    shfl_up4(xhi, xmh, 1);  // minus-side trace of x-face (lane-1 | lane)
+    double fx[4], fy[4];
+    bool okx = true, oky = true;
+    face_fast<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
+    face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3], C,
+                 fy, oky);
+    const bool need_x = it >= 4 && lane >= 2 && lane <= LANES - 2 && c <= a.nx;
+    const bool need_y = it >= 3 && lane >= 2 && lane <= LANES - 3 && col_interior;
+    if (need_x && !okx)
+      face_ref<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
+    if (need_y && !oky)
+      face_ref<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3], C.k,
+                  fy);
+    if (need_x && !traces_ok(xmh[0], xmh[3], xlo[0], xlo[3]) && c >= 0 && row >= 0 && row < a.ny)
+      fail = 1;
+    if (need_y && !traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && r - 1 >= 0 && r - 1 <= a.ny)
+      fail = 1;
+    if (CORR) {
+      // Heun average 0.5 (F^n + F*) per face (solver.cpp:284-289)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        fx[q] = 0.5 * (fnx[q] + fx[q]);
+        fy[q] = 0.5 * (fny[q] + fy[q]);
+      }
+    }
+    double fxr[4];
+    shfl_down4(fx, fxr, 1);  // x-face (lane | lane+1)
+    if (it >= 4) {
+      if (!CORR) {
+        // F^n faces for the corrector
+        const int64_t o = (int64_t)row * a.pitch + c;
+        if (store_fx)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a.fxo[q * a.fx_stride + o] = fx[q];
+        if (upd)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a.fyo[q * a.fy_stride + o + a.pitch] = fy[q];
+      }
+      if (upd) {
+        // solver.cpp:283-291
+        const int64_t o = (int64_t)row * a.pitch + c;
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          double val = base[q] - lam_x * (fxr[q] - fx[q]);
+          val -= lam_y * (fy[q] - fyprev[q]);
+          v[q] = val;
+          a.out[q * a.fstride + o] = val;
+        }
+        if (!CORR) {
+          // e_int > 0 without the division (conservative, see fused_kernel.cu)
+          const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
+          const double lhs = v[3] * v[0];
+          if (!(v[0] > 0.0) || !(lhs > kin * (1.0 + 0x1p-48)) || !(lhs >= 0x1p-960)) fail = 1;
+        } else {
+          bool ok = true;
+          const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
+          double eint = v[3] - div1_fast(kin, v[0], ok);
+          if (!ok) eint = internal_energy(v[0], v[1], v[2], v[3]);
+          if (!(v[0] > 0.0) || !(eint > 0.0)) {
+            fail = 1;
+          } else {
+            const unsigned long long kr = ~pos_bits(v[0]), ke = ~pos_bits(eint);
+            nmin_r = kr > nmin_r ? kr : nmin_r;
+            nmin_e = ke > nmin_e ? ke : nmin_e;
+          }
+          double rr;
+          if (rate_fast(v, C, rr)) {
+            if (rr == rr) {
+              const unsigned long long b = pos_bits(rr);
+              rate_key = b > rate_key ? b : rate_key;
+            }
+          } else {
+            dtfail = 1;
+          }
+          // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
+          const int jg = row + a.y0g;
+          if (c == 0)
+            for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = fx[q];
+          if (c == a.nx - 1)
+            for (int q = 0; q < 4; ++q) a.bnd[4 * (int64_t)a.nyg + (int64_t)q * a.nyg + jg] = fxr[q];
+          if (jg == 0)
+            for (int q = 0; q < 4; ++q) a.bnd[8 * (int64_t)a.nyg + (int64_t)q * a.nx + c] = fyprev[q];
+          if (jg == a.nyg - 1)
+            for (int q = 0; q < 4; ++q)
+              a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fy[q];
+        }
+      }
+    } else if (!CORR && it == 3 && y0 == 0 && upd) {
+      // the domain's first y-face (-1 | 0) belongs to no updated row of a chunk
+      // other than the bottom one
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a.fyo[q * a.fy_stride + c] = fy[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      fyprev[q] = fy[q];
+      hiprev[q] = yhi[q];
+      wm2[q] = wm1[q];
+      wm1[q] = w[q];
+    }
+  }
+  // warp reductions, one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long r2 = __shfl_xor_sync(FULL, rate_key, o);
+    const unsigned long long a2 = __shfl_xor_sync(FULL, nmin_r, o);
+    const unsigned long long b2 = __shfl_xor_sync(FULL, nmin_e, o);
+    rate_key = r2 > rate_key ? r2 : rate_key;
+    nmin_r = a2 > nmin_r ? a2 : nmin_r;
+    nmin_e = b2 > nmin_e ? b2 : nmin_e;
+  }
+  const unsigned anyfail = __any_sync(FULL, fail);
+  dtfail = __any_sync(FULL, dtfail);
+  if (lane == 0) {
+    if (anyfail) atomicMax(&a.acc->fail, 1ull);
+    if (CORR) {
+      if (rate_key) atomicMax(&a.acc->rate_next, rate_key);
+      if (nmin_r != NINF_KEY) atomicMax(&a.acc->nmin_rho, nmin_r);
+      if (nmin_e != NINF_KEY) atomicMax(&a.acc->nmin_eint, nmin_e);
+      if (dtfail) atomicMax(&a.acc->dtfail_next, 1ull);
+    }
+  }
+}
+
+}  // namespace
+
+int tp_strips(int nx) { return (nx + TXW - 1) / TXW; }
+
+void launch_pass(const PassArgs& a, bool corr, bool muscl, cudaStream_t st) {
+  const int warps = a.strips * ((a.ny + a.rows_per_chunk - 1) / a.rows_per_chunk);
+  const int blocks = (warps + TP_THREADS / 32 - 1) / (TP_THREADS / 32);
+  count_launch();
+  if (corr) {
+    if (muscl)
+      k_pass<true, true><<<blocks, TP_THREADS, 0, st>>>(a);
+    else
+      k_pass<true, false><<<blocks, TP_THREADS, 0, st>>>(a);
+  } else {
+    if (muscl)
+      k_pass<false, true><<<blocks, TP_THREADS, 0, st>>>(a);
+    else
+      k_pass<false, false><<<blocks, TP_THREADS, 0, st>>>(a);
+  }
+}
+
+}  // namespace lfb

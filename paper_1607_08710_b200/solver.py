@@ -44,7 +44,8 @@ class LagfluxSolver:
 
     devices: one entry per y-slab driven from this process (repeats allowed).
     dist:    (rank, nranks, device, nccl_id_bytes) for one-process-per-GPU slabs.
-    path:    "auto" | "fused" | "staged" (Heun step implementation)."""
+    path:    "auto" | "twopass" | "fused" | "staged" (Heun step implementation;
+             all produce identical results)."""
 
     def __init__(self, g: G.CartesianGrid, bc: G.BoundaryCondition, gamma: float = 1.4,
                  params: G.SchemeParams = G.SchemeParams(), threads: int = 1,
@@ -106,7 +107,8 @@ class LagfluxSolver:
         return self._h
 
     def set_path(self, path: str):
-        code = {"auto": N.LF_PATH_AUTO, "fused": N.LF_PATH_FUSED, "staged": N.LF_PATH_STAGED}[path]
+        code = {"auto": N.LF_PATH_AUTO, "fused": N.LF_PATH_FUSED, "staged": N.LF_PATH_STAGED,
+                "twopass": N.LF_PATH_TWOPASS}[path]
         self._check(self._lib.lf_set_path(self._h, code))
 
     def set_stream(self, stream_ptr: Optional[int]):

@@ -17,7 +17,7 @@ from helpers import (assert_fields_equal, diag_array, golden_cases, load_golden,
 pytestmark = pytest.mark.gpu
 
 GOLDEN = list(golden_cases().items())
-PATHS = ["staged", "auto"]
+PATHS = ["staged", "twopass", "fused"]
 
 
 def run_gpu(case, steps, path="auto", devices=(0,), field=None, use_advance=False):

@@ -20,19 +20,19 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "tools", "_variants")
 CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 
+# name -> (extra nvcc flags, LF_PATH_*)
 VARIANTS = {
-    "pair1_mb2": "-DLF_PAIR=1 -DLF_MINBLOCKS=2",
-    "pair0_mb2": "-DLF_PAIR=0 -DLF_MINBLOCKS=2",
-    "pair1_mb1": "-DLF_PAIR=1 -DLF_MINBLOCKS=1",
-    "pair0_mb1": "-DLF_PAIR=0 -DLF_MINBLOCKS=1",
-    "pair1_mb2_int": "-DLF_PAIR=1 -DLF_MINBLOCKS=2 -DLF_INTMINMAX=1",
+    "fused_pair0": ("-DLF_PAIR=0 -DLF_MINBLOCKS=2", 1),
+    "tp_mb4": ("-DLF_TP_MINBLOCKS=4", 3),
+    "tp_mb3": ("-DLF_TP_MINBLOCKS=3", 3),
+    "tp_mb2": ("-DLF_TP_MINBLOCKS=2", 3),
 }
 
 
 def build(names=None):
     os.makedirs(OUT, exist_ok=True)
     procs = []
-    for name, flags in VARIANTS.items():
+    for name, (flags, _path) in VARIANTS.items():
         if names and name not in names:
             continue
         so = os.path.join(OUT, f"{name}.so")
@@ -64,6 +64,7 @@ def run(n=8192, steps=10):
         desc = make_desc(g, case.bc, case.gamma, case.params)
         h = C.c_void_p()
         assert lib.lf_create(C.byref(desc), (C.c_int * 1)(0), 1, C.byref(h)) == 0
+        assert lib.lf_set_path(h, VARIANTS[name][1]) == 0
         assert lib.lf_init_fourier(h, case.seed) == 0
         km, lm, nl = C.c_double(), C.c_double(), C.c_int()
         assert lib.lf_time_steps(h, 3, case.cfl, C.byref(km), C.byref(lm), C.byref(nl)) == 0
