@@ -2,10 +2,13 @@
 //
 // The reference's fp64 evaluation order throughout (compiled with
 // --fmad=false); divisions and square roots through fastmath.cuh, whose
-// results equal the IEEE operators bit for bit whenever the deferred range
-// check holds -- otherwise the face is recomputed by face_ref (plain
-// operators, reference structure).  Shared by fused_kernel.cu and
-// twopass_kernel.cu.
+// results equal the IEEE operators bit for bit (up to the sign of a zero
+// quotient) whenever the range checks hold.  A failed range check -- possible
+// only for magnitudes beyond 2^+-960, i.e. never for physical data -- is
+// reported through `ok`; the kernels turn it into a failure flag, and the host
+// then recomputes the step with the stage-wise IEEE kernels.  Keeping the
+// IEEE slow paths out of these kernels keeps CALLs (and the registers they pin)
+// out of the hot loops.  Shared by fused_kernel.cu and twopass_kernel.cu.
 #pragma once
 
 #include "fastmath.cuh"
@@ -18,7 +21,6 @@ namespace lfb {
 struct FK {
   double gamma, gm1, beta;
   Recip rgm1, rdx, rdy;  // shared reciprocals of the constant divisors
-  Consts k;              // for the IEEE fallbacks
 };
 
 __device__ __forceinline__ FK make_fk(double gamma, double gm1, double beta, double dx, double dy) {
@@ -29,24 +31,11 @@ __device__ __forceinline__ FK make_fk(double gamma, double gm1, double beta, dou
   c.rgm1 = recip_of(gm1);
   c.rdx = recip_of(dx);
   c.rdy = recip_of(dy);
-  c.k.gamma = gamma;
-  c.k.gm1 = gm1;
-  c.k.beta = beta;
-  c.k.dx = dx;
-  c.k.dy = dy;
   return c;
 }
 
-// The reference-order IEEE face flux, out of line: taken only when a range
-// check of the fast path fails or u* is not strictly signed (the mean state).
-template <int AXIS>
-__device__ __noinline__ void face_ref(double m0, double m1, double m2, double m3, double p0,
-                                      double p1, double p2, double p3, Consts k, double* f) {
-  face_flux<AXIS>(m0, m1, m2, m3, p0, p1, p2, p3, k, f);
-}
-
 // Lagrange-flux face flux (riemann_hll.hpp:29-39, solver.cpp:26-43) on the fast
-// paths.  ok &= every range check, and is cleared when u* is 0 or NaN.
+// paths.  ok &= every range check.
 template <int AXIS>
 __device__ __forceinline__ void face_fast(double m0, double m1, double m2, double m3, double p0,
                                           double p1, double p2, double p3, const FK& c,
@@ -61,11 +50,23 @@ __device__ __forceinline__ void face_fast(double m0, double m1, double m2, doubl
   const double ps = div_fast(p0 * m3 + m0 * p3, rs, ok) - div_fast(m0 * p0, rs, ok) * cmax * (ur - ul);
   const double us = div_fast(m0 * ul + p0 * ur, rs, ok) - div1_fast(p3 - m3, cmax * rho_sum, ok);
   const bool pos = us > 0.0;
-  ok = ok && (pos || us < 0.0);
-  const double s0 = pos ? m0 : p0, s1 = pos ? m1 : p1, s2 = pos ? m2 : p2, s3 = pos ? m3 : p3;
-  const double a1 = s0 * s1, a2 = s0 * s2;
-  const double a3 = div_fast(s3, c.rgm1, ok) + 0.5 * s0 * (s1 * s1 + s2 * s2);
-  f[0] = s0 * us;
+  double a0, a1, a2, a3;
+  if (pos || us < 0.0) {
+    const double s0 = pos ? m0 : p0, s1 = pos ? m1 : p1, s2 = pos ? m2 : p2, s3 = pos ? m3 : p3;
+    a0 = s0;
+    a1 = s0 * s1;
+    a2 = s0 * s2;
+    a3 = div_fast(s3, c.rgm1, ok) + 0.5 * s0 * (s1 * s1 + s2 * s2);
+  } else {
+    // u* == 0 (or NaN): the mean of the two conserved traces (solver.cpp:33-35)
+    const double m3c = div_fast(m3, c.rgm1, ok) + 0.5 * m0 * (m1 * m1 + m2 * m2);
+    const double p3c = div_fast(p3, c.rgm1, ok) + 0.5 * p0 * (p1 * p1 + p2 * p2);
+    a0 = 0.5 * (m0 + p0);
+    a1 = 0.5 * (m0 * m1 + p0 * p1);
+    a2 = 0.5 * (m0 * m2 + p0 * p2);
+    a3 = 0.5 * (m3c + p3c);
+  }
+  f[0] = a0 * us;
   f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
   f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
   f[3] = a3 * us + ps * us;
@@ -86,36 +87,28 @@ __device__ __forceinline__ void cell_traces(double qm, double q0, double qp, dou
   }
 }
 
-// Primitives (solver.cpp:153-157) with the fast reciprocal; IEEE fallback.
+// Primitives (solver.cpp:153-157) with the fast reciprocal; ok &= range check.
 __device__ __forceinline__ void prim_fast(double r, double mx, double my, double e, double gm1,
-                                          double w[4]) {
-  bool ok = true;
+                                          double w[4], bool& ok) {
   const double inv = div1_fast(1.0, r, ok);
   w[0] = r;
-  if (ok) {
-    w[1] = mx * inv;
-    w[2] = my * inv;
-    w[3] = gm1 * (e - (0.5 * (mx * mx + my * my)) * inv);
-  } else {
-    primitive(r, mx, my, e, gm1, w[1], w[2], w[3]);
-  }
+  w[1] = mx * inv;
+  w[2] = my * inv;
+  w[3] = gm1 * (e - (0.5 * (mx * mx + my * my)) * inv);
 }
 
-// CFL rate (solver.cpp:457-468) on the fast paths; false for a non-physical cell.
-__device__ __forceinline__ bool rate_fast(const double v[4], const FK& c, double& rr) {
+// CFL rate (solver.cpp:457-468) on the fast paths; false for a non-physical
+// cell; ok &= range checks.
+__device__ __forceinline__ bool rate_fast(const double v[4], const FK& c, double& rr, bool& ok) {
   if (!(v[0] > 0.0)) return false;
-  bool ok = true;
   const double inv = div1_fast(1.0, v[0], ok);
   const double uu = v[1] * inv, vv = v[2] * inv;
   const double p = c.gm1 * (v[3] - 0.5 * (v[1] * v[1] + v[2] * v[2]) * inv);
-  bool phys = p > 0.0;
-  if (phys) {
-    const double cs = sqrt_fast(c.gamma * p * inv, ok);
-    rr = div_fast(abs_bits(uu) + cs, c.rdx, ok);
-    rr += div_fast(abs_bits(vv) + cs, c.rdy, ok);
-  }
-  if (!ok) phys = cfl_rate<true>(v[0], v[1], v[2], v[3], c.k, rr);
-  return phys;
+  if (!(p > 0.0)) return false;
+  const double cs = sqrt_fast(c.gamma * p * inv, ok);
+  rr = div_fast(abs_bits(uu) + cs, c.rdx, ok);
+  rr += div_fast(abs_bits(vv) + cs, c.rdy, ok);
+  return true;
 }
 
 #endif  // __CUDACC__

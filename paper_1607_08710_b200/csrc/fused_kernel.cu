@@ -35,12 +35,7 @@
 #include "lagflux_device.cuh"
 
 // Build-time tuning knobs (tools/variants.py sweeps them):
-//   LF_PAIR       1: solve the x- and y-face Riemann problems of a thread in one
-//                 straight line (ILP); 0: one after the other (fewer registers)
 //   LF_MINBLOCKS  resident blocks per SM requested from ptxas (register budget)
-#ifndef LF_PAIR
-#define LF_PAIR 1
-#endif
 
 namespace lfb {
 
@@ -127,18 +122,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
   const double lam_x = dt / a.dx;
   const double lam_y = dt / a.dy;
 
-  FK C;
-  C.gamma = a.gamma;
-  C.gm1 = a.gm1;
-  C.beta = a.beta;
-  C.rgm1 = recip_of(a.gm1);
-  C.rdx = recip_of(a.dx);
-  C.rdy = recip_of(a.dy);
-  C.k.gamma = a.gamma;
-  C.k.gm1 = a.gm1;
-  C.k.beta = a.beta;
-  C.k.dx = a.dx;
-  C.k.dy = a.dy;
+  const FK C = make_fk(a.gamma, a.gm1, a.beta, a.dx, a.dy);
 
   const int t = threadIdx.x & (NC - 1);
   const bool is_p = threadIdx.x < NC;
@@ -196,8 +180,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         if (col_in_mem) {
           const double* u = sU + (k & (URING - 1)) * 4 * NC + t;
           const double r0 = u[0], m1 = u[NC], m2 = u[2 * NC], e3 = u[3 * NC];
-          prim_fast(r0, m1, m2, e3, a.gm1, w);
-          if ((!(r0 > 0.0) || !(w[3] > 0.0)) && col_interior && r >= 0 && r < a.ny) fail = 1;
+          bool okw = true;
+          prim_fast(r0, m1, m2, e3, a.gm1, w, okw);
+          if ((!(r0 > 0.0) || !(w[3] > 0.0) || !okw) && col_interior && r >= 0 && r < a.ny)
+            fail = 1;
         }
         if (k >= 2) {
 #pragma unroll
@@ -229,21 +215,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         double fx[4];
         bool okx = true, oky = true;
         face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
-#if !LF_PAIR
-        if (dox && !okx)
-          face_ref<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
-#endif
         face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
                      C, fy, oky);
-#if LF_PAIR
-        if (dox && !okx)
-          face_ref<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
-#endif
-        // (lanes whose face is never consumed -- halo lanes, columns past the
-        // grid -- must not take the fallback: their dummy states have u* = 0)
-        if (k >= 3 && !oky && t >= 2 && t <= NC - 3 && col_in_mem)
-          face_ref<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
-                      C.k, fy);
+        // a range-check failure on a consumed face hands the step to the
+        // stage-wise IEEE kernels (halo lanes and columns past the grid hold
+        // dummy states and never count)
+        if ((dox && !okx) || (k >= 3 && !oky && t >= 2 && t <= NC - 3 && col_in_mem)) fail = 1;
         if (dox) {
           if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && r - 2 >= 0 &&
               r - 2 < a.ny)
@@ -277,7 +254,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           v[q] = val;
         }
         double ws[4];
-        prim_fast(v[0], v[1], v[2], v[3], a.gm1, ws);
+        bool okw = true;
+        prim_fast(v[0], v[1], v[2], v[3], a.gm1, ws, okw);
 #pragma unroll
         for (int q = 0; q < 4; ++q) sWs[((k & 1) * 4 + q) * NC + t] = ws[q];
         if (col_interior && row >= 0 && row < a.ny) {
@@ -287,7 +265,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
           const double lhs = v[3] * v[0];
           if (!(v[0] > 0.0) || !(lhs > kin * (1.0 + 0x1p-48)) || !(lhs >= 0x1p-960)) fail = 1;
-          if (!(ws[3] > 0.0)) fail = 1;
+          if (!(ws[3] > 0.0) || !okw) fail = 1;
         }
       }
       if (p_active && k >= 3) {
@@ -403,19 +381,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         double fx[4], fs[4];
         bool okx = true, oky = true;
         face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
-#if !LF_PAIR
-        if (dx_ && !okx)
-          face_ref<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
-#endif
         face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
                      C, fs, oky);
-#if LF_PAIR
-        if (dx_ && !okx)
-          face_ref<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
-#endif
-        if (k >= 8 && !oky && t >= 4 && t <= NC - 5 && col_interior)
-          face_ref<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
-                      C.k, fs);
+        if ((dx_ && !okx) || (k >= 8 && !oky && t >= 4 && t <= NC - 5 && col_interior)) fail = 1;
         if (dx_) {
           if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && j >= 0 &&
               j < a.ny)
@@ -450,9 +418,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         // positivity (solver.cpp:300-307) and the diagnostics minima
         bool ok = true;
         const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
-        double eint = v[3] - div1_fast(kin, v[0], ok);
-        if (!ok) eint = internal_energy(v[0], v[1], v[2], v[3]);
-        if (!(v[0] > 0.0) || !(eint > 0.0)) {
+        const double eint = v[3] - div1_fast(kin, v[0], ok);
+        if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
           fail = 1;
         } else {
           const unsigned long long kr = ~pos_bits(v[0]), ke = ~pos_bits(eint);
@@ -460,22 +427,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           nmin_e = ke > nmin_e ? ke : nmin_e;
         }
         // CFL rate of U^{n+1} for the next step's dt (solver.cpp:457-469)
-        double rr = 0.0;
-        bool rok = false;
-        if (v[0] > 0.0) {
-          bool okr = true;
-          const double inv = div1_fast(1.0, v[0], okr);
-          const double uu = v[1] * inv, vv = v[2] * inv;
-          const double p = C.gm1 * (v[3] - 0.5 * (v[1] * v[1] + v[2] * v[2]) * inv);
-          if (p > 0.0) {
-            const double cs = sqrt_fast(C.gamma * p * inv, okr);
-            rr = div_fast(abs_bits(uu) + cs, C.rdx, okr);
-            rr += div_fast(abs_bits(vv) + cs, C.rdy, okr);
-            rok = true;
-          }
-          if (!okr) rok = cfl_rate<true>(v[0], v[1], v[2], v[3], C.k, rr);
-        }
-        if (rok) {
+        double rr;
+        bool okr = true;
+        if (rate_fast(v, C, rr, okr)) {
           if (rr == rr) {
             const unsigned long long b = pos_bits(rr);
             rate_key = b > rate_key ? b : rate_key;
@@ -483,6 +437,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         } else {
           dtfail = 1;
         }
+        if (!okr) fail = 1;
         // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
         const int jg = j + a.y0g;
         if (c == 0)

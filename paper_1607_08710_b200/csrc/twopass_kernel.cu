@@ -49,8 +49,18 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
   for (int q = 0; q < N; ++q) o[q] = __shfl_down_sync(FULL, v[q], d);
 }
 
+// Build-time tuning knobs (tools/variants.py sweeps them):
+//   LF_TP_MINBLOCKS  resident blocks per SM requested from ptxas (register budget)
+//   LF_TP_PAIR       1: x- and y-face Riemann solves in one straight line
+//   LF_TP_LATELOAD   1: load the update operands after the face solves
 #ifndef LF_TP_MINBLOCKS
 #define LF_TP_MINBLOCKS 3
+#endif
+#ifndef LF_TP_PAIR
+#define LF_TP_PAIR 1
+#endif
+#ifndef LF_TP_LATELOAD
+#define LF_TP_LATELOAD 0
 #endif
 
 template <bool CORR, bool MUSCL>
@@ -115,8 +125,9 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
 #pragma unroll
       for (int q = 0; q < 4; ++q) nxt[q] = __ldg(xin + q * a.fstride + o);
     }
-    // operands of this iteration's update, issued early
+    // operands of this iteration's update (issued early unless LF_TP_LATELOAD)
     double base[4] = {0.0, 0.0, 0.0, 0.0}, fnx[4] = {0.0, 0.0, 0.0, 0.0}, fny[4] = {0.0, 0.0, 0.0, 0.0};
+    auto load_operands = [&]() {
     if (it >= 4 && col_in_mem) {
       const int64_t o = (int64_t)row * a.pitch + c;
 #pragma unroll
@@ -132,11 +143,17 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
 #pragma unroll
       for (int q = 0; q < 4; ++q) fny[q] = __ldg(a.fy + q * a.fy_stride + o);
     }
+    };
+#if !LF_TP_LATELOAD
+    load_operands();
+#endif
     // -- W(r) (solver.cpp:145-163)
     double w[4] = {1.0, 0.0, 0.0, 1.0};
     if (col_in_mem) {
-      prim_fast(cur[0], cur[1], cur[2], cur[3], a.gm1, w);
-      if ((!(cur[0] > 0.0) || !(w[3] > 0.0)) && col_interior && r >= 0 && r < a.ny) fail = 1;
+      bool okw = true;
+      prim_fast(cur[0], cur[1], cur[2], cur[3], a.gm1, w, okw);
+      if ((!(cur[0] > 0.0) || !(w[3] > 0.0) || !okw) && col_interior && r >= 0 && r < a.ny)
+        fail = 1;
     }
     // -- y: traces of row r-1, face (r-2 | r-1); x: traces of row r-2 (shuffles)
     double ylo[4], yhi[4], xlo[4], xhi[4], xm[4], xp[4];
@@ -151,16 +168,17 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     shfl_up4(xhi, xmh, 1);  // minus-side trace of x-face (lane-1 | lane)
     double fx[4], fy[4];
     bool okx = true, oky = true;
+    const bool need_x = it >= 4 && lane >= 2 && lane <= LANES - 2 && c <= a.nx;
+    const bool need_y = it >= 3 && lane >= 2 && lane <= LANES - 3 && col_interior;
     face_fast<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
     face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3], C,
                  fy, oky);
-    const bool need_x = it >= 4 && lane >= 2 && lane <= LANES - 2 && c <= a.nx;
-    const bool need_y = it >= 3 && lane >= 2 && lane <= LANES - 3 && col_interior;
-    if (need_x && !okx)
-      face_ref<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C.k, fx);
-    if (need_y && !oky)
-      face_ref<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3], C.k,
-                  fy);
+#if LF_TP_LATELOAD
+    load_operands();
+#endif
+    // a range-check failure (|values| beyond 2^+-960) hands the step to the
+    // stage-wise IEEE kernels
+    if ((need_x && !okx) || (need_y && !oky)) fail = 1;
     if (need_x && !traces_ok(xmh[0], xmh[3], xlo[0], xlo[3]) && c >= 0 && row >= 0 && row < a.ny)
       fail = 1;
     if (need_y && !traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && r - 1 >= 0 && r - 1 <= a.ny)
@@ -205,9 +223,8 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
         } else {
           bool ok = true;
           const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
-          double eint = v[3] - div1_fast(kin, v[0], ok);
-          if (!ok) eint = internal_energy(v[0], v[1], v[2], v[3]);
-          if (!(v[0] > 0.0) || !(eint > 0.0)) {
+          const double eint = v[3] - div1_fast(kin, v[0], ok);
+          if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
             fail = 1;
           } else {
             const unsigned long long kr = ~pos_bits(v[0]), ke = ~pos_bits(eint);
@@ -215,7 +232,8 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
             nmin_e = ke > nmin_e ? ke : nmin_e;
           }
           double rr;
-          if (rate_fast(v, C, rr)) {
+          bool okr = true;
+          if (rate_fast(v, C, rr, okr)) {
             if (rr == rr) {
               const unsigned long long b = pos_bits(rr);
               rate_key = b > rate_key ? b : rate_key;
@@ -223,6 +241,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
           } else {
             dtfail = 1;
           }
+          if (!okr) fail = 1;
           // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
           const int jg = row + a.y0g;
           if (c == 0)

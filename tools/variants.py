@@ -22,10 +22,11 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 
 # name -> (extra nvcc flags, LF_PATH_*)
 VARIANTS = {
-    "fused_pair0": ("-DLF_PAIR=0 -DLF_MINBLOCKS=2", 1),
-    "tp_mb4": ("-DLF_TP_MINBLOCKS=4", 3),
     "tp_mb3": ("-DLF_TP_MINBLOCKS=3", 3),
-    "tp_mb2": ("-DLF_TP_MINBLOCKS=2", 3),
+    "tp_mb4": ("-DLF_TP_MINBLOCKS=4", 3),
+    "tp_mb4_late": ("-DLF_TP_MINBLOCKS=4 -DLF_TP_LATELOAD=1", 3),
+    "tp_mb3_late": ("-DLF_TP_MINBLOCKS=3 -DLF_TP_LATELOAD=1", 3),
+    "fused_mb2": ("-DLF_MINBLOCKS=2", 1),
 }
 
 
