@@ -87,6 +87,21 @@ __device__ __forceinline__ void cell_traces(double qm, double q0, double qp, dou
   }
 }
 
+// Traces from the two one-sided differences a = q+ - q0, b = q0 - q- (the
+// caller shares them between neighbouring cells).
+template <bool MUSCL>
+__device__ __forceinline__ void traces_ab(double a, double b, double q0, double beta, double& lo,
+                                          double& hi) {
+  if (MUSCL) {
+    const double hs = 0.5 * sweby_fast(a, b, beta);
+    lo = q0 - hs;
+    hi = q0 + hs;
+  } else {
+    lo = q0;
+    hi = q0;
+  }
+}
+
 // Primitives (solver.cpp:153-157) with the fast reciprocal; ok &= range check.
 __device__ __forceinline__ void prim_fast(double r, double mx, double my, double e, double gm1,
                                           double w[4], bool& ok) {

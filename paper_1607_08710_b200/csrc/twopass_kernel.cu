@@ -156,13 +156,15 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
         fail = 1;
     }
     // -- y: traces of row r-1, face (r-2 | r-1); x: traces of row r-2 (shuffles)
-    double ylo[4], yhi[4], xlo[4], xhi[4], xm[4], xp[4];
-    shfl_up4(wm2, xm, 1);
+    double ylo[4], yhi[4], xlo[4], xhi[4], xp[4], da[4], db[4];
     shfl_down4(wm2, xp, 1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) da[q] = xp[q] - wm2[q];  // q(t+1) - q(t)
+    shfl_up4(da, db, 1);                                 // q(t) - q(t-1), lane t-1's a
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       cell_traces<MUSCL>(wm2[q], wm1[q], w[q], a.beta, ylo[q], yhi[q]);
-      cell_traces<MUSCL>(xm[q], wm2[q], xp[q], a.beta, xlo[q], xhi[q]);
+      traces_ab<MUSCL>(da[q], db[q], wm2[q], a.beta, xlo[q], xhi[q]);
     }
     double xmh[4];
     shfl_up4(xhi, xmh, 1);  // minus-side trace of x-face (lane-1 | lane)
