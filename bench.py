@@ -237,7 +237,8 @@ def run_ours(args):
     # dominant kernel: per-launch CUDA events around the fused step kernel
     try:
         kernel_ms, loop_ms, k_launches = solver.time_steps(max(5, min(args.steps, 20)), case.cfl)
-        kernel_name = "fused Heun step (lfb::k_fused_step)"
+        kernel_name = ("one-kernel Heun step (lfb::k_fused_step)" if args.path == "fused" else
+                       "two-pass Heun step (lfb::k_pass predictor + corrector, one launch pair)")
     except ValueError:  # stage-wise path: no single dominant kernel, use the whole step
         kernel_ms, loop_ms, k_launches = ms_max, ms_max, max(taken, 1)
         kernel_name = "whole stage-wise step (no fused kernel on this path)"

@@ -1,0 +1,164 @@
+// lagflux_b200.hpp -- C++ drop-in for lagflux::LagfluxSolver over the C ABI.
+//
+// Header-only adapter compiled inside the reference's C++ build: it takes and
+// returns the reference's own types (include/lagflux/solver.hpp:39-131) and
+// throws the reference's exception types with the reference's what() texts
+// (include/lagflux/error.hpp:9-64), so a caller swaps
+//
+//     lagflux::LagfluxSolver solver(g, bc, eos, params, threads);        // run.cpp:154
+// for
+//     lagflux::b200::LagfluxSolver solver(g, bc, eos, params, threads);
+//
+// and links liblagflux_b200.so.  Residency: the GPU keeps SolverState::field
+// between steps.  With auto_sync (the default) every heun_step copies the
+// interior back to state.field, exactly like the reference; a driver that only
+// reads the field at dumps calls set_auto_sync(false) and sync_to_host(state)
+// before each dump (one line in run.cpp's dump lambda) to avoid the copies.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "lagflux/error.hpp"
+#include "lagflux/solver.hpp"
+#include "lagflux_b200.h"
+
+namespace lagflux::b200 {
+
+class LagfluxSolver {
+ public:
+  LagfluxSolver(const CartesianGrid& g, const BoundaryCondition& bc, PerfectGasEos eos,
+                SchemeParams params, int threads = 1, const MaterialSet* materials = nullptr,
+                int device = 0)
+      : grid_(g), threads_(threads < 1 ? 1 : threads) {
+    // constructor checks of solver.cpp:66-69
+    if (g.nx < 1 || g.ny < 1) throw ConfigError("grid has no interior cells");
+    if (g.gx < 2 || (g.dim == 2 && g.gy < 2))
+      throw ConfigError("MUSCL stencils need at least two ghost layers");
+    validate_boundary(bc, g.dim);
+    if (materials != nullptr)
+      throw ConfigError("multimaterial transport is not available on the B200 path");
+    if (g.gx != 2 || g.gy != (g.dim == 2 ? 2 : 0))
+      throw ConfigError("the B200 path uses the reference's ghost width 2");
+    lf_desc d{};
+    d.dim = g.dim;
+    d.nx = g.nx;
+    d.ny = g.ny;
+    d.dx = g.dx;
+    d.dy = g.dy;
+    d.x0 = g.x0;
+    d.y0 = g.y0;
+    d.gamma = eos.gamma;
+    d.beta = params.limiter.beta;
+    d.spatial_order = params.spatial_order;
+    d.time_order = params.time_order;
+    d.bc[0] = kind(bc.x_low);
+    d.bc[1] = kind(bc.x_high);
+    d.bc[2] = kind(bc.y_low);
+    d.bc[3] = kind(bc.y_high);
+    const int rc = lf_create(&d, &device, 1, &h_);
+    if (rc) {
+      const std::string msg = error_text();
+      lf_destroy(h_);
+      h_ = nullptr;
+      throw ConfigError(msg);
+    }
+  }
+  ~LagfluxSolver() { lf_destroy(h_); }
+  LagfluxSolver(const LagfluxSolver&) = delete;
+  LagfluxSolver& operator=(const LagfluxSolver&) = delete;
+
+  // solver.cpp:482-487 -- `in`'s ghosts are not refilled on the host (the
+  // device fills its own copy); `out`'s interior receives the stage.
+  void euler_stage(CellField& in, double dt, CellField& out, std::int64_t step = -1) {
+    upload(in);
+    resident_ = nullptr;
+    check(lf_euler_stage(h_, dt, step));
+    download(out);
+  }
+
+  // solver.cpp:489-546
+  double heun_step(SolverState& state, const TimeControls& controls, double limit_time,
+                   MaterialCells* materials = nullptr) {
+    if (materials != nullptr)
+      throw ConfigError("multimaterial transport is not available on the B200 path");
+    if (resident_ != &state) {
+      upload(state.field);
+      resident_ = &state;
+    }
+    lf_step_out o{};
+    const int rc = lf_heun_step(h_, controls.cfl, state.time, limit_time, state.step,
+                                state.boundary_outflow.data(), &o);
+    if (rc) {
+      if (auto_sync_) download(state.field);  // a corrector failure leaves its output, as in the reference
+      check(rc);
+    }
+    state.time = o.time;
+    state.step = o.step;
+    state.diagnostics.push_back({o.step, o.time, o.dt, o.min_rho, o.min_p});
+    if (auto_sync_) download(state.field);
+    return o.dt;
+  }
+
+  // solver.cpp:434-480
+  double compute_dt(const CellField& field, const TimeControls& controls, double time,
+                    double limit_time) const {
+    upload(field);
+    resident_ = nullptr;
+    double dt = 0.0;
+    check(lf_compute_dt(h_, controls.cfl, time, limit_time, &dt));
+    return dt;
+  }
+
+  const CartesianGrid& grid() const { return grid_; }
+  int threads() const { return threads_; }
+
+  // residency control (see the header comment)
+  void set_auto_sync(bool on) { auto_sync_ = on; }
+  void sync_to_host(SolverState& state) const {
+    if (resident_ != &state) throw Error("state is not resident on this solver");
+    download(state.field);
+  }
+  lf_handle* handle() const { return h_; }
+
+ private:
+  static int kind(BcKind k) {
+    return k == BcKind::reflective ? LF_REFLECTIVE
+                                   : (k == BcKind::periodic ? LF_PERIODIC : LF_TRANSMISSIVE);
+  }
+  std::string error_text() const {
+    lf_error e{};
+    lf_last_error(h_, &e);
+    return e.message;
+  }
+  void check(int rc) const {
+    if (!rc) return;
+    lf_error e{};
+    lf_last_error(h_, &e);
+    switch (e.kind) {
+      case LF_ERR_POSITIVITY: throw PositivityError(e.message, e.i, e.j, e.step, e.dt);
+      case LF_ERR_CONFIG: throw ConfigError(e.message);
+      case LF_ERR_DT_STATE:
+      case LF_ERR_PRIMITIVE:
+      case LF_ERR_TRACE: throw InvalidStateError(e.message);
+      default: throw Error(e.message);
+    }
+  }
+  void upload(const CellField& f) const {
+    double* p[4] = {const_cast<double*>(f.comp[0].data()), const_cast<double*>(f.comp[1].data()),
+                    const_cast<double*>(f.comp[2].data()), const_cast<double*>(f.comp[3].data())};
+    check(lf_upload(h_, p, grid_.nxt()));
+  }
+  void download(CellField& f) const {
+    double* p[4] = {f.comp[0].data(), f.comp[1].data(), f.comp[2].data(), f.comp[3].data()};
+    check(lf_download(h_, p, grid_.nxt(), 0));
+  }
+
+  CartesianGrid grid_;
+  int threads_;
+  lf_handle* h_ = nullptr;
+  mutable const SolverState* resident_ = nullptr;
+  bool auto_sync_ = true;
+};
+
+}  // namespace lagflux::b200

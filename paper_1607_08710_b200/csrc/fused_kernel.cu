@@ -491,7 +491,9 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
                            StepRec* rec, const double* __restrict__ bnd, double* outflow,
                            int nx, int nyg, double dx, double dy, double cfl, double limit,
                            double t_final) {
+  constexpr int TILE = 512;
   __shared__ double sums[8];
+  __shared__ double dif[8][TILE];
   const int tid = threadIdx.x;
   const StepCtl c = *ctl;
   const bool skip = c.done != 0;
@@ -502,20 +504,33 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
     if (c.time + dt > limit) dt = limit - c.time;
   }
   const bool failed = !skip && (acc->fail != 0 || c.dtfail || !(dt > 0.0));
-  if (!skip && !failed && tid < 8) {
-    // solver.cpp:412-430: per component, right - left over rows in order; then top - bottom
-    const int q = tid & 3;
+  if (!skip && !failed) {
+    // solver.cpp:412-430: per component, s += (right - left) over the rows in
+    // order, then s += (top - bottom) over the columns in order.  The
+    // differences are independent (all threads, one tile at a time); only the
+    // accumulation is sequential (one thread per component and direction).
     double s = 0.0;
-    if (tid < 4) {
-      const double* l = bnd + (int64_t)q * nyg;
-      const double* r = bnd + 4 * (int64_t)nyg + (int64_t)q * nyg;
-      for (int jj = 0; jj < nyg; ++jj) s += r[jj] - l[jj];
-    } else {
-      const double* b = bnd + 8 * (int64_t)nyg + (int64_t)q * nx;
-      const double* tp = bnd + 8 * (int64_t)nyg + 4 * (int64_t)nx + (int64_t)q * nx;
-      for (int ii = 0; ii < nx; ++ii) s += tp[ii] - b[ii];
+    const int nmax = nyg > nx ? nyg : nx;
+    for (int base = 0; base < nmax; base += TILE) {
+      for (int k = tid; k < 8 * TILE; k += blockDim.x) {
+        const int ch = k / TILE, e = base + k % TILE, q = ch & 3;
+        double d = 0.0;
+        if (ch < 4 && e < nyg)
+          d = bnd[4 * (int64_t)nyg + (int64_t)q * nyg + e] - bnd[(int64_t)q * nyg + e];
+        else if (ch >= 4 && e < nx)
+          d = bnd[8 * (int64_t)nyg + 4 * (int64_t)nx + (int64_t)q * nx + e] -
+              bnd[8 * (int64_t)nyg + (int64_t)q * nx + e];
+        dif[ch][k % TILE] = d;
+      }
+      __syncthreads();
+      if (tid < 8) {
+        const int n = (tid < 4 ? nyg : nx) - base;
+        const int m = n < TILE ? n : TILE;
+        for (int e = 0; e < m; ++e) s += dif[tid][e];
+      }
+      __syncthreads();
     }
-    sums[tid] = s;
+    if (tid < 8) sums[tid] = s;
   }
   __syncthreads();
   if (tid != 0) return;
@@ -597,7 +612,7 @@ void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* re
                      const double* bnd, double* outflow, int nx, int nyg, double dx, double dy,
                      double cfl, double limit, double t_final, cudaStream_t st) {
   count_launch();
-  k_finalize<<<1, 32, 0, st>>>(ctl, acc, nxt, rec, bnd, outflow, nx, nyg, dx, dy, cfl, limit,
+  k_finalize<<<1, 256, 0, st>>>(ctl, acc, nxt, rec, bnd, outflow, nx, nyg, dx, dy, cfl, limit,
                                t_final);
 }
 

@@ -1,0 +1,154 @@
+// dropin_check.cpp -- the reference's own LagfluxSolver next to the drop-in
+// lagflux::b200::LagfluxSolver (include/lagflux_b200.hpp), through the
+// reference's C++ types only.
+//
+// Built by oracle/Makefile together with the reference sources (so the binary
+// lands in oracle/_ref/, git-ignored) and run by tests/test_gpu_dropin.py on
+// the GPU box.  Exit status 0 iff every field value (==), dt, diagnostic,
+// boundary outflow and error text agrees.
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "lagflux/error.hpp"
+#include "lagflux/solver.hpp"
+#include "lagflux_b200.hpp"
+
+using namespace lagflux;
+
+namespace {
+
+int failures = 0;
+
+void expect(bool ok, const std::string& what) {
+  if (!ok) {
+    ++failures;
+    std::printf("MISMATCH: %s\n", what.c_str());
+  }
+}
+
+bool same_interior(const CartesianGrid& g, const CellField& a, const CellField& b) {
+  for (int c = 0; c < 4; ++c)
+    for (int j = g.gy; j < g.gy + g.ny; ++j)
+      for (int i = g.gx; i < g.gx + g.nx; ++i)
+        if (!(a.comp[c][g.idx(i, j)] == b.comp[c][g.idx(i, j)])) return false;
+  return true;
+}
+
+CellField smooth_field(const CartesianGrid& g, PerfectGasEos eos) {
+  constexpr double two_pi = 6.283185307179586476925286766559;
+  CellField f(g);
+  for (int j = g.gy; j < g.gy + g.ny; ++j)
+    for (int i = g.gx; i < g.gx + g.nx; ++i) {
+      const double x = g.xc(i), y = g.yc(j);
+      PrimitiveState w;
+      w.rho = 1.0 + 0.3 * std::sin(two_pi * x) * std::sin(two_pi * y);
+      w.u = 0.2 * std::cos(two_pi * x);
+      w.v = -0.3 * std::sin(two_pi * y);
+      w.p = 1.0 + 0.2 * std::cos(two_pi * x) * std::cos(two_pi * y);
+      f.set_state(g, i, j, conserved_from_primitive(w, eos));
+    }
+  return f;
+}
+
+CellField sod_field(const CartesianGrid& g, PerfectGasEos eos) {
+  CellField f(g);
+  for (int j = g.gy; j < g.gy + g.ny; ++j)
+    for (int i = g.gx; i < g.gx + g.nx; ++i) {
+      const PrimitiveState w = g.xc(i) < 0.5 ? PrimitiveState{1.0, 0.0, 0.0, 1.0}
+                                             : PrimitiveState{0.125, 0.0, 0.0, 0.1};
+      f.set_state(g, i, j, conserved_from_primitive(w, eos));
+    }
+  return f;
+}
+
+void run_pair(const char* name, const CartesianGrid& g, const BoundaryCondition& bc,
+              CellField f0, int steps, double cfl, double limit, bool auto_sync) {
+  const PerfectGasEos eos{1.4};
+  const SchemeParams params{};
+  const TimeControls controls{cfl, limit, 1 << 30};
+  LagfluxSolver ref(g, bc, eos, params, 1);
+  b200::LagfluxSolver gpu(g, bc, eos, params, 1);
+  gpu.set_auto_sync(auto_sync);
+  SolverState a, b;
+  a.field = f0;
+  b.field = f0;
+  for (int s = 0; s < steps && a.time < limit; ++s) {
+    const double da = ref.heun_step(a, controls, limit);
+    const double db = gpu.heun_step(b, controls, limit);
+    if (da != db) {
+      expect(false, std::string(name) + ": dt of step " + std::to_string(s));
+      return;
+    }
+  }
+  if (!auto_sync) gpu.sync_to_host(b);
+  expect(same_interior(g, a.field, b.field), std::string(name) + ": final field");
+  expect(a.time == b.time && a.step == b.step, std::string(name) + ": time / step");
+  expect(a.diagnostics.size() == b.diagnostics.size(), std::string(name) + ": diagnostics count");
+  for (size_t k = 0; k < a.diagnostics.size() && k < b.diagnostics.size(); ++k) {
+    const StepDiagnostics &x = a.diagnostics[k], &y = b.diagnostics[k];
+    if (!(x.dt == y.dt && x.time == y.time && x.min_rho == y.min_rho && x.min_p == y.min_p &&
+          x.step == y.step)) {
+      expect(false, std::string(name) + ": diagnostics " + std::to_string(k));
+      break;
+    }
+  }
+  for (int c = 0; c < 4; ++c)
+    expect(a.boundary_outflow[size_t(c)] == b.boundary_outflow[size_t(c)],
+           std::string(name) + ": boundary outflow");
+  std::printf("%s: %zu steps compared\n", name, a.diagnostics.size());
+}
+
+}  // namespace
+
+int main() {
+  const PerfectGasEos eos{1.4};
+  {
+    const CartesianGrid g = make_grid_2d(64, 48, 0.0, 1.0, 0.0, 0.75);
+    run_pair("smooth-periodic", g, {BcKind::periodic, BcKind::periodic, BcKind::periodic, BcKind::periodic},
+             smooth_field(g, eos), 40, 0.5, 1e30, true);
+    run_pair("smooth-periodic-resident", g,
+             {BcKind::periodic, BcKind::periodic, BcKind::periodic, BcKind::periodic},
+             smooth_field(g, eos), 40, 0.5, 1e30, false);
+  }
+  {
+    const CartesianGrid g = make_grid_2d(400, 4, 0.0, 1.0, 0.0, 1.0);
+    run_pair("sod-reflective", g, {BcKind::reflective, BcKind::reflective, BcKind::reflective, BcKind::reflective},
+             sod_field(g, eos), 1000, 0.5, 0.2, true);
+  }
+  {
+    const CartesianGrid g = make_grid_2d(50, 30, 0.0, 1.0, 0.0, 0.6);
+    run_pair("mixed-bc", g, {BcKind::reflective, BcKind::transmissive, BcKind::periodic, BcKind::periodic},
+             smooth_field(g, eos), 30, 0.45, 1e30, true);
+  }
+  {
+    // compute_dt, euler_stage and the PositivityError text (test_solver.cpp:161-180, 371-384)
+    const CartesianGrid g = make_grid_1d(50, 0.0, 1.0);
+    LagfluxSolver ref(g, BoundaryCondition{}, eos, SchemeParams{}, 1);
+    b200::LagfluxSolver gpu(g, BoundaryCondition{}, eos, SchemeParams{}, 1);
+    CellField f = sod_field(g, eos);
+    const TimeControls controls{0.25, 10.0, 1000};
+    expect(ref.compute_dt(f, controls, 0.0, 10.0) == gpu.compute_dt(f, controls, 0.0, 10.0), "compute_dt");
+    CellField oa(g), ob(g), fa = f, fb = f;
+    ref.euler_stage(fa, 8e-4, oa);
+    gpu.euler_stage(fb, 8e-4, ob);
+    expect(same_interior(g, oa, ob), "euler_stage");
+    std::string ea, eb;
+    try {
+      CellField x = f;
+      ref.euler_stage(x, 10.0, oa, 7);
+    } catch (const PositivityError& e) {
+      ea = e.what();
+    }
+    try {
+      CellField x = f;
+      gpu.euler_stage(x, 10.0, ob, 7);
+    } catch (const PositivityError& e) {
+      eb = e.what();
+    }
+    expect(!ea.empty() && ea == eb, "PositivityError text: '" + ea + "' vs '" + eb + "'");
+  }
+  std::printf("%s (%d mismatches)\n", failures ? "FAIL" : "OK", failures);
+  return failures ? 1 : 0;
+}
