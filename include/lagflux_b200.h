@@ -109,6 +109,9 @@ void lf_destroy(lf_handle* h);
 
 /* Rows [row0, row0 + nrows) of this handle's slab, as global rows. */
 int lf_local_rows(lf_handle* h, int* row0, int* nrows);
+/* The y-slab partition used by lf_create / lf_create_dist (host only, no GPU):
+ * rank's first global row and row count for ny rows over nranks slabs. */
+int lf_slab_partition(int ny, int nranks, int rank, int* row0, int* nrows);
 
 /* Host <-> device field transfer in the reference's ghosted layout:
  * component c of cell (i, j) (total indices, ghosts included) at field[c][j*ld + i],
@@ -150,6 +153,10 @@ int lf_launch_count(lf_handle* h, int64_t* launches);
 /* One scalar per interior cell: the CFL rate field is not kept; this returns the
  * max rate of the current state (diagnostic for tests). */
 int lf_max_rate(lf_handle* h, double* rate);
+/* Device self-check of the exact fast-path division / sqrt / limiter on n random
+ * operands (csrc/selftest.cu).  counts[7] = {tested, div valid, div mismatches,
+ * shared-reciprocal mismatches, sqrt valid, sqrt mismatches, limiter mismatches}. */
+int lf_selftest_fastmath(int64_t n, uint64_t seed, int64_t* counts);
 
 #ifdef __cplusplus
 }

@@ -866,3 +866,9 @@ extern "C" int lf_launch_count(lf_handle* h, int64_t* launches) {
   *launches = lfb::launch_count();
   return 0;
 }
+
+extern "C" int lf_slab_partition(int ny, int nranks, int rank, int* row0, int* nrows) {
+  if (!row0 || !nrows || nranks < 1 || rank < 0 || rank >= nranks || ny < 1) return LF_ERR_ARGUMENT;
+  slab_rows(ny, nranks, rank, row0, nrows);
+  return LF_OK;
+}

@@ -1,0 +1,102 @@
+// selftest.cu -- device self-check of fastmath.cuh against the IEEE operators.
+//
+// lf_selftest_fastmath draws n operand pairs (splitmix64 bit patterns over the
+// whole finite range, half of them concentrated in the physical range) and
+// counts, for the division (with and without a shared reciprocal), the square
+// root and the Sweby limiter, how often the fast path claims validity and how
+// often a valid fast result differs from the IEEE / reference result.
+// tests/test_gpu_fastmath.py requires zero differences.
+#include <cuda_runtime.h>
+
+#include "../../include/lagflux_b200.h"
+#include "fastmath.cuh"
+#include "kernels.h"
+#include "lagflux_device.cuh"
+
+namespace lfb {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long& s) {
+  unsigned long long z = (s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// finite double: either any exponent (raw bits) or a physical-range magnitude
+__device__ __forceinline__ double draw(unsigned long long& s, bool wide) {
+  const unsigned long long r = splitmix(s);
+  if (wide) {
+    unsigned long long b = r;
+    const unsigned long long e = (b >> 52) & 0x7ff;
+    if (e == 0x7ff) b ^= 0x4000000000000000ull;  // no inf / nan
+    return __longlong_as_double((long long)b);
+  }
+  // mantissa random, exponent in [-40, 40]
+  const unsigned long long mant = r & 0x000fffffffffffffull;
+  const long long e = (long long)((r >> 52) % 81) - 40 + 1023;
+  const unsigned long long sign = r & 0x8000000000000000ull;
+  return __longlong_as_double((long long)(sign | ((unsigned long long)e << 52) | mant));
+}
+
+__device__ __forceinline__ bool same(double x, double y) {
+  return x == y || (x != x && y != y);
+}
+
+__global__ void k_selftest(long long n, unsigned long long seed, unsigned long long* out) {
+  unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long s = seed ^ (unsigned long long)i * 0x632be59bd9b4e019ull;
+    const bool wide = (i & 1) != 0;
+    const double a = draw(s, wide);
+    double b = draw(s, wide);
+    if (b == 0.0) b = 1.0;
+    const double a2 = draw(s, false);
+    c[0] += 1;
+    // division a / b, and a second quotient a2 / b through the same reciprocal
+    bool ok = true;
+    const Recip r = recip_of(b);
+    const double q = div_fast(a, r, ok);
+    if (ok) {
+      c[1] += 1;
+      if (!same(q, a / b)) c[2] += 1;
+    }
+    bool ok2 = true;
+    const double q2 = div_fast(a2, r, ok2);
+    if (ok2 && !same(q2, a2 / b)) c[3] += 1;
+    // square root of |a|
+    const double x = fabs(a);
+    bool oks = true;
+    const double sq = sqrt_fast(x, oks);
+    if (oks) {
+      c[4] += 1;
+      if (!same(sq, sqrt(x))) c[5] += 1;
+    }
+    // limiter against the reference formula (reconstruct.hpp:24-30)
+    const double beta = 1.0 + (double)(splitmix(s) >> 11) * 0x1.0p-53;
+    const double la = draw(s, false), lb = draw(s, false);
+    if (!same(sweby_fast(la, lb, beta), sweby(la, lb, beta))) c[6] += 1;
+  }
+  for (int k = 0; k < 7; ++k) atomicAdd(&out[k], c[k]);
+}
+
+}  // namespace
+
+}  // namespace lfb
+
+extern "C" int lf_selftest_fastmath(int64_t n, uint64_t seed, int64_t* counts) {
+  if (!counts || n < 0) return LF_ERR_ARGUMENT;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 8 * sizeof(unsigned long long)) != cudaSuccess) return LF_ERR_DEVICE;
+  cudaMemset(d, 0, 8 * sizeof(unsigned long long));
+  lfb::count_launch();
+  lfb::k_selftest<<<148 * 8, 256>>>((long long)n, (unsigned long long)seed, d);
+  unsigned long long h[8];
+  const cudaError_t e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return LF_ERR_DEVICE;
+  for (int k = 0; k < 7; ++k) counts[k] = (int64_t)h[k];
+  return LF_OK;
+}
