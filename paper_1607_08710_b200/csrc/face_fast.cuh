@@ -35,11 +35,12 @@ __device__ __forceinline__ FK make_fk(double gamma, double gm1, double beta, dou
 }
 
 // Lagrange-flux face flux (riemann_hll.hpp:29-39, solver.cpp:26-43) on the fast
-// paths.  ok &= every range check.
+// paths, for u* != 0; ok &= every range check.  When needs_mean(us_out) the
+// caller replaces f with face_mean (the reference's mean-state branch).
 template <int AXIS>
 __device__ __forceinline__ void face_fast(double m0, double m1, double m2, double m3, double p0,
                                           double p1, double p2, double p3, const FK& c,
-                                          double f[4], bool& ok) {
+                                          double f[4], bool& ok, double& ps_out, double& us_out) {
   const double ul = AXIS == 0 ? m1 : m2;
   const double ur = AXIS == 0 ? p1 : p2;
   const double cl = sqrt_fast(div1_fast(c.gamma * m3, m0, ok), ok);
@@ -49,23 +50,35 @@ __device__ __forceinline__ void face_fast(double m0, double m1, double m2, doubl
   const Recip rs = recip_of(rho_sum);
   const double ps = div_fast(p0 * m3 + m0 * p3, rs, ok) - div_fast(m0 * p0, rs, ok) * cmax * (ur - ul);
   const double us = div_fast(m0 * ul + p0 * ur, rs, ok) - div1_fast(p3 - m3, cmax * rho_sum, ok);
+  // upwind side, branch-free (u* > 0: minus trace, else plus trace); the mean
+  // state of u* == 0 is patched afterwards by face_mean (rare), so the main
+  // path stays one straight line the compiler can interleave with other faces
   const bool pos = us > 0.0;
-  double a0, a1, a2, a3;
-  if (pos || us < 0.0) {
-    const double s0 = pos ? m0 : p0, s1 = pos ? m1 : p1, s2 = pos ? m2 : p2, s3 = pos ? m3 : p3;
-    a0 = s0;
-    a1 = s0 * s1;
-    a2 = s0 * s2;
-    a3 = div_fast(s3, c.rgm1, ok) + 0.5 * s0 * (s1 * s1 + s2 * s2);
-  } else {
-    // u* == 0 (or NaN): the mean of the two conserved traces (solver.cpp:33-35)
-    const double m3c = div_fast(m3, c.rgm1, ok) + 0.5 * m0 * (m1 * m1 + m2 * m2);
-    const double p3c = div_fast(p3, c.rgm1, ok) + 0.5 * p0 * (p1 * p1 + p2 * p2);
-    a0 = 0.5 * (m0 + p0);
-    a1 = 0.5 * (m0 * m1 + p0 * p1);
-    a2 = 0.5 * (m0 * m2 + p0 * p2);
-    a3 = 0.5 * (m3c + p3c);
-  }
+  const double s0 = pos ? m0 : p0, s1 = pos ? m1 : p1, s2 = pos ? m2 : p2, s3 = pos ? m3 : p3;
+  const double a1 = s0 * s1, a2 = s0 * s2;
+  const double a3 = div_fast(s3, c.rgm1, ok) + 0.5 * s0 * (s1 * s1 + s2 * s2);
+  f[0] = s0 * us;
+  f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
+  f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
+  f[3] = a3 * us + ps * us;
+  ps_out = ps;
+  us_out = us;
+}
+
+__device__ __forceinline__ bool needs_mean(double us) { return !(us > 0.0 || us < 0.0); }
+
+// u* == 0 (or NaN): the flux from the mean of the two conserved traces
+// (solver.cpp:33-41), given the face's p* and u*.
+template <int AXIS>
+__device__ __forceinline__ void face_mean(double m0, double m1, double m2, double m3, double p0,
+                                          double p1, double p2, double p3, double ps, double us,
+                                          const FK& c, double f[4], bool& ok) {
+  const double m3c = div_fast(m3, c.rgm1, ok) + 0.5 * m0 * (m1 * m1 + m2 * m2);
+  const double p3c = div_fast(p3, c.rgm1, ok) + 0.5 * p0 * (p1 * p1 + p2 * p2);
+  const double a0 = 0.5 * (m0 + p0);
+  const double a1 = 0.5 * (m0 * m1 + p0 * p1);
+  const double a2 = 0.5 * (m0 * m2 + p0 * p2);
+  const double a3 = 0.5 * (m3c + p3c);
   f[0] = a0 * us;
   f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
   f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;

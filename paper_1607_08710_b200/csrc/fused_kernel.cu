@@ -214,9 +214,17 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         for (int q = 0; q < 4; ++q) mx[q] = dox ? sTx[q * NC + tm] : xlo[q];
         double fx[4];
         bool okx = true, oky = true;
-        face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
+        double psx, usx, psy, usy;
+        face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx, psx,
+                     usx);
         face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
-                     C, fy, oky);
+                     C, fy, oky, psy, usy);
+        if (needs_mean(usx))
+          face_mean<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], psx, usx, C,
+                       fx, okx);
+        if (needs_mean(usy))
+          face_mean<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2],
+                       ylo[3], psy, usy, C, fy, oky);
         // a range-check failure on a consumed face hands the step to the
         // stage-wise IEEE kernels (halo lanes and columns past the grid hold
         // dummy states and never count)
@@ -380,9 +388,17 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         for (int q = 0; q < 4; ++q) mx[q] = dx_ ? sTc[q * NC + tm] : xlo[q];
         double fx[4], fs[4];
         bool okx = true, oky = true;
-        face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
+        double psx, usx, psy, usy;
+        face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx, psx,
+                     usx);
         face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
-                     C, fs, oky);
+                     C, fs, oky, psy, usy);
+        if (needs_mean(usx))
+          face_mean<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], psx, usx, C,
+                       fx, okx);
+        if (needs_mean(usy))
+          face_mean<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2],
+                       ylo[3], psy, usy, C, fs, oky);
         if ((dx_ && !okx) || (k >= 8 && !oky && t >= 4 && t <= NC - 5 && col_interior)) fail = 1;
         if (dx_) {
           if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && j >= 0 &&

@@ -172,9 +172,17 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     bool okx = true, oky = true;
     const bool need_x = it >= 4 && lane >= 2 && lane <= LANES - 2 && c <= a.nx;
     const bool need_y = it >= 3 && lane >= 2 && lane <= LANES - 3 && col_interior;
-    face_fast<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx);
+    double psx, usx, psy, usy;
+    face_fast<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx, psx,
+                 usx);
     face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3], C,
-                 fy, oky);
+                 fy, oky, psy, usy);
+    if (needs_mean(usx))
+      face_mean<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], psx, usx, C,
+                   fx, okx);
+    if (needs_mean(usy))
+      face_mean<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
+                   psy, usy, C, fy, oky);
 #if LF_TP_LATELOAD
     load_operands();
 #endif

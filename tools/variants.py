@@ -23,9 +23,9 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # name -> (extra nvcc flags, LF_PATH_*)
 VARIANTS = {
     "tp_mb3": ("-DLF_TP_MINBLOCKS=3", 3),
+    "tp_mb3_u2": ("-DLF_TP_MINBLOCKS=3 -DLF_TP_UNROLL=2", 3),
+    "tp_mb2_u2": ("-DLF_TP_MINBLOCKS=2 -DLF_TP_UNROLL=2", 3),
     "tp_mb4": ("-DLF_TP_MINBLOCKS=4", 3),
-    "tp_mb4_late": ("-DLF_TP_MINBLOCKS=4 -DLF_TP_LATELOAD=1", 3),
-    "tp_mb3_late": ("-DLF_TP_MINBLOCKS=3 -DLF_TP_LATELOAD=1", 3),
     "fused_mb2": ("-DLF_MINBLOCKS=2", 1),
 }
 
@@ -54,7 +54,8 @@ def run(n=8192, steps=10):
     g = case.grid
     ref = None
     results = {}
-    for name in VARIANTS:
+    names = ["base_tp"] + list(VARIANTS) if os.path.exists(os.path.join(OUT, "base_tp.so")) else list(VARIANTS)
+    for name in names:
         so = os.path.join(OUT, f"{name}.so")
         if not os.path.exists(so):
             continue
@@ -65,7 +66,7 @@ def run(n=8192, steps=10):
         desc = make_desc(g, case.bc, case.gamma, case.params)
         h = C.c_void_p()
         assert lib.lf_create(C.byref(desc), (C.c_int * 1)(0), 1, C.byref(h)) == 0
-        assert lib.lf_set_path(h, VARIANTS[name][1]) == 0
+        assert lib.lf_set_path(h, VARIANTS[name][1] if name in VARIANTS else 3) == 0
         assert lib.lf_init_fourier(h, case.seed) == 0
         km, lm, nl = C.c_double(), C.c_double(), C.c_int()
         assert lib.lf_time_steps(h, 3, case.cfl, C.byref(km), C.byref(lm), C.byref(nl)) == 0
