@@ -157,6 +157,12 @@ int lf_max_rate(lf_handle* h, double* rate);
  * operands (csrc/selftest.cu).  counts[7] = {tested, div valid, div mismatches,
  * shared-reciprocal mismatches, sqrt valid, sqrt mismatches, limiter mismatches}. */
 int lf_selftest_fastmath(int64_t n, uint64_t seed, int64_t* counts);
+/* Device self-check of the cell box (csrc/face_fast.cuh): n random faces whose
+ * four stencil cells lie in the box, extremes and one-ulp neighbours
+ * over-represented; every division / square root of the face solves and of the
+ * primitives must pass its fast-path range check.  counts[2] = {faces solved,
+ * faces with a failed range check}. */
+int lf_selftest_box(int64_t n, uint64_t seed, int64_t* counts);
 
 #ifdef __cplusplus
 }

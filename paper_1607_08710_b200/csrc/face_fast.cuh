@@ -115,6 +115,37 @@ __device__ __forceinline__ void traces_ab(double a, double b, double q0, double 
   }
 }
 
+// The cell box.  If every cell feeding a face has rho, p in [2^-100, 2^100) and
+// |u|, |v| in {0} u [2^-500, 2^100), every division and square root of the face
+// (face_fast / face_mean) is on its fast path, so the kernels test the box once
+// per cell instead of range-checking each operation:
+//   * traces: rho0 - hs > 0 is either >= rho0/2 or, by Sterbenz, an exact
+//     difference of two values >= 2^-101, hence >= 2^-153; all traces are below
+//     2^101; a velocity trace is 0 or >= 2^-605 (the same argument one level down);
+//   * dividends: rho_L u_L + rho_R u_R is 0 or >= 2^-810, p_R - p_L is 0 or
+//     >= 2^-205, every other dividend is a product of traces >= 2^-306;
+//   * divisors rho_L + rho_R, cmax (rho_L + rho_R), rho, gamma - 1 lie in
+//     [2^-280, 2^233], so every quotient is in [2^-913, 2^400] -- normal, where
+//     the fast path is exact (fastmath.cuh; gamma - 1 in [2^-14, 2^6) is checked
+//     by const_in_box).
+// A cell outside the box raises the failure flag: the stage-wise IEEE kernels
+// then compute the step exactly (never for physical data).
+__device__ __forceinline__ bool pos_in_box(double x) {
+  // hi word of 2^-100 = 0x39b00000, of 2^100 = 0x46300000
+  return ((unsigned)__double2hiint(x) - 0x39b00000u) < (0x46300000u - 0x39b00000u);
+}
+__device__ __forceinline__ bool vel_in_box(double x) {
+  // |x| in [2^-500 (hi 0x20b00000), 2^100) or x == +-0
+  const unsigned h = (unsigned)__double2hiint(x) & 0x7fffffffu;
+  return (h - 0x20b00000u) < (0x46300000u - 0x20b00000u) || (h | (unsigned)__double2loint(x)) == 0u;
+}
+__device__ __forceinline__ bool cell_in_box(const double w[4]) {
+  return pos_in_box(w[0]) && pos_in_box(w[3]) && vel_in_box(w[1]) && vel_in_box(w[2]);
+}
+__device__ __forceinline__ bool const_in_box(double gamma, double gm1) {
+  return gm1 >= 0x1p-14 && gm1 < 0x1p6 && gamma < 0x1p7;
+}
+
 // Primitives (solver.cpp:153-157) with the fast reciprocal; ok &= range check.
 __device__ __forceinline__ void prim_fast(double r, double mx, double my, double e, double gm1,
                                           double w[4], bool& ok) {

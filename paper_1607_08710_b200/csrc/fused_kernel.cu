@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
   }
   __syncthreads();
 
-  unsigned fail = 0;
+  unsigned fail = const_in_box(a.gamma, a.gm1) ? 0u : 1u;
 
   if (is_p) {
     // ================================================================ stage 1 (P)
@@ -180,10 +180,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         if (col_in_mem) {
           const double* u = sU + (k & (URING - 1)) * 4 * NC + t;
           const double r0 = u[0], m1 = u[NC], m2 = u[2 * NC], e3 = u[3 * NC];
-          bool okw = true;
+          bool okw = true;  // implied by the box
           prim_fast(r0, m1, m2, e3, a.gm1, w, okw);
-          if ((!(r0 > 0.0) || !(w[3] > 0.0) || !okw) && col_interior && r >= 0 && r < a.ny)
-            fail = 1;
+          if (!cell_in_box(w) && col_interior && r >= 0 && r < a.ny) fail = 1;
         }
         if (k >= 2) {
 #pragma unroll
@@ -213,7 +212,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 #pragma unroll
         for (int q = 0; q < 4; ++q) mx[q] = dox ? sTx[q * NC + tm] : xlo[q];
         double fx[4];
-        bool okx = true, oky = true;
+        bool okx = true, oky = true;  // implied by the cell box (face_fast.cuh): unused
         double psx, usx, psy, usy;
         face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx, psx,
                      usx);
@@ -225,10 +224,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         if (needs_mean(usy))
           face_mean<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2],
                        ylo[3], psy, usy, C, fy, oky);
-        // a range-check failure on a consumed face hands the step to the
+        // a trace-positivity failure on a consumed face hands the step to the
         // stage-wise IEEE kernels (halo lanes and columns past the grid hold
         // dummy states and never count)
-        if ((dox && !okx) || (k >= 3 && !oky && t >= 2 && t <= NC - 3 && col_in_mem)) fail = 1;
         if (dox) {
           if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && r - 2 >= 0 &&
               r - 2 < a.ny)
@@ -273,7 +271,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
           const double lhs = v[3] * v[0];
           if (!(v[0] > 0.0) || !(lhs > kin * (1.0 + 0x1p-48)) || !(lhs >= 0x1p-960)) fail = 1;
-          if (!(ws[3] > 0.0) || !okw) fail = 1;
+          if (!cell_in_box(ws)) fail = 1;
         }
       }
       if (p_active && k >= 3) {
@@ -387,7 +385,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 #pragma unroll
         for (int q = 0; q < 4; ++q) mx[q] = dx_ ? sTc[q * NC + tm] : xlo[q];
         double fx[4], fs[4];
-        bool okx = true, oky = true;
+        bool okx = true, oky = true;  // implied by the cell box (face_fast.cuh): unused
         double psx, usx, psy, usy;
         face_fast<0>(mx[0], mx[1], mx[2], mx[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx, psx,
                      usx);
@@ -399,7 +397,6 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         if (needs_mean(usy))
           face_mean<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2],
                        ylo[3], psy, usy, C, fs, oky);
-        if ((dx_ && !okx) || (k >= 8 && !oky && t >= 4 && t <= NC - 5 && col_interior)) fail = 1;
         if (dx_) {
           if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && j >= 0 &&
               j < a.ny)

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/lagflux_b200.h"
+#include "face_fast.cuh"
 #include "fastmath.cuh"
 #include "kernels.h"
 #include "lagflux_device.cuh"
@@ -82,9 +83,113 @@ __global__ void k_selftest(long long n, unsigned long long seed, unsigned long l
   for (int k = 0; k < 7; ++k) atomicAdd(&out[k], c[k]);
 }
 
+// ---- the cell box (face_fast.cuh) --------------------------------------
+// A value of the box drawn with its extremes over-represented: exponent at
+// either end of the range, all-zero or all-one mantissas, and (through
+// `near`) neighbours one ulp apart, the worst case of the cancellation bounds.
+__device__ __forceinline__ double box_mag(unsigned long long& s, int emin, int emax) {
+  const unsigned long long r = splitmix(s);
+  int e;
+  switch (r & 3) {
+    case 0: e = emin; break;
+    case 1: e = emax - 1; break;
+    default: e = emin + (int)((r >> 2) % (unsigned long long)(emax - emin));
+  }
+  unsigned long long mant = (r >> 12) & 0x000fffffffffffffull;
+  if (((r >> 8) & 7) == 0) mant = 0;
+  if (((r >> 8) & 7) == 1) mant = 0x000fffffffffffffull;
+  return __longlong_as_double((long long)(((unsigned long long)(e + 1023) << 52) | mant));
+}
+__device__ __forceinline__ double nudge(unsigned long long& s, double x) {
+  const unsigned long long r = splitmix(s);
+  const long long b = __double_as_longlong(x);
+  switch (r & 3) {
+    case 0: return __longlong_as_double(b + 1);
+    case 1: return __longlong_as_double(b - 1);
+    default: return x;
+  }
+}
+__device__ __forceinline__ void box_cell(unsigned long long& s, const double* prev, double w[4]) {
+  const unsigned long long r = splitmix(s);
+  const bool near = prev && (r & 1);
+  w[0] = near ? nudge(s, prev[0]) : box_mag(s, -100, 100);
+  w[3] = near ? nudge(s, prev[3]) : box_mag(s, -100, 100);
+  for (int q = 1; q <= 2; ++q) {
+    const unsigned long long k = splitmix(s);
+    if (near && (k & 1)) {
+      w[q] = prev[q] == 0.0 ? 0.0 : nudge(s, prev[q]);
+    } else if ((k & 7) == 2) {
+      w[q] = 0.0;
+    } else {
+      const double m = box_mag(s, -500, 100);
+      w[q] = (k & 8) ? -m : m;
+    }
+  }
+  // a nudge can step out of the box at its edges; the kernels would flag it
+  if (!cell_in_box(w)) {
+    w[0] = 1.0;
+    w[1] = 0.0;
+    w[2] = 0.0;
+    w[3] = 1.0;
+  }
+}
+
+// counts: {faces solved, faces with a failed range check}
+__global__ void k_selftest_box(long long n, unsigned long long seed, unsigned long long* out) {
+  unsigned long long c[2] = {0, 0};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long s = seed ^ (unsigned long long)i * 0x9e3779b97f4a7c15ull;
+    const double gm1 = box_mag(s, -14, 6);
+    const double gamma = 1.0 + gm1;
+    if (!const_in_box(gamma, gm1)) continue;
+    const double beta = 1.0 + (double)(splitmix(s) >> 11) * 0x1.0p-53;
+    const FK C = make_fk(gamma, gm1, beta, 1.0, 1.0);
+    // four cells along the face normal: i-1, i | i+1, i+2
+    double w[4][4];
+    for (int k = 0; k < 4; ++k) box_cell(s, k ? w[k - 1] : nullptr, w[k]);
+    double mh[4], pl[4];
+    for (int q = 0; q < 4; ++q) {
+      double lo, hi;
+      cell_traces<true>(w[0][q], w[1][q], w[2][q], beta, lo, hi);
+      mh[q] = hi;
+      cell_traces<true>(w[1][q], w[2][q], w[3][q], beta, lo, hi);
+      pl[q] = lo;
+    }
+    if (!traces_ok(mh[0], mh[3], pl[0], pl[3])) continue;  // the reference's own failure
+    bool ok0 = true, ok1 = true;
+    double f[4], ps, us;
+    face_fast<0>(mh[0], mh[1], mh[2], mh[3], pl[0], pl[1], pl[2], pl[3], C, f, ok0, ps, us);
+    face_mean<0>(mh[0], mh[1], mh[2], mh[3], pl[0], pl[1], pl[2], pl[3], ps, us, C, f, ok0);
+    face_fast<1>(mh[0], mh[1], mh[2], mh[3], pl[0], pl[1], pl[2], pl[3], C, f, ok1, ps, us);
+    face_mean<1>(mh[0], mh[1], mh[2], mh[3], pl[0], pl[1], pl[2], pl[3], ps, us, C, f, ok1);
+    bool okp = true;
+    double wp[4];
+    prim_fast(w[1][0], w[1][0] * w[1][1], w[1][0] * w[1][2], 1.0, gm1, wp, okp);
+    c[0] += 1;
+    if (!ok0 || !ok1 || !okp) c[1] += 1;
+  }
+  for (int k = 0; k < 2; ++k) atomicAdd(&out[k], c[k]);
+}
+
 }  // namespace
 
 }  // namespace lfb
+
+extern "C" int lf_selftest_box(int64_t n, uint64_t seed, int64_t* counts) {
+  if (!counts || n < 0) return LF_ERR_ARGUMENT;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 4 * sizeof(unsigned long long)) != cudaSuccess) return LF_ERR_DEVICE;
+  cudaMemset(d, 0, 4 * sizeof(unsigned long long));
+  lfb::count_launch();
+  lfb::k_selftest_box<<<148 * 8, 256>>>((long long)n, (unsigned long long)seed, d);
+  unsigned long long h[4];
+  const cudaError_t e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return LF_ERR_DEVICE;
+  for (int k = 0; k < 2; ++k) counts[k] = (int64_t)h[k];
+  return LF_OK;
+}
 
 extern "C" int lf_selftest_fastmath(int64_t n, uint64_t seed, int64_t* counts) {
   if (!counts || n < 0) return LF_ERR_ARGUMENT;

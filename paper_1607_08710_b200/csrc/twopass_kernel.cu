@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
   const bool store_fx = (lane >= 2 && lane <= LANES - 3 && c <= a.nx) || (lane == LANES - 2 && c == a.nx);
   const int nit = (y1 - y0) + 4;
 
-  unsigned fail = 0;
+  unsigned fail = const_in_box(a.gamma, a.gm1) ? 0u : 1u;
   unsigned long long rate_key = 0ull, nmin_r = NINF_KEY, nmin_e = NINF_KEY;
   unsigned dtfail = 0;
 
@@ -150,10 +150,9 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     // -- W(r) (solver.cpp:145-163)
     double w[4] = {1.0, 0.0, 0.0, 1.0};
     if (col_in_mem) {
-      bool okw = true;
+      bool okw = true;  // implied by the box
       prim_fast(cur[0], cur[1], cur[2], cur[3], a.gm1, w, okw);
-      if ((!(cur[0] > 0.0) || !(w[3] > 0.0) || !okw) && col_interior && r >= 0 && r < a.ny)
-        fail = 1;
+      if (!cell_in_box(w) && col_interior && r >= 0 && r < a.ny) fail = 1;
     }
     // -- y: traces of row r-1, face (r-2 | r-1); x: traces of row r-2 (shuffles)
     double ylo[4], yhi[4], xlo[4], xhi[4], xp[4], da[4], db[4];
@@ -169,7 +168,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     double xmh[4];
     shfl_up4(xhi, xmh, 1);  // minus-side trace of x-face (lane-1 | lane)
     double fx[4], fy[4];
-    bool okx = true, oky = true;
+    bool okx = true, oky = true;  // implied by the cell box (face_fast.cuh): unused
     const bool need_x = it >= 4 && lane >= 2 && lane <= LANES - 2 && c <= a.nx;
     const bool need_y = it >= 3 && lane >= 2 && lane <= LANES - 3 && col_interior;
     double psx, usx, psy, usy;
@@ -186,9 +185,6 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
 #if LF_TP_LATELOAD
     load_operands();
 #endif
-    // a range-check failure (|values| beyond 2^+-960) hands the step to the
-    // stage-wise IEEE kernels
-    if ((need_x && !okx) || (need_y && !oky)) fail = 1;
     if (need_x && !traces_ok(xmh[0], xmh[3], xlo[0], xlo[3]) && c >= 0 && row >= 0 && row < a.ny)
       fail = 1;
     if (need_y && !traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && r - 1 >= 0 && r - 1 <= a.ny)

@@ -19,3 +19,16 @@ def test_fast_division_sqrt_limiter_exact(cuda):
     assert div_bad == 0 and shared_bad == 0 and sqrt_bad == 0 and lim_bad == 0
     # the fast paths must cover the physical range (half the draws) and more
     assert div_ok > 0.5 * n and sqrt_ok > 0.5 * n
+
+
+def test_cell_box_implies_fast_path_validity(cuda):
+    """The kernels test one box per cell instead of range-checking every
+    division (face_fast.cuh): faces built from in-box cells -- box edges,
+    one-ulp neighbours and zero velocities over-represented -- never fail a
+    fast-path range check."""
+    counts = (C.c_int64 * 2)()
+    n = 1 << 26
+    assert N.lib().lf_selftest_box(n, 0x1607087101, counts) == 0
+    solved, failed = list(counts)
+    assert solved > n // 4
+    assert failed == 0

@@ -222,3 +222,45 @@ def test_download_fill_ghosts_matches_reference_fill(cuda):
                                 arr.ctypes.data_as(O.DP))
             ref[c] = arr
         assert_fields_equal(out, ref, str(bcs))
+
+
+def _box_cases():
+    """States outside the fast kernels' cell box (face_fast.cuh): each must take
+    the stage-wise IEEE re-run and still equal the oracle."""
+    base = CS.quadrant(48, 4)
+    f = CS.initial_field(base)
+    g = base.grid
+    tiny_u = f.copy()
+    tiny_u[1][g.gy + 10, g.gx + 5:g.gx + 9] = 1e-200 * tiny_u[0][g.gy + 10, g.gx + 5:g.gx + 9]
+    light = f.copy()
+    light[:, g.gy + 20:g.gy + 24, g.gx + 20:g.gx + 24] *= 1e-35   # rho, p ~ 1e-35 < 2^-100
+    near_iso = CS.Case("q", g, base.bc, 1.00001, base.params, base.cfl, base.t_final, 4,
+                       "quadrant")                                 # gamma - 1 < 2^-14
+    return {"tiny_velocity": (base, tiny_u), "light_region": (base, light),
+            "gamma_near_one": (near_iso, f)}
+
+
+@pytest.mark.parametrize("path", ["twopass", "fused"])
+@pytest.mark.parametrize("which", ["tiny_velocity", "light_region", "gamma_near_one"])
+def test_out_of_box_states_rerun_exactly(cuda, which, path):
+    case, field = _box_cases()[which]
+    ref, rdiag = run_oracle(case, 4, field=field)
+
+    def run(cs, fld):
+        s = LagfluxSolver(cs.grid, cs.bc, cs.gamma, cs.params, path=path)
+        state = G.SolverState(field=np.array(fld))
+        n0 = s.launch_count()   # process-wide counter
+        for _ in range(4):
+            s.heun_step(state, G.TimeControls(cs.cfl, cs.t_final), cs.t_final)
+        s.sync_to_host(state)
+        n = s.launch_count() - n0
+        s.close()
+        return state, n
+
+    state, n_out = run(case, field)
+    assert_fields_equal(case.grid.interior(state.field), case.grid.interior(ref.field), which)
+    assert np.array_equal(diag_array(state)[:, :4], rdiag[:, :4])
+    # the fast kernel flagged every step and the stage-wise kernels recomputed it
+    inbox = CS.quadrant(48, 4)
+    _, n_in = run(inbox, CS.initial_field(inbox))
+    assert n_out > n_in

@@ -20,24 +20,39 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "tools", "_variants")
 CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 
-# name -> (extra nvcc flags, LF_PATH_*)
+# name -> (extra nvcc flags, LF_PATH_*); "base_*" variants build the same path
+# from the committed sources (git HEAD) for an A/B against the working tree
 VARIANTS = {
-    "tp_mb3": ("-DLF_TP_MINBLOCKS=3", 3),
-    "tp_mb3_u2": ("-DLF_TP_MINBLOCKS=3 -DLF_TP_UNROLL=2", 3),
-    "tp_mb2_u2": ("-DLF_TP_MINBLOCKS=2 -DLF_TP_UNROLL=2", 3),
-    "tp_mb4": ("-DLF_TP_MINBLOCKS=4", 3),
-    "fused_mb2": ("-DLF_MINBLOCKS=2", 1),
+    "base_fused": ("", 1),
+    "fused": ("", 1),
+    "base_tp": ("", 3),
+    "tp": ("", 3),
 }
+
+
+def _head_tree():
+    tmp = "/tmp/lf_variants_head"
+    subprocess.run(["rm", "-rf", tmp], check=True)
+    os.makedirs(tmp)
+    arch = subprocess.run(["git", "-C", ROOT, "archive", "HEAD", "paper_1607_08710_b200/csrc", "include"],
+                          check=True, stdout=subprocess.PIPE).stdout
+    subprocess.run(["tar", "-x", "-C", tmp], input=arch, check=True)
+    return os.path.join(tmp, "paper_1607_08710_b200", "csrc")
 
 
 def build(names=None):
     os.makedirs(OUT, exist_ok=True)
+    head = None
     procs = []
     for name, (flags, _path) in VARIANTS.items():
         if names and name not in names:
             continue
+        src = CSRC
+        if name.startswith("base_"):
+            head = head or _head_tree()
+            src = head
         so = os.path.join(OUT, f"{name}.so")
-        cmd = ["make", "-s", "-C", CSRC, f"OUT={so}", f"EXTRA_NVFLAGS={flags}", so]
+        cmd = ["make", "-s", "-C", src, f"OUT={so}", f"EXTRA_NVFLAGS={flags}", so]
         procs.append((name, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     for name, p in procs:
         out = p.communicate()[0].decode()
@@ -54,7 +69,7 @@ def run(n=8192, steps=10):
     g = case.grid
     ref = None
     results = {}
-    names = ["base_tp"] + list(VARIANTS) if os.path.exists(os.path.join(OUT, "base_tp.so")) else list(VARIANTS)
+    names = list(VARIANTS)
     for name in names:
         so = os.path.join(OUT, f"{name}.so")
         if not os.path.exists(so):
@@ -66,7 +81,7 @@ def run(n=8192, steps=10):
         desc = make_desc(g, case.bc, case.gamma, case.params)
         h = C.c_void_p()
         assert lib.lf_create(C.byref(desc), (C.c_int * 1)(0), 1, C.byref(h)) == 0
-        assert lib.lf_set_path(h, VARIANTS[name][1] if name in VARIANTS else 3) == 0
+        assert lib.lf_set_path(h, VARIANTS[name][1]) == 0
         assert lib.lf_init_fourier(h, case.seed) == 0
         km, lm, nl = C.c_double(), C.c_double(), C.c_int()
         assert lib.lf_time_steps(h, 3, case.cfl, C.byref(km), C.byref(lm), C.byref(nl)) == 0
