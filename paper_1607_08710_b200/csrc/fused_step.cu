@@ -68,11 +68,20 @@ bool fused_supported(lf_handle* h) {
   return true;
 }
 
+// the two-pass kernels unless the fused one is asked for (or the slab is too
+// large for their 32-bit offsets)
+static bool use_twopass(lf_handle* h) {
+  if (h->path == LF_PATH_FUSED) return false;
+  for (auto& s : h->slabs)
+    if (!tp_fits(s.L.pitch, s.L.ny)) return false;
+  return true;
+}
+
 static void fused_alloc(lf_handle* h, int steps) {
   FusedState* f = fstate(h);
   SlabState& s0 = h->slabs[0];
   FK(cudaSetDevice(s0.device));
-  if (h->path != LF_PATH_FUSED) alloc_staged_public(h);  // U*, F^n faces of the two passes
+  if (use_twopass(h)) alloc_staged_public(h);  // U*, F^n faces of the two passes
   if (!f) {
     f = new FusedState;
     h->fused = f;
@@ -174,7 +183,7 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   double* bnd = f->bnd + (size_t)cur * bnd_words(h);
   if (h->nccl) FK(cudaMemsetAsync(bnd, 0, bnd_words(h) * sizeof(double), s0.stream));
   if (k0) FK(cudaEventRecord(k0, s0.stream));
-  if (h->path != LF_PATH_FUSED) {
+  if (use_twopass(h)) {
     // two passes: predictor U^n -> U*, F^n; ghosts / halos of U*; corrector
     for (int pass = 0; pass < 2; ++pass) {
       if (pass == 1) fill_all_public(h, &SlabState::Us);
@@ -212,7 +221,7 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
     }
   }
   for (auto& s : h->slabs) {
-    if (h->path != LF_PATH_FUSED) break;
+    if (use_twopass(h)) break;
     FusedArgs a;
     a.u = s.U + s.L.origin();
     a.un = s.U2 + s.L.origin();

@@ -9,7 +9,10 @@
 
 namespace lfb {
 
-constexpr int TP_THREADS = 128;   // 4 independent warps per block
+#ifndef LF_TP_THREADS
+#define LF_TP_THREADS 128
+#endif
+constexpr int TP_THREADS = LF_TP_THREADS;   // independent warps per block x 32
 
 struct PassArgs {
   const double* x;      // stage input, ghost-filled: U^n (predictor) or U* (corrector)
@@ -31,6 +34,7 @@ struct PassArgs {
 };
 
 int tp_strips(int nx);
+bool tp_fits(int64_t pitch, int ny);  // 32-bit offsets suffice for the slab
 void launch_pass(const PassArgs& a, bool corr, bool muscl, cudaStream_t st);
 
 }  // namespace lfb

@@ -53,6 +53,7 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 //   LF_TP_MINBLOCKS  resident blocks per SM requested from ptxas (register budget)
 //   LF_TP_PAIR       1: x- and y-face Riemann solves in one straight line
 //   LF_TP_LATELOAD   1: load the update operands after the face solves
+//   LF_TP_UNROLL     2: unroll the row loop twice (state rotation by renaming)
 #ifndef LF_TP_MINBLOCKS
 #define LF_TP_MINBLOCKS 3
 #endif
@@ -61,6 +62,9 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 #endif
 #ifndef LF_TP_LATELOAD
 #define LF_TP_LATELOAD 0
+#endif
+#ifndef LF_TP_UNROLL
+#define LF_TP_UNROLL 1
 #endif
 
 template <bool CORR, bool MUSCL>
@@ -104,44 +108,48 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
   unsigned long long rate_key = 0ull, nmin_r = NINF_KEY, nmin_e = NINF_KEY;
   unsigned dtfail = 0;
 
-  const double* xin = a.x + c;
+  // element offsets of (row, column c) from the origin pointers fit in 32 bits
+  // (launch_pass checks); one running offset serves every array
+  const int P = (int)a.pitch;
+  int o_in = (y0 - 2) * P + c;   // offset of this iteration's input row r
   double nxt[4] = {1.0, 0.0, 0.0, 1.0};
   if (col_in_mem) {
-    const int64_t o = (int64_t)(y0 - 2) * a.pitch;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) nxt[q] = __ldg(xin + q * a.fstride + o);
+    for (int q = 0; q < 4; ++q) nxt[q] = __ldg(a.x + q * a.fstride + o_in);
   }
   double wm2[4] = {1.0, 0.0, 0.0, 1.0}, wm1[4] = {1.0, 0.0, 0.0, 1.0};
   double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fyprev[4] = {0.0, 0.0, 0.0, 0.0};
 
+#if LF_TP_UNROLL == 2
+#pragma unroll 2
+#endif
   for (int it = 0; it < nit; ++it) {
     const int r = y0 - 2 + it;   // input row
     const int row = r - 2;       // row updated this iteration (when it >= 4)
     double cur[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+    const int o_row = o_in - 2 * P;   // row r-2 (updated this iteration)
+    o_in += P;                        // row r+1
     if (it + 1 < nit && col_in_mem) {
-      const int64_t o = (int64_t)(r + 1) * a.pitch;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) nxt[q] = __ldg(xin + q * a.fstride + o);
+      for (int q = 0; q < 4; ++q) nxt[q] = __ldg(a.x + q * a.fstride + o_in);
     }
     // operands of this iteration's update (issued early unless LF_TP_LATELOAD)
     double base[4] = {0.0, 0.0, 0.0, 0.0}, fnx[4] = {0.0, 0.0, 0.0, 0.0}, fny[4] = {0.0, 0.0, 0.0, 0.0};
     auto load_operands = [&]() {
     if (it >= 4 && col_in_mem) {
-      const int64_t o = (int64_t)row * a.pitch + c;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) base[q] = __ldg(a.base + q * a.fstride + o);
+      for (int q = 0; q < 4; ++q) base[q] = __ldg(a.base + q * a.fstride + o_row);
       if (CORR && c >= 0 && c <= a.nx) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) fnx[q] = __ldg(a.fx + q * a.fx_stride + o);
+        for (int q = 0; q < 4; ++q) fnx[q] = __ldg(a.fx + q * a.fx_stride + o_row);
       }
     }
     if (CORR && it >= 3 && col_interior) {
       // face (row | row+1); at it == 3 this is the chunk's first face (y0-1 | y0)
-      const int64_t o = (int64_t)(row + 1) * a.pitch + c;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) fny[q] = __ldg(a.fy + q * a.fy_stride + o);
+      for (int q = 0; q < 4; ++q) fny[q] = __ldg(a.fy + q * a.fy_stride + (o_row + P));
     }
     };
 #if !LF_TP_LATELOAD
@@ -202,24 +210,22 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     if (it >= 4) {
       if (!CORR) {
         // F^n faces for the corrector
-        const int64_t o = (int64_t)row * a.pitch + c;
         if (store_fx)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a.fxo[q * a.fx_stride + o] = fx[q];
+          for (int q = 0; q < 4; ++q) a.fxo[q * a.fx_stride + o_row] = fx[q];
         if (upd)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a.fyo[q * a.fy_stride + o + a.pitch] = fy[q];
+          for (int q = 0; q < 4; ++q) a.fyo[q * a.fy_stride + (o_row + P)] = fy[q];
       }
       if (upd) {
         // solver.cpp:283-291
-        const int64_t o = (int64_t)row * a.pitch + c;
         double v[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           double val = base[q] - lam_x * (fxr[q] - fx[q]);
           val -= lam_y * (fy[q] - fyprev[q]);
           v[q] = val;
-          a.out[q * a.fstride + o] = val;
+          a.out[q * a.fstride + o_row] = val;
         }
         if (!CORR) {
           // e_int > 0 without the division (conservative, see fused_kernel.cu)
@@ -300,6 +306,11 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
 }  // namespace
 
 int tp_strips(int nx) { return (nx + TXW - 1) / TXW; }
+
+bool tp_fits(int64_t pitch, int ny) {
+  // k_pass addresses (row, column) with 32-bit element offsets, rows -NG .. ny+NG
+  return pitch * (int64_t)(ny + NG + 1) < (int64_t)1 << 31;
+}
 
 void launch_pass(const PassArgs& a, bool corr, bool muscl, cudaStream_t st) {
   const int warps = a.strips * ((a.ny + a.rows_per_chunk - 1) / a.rows_per_chunk);

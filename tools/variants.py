@@ -23,10 +23,12 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # name -> (extra nvcc flags, LF_PATH_*); "base_*" variants build the same path
 # from the committed sources (git HEAD) for an A/B against the working tree
 VARIANTS = {
-    "base_fused": ("", 1),
-    "fused": ("", 1),
     "base_tp": ("", 3),
     "tp": ("", 3),
+    "tp_swint": ("-DLF_SWEBY_INT=1", 3),
+    "tp_swint_imm": ("-DLF_SWEBY_INT=1 -DLF_INTMINMAX=1", 3),
+    "fused": ("", 1),
+    "fused_swint": ("-DLF_SWEBY_INT=1", 1),
 }
 
 
