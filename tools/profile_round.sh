@@ -1,3 +1,5 @@
+# Round-end evidence on one GPU: bench (both arms), ncu launch list, ncu --set full captures.
+# Run from the repo root under gpurun; outputs land in gpurun_out/ (summarise with tools/ncu_summary.py).
 set -x
 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
