@@ -25,6 +25,12 @@ struct lfo_solver {
   double* ustar_x[2];
   double* ustar_y[2];
   double* pred[4];         /* predictor_ */
+  /* multimaterial (solver.hpp:126-130): NULL / 0 without a material set */
+  int n_mat;
+  double mat_gamma[LFO_MAX_MATERIALS];
+  double* gamma_cells[2];                 /* gamma_[slot] */
+  double* frac[2][LFO_MAX_MATERIALS];     /* frac_[slot][k] */
+  double* pred_mat[LFO_MAX_MATERIALS];    /* predictor_mat_ */
 };
 
 static int nxt_of(const lfo_grid* g) { return g->nx + 2 * g->gx; }
@@ -250,6 +256,11 @@ void lfo_destroy(lfo_solver* so) {
     free(so->ustar_y[k]);
   }
   for (int c = 0; c < 4; ++c) free(so->pred[c]);
+  for (int s2 = 0; s2 < 2; ++s2) {
+    free(so->gamma_cells[s2]);
+    for (int k = 0; k < so->n_mat; ++k) free(so->frac[s2][k]);
+  }
+  for (int k = 0; k < so->n_mat; ++k) free(so->pred_mat[k]);
   free(so);
 }
 
@@ -257,7 +268,8 @@ void lfo_destroy(lfo_solver* so) {
 int lfo_compute_dt(lfo_solver* so, double* const field[4], double cfl, double time,
                    double limit_time, double* dt_out, lfo_error* err) {
   const lfo_grid* g = &so->g;
-  const double gamma = so->s.gamma;
+  const double gamma0 = so->s.gamma;
+  const double* gamma_cells = so->n_mat ? so->gamma_cells[0] : NULL;
   const int nx = g->nx, ny = g->ny;
   const int dim2 = g->dim == 2;
   const int64_t n_cells = (int64_t)nx * ny;
@@ -274,6 +286,7 @@ int lfo_compute_dt(lfo_solver* so, double* const field[4], double cfl, double ti
     const double inv = 1.0 / r;
     const double u = field[1][cell] * inv;
     const double v = field[2][cell] * inv;
+    const double gamma = gamma_cells ? gamma_cells[cell] : gamma0;
     const double p = (gamma - 1.0) *
                      (field[3][cell] -
                       0.5 * (field[1][cell] * field[1][cell] + field[2][cell] * field[2][cell]) *
@@ -313,7 +326,8 @@ int lfo_compute_dt(lfo_solver* so, double* const field[4], double cfl, double ti
 static int build_primitives(lfo_solver* so, double* const field[4], int slot, int64_t step,
                             lfo_error* err) {
   const lfo_grid* g = &so->g;
-  const double g0 = so->s.gamma;
+  const double gamma0 = so->s.gamma;
+  const double* gamma_cells = so->n_mat ? so->gamma_cells[slot] : NULL;
   double* rho = so->prim[slot][0];
   double* u = so->prim[slot][1];
   double* v = so->prim[slot][2];
@@ -333,6 +347,7 @@ static int build_primitives(lfo_solver* so, double* const field[4], int slot, in
     const double inv = 1.0 / r;
     const double uu = mx[c] * inv;
     const double vv = my[c] * inv;
+    const double g0 = gamma_cells ? gamma_cells[c] : gamma0;
     const double pp = (g0 - 1.0) * (re[c] - 0.5 * (mx[c] * mx[c] + my[c] * my[c]) * inv);
     rho[c] = r;
     u[c] = uu;
@@ -345,6 +360,7 @@ static int build_primitives(lfo_solver* so, double* const field[4], int slot, in
   if (fail == INT64_MAX) return 0;
   /* primitive_from_conserved with CellContext (euler.hpp:73-85, 56-66) */
   const int64_t c = fail;
+  const double g0 = gamma_cells ? gamma_cells[c] : gamma0;
   set_err(err, LFO_ERR_PRIMITIVE);
   err->i = c % nxt_of(g) - g->gx;
   err->j = c / nxt_of(g) - g->gy;
@@ -376,7 +392,8 @@ static int compute_fluxes(lfo_solver* so, int fs, int slot, int64_t step, lfo_er
   const double* u = so->prim[slot][1];
   const double* v = so->prim[slot][2];
   const double* p = so->prim[slot][3];
-  const double gamma = so->s.gamma;
+  const double gamma0 = so->s.gamma;
+  const double* gamma_cells = so->n_mat ? so->gamma_cells[slot] : NULL;
   const double beta = so->s.beta;
   const int muscl = so->s.spatial_order >= 2;
   const int nx = g->nx, ny = g->ny, nxt = nxt_of(g);
@@ -415,10 +432,12 @@ static int compute_fluxes(lfo_solver* so, int fs, int slot, int64_t step, lfo_er
         continue;
       }
       double ps, us, um[4], up[4], f[4];
-      lfo_lagrangian_hll(wm, wp, nrm_x, nrm_y, gamma, gamma, &ps, &us);
+      const double el = gamma_cells ? gamma_cells[clow] : gamma0;
+      const double er = gamma_cells ? gamma_cells[chigh] : gamma0;
+      lfo_lagrangian_hll(wm, wp, nrm_x, nrm_y, el, er, &ps, &us);
       ustar[e] = us;
-      cons_from_prim(wm, gamma, um);
-      cons_from_prim(wp, gamma, up);
+      cons_from_prim(wm, el, um);
+      cons_from_prim(wp, er, up);
       contact_flux(um, up, nrm_x, nrm_y, ps, us, f);
       for (int c = 0; c < 4; ++c) out[c][e] = f[c];
     }
@@ -559,14 +578,210 @@ int lfo_euler_stage(lfo_solver* so, double* const in[4], double dt, double* cons
   return apply_update(so, in, 0, -1, dt, out, step, NULL, NULL, err);
 }
 
-/* solver.cpp:489-546 (single material) */
-int lfo_heun_step(lfo_solver* so, double* const field[4], double cfl, double limit_time,
-                  double* time, int64_t* step, double* boundary_outflow, lfo_step_out* out,
-                  lfo_error* err) {
+/* ---- multimaterial (multimat.cpp:7-44; solver.cpp:90-129, 331-404) ---- */
+
+/* make_material_set, multimat.cpp:7-15 */
+int lfo_set_materials(lfo_solver* so, int n, const double* gammas, lfo_error* err) {
   set_err(err, 0);
-  lfo_apply_boundary(&so->g, so->s.bc, field);
+  char msg[160];
+  msg[0] = 0;
+  if (n < 1) snprintf(msg, sizeof msg, "material set needs at least one material");
+  else if (n > LFO_MAX_MATERIALS) snprintf(msg, sizeof msg, "at most 16 materials are supported");
+  else
+    for (int k = 0; k < n; ++k)
+      if (!(gammas[k] > 1.0) || !(gammas[k] <= 3.0)) {
+        char num[64];
+        fmt_f(num, sizeof num, gammas[k]);
+        snprintf(msg, sizeof msg, "material adiabatic index must lie in (1, 3], got %s", num);
+        break;
+      }
+  if (msg[0]) {
+    set_err(err, LFO_ERR_CONFIG);
+    if (err) snprintf(err->message, sizeof err->message, "%s", msg);
+    return LFO_ERR_CONFIG;
+  }
+  if (so->n_mat) return LFO_ERR_CONFIG; /* once, like the constructor argument */
+  so->n_mat = n;
+  for (int k = 0; k < n; ++k) so->mat_gamma[k] = gammas[k];
+  for (int s2 = 0; s2 < 2; ++s2) {
+    /* solver.cpp:80-83: gamma_[s].assign(cells, eos.gamma), frac_ zeros */
+    so->gamma_cells[s2] = (double*)malloc((size_t)so->cells * sizeof(double));
+    for (int64_t c = 0; c < so->cells; ++c) so->gamma_cells[s2][c] = so->s.gamma;
+    for (int k = 0; k < n; ++k) so->frac[s2][k] = (double*)calloc((size_t)so->cells, sizeof(double));
+  }
+  for (int k = 0; k < n; ++k) so->pred_mat[k] = (double*)calloc((size_t)so->cells, sizeof(double));
+  return 0;
+}
+
+/* clamped_fraction, multimat.cpp:17-23 (without the CellContext variant) */
+int lfo_clamped_fraction(double partial, double rho, double* y_out) {
+  const double y = partial / rho;
+  if (y >= 0.0 && y <= 1.0) {
+    *y_out = y;
+    return 0;
+  }
+  if (y < -1e-11 || y > 1.0 + 1e-11) return LFO_ERR_FRACTION;
+  *y_out = y < 0.0 ? 0.0 : 1.0;
+  return 0;
+}
+
+/* mixed_cell_gamma, multimat.cpp:25-32 */
+double lfo_mixed_cell_gamma(int n, const double* gammas, const double* fractions) {
+  double s = 0.0;
+  for (int k = 0; k < n; ++k) {
+    if (fractions[k] == 1.0) return gammas[k];
+    s += fractions[k] / (gammas[k] - 1.0);
+  }
+  return 1.0 + 1.0 / s;
+}
+
+/* mass_fraction_fluxes, multimat.cpp:34-44 */
+void lfo_mass_fraction_fluxes(double mass_flux, int n, const double* y_upwind, double* out) {
+  double rest = mass_flux;
+  for (int k = 0; k + 1 < n; ++k) {
+    out[k] = mass_flux * y_upwind[k];
+    rest -= out[k];
+  }
+  out[n - 1] = rest;
+}
+
+/* fill_all_ghosts, solver.cpp:90-129: ghost cells of the field and of every
+ * partial density (even parity), then the clamped fractions and the mixed-cell
+ * gamma of every (ghosted) cell into slot `slot`. */
+static int fill_all_ghosts(lfo_solver* so, double* const field[4], double* const* partials,
+                           int slot, lfo_error* err) {
+  const lfo_grid* g = &so->g;
+  lfo_apply_boundary(g, so->s.bc, field);
+  if (partials == NULL || so->n_mat == 0) return 0;
+  const int n_mat = so->n_mat;
+  for (int k = 0; k < n_mat; ++k) lfo_fill_ghosts(g, so->s.bc, 0, partials[k]);
+  const double* rho = field[0];
+  int64_t fail = INT64_MAX;
+  for (int64_t c = 0; c < so->cells; ++c) {
+    double ysum_gamma = 0.0;
+    int pure = -1;
+    for (int k = 0; k < n_mat; ++k) {
+      const double raw = partials[k][c] / rho[c];
+      double y = raw;
+      if (y < 0.0 || y > 1.0) {
+        if (raw < -1e-11 || raw > 1.0 + 1e-11) {
+          if (c < fail) fail = c;
+          y = 0.0;
+        } else {
+          y = raw < 0.0 ? 0.0 : 1.0;
+        }
+      }
+      so->frac[slot][k][c] = y;
+      if (y == 1.0) pure = k;
+      ysum_gamma += y / (so->mat_gamma[k] - 1.0);
+    }
+    so->gamma_cells[slot][c] = pure >= 0 ? so->mat_gamma[pure] : 1.0 + 1.0 / ysum_gamma;
+  }
+  if (fail == INT64_MAX) return 0;
+  set_err(err, LFO_ERR_FRACTION);
+  err->i = fail % nxt_of(g) - g->gx;
+  err->j = fail / nxt_of(g) - g->gy;
+  snprintf(err->message, sizeof err->message,
+           "mass fraction out of [0,1] beyond round-off at cell (%lld,%lld)", (long long)err->i,
+           (long long)err->j);
+  return LFO_ERR_FRACTION;
+}
+
+/* update_partials, solver.cpp:331-404.  Stage fluxes: mass component of flux
+ * set fa (and fb), u* of the same sets, fractions of slot sa (and sb). */
+static void edge_material_flux(const lfo_solver* so, int fs, int slot, int is_x, size_t e,
+                               int64_t clow, int64_t chigh, double* out_k) {
+  const double mass = is_x ? so->fx[fs][0][e] : so->fy[fs][0][e];
+  const double us = is_x ? so->ustar_x[fs][e] : so->ustar_y[fs][e];
+  const int64_t up = us > 0.0 ? clow : chigh;
+  double rest = mass;
+  for (int k = 0; k < so->n_mat - 1; ++k) {
+    const double fk = us == 0.0 ? 0.0 : mass * so->frac[slot][k][up];
+    out_k[k] = fk;
+    rest -= fk;
+  }
+  out_k[so->n_mat - 1] = us == 0.0 ? 0.0 : rest;
+}
+
+static void update_partials(lfo_solver* so, double* const* base, int fa, int fb, double dt,
+                            int sa, int sb, double* const* out) {
+  const lfo_grid* g = &so->g;
+  const int n_mat = so->n_mat;
+  const int nx = g->nx, ny = g->ny;
+  const double lam_x = dt / g->dx;
+  const double lam_y = dt / g->dy;
+  const int dim2 = g->dim == 2;
+  const int nxt = nxt_of(g);
+  for (int64_t cc = 0; cc < (int64_t)nx * ny; ++cc) {
+    const int i = (int)(cc % nx), j = (int)(cc / nx);
+    const int64_t cell = idx_of(g, g->gx + i, g->gy + j);
+    const size_t exl = (size_t)j * (nx + 1) + i, exr = exl + 1;
+    const size_t eyb = (size_t)j * nx + i, eyt = eyb + (size_t)nx;
+    double fl[LFO_MAX_MATERIALS], fr[LFO_MAX_MATERIALS], fb2[LFO_MAX_MATERIALS],
+        ft[LFO_MAX_MATERIALS];
+    for (int k = 0; k < n_mat; ++k) fl[k] = fr[k] = fb2[k] = ft[k] = 0.0;
+    for (int stage = 0; stage < (fb >= 0 ? 2 : 1); ++stage) {
+      const int fs = stage == 0 ? fa : fb, slot = stage == 0 ? sa : sb;
+      const double w = fb >= 0 ? 0.5 : 1.0;
+      double tl[LFO_MAX_MATERIALS], tr[LFO_MAX_MATERIALS], tb[LFO_MAX_MATERIALS],
+          tt[LFO_MAX_MATERIALS];
+      edge_material_flux(so, fs, slot, 1, exl, cell - 1, cell, tl);
+      edge_material_flux(so, fs, slot, 1, exr, cell, cell + 1, tr);
+      if (dim2) {
+        edge_material_flux(so, fs, slot, 0, eyb, cell - nxt, cell, tb);
+        edge_material_flux(so, fs, slot, 0, eyt, cell, cell + nxt, tt);
+      }
+      for (int k = 0; k < n_mat; ++k) {
+        fl[k] += w * tl[k];
+        fr[k] += w * tr[k];
+        if (dim2) {
+          fb2[k] += w * tb[k];
+          ft[k] += w * tt[k];
+        }
+      }
+    }
+    for (int k = 0; k < n_mat; ++k) {
+      double val = base[k][cell] - lam_x * (fr[k] - fl[k]);
+      if (dim2) val -= lam_y * (ft[k] - fb2[k]);
+      out[k][cell] = val;
+    }
+  }
+}
+
+/* solver.cpp:519-540: with materials, min p from the fresh partial masses */
+static double mat_min_p(const lfo_solver* so, double* const field[4], double* const* partials) {
+  const lfo_grid* g = &so->g;
+  const int nx = g->nx, ny = g->ny;
+  double min_p = INFINITY;
+  for (int64_t cc = 0; cc < (int64_t)nx * ny; ++cc) {
+    const int64_t cell = idx_of(g, g->gx + (int)(cc % nx), g->gy + (int)(cc / nx));
+    const double r = field[0][cell];
+    double s = 0.0;
+    for (int k = 0; k < so->n_mat; ++k) s += (partials[k][cell] / r) / (so->mat_gamma[k] - 1.0);
+    const double eint =
+        field[3][cell] - 0.5 * (field[1][cell] * field[1][cell] + field[2][cell] * field[2][cell]) / r;
+    min_p = smin(min_p, eint / s);
+  }
+  return min_p;
+}
+
+/* solver.cpp:489-546.  partials: the MaterialCells (n_mat arrays in grid
+ * layout, updated in place) or NULL without a material set. */
+int lfo_heun_step_mat(lfo_solver* so, double* const field[4], double* const* partials,
+                      double cfl, double limit_time, double* time, int64_t* step,
+                      double* boundary_outflow, lfo_step_out* out, lfo_error* err) {
+  set_err(err, 0);
+  if (so->n_mat == 0) partials = NULL;
+  if (so->n_mat && partials == NULL) {
+    /* the reference dereferences the missing MaterialCells (solver.cpp:529) */
+    set_err(err, LFO_ERR_CONFIG);
+    snprintf(err->message, sizeof err->message, "multimaterial step needs material storage");
+    return LFO_ERR_CONFIG;
+  }
+  int rc = fill_all_ghosts(so, field, partials, 0, err);
+  if (rc) return rc;
   double dt = 0.0;
-  int rc = lfo_compute_dt(so, field, cfl, *time, limit_time, &dt, err);
+  rc = lfo_compute_dt(so, field, cfl, *time, limit_time, &dt, err);
   if (rc) return rc;
   const int hits_limit = *time + dt >= limit_time;
 
@@ -577,25 +792,28 @@ int lfo_heun_step(lfo_solver* so, double* const field[4], double cfl, double lim
   double min_rho = 0.0, min_eint = 0.0;
   rc = apply_update(so, field, 0, -1, dt, so->pred, *step, &min_rho, &min_eint, err);
   if (rc) return rc;
+  if (partials) update_partials(so, partials, 0, -1, dt, 0, -1, so->pred_mat);
 
   if (so->s.time_order >= 2) {
-    lfo_apply_boundary(&so->g, so->s.bc, so->pred);
+    rc = fill_all_ghosts(so, so->pred, partials ? so->pred_mat : NULL, 1, err);
+    if (rc) return rc;
     rc = build_primitives(so, so->pred, 1, *step, err);
     if (rc) return rc;
     rc = compute_fluxes(so, 1, 1, *step, err);
     if (rc) return rc;
     rc = apply_update(so, field, 0, 1, dt, field, *step, &min_rho, &min_eint, err);
     if (rc) return rc;
+    if (partials) update_partials(so, partials, 0, 1, dt, 0, 1, partials);
     accumulate_boundary_outflow(so, 0, 1, dt, boundary_outflow);
   } else {
-    /* std::swap(state.field.comp, predictor_.comp): copy the predictor out. */
-    for (int c = 0; c < 4; ++c) {
-      double* t = field[c];
-      memcpy(t, so->pred[c], (size_t)so->cells * sizeof(double));
-    }
+    /* std::swap(state.field.comp, predictor_.comp) (and the partials): copy out */
+    for (int c = 0; c < 4; ++c) memcpy(field[c], so->pred[c], (size_t)so->cells * sizeof(double));
+    if (partials)
+      for (int k = 0; k < so->n_mat; ++k)
+        memcpy(partials[k], so->pred_mat[k], (size_t)so->cells * sizeof(double));
     accumulate_boundary_outflow(so, 0, -1, dt, boundary_outflow);
   }
-  const double min_p = (so->s.gamma - 1.0) * min_eint;
+  const double min_p = partials ? mat_min_p(so, field, partials) : (so->s.gamma - 1.0) * min_eint;
   *time = hits_limit ? limit_time : *time + dt;
   *step += 1;
   if (out) {
@@ -608,6 +826,14 @@ int lfo_heun_step(lfo_solver* so, double* const field[4], double cfl, double lim
     for (int c = 0; c < 4; ++c) out->boundary_outflow[c] = boundary_outflow[c];
   }
   return 0;
+}
+
+/* solver.cpp:489-546 without materials */
+int lfo_heun_step(lfo_solver* so, double* const field[4], double cfl, double limit_time,
+                  double* time, int64_t* step, double* boundary_outflow, lfo_step_out* out,
+                  lfo_error* err) {
+  return lfo_heun_step_mat(so, field, NULL, cfl, limit_time, time, step, boundary_outflow, out,
+                           err);
 }
 
 /* ---- Seeded smooth-perturbation generator ----

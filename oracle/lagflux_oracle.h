@@ -6,7 +6,7 @@
  * cpu_baseline / --impl reference legs may load it.  The product never links it.
  *
  * It restates, in plain C with the reference's exact operation order, the
- * single-material hot path of /root/reference/proj:
+ * hot path of /root/reference/proj, single- and multimaterial:
  *   LagfluxSolver::heun_step        src/solver.cpp:489-546
  *   LagfluxSolver::euler_stage      src/solver.cpp:482-487
  *   LagfluxSolver::compute_dt       src/solver.cpp:434-480
@@ -18,6 +18,11 @@
  *   lagrangian_hll                  include/lagflux/riemann_hll.hpp:27-40
  *   sweby_limiter / muscl_face_trace include/lagflux/reconstruct.hpp:24-49
  *   conserved_from_primitive        include/lagflux/euler.hpp:87-97
+ *   fill_all_ghosts (materials)     src/solver.cpp:90-129
+ *   update_partials                 src/solver.cpp:331-404
+ *   multimaterial min p             src/solver.cpp:519-540
+ *   make_material_set, clamped_fraction, mixed_cell_gamma,
+ *   mass_fraction_fluxes            src/multimat.cpp:7-44
  *
  * Parity is pinned two ways (see tests/test_oracle_cpu.py):
  *   - bit-for-bit against the reference itself, compiled from its own sources
@@ -47,8 +52,11 @@ enum {
   LFO_ERR_DT_NONPOS = 3,     /* Error "non-positive time step" (solver.cpp:478) */
   LFO_ERR_PRIMITIVE = 4,     /* InvalidStateError from build_primitives (solver.cpp:164-170) */
   LFO_ERR_TRACE = 5,         /* InvalidStateError from compute_fluxes (solver.cpp:245-255) */
-  LFO_ERR_POSITIVITY = 6     /* PositivityError from apply_update (solver.cpp:310-326) */
+  LFO_ERR_POSITIVITY = 6,    /* PositivityError from apply_update (solver.cpp:310-326) */
+  LFO_ERR_FRACTION = 9       /* InvalidStateError from fill_all_ghosts (solver.cpp:122-127) */
 };
+
+#define LFO_MAX_MATERIALS 16   /* make_material_set, multimat.cpp:10 */
 
 typedef struct {
   int dim;          /* 1 or 2 */
@@ -105,6 +113,17 @@ int lfo_compute_dt(lfo_solver* s, double* const field[4], double cfl, double tim
 int lfo_euler_stage(lfo_solver* s, double* const in[4], double dt, double* const out[4],
                     int64_t step, lfo_error* err);
 /* state: field (in place), time/step in-out, boundary_outflow in-out (4). */
+/* Multimaterial (solver.cpp:90-129, 331-404, 519-540; multimat.cpp:7-44):
+ * lfo_set_materials is the constructor's MaterialSet (make_material_set's
+ * validation); lfo_heun_step_mat is heun_step(state, controls, limit, &mat)
+ * with the partial densities as n_mat arrays in the ghosted grid layout. */
+int lfo_set_materials(lfo_solver* s, int n, const double* gammas, lfo_error* err);
+int lfo_heun_step_mat(lfo_solver* s, double* const field[4], double* const* partials,
+                      double cfl, double limit_time, double* time, int64_t* step,
+                      double* boundary_outflow, lfo_step_out* out, lfo_error* err);
+int lfo_clamped_fraction(double partial, double rho, double* y_out);
+double lfo_mixed_cell_gamma(int n, const double* gammas, const double* fractions);
+void lfo_mass_fraction_fluxes(double mass_flux, int n, const double* y_upwind, double* out);
 int lfo_heun_step(lfo_solver* s, double* const field[4], double cfl, double limit_time,
                   double* time, int64_t* step, double* boundary_outflow, lfo_step_out* out,
                   lfo_error* err);

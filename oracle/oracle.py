@@ -26,6 +26,7 @@ REF_SO = os.path.join(HERE, "_ref", "libref_lagflux.so")
 
 # error kinds (lagflux_oracle.h)
 ERR_CONFIG, ERR_DT_STATE, ERR_DT_NONPOS, ERR_PRIMITIVE, ERR_TRACE, ERR_POSITIVITY = 1, 2, 3, 4, 5, 6
+ERR_FRACTION = 9
 
 
 class lfo_grid(C.Structure):
@@ -60,6 +61,12 @@ def _ptrs(field: np.ndarray):
     return P4(*[field[c].ctypes.data_as(DP) for c in range(4)])
 
 
+def _kptrs(partial: np.ndarray):
+    """(n, nyt, nxt) partial densities -> double*[n]."""
+    assert partial.dtype == np.float64 and partial.flags.c_contiguous
+    return (DP * partial.shape[0])(*[partial[k].ctypes.data_as(DP) for k in range(partial.shape[0])])
+
+
 def _cgrid(g: G.CartesianGrid) -> lfo_grid:
     return lfo_grid(g.dim, g.nx, g.ny, g.gx, g.gy, g.dx, g.dy, g.x0, g.y0)
 
@@ -76,7 +83,7 @@ def raise_error(e: lfo_error):
         raise G.PositivityError(msg, e.i, e.j, e.step, e.dt)
     if e.kind == ERR_CONFIG:
         raise G.ConfigError(msg)
-    if e.kind in (ERR_DT_STATE, ERR_PRIMITIVE, ERR_TRACE):
+    if e.kind in (ERR_DT_STATE, ERR_PRIMITIVE, ERR_TRACE, ERR_FRACTION):
         raise G.InvalidStateError(msg)
     raise G.Error(msg)
 
@@ -103,6 +110,14 @@ def oracle_lib():
     lib.lfo_heun_step.argtypes = [C.c_void_p, P4, C.c_double, C.c_double, DP,
                                   C.POINTER(C.c_int64), DP, C.POINTER(lfo_step_out),
                                   C.POINTER(lfo_error)]
+    lib.lfo_set_materials.argtypes = [C.c_void_p, C.c_int, DP, C.POINTER(lfo_error)]
+    lib.lfo_heun_step_mat.argtypes = [C.c_void_p, P4, C.c_void_p, C.c_double, C.c_double, DP,
+                                      C.POINTER(C.c_int64), DP, C.POINTER(lfo_step_out),
+                                      C.POINTER(lfo_error)]
+    lib.lfo_clamped_fraction.argtypes = [C.c_double, C.c_double, DP]
+    lib.lfo_mixed_cell_gamma.restype = C.c_double
+    lib.lfo_mixed_cell_gamma.argtypes = [C.c_int, DP, DP]
+    lib.lfo_mass_fraction_fluxes.argtypes = [C.c_double, C.c_int, DP, DP]
     lib.lfo_fill_ghosts.argtypes = [C.POINTER(lfo_grid), C.c_int * 4, C.c_int, DP]
     lib.lfo_sweby.restype = C.c_double
     lib.lfo_sweby.argtypes = [C.c_double, C.c_double, C.c_double]
@@ -134,6 +149,17 @@ def ref_lib():
     lib.lfr_lagrangian_hll.argtypes = [DP, DP, C.c_double, C.c_double, C.c_double, DP, DP]
     lib.lfr_edge_flux.argtypes = [DP, DP, C.c_double, C.c_double, C.c_double, DP]
     lib.lfr_omp_max_threads.restype = C.c_int
+    lib.lfr_create_mat.restype = C.c_void_p
+    lib.lfr_create_mat.argtypes = [C.POINTER(lfo_grid), C.POINTER(lfo_scheme), C.c_int, C.c_int,
+                                   DP, C.POINTER(lfo_error)]
+    lib.lfr_make_material_set.argtypes = [C.c_int, DP, C.POINTER(lfo_error)]
+    lib.lfr_set_partials.argtypes = [C.c_void_p, C.c_void_p]
+    lib.lfr_get_partials.argtypes = [C.c_void_p, C.c_void_p]
+    lib.lfr_clamped_fraction.restype = C.c_double
+    lib.lfr_clamped_fraction.argtypes = [C.c_double, C.c_double, C.POINTER(C.c_int)]
+    lib.lfr_mixed_cell_gamma.restype = C.c_double
+    lib.lfr_mixed_cell_gamma.argtypes = [C.c_int, DP, DP]
+    lib.lfr_mass_fraction_fluxes.argtypes = [C.c_double, C.c_int, DP, DP]
     return lib
 
 
@@ -145,7 +171,7 @@ class OracleSolver:
     """The C restatement behind the LagfluxSolver API (solver.hpp:78-131)."""
 
     def __init__(self, g: G.CartesianGrid, bc: G.BoundaryCondition, gamma: float = 1.4,
-                 params: G.SchemeParams = G.SchemeParams()):
+                 params: G.SchemeParams = G.SchemeParams(), materials=None):
         self.lib = oracle_lib()
         self.g, self.bc, self.gamma, self.params = g, bc, gamma, params
         err = lfo_error()
@@ -153,6 +179,11 @@ class OracleSolver:
                                      C.byref(err))
         if not self.h:
             raise_error(err)
+        self.materials = materials
+        if materials is not None:
+            gs = np.array(materials.gammas, dtype=np.float64)
+            if self.lib.lfo_set_materials(self.h, len(gs), gs.ctypes.data_as(DP), C.byref(err)):
+                raise_error(err)
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -170,12 +201,15 @@ class OracleSolver:
         if self.lib.lfo_euler_stage(self.h, _ptrs(field), dt, _ptrs(out), step, C.byref(err)):
             raise_error(err)
 
-    def heun_step(self, state: G.SolverState, cfl: float, limit_time: float) -> float:
+    def heun_step(self, state: G.SolverState, cfl: float, limit_time: float, mat=None) -> float:
+        """heun_step(state, controls, limit_time, mat) -- mat: multimat.MaterialCells."""
         err, out = lfo_error(), lfo_step_out()
         t, s = C.c_double(state.time), C.c_int64(state.step)
         acc = (C.c_double * 4)(*state.boundary_outflow)
-        rc = self.lib.lfo_heun_step(self.h, _ptrs(state.field), cfl, limit_time, C.byref(t),
-                                    C.byref(s), C.cast(acc, DP), C.byref(out), C.byref(err))
+        parts = _kptrs(mat.partial) if mat is not None else None
+        rc = self.lib.lfo_heun_step_mat(self.h, _ptrs(state.field), parts, cfl, limit_time,
+                                        C.byref(t), C.byref(s), C.cast(acc, DP), C.byref(out),
+                                        C.byref(err))
         if rc:
             raise_error(err)
         state.time, state.step = t.value, s.value
@@ -188,14 +222,24 @@ class RefSolver:
     """The reference's own LagfluxSolver (compiled from /root/reference sources)."""
 
     def __init__(self, g: G.CartesianGrid, bc: G.BoundaryCondition, gamma: float = 1.4,
-                 params: G.SchemeParams = G.SchemeParams(), threads: int = 1):
+                 params: G.SchemeParams = G.SchemeParams(), threads: int = 1, materials=None):
         self.lib = ref_lib()
         self.g, self.bc, self.gamma, self.params = g, bc, gamma, params
         err = lfo_error()
-        self.h = self.lib.lfr_create(C.byref(_cgrid(g)), C.byref(_cscheme(gamma, params, bc)),
-                                     threads, C.byref(err))
+        gs = np.array(materials.gammas if materials is not None else [0.0], dtype=np.float64)
+        self.n_mat = len(materials.gammas) if materials is not None else 0
+        self.h = self.lib.lfr_create_mat(C.byref(_cgrid(g)), C.byref(_cscheme(gamma, params, bc)),
+                                         threads, self.n_mat, gs.ctypes.data_as(DP), C.byref(err))
         if not self.h:
             raise_error(err)
+
+    def set_partials(self, partial: np.ndarray) -> None:
+        self.lib.lfr_set_partials(self.h, _kptrs(np.ascontiguousarray(partial)))
+
+    def get_partials(self) -> np.ndarray:
+        out = np.zeros((self.n_mat, self.g.nyt, self.g.nxt))
+        self.lib.lfr_get_partials(self.h, _kptrs(out))
+        return out
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -258,3 +302,53 @@ def fourier_tables_oracle(seed: int, g: G.CartesianGrid):
     lib.lfo_fourier_tables(seed, g.nx, g.ny, g.x0, g.y0, g.dx, g.dy, tx.ctypes.data_as(DP),
                            ty.ctypes.data_as(DP), amp.ctypes.data_as(DP))
     return tx.reshape(4, 8, 2, g.nx), ty.reshape(4, 8, 2, g.ny), amp.reshape(4, 8)
+
+
+# ---- multimat.cpp element functions (known-answer tests) -------------------
+def ref_make_material_set(gammas):
+    err = lfo_error()
+    gs = np.array(list(gammas) or [0.0], dtype=np.float64)
+    if ref_lib().lfr_make_material_set(len(gammas), gs.ctypes.data_as(DP), C.byref(err)):
+        raise_error(err)
+
+
+def ref_clamped_fraction(partial: float, rho: float):
+    """(value, failed)"""
+    failed = C.c_int()
+    v = ref_lib().lfr_clamped_fraction(partial, rho, C.byref(failed))
+    return v, bool(failed.value)
+
+
+def oracle_clamped_fraction(partial: float, rho: float):
+    y = C.c_double()
+    rc = oracle_lib().lfo_clamped_fraction(partial, rho, C.byref(y))
+    return y.value, rc != 0
+
+
+def _mixed(lib_fn, gammas, fractions):
+    gs = np.array(gammas, dtype=np.float64)
+    fs = np.array(fractions, dtype=np.float64)
+    return lib_fn(len(gs), gs.ctypes.data_as(DP), fs.ctypes.data_as(DP))
+
+
+def ref_mixed_cell_gamma(gammas, fractions):
+    return _mixed(ref_lib().lfr_mixed_cell_gamma, gammas, fractions)
+
+
+def oracle_mixed_cell_gamma(gammas, fractions):
+    return _mixed(oracle_lib().lfo_mixed_cell_gamma, gammas, fractions)
+
+
+def _mff(lib_fn, mass_flux, y):
+    ys = np.array(y, dtype=np.float64)
+    out = np.zeros(len(ys))
+    lib_fn(mass_flux, len(ys), ys.ctypes.data_as(DP), out.ctypes.data_as(DP))
+    return out
+
+
+def ref_mass_fraction_fluxes(mass_flux, y):
+    return _mff(ref_lib().lfr_mass_fraction_fluxes, mass_flux, y)
+
+
+def oracle_mass_fraction_fluxes(mass_flux, y):
+    return _mff(oracle_lib().lfo_mass_fraction_fluxes, mass_flux, y)

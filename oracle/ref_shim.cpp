@@ -17,6 +17,7 @@
 #endif
 
 #include "lagflux/error.hpp"
+#include "lagflux/multimat.hpp"
 #include "lagflux/solver.hpp"
 #include "lagflux_oracle.h"
 
@@ -30,6 +31,8 @@ struct lfr_solver {
   LagfluxSolver* solver = nullptr;
   SolverState state;
   CellField scratch;  // euler_stage output
+  MaterialSet materials;   // outlives `solver` (constructor argument by pointer)
+  MaterialCells mat;
 };
 
 namespace {
@@ -66,6 +69,8 @@ int map_exception(lfo_error* e, int default_kind) {
     const std::string w = x.what();
     if (w.rfind("non-physical state while computing the time step", 0) == 0)
       kind = LFO_ERR_DT_STATE;
+    else if (w.rfind("mass fraction out of [0,1]", 0) == 0)
+      kind = LFO_ERR_FRACTION;
     else if (w.rfind("non-physical reconstructed trace", 0) == 0)
       kind = LFO_ERR_TRACE;
     else
@@ -109,7 +114,9 @@ void copy_out(const CellField& f, double* const dst[4]) {
 
 extern "C" {
 
-lfr_solver* lfr_create(const lfo_grid* g, const lfo_scheme* s, int threads, lfo_error* err) {
+// n_mat > 0: the solver gets make_material_set(gammas) (multimat.cpp:7-15).
+lfr_solver* lfr_create_mat(const lfo_grid* g, const lfo_scheme* s, int threads, int n_mat,
+                           const double* gammas, lfo_error* err) {
   clear(err);
   auto* r = new lfr_solver;
   try {
@@ -119,7 +126,12 @@ lfr_solver* lfr_create(const lfo_grid* g, const lfo_scheme* s, int threads, lfo_
     r->params.limiter = LimiterParams{s->beta};
     r->params.spatial_order = s->spatial_order;
     r->params.time_order = s->time_order;
-    r->solver = new LagfluxSolver(r->g, r->bc, r->eos, r->params, threads);
+    if (n_mat > 0) {
+      r->materials = make_material_set(std::vector<double>(gammas, gammas + n_mat));
+      r->mat = MaterialCells(r->g, r->materials.count());
+    }
+    r->solver = new LagfluxSolver(r->g, r->bc, r->eos, r->params, threads,
+                                  n_mat > 0 ? &r->materials : nullptr);
     r->state.field = CellField(r->g);
     r->scratch = CellField(r->g);
   } catch (...) {
@@ -129,6 +141,53 @@ lfr_solver* lfr_create(const lfo_grid* g, const lfo_scheme* s, int threads, lfo_
     return nullptr;
   }
   return r;
+}
+
+lfr_solver* lfr_create(const lfo_grid* g, const lfo_scheme* s, int threads, lfo_error* err) {
+  return lfr_create_mat(g, s, threads, 0, nullptr, err);
+}
+
+// make_material_set's validation alone (0 or LFO_ERR_CONFIG with the message).
+int lfr_make_material_set(int n, const double* gammas, lfo_error* err) {
+  clear(err);
+  try {
+    (void)make_material_set(std::vector<double>(gammas, gammas + n));
+  } catch (...) {
+    return map_exception(err, LFO_ERR_CONFIG);
+  }
+  return 0;
+}
+
+void lfr_set_partials(lfr_solver* r, double* const* partials) {
+  for (int k = 0; k < r->mat.count(); ++k)
+    std::memcpy(r->mat.partial[size_t(k)].data(), partials[k],
+                r->mat.partial[size_t(k)].size() * sizeof(double));
+}
+
+void lfr_get_partials(lfr_solver* r, double* const* partials) {
+  for (int k = 0; k < r->mat.count(); ++k)
+    std::memcpy(partials[k], r->mat.partial[size_t(k)].data(),
+                r->mat.partial[size_t(k)].size() * sizeof(double));
+}
+
+double lfr_clamped_fraction(double partial, double rho, int* failed) {
+  *failed = 0;
+  try {
+    return clamped_fraction(partial, rho);
+  } catch (...) {
+    *failed = 1;
+    return 0.0;
+  }
+}
+
+double lfr_mixed_cell_gamma(int n, const double* gammas, const double* fractions) {
+  const MaterialSet set{std::vector<double>(gammas, gammas + n)};
+  return mixed_cell_gamma(set, std::span<const double>(fractions, size_t(n)));
+}
+
+void lfr_mass_fraction_fluxes(double mass_flux, int n, const double* y_upwind, double* out) {
+  mass_fraction_fluxes(mass_flux, std::span<const double>(y_upwind, size_t(n)),
+                       std::span<double>(out, size_t(n)));
 }
 
 void lfr_destroy(lfr_solver* r) {
@@ -165,7 +224,8 @@ int lfr_heun_steps(lfr_solver* r, int n, double cfl, double limit_time, double* 
   int k = 0;
   try {
     for (; k < n; ++k) {
-      const double dt = r->solver->heun_step(r->state, controls, limit_time, nullptr);
+      const double dt = r->solver->heun_step(r->state, controls, limit_time,
+                                             r->mat.count() > 0 ? &r->mat : nullptr);
       if (dts) dts[k] = dt;
       if (diag) {
         const StepDiagnostics& d = r->state.diagnostics.back();

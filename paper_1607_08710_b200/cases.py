@@ -87,6 +87,91 @@ def smooth_weak(n_gpus: int, n: int = 16384, steps: int = 20) -> Case:
 CONFIGS = {1: sod, 2: quadrant, 3: sedov, 4: smooth, 5: lambda: smooth(32768, 20)}
 
 
+# ---------------------------------------------------------------- multimaterial
+@dataclass(frozen=True)
+class Region:
+    """RegionSpec (config.hpp): a rectangle [x_min, x_max) x [y_min, y_max) of one
+    primitive state and one material (1-based, as in the case files)."""
+    x_min: float
+    x_max: float
+    y_min: float
+    y_max: float
+    rho: float
+    u: float
+    v: float
+    p: float
+    material: int = 1
+
+
+@dataclass(frozen=True)
+class MatCase:
+    """A region-initialised multimaterial case (run.cpp:29-78, 140-190)."""
+    name: str
+    grid: G.CartesianGrid
+    bc: G.BoundaryCondition
+    gamma: float                    # the solver's eos (CaseConfig::gamma)
+    material_gammas: tuple
+    regions: tuple
+    params: G.SchemeParams
+    cfl: float
+    t_final: float
+    max_steps: int
+
+
+def regions_field(c: MatCase):
+    """initialize_hydro (run.cpp:29-78) for InitKind::regions: the ghosted field
+    and the partial densities (n_mat, nyt, nxt); ghosts are zero."""
+    from . import multimat as MM
+    g = c.grid
+    f = G.new_field(g)
+    n_mat = len(c.material_gammas) if c.material_gammas else 1
+    mat = MM.MaterialCells(g, n_mat)
+    for j in range(g.gy, g.gy + g.ny):
+        y = g.yc(j)
+        for i in range(g.gx, g.gx + g.nx):
+            x = g.xc(i)
+            hits, w, material = 0, None, 0
+            for r in c.regions:
+                in_x = x >= r.x_min and x < r.x_max
+                in_y = g.dim == 1 or (y >= r.y_min and y < r.y_max)
+                if in_x and in_y:
+                    hits += 1
+                    w = (r.rho, r.u, r.v, r.p)
+                    material = r.material - 1
+            if hits != 1:
+                raise G.ConfigError("cell center (%f,%f) is covered by %d regions; regions must "
+                                    "tile the domain exactly" % (x, y, hits))
+            gamma = c.material_gammas[material] if c.material_gammas else c.gamma
+            r0, m1, m2, e3 = G.conserved_from_primitive(*w, gamma)
+            f[0, j, i], f[1, j, i], f[2, j, i], f[3, j, i] = r0, m1, m2, e3
+            if c.material_gammas:
+                for k in range(n_mat):
+                    mat.partial[k, j, i] = w[0] if k == material else 0.0
+    return f, (mat if c.material_gammas else None)
+
+
+def triple_point(nx: int = 256, ny: int = 110, steps: int = G.INT64_MAX) -> MatCase:
+    """proj/cases/triple_point.case: three states, three materials, closed vessel."""
+    g = G.make_grid_2d(nx, ny, 0.0, 7.0, 0.0, 3.0)
+    regions = (Region(0.0, 1.0, 0.0, 3.0, 1.0, 0.0, 0.0, 1.0, 1),
+               Region(1.0, 7.0, 1.5, 3.0, 0.125, 0.0, 0.0, 0.1, 2),
+               Region(1.0, 7.0, 0.0, 1.5, 1.0, 0.0, 0.0, 0.1, 3))
+    return MatCase("triple_point", g, G.BoundaryCondition.uniform(G.REFLECTIVE), 1.4,
+                   (1.5, 1.4, 1.5), regions, G.SchemeParams(beta=1.5), 0.25, 3.3530, steps)
+
+
+def material_contact_1d(n: int = 64, gammas=(1.4, 1.4), gamma: float = 1.4,
+                        steps: int = 100) -> MatCase:
+    """test_multimat.cpp:62-110 / 112-137: a density contact advected through a
+    periodic box (equal or unequal gammas), CFL 0.25, no time limit."""
+    g = G.make_grid_1d(n, 0.0, 1.0)
+    regions = (Region(0.0, 0.5, 0.0, 1.0, 1.0, 1.0, 0.0, 1.0, 1),
+               Region(0.5, 1.0, 0.0, 1.0, 0.35, 1.0, 0.0, 1.0, 2))
+    bc = G.BoundaryCondition(G.PERIODIC, G.PERIODIC, G.TRANSMISSIVE, G.TRANSMISSIVE)
+    return MatCase("contact_1d", g, bc, gamma, tuple(gammas), regions, G.SchemeParams(), 0.25,
+                   1e30, steps)
+
+
 # ---------------------------------------------------------------- generators
 class _MT19937_64:
     """std::mt19937_64 with integer seeding (the oracle restates the same)."""

@@ -45,6 +45,43 @@ def golden_cases():
     }
 
 
+def golden_mat_cases():
+    """name -> MatCase (steps in max_steps): the reference's multimaterial cases
+    (test_multimat.cpp:62-137, cases/triple_point.case) at small sizes, plus a
+    2D four-material quadrant whose contacts shear and mix."""
+    quad_regions = (CS.Region(0.5, 1.0, 0.5, 1.0, 1.5, 0.0, 0.0, 1.5, 1),
+                    CS.Region(0.0, 0.5, 0.5, 1.0, 0.5323, 1.206, 0.0, 0.3, 2),
+                    CS.Region(0.0, 0.5, 0.0, 0.5, 0.138, 1.206, 1.206, 0.029, 3),
+                    CS.Region(0.5, 1.0, 0.0, 0.5, 0.5323, 0.0, 1.206, 0.3, 4))
+    quad = CS.MatCase("mm_quadrant", G.make_grid_2d(48, 40, 0.0, 1.0, 0.0, 1.0),
+                      G.BoundaryCondition(G.TRANSMISSIVE, G.TRANSMISSIVE, G.PERIODIC, G.PERIODIC),
+                      1.4, (1.4, 1.67, 1.3, 1.5), quad_regions, G.SchemeParams(beta=1.3), 0.4,
+                      1e30, 30)
+    first = CS.MatCase("mm_first_order", G.make_grid_2d(40, 20, 0.0, 7.0, 0.0, 3.0),
+                       G.BoundaryCondition.uniform(G.REFLECTIVE), 1.4, (1.5, 1.4, 1.5),
+                       CS.triple_point().regions,
+                       G.SchemeParams(beta=1.5, spatial_order=1, time_order=1), 0.25, 1e30, 30)
+    return {
+        "mm_contact_equal_64": CS.material_contact_1d(64, (1.4, 1.4), 1.4, 100),
+        "mm_contact_unequal_64": CS.material_contact_1d(64, (1.5, 1.4), 1.5, 50),
+        "mm_triple_70x30": CS.triple_point(70, 30, 40),
+        "mm_quadrant_48x40": quad,
+        "mm_first_order_40x20": first,
+    }
+
+
+def run_reference_mat(c):
+    from paper_1607_08710_b200 import multimat as MM
+    f0, mat0 = CS.regions_field(c)
+    r = O.RefSolver(c.grid, c.bc, c.gamma, c.params, threads=1,
+                    materials=MM.make_material_set(c.material_gammas))
+    r.set_state(f0)
+    r.set_partials(mat0.partial)
+    diag = r.heun_steps(c.max_steps, c.cfl, c.t_final)
+    f, t, s, acc = r.get_state()
+    return f0, mat0.partial, diag, f, r.get_partials(), np.array(acc)
+
+
 def run_reference(case, steps):
     f0 = CS.initial_field(case)
     r = O.RefSolver(case.grid, case.bc, case.gamma, case.params, threads=1)
@@ -61,6 +98,19 @@ def run_reference(case, steps):
         diag = r.heun_steps(steps, case.cfl, case.t_final)
     f, t, s, acc = r.get_state()
     return f0, diag, f, np.array(acc)
+
+
+def main_mat(force=False):
+    for name, c in golden_mat_cases().items():
+        path = os.path.join(OUT, f"{name}.npz")
+        if os.path.exists(path) and not force:
+            continue
+        f0, p0, diag, f, p, acc = run_reference_mat(c)
+        g = c.grid
+        np.savez_compressed(path, initial=g.interior(f0), initial_partial=g.interior(p0),
+                            final=g.interior(f), final_partial=g.interior(p), diag=diag,
+                            outflow=acc)
+        print(name, c.max_steps, diag[0, 0], diag[-1, 0], diag[-1, 1], diag[-1, 3])
 
 
 def main():
@@ -113,4 +163,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "mat" in sys.argv[1:]:
+        main_mat(force="--force" in sys.argv)
+    else:
+        main()
