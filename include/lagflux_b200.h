@@ -21,6 +21,11 @@
  *                                  time / diagnostics kept on the device
  *   lf_init_fourier                (new) on-device seeded smooth-flow IC (BASELINE 4-5)
  *   lf_last_error                  the exception object (what(), PositivityError fields)
+ *   lf_set_materials               the constructor's `const MaterialSet*` (solver.cpp:61-88)
+ *                                  with make_material_set's checks (multimat.cpp:7-15)
+ *   lf_upload_partials /           MaterialCells::partial host <-> device
+ *   lf_download_partials           (multimat.hpp:21-30); heun_step(state, controls,
+ *                                  limit, &mat) is lf_heun_step once they are resident
  */
 #ifndef LAGFLUX_B200_H
 #define LAGFLUX_B200_H
@@ -46,7 +51,8 @@ enum {
   LF_ERR_TRACE = 5,        /* InvalidStateError in compute_fluxes (solver.cpp:245-255) */
   LF_ERR_POSITIVITY = 6,   /* PositivityError in apply_update (solver.cpp:310-326) */
   LF_ERR_DEVICE = 7,       /* CUDA / NCCL failure (no reference counterpart) */
-  LF_ERR_ARGUMENT = 8      /* invalid argument to this ABI */
+  LF_ERR_ARGUMENT = 8,     /* invalid argument to this ABI */
+  LF_ERR_FRACTION = 9      /* InvalidStateError in fill_all_ghosts (solver.cpp:122-127) */
 };
 
 /* Heun-step implementation for lf_heun_step / lf_advance (all give identical results):
@@ -121,6 +127,19 @@ int lf_slab_partition(int ny, int nranks, int rank, int* row0, int* nrows);
  * (apply_boundary, grid.cpp:116-121). */
 int lf_upload(lf_handle* h, double* const field[4], int64_t ld);
 int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghosts);
+
+/* Multimaterial partial-density transport (solver.cpp:90-129, 331-404, 519-540).
+ * lf_set_materials: once, before stepping; n in [1, 16], gammas in (1, 3]
+ * (LF_ERR_CONFIG with make_material_set's message otherwise).  With a material
+ * set every Heun step also advects the n partial densities rho*y_k, uses the
+ * mixed-cell gamma of each cell (each face side its own EOS), reports a fraction
+ * outside [0,1] beyond round-off as LF_ERR_FRACTION, and returns the min
+ * pressure from the fresh partials; the stage-wise kernels run these steps.
+ * Partials: n arrays in the ghosted field layout (partials[k][j*ld + i],
+ * ld >= nx + 4); interior cells are transferred. */
+int lf_set_materials(lf_handle* h, int n, const double* gammas);
+int lf_upload_partials(lf_handle* h, double* const* partials, int64_t ld);
+int lf_download_partials(lf_handle* h, double* const* partials, int64_t ld);
 
 /* Seeded smooth-perturbation initial state (BASELINE configs 4-5), generated on the device. */
 int lf_init_fourier(lf_handle* h, uint64_t seed);

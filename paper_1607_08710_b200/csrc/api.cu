@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -114,6 +115,14 @@ void free_slab(SlabState& s) {
   cudaFree(s.scal);
   cudaFreeHost(s.scal_host);
   cudaFree(s.aux);
+  cudaFree(s.P);
+  cudaFree(s.Ps);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(s.Y[k]);
+    cudaFree(s.GC[k]);
+    cudaFree(s.USX[k]);
+    cudaFree(s.USY[k]);
+  }
   if (s.ev_a) cudaEventDestroy(s.ev_a);
   if (s.ev_b) cudaEventDestroy(s.ev_b);
   if (s.own_stream) cudaStreamDestroy(s.own_stream);
@@ -158,7 +167,7 @@ void slab_rows(int ny, int n, int s, int* y0, int* rows) {
 // ---------------------------------------------------------------- halos
 // Copy the NG boundary rows (full padded width, x ghosts included, so corners
 // wrap as in grid.cpp:98-113) between neighbouring in-process slabs.
-void exchange_local(lf_handle* h, double* SlabState::*buf) {
+void exchange_local(lf_handle* h, double* SlabState::*buf, int ncomp = 4) {
   const int n = (int)h->slabs.size();
   if (n == 1) return;
   const bool periodic = h->d.bc[2] == LF_PERIODIC;
@@ -179,7 +188,7 @@ void exchange_local(lf_handle* h, double* SlabState::*buf) {
       CK(cudaStreamWaitEvent(dst.stream, src.ev_a, 0));
       const int src_row = side == 0 ? src.L.ny - NG : 0;
       const int dst_row = side == 0 ? -NG : dst.L.ny;
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < ncomp; ++c) {
         const double* sp = (src.*buf) + src.L.origin() + c * src.L.fstride +
                            (int64_t)src_row * src.L.pitch - NG;
         double* dp = (dst.*buf) + dst.L.origin() + c * dst.L.fstride +
@@ -204,24 +213,28 @@ void exchange_local(lf_handle* h, double* SlabState::*buf) {
 }
 
 // Ghost cells of `buf` on every slab: x sides, halo rows, then y sides at the
-// domain edges (grid.cpp:79-113 order).
-void fill_all(lf_handle* h, double* SlabState::*buf) {
+// domain edges (grid.cpp:79-113 order).  A conserved field by default; the
+// partial densities are ncomp = n_mat even-parity components (odd = -1).
+void fill_all(lf_handle* h, double* SlabState::*buf, int ncomp = 4, int odd_x = 1,
+              int odd_y = 2) {
   const int xbc[4] = {h->d.bc[0], h->d.bc[1], h->d.bc[2], h->d.bc[3]};
   for (auto& s : h->slabs) {
     CK(cudaSetDevice(s.device));
-    launch_fill_x(s.field(s.*buf), s.L, xbc, s.stream);
+    launch_fill_x(s.field(s.*buf), s.L, xbc, s.stream, ncomp, odd_x);
   }
   if (h->nccl)
-    nccl_exchange_halos(h, buf);
+    nccl_exchange_halos(h, buf, ncomp);
   else
-    exchange_local(h, buf);
+    exchange_local(h, buf, ncomp);
   for (auto& s : h->slabs) {
     if (!h->dim2 || !(s.sl.fill_lo || s.sl.fill_hi)) continue;
     CK(cudaSetDevice(s.device));
-    launch_fill_y_only(s.field(s.*buf), s.L, xbc, s.sl, s.stream);
+    launch_fill_y_only(s.field(s.*buf), s.L, xbc, s.sl, s.stream, ncomp, odd_y);
   }
   CK(cudaGetLastError());
 }
+
+void fill_partials(lf_handle* h, double* SlabState::*buf) { fill_all(h, buf, h->mc.n, -1, -1); }
 
 void sync_all(lf_handle* h) {
   for (auto& s : h->slabs) {
@@ -255,6 +268,8 @@ Scalars combined_scalars(lf_handle* h, int slot) {
     r.fail_update = std::min(r.fail_update, x.fail_update);
     r.min_rho_bits = std::min(r.min_rho_bits, x.min_rho_bits);
     r.min_eint_bits = std::min(r.min_eint_bits, x.min_eint_bits);
+    r.fail_frac = std::min(r.fail_frac, x.fail_frac);
+    r.min_p_key = std::min(r.min_p_key, x.min_p_key);
   }
   if (h->nccl) nccl_combine_scalars(h, &r);
   return r;
@@ -278,12 +293,31 @@ bool fetch_cell(lf_handle* h, double* SlabState::*buf, int i, int jg, double v[4
 }
 
 // ---------------------------------------------------------------- error records
-int report_prim(lf_handle* h, double* SlabState::*buf, long long c, int64_t step) {
+// The mixed-cell gamma of cell (i, jg) in slot gslot.
+bool fetch_gamma(lf_handle* h, int gslot, int i, int jg, double* v) {
+  for (auto& s : h->slabs) {
+    const int jl = jg - s.sl.y0;
+    const bool inside = jl >= 0 && jl < s.L.ny;
+    const bool ghost_lo = s.sl.fill_lo && jl >= -2 && jl < 0;
+    const bool ghost_hi = s.sl.fill_hi && jl >= s.L.ny && jl < s.L.ny + 2;
+    if (!(inside || ghost_lo || ghost_hi)) continue;
+    CK(cudaSetDevice(s.device));
+    CK(cudaMemcpy(v, s.GC[gslot] + s.L.origin() + (int64_t)jl * s.L.pitch + i, sizeof(double),
+                  cudaMemcpyDeviceToHost));
+    return true;
+  }
+  return false;
+}
+
+int report_prim(lf_handle* h, double* SlabState::*buf, long long c, int64_t step, int gslot = 0) {
   const int gy = h->dim2 ? 2 : 0;
   const long long nxt = h->d.nx + 4;
   const long long ii = c % nxt - 2, jj = c / nxt - gy;
   double v[4] = {0, 0, 0, 0};
   fetch_cell(h, buf, (int)ii, (int)jj, v);
+  // build_primitives reports with the cell's own EOS (solver.cpp:165-167)
+  double gamma = h->d.gamma;
+  if (h->mc.n) fetch_gamma(h, gslot, (int)ii, (int)jj, &gamma);
   // primitive_from_conserved with CellContext (euler.hpp:73-85)
   const char* what;
   double value;
@@ -293,7 +327,7 @@ int report_prim(lf_handle* h, double* SlabState::*buf, long long c, int64_t step
   } else {
     const double inv = 1.0 / v[0];
     const double kinetic = 0.5 * (v[1] * v[1] + v[2] * v[2]) * inv;
-    value = (h->d.gamma - 1.0) * (v[3] - kinetic);
+    value = (gamma - 1.0) * (v[3] - kinetic);
     what = "non-positive pressure";
   }
   char suffix[96];
@@ -344,6 +378,17 @@ int report_update(lf_handle* h, double* SlabState::*out, long long cc, int64_t s
   return LF_ERR_POSITIVITY;
 }
 
+// fill_all_ghosts' fraction check (solver.cpp:122-127): smallest ghosted index
+int report_frac(lf_handle* h, long long c) {
+  const int gy = h->dim2 ? 2 : 0;
+  const long long nxt = h->d.nx + 4;
+  const long long i = c % nxt - 2, j = c / nxt - gy;
+  set_err(h, LF_ERR_FRACTION, "mass fraction out of [0,1] beyond round-off at cell (%lld,%lld)", i, j);
+  h->err.i = i;
+  h->err.j = j;
+  return LF_ERR_FRACTION;
+}
+
 // dt from the combined rate (solver.cpp:471-479)
 int finish_dt(lf_handle* h, const Scalars& sc, double cfl, double time, double limit, double* dt) {
   if (sc.fail_dt != LLONG_MAX) {
@@ -368,26 +413,53 @@ int finish_dt(lf_handle* h, const Scalars& sc, double cfl, double time, double l
 }
 
 // CFL rate of `buf` (ghosts not needed) into scalars slot 0.
-void launch_rate_all(lf_handle* h, double* SlabState::*buf) {
+// With materials: gamma_[0] of the last fill (solver.cpp:441), and when `part`
+// is given the fraction closure of (buf, part) is computed first (heun_step's
+// fill_all_ghosts(state.field, mat, 0), solver.cpp:491).
+void launch_rate_all(lf_handle* h, double* SlabState::*buf, double* SlabState::*part = nullptr) {
   for (auto& s : h->slabs) {
     CK(cudaSetDevice(s.device));
     reset_scalars(&s.scal[0], s.stream);
-    launch_rate(s.field(s.*buf), s.L, s.sl, h->k, h->dim2, &s.scal[0], s.stream);
+    if (h->mc.n) {
+      if (part)
+        launch_mat_fractions(s.field(s.*buf), s.field(s.*part), s.field(s.Y[0]), s.field(s.GC[0]),
+                             s.L, s.sl, h->mc, h->dim2, &s.scal[0], s.stream);
+      launch_rate_g(s.field(s.*buf), s.field(s.GC[0]), s.L, s.sl, h->k, h->dim2, &s.scal[0],
+                    s.stream);
+    } else {
+      launch_rate(s.field(s.*buf), s.L, s.sl, h->k, h->dim2, &s.scal[0], s.stream);
+    }
   }
 }
 
 // One stage on every slab: prims(in) -> fluxes(set k) -> update(base, ...) -> out.
+// With materials the stage uses the mixed-cell gamma of slot gslot; when
+// `part` is given (the corrector's fill_all_ghosts(predictor_, &predictor_mat_,
+// 1), solver.cpp:504) that slot's fractions are computed from (in, part) first.
 void staged_stage(lf_handle* h, double* SlabState::*in, double* SlabState::*base,
-                  double* SlabState::*out, int k, bool two, double dt, int slot) {
+                  double* SlabState::*out, int k, bool two, double dt, int slot,
+                  double* SlabState::*part = nullptr, int gslot = 0) {
   fill_all(h, in);
+  if (h->mc.n && part) fill_partials(h, part);
   for (auto& s : h->slabs) {
     CK(cudaSetDevice(s.device));
     reset_scalars(&s.scal[slot], s.stream);
-    launch_prims(s.field(s.*in), s.field(s.W), s.L, s.sl, h->k.gm1, h->dim2, &s.scal[slot],
-                 s.stream);
     const FluxArr fx = s.fluxx(k), fy = s.fluxy(k);
-    launch_fluxes(s.field(s.W), fx, fy, s.L, s.sl, h->k, h->d.spatial_order >= 2, h->dim2,
-                  &s.scal[slot], s.stream);
+    if (h->mc.n) {
+      if (part)
+        launch_mat_fractions(s.field(s.*in), s.field(s.*part), s.field(s.Y[gslot]),
+                             s.field(s.GC[gslot]), s.L, s.sl, h->mc, h->dim2, &s.scal[slot],
+                             s.stream);
+      launch_prims_g(s.field(s.*in), s.field(s.W), s.field(s.GC[gslot]), s.L, s.sl, h->dim2,
+                     &s.scal[slot], s.stream);
+      launch_fluxes_g(s.field(s.W), s.field(s.GC[gslot]), fx, fy, s.ustx(k), s.usty(k), s.L,
+                      s.sl, h->k, h->d.spatial_order >= 2, h->dim2, &s.scal[slot], s.stream);
+    } else {
+      launch_prims(s.field(s.*in), s.field(s.W), s.L, s.sl, h->k.gm1, h->dim2, &s.scal[slot],
+                   s.stream);
+      launch_fluxes(s.field(s.W), fx, fy, s.L, s.sl, h->k, h->d.spatial_order >= 2, h->dim2,
+                    &s.scal[slot], s.stream);
+    }
     const FluxArr fx0 = s.fluxx(0), fy0 = s.fluxy(0);
     launch_update(s.field(s.*base), fx0, fy0, two ? &fx : nullptr, two ? &fy : nullptr,
                   s.field(s.*out), s.L, s.sl, dt, h->d.dx, h->d.dy, h->dim2, &s.scal[slot],
@@ -449,20 +521,58 @@ void swap_state(lf_handle* h, double* SlabState::*a, double* SlabState::*b) {
 
 // Check the stage scalars in the reference's order.
 int check_stage(lf_handle* h, const Scalars& sc, double* SlabState::*in,
-                double* SlabState::*out, int64_t step, double dt) {
-  if (sc.fail_prim != LLONG_MAX) return report_prim(h, in, sc.fail_prim, step);
+                double* SlabState::*out, int64_t step, double dt, int gslot = 0) {
+  if (sc.fail_frac != LLONG_MAX) return report_frac(h, sc.fail_frac);
+  if (sc.fail_prim != LLONG_MAX) return report_prim(h, in, sc.fail_prim, step, gslot);
   if (sc.fail_trace != LLONG_MAX) return report_trace(h, sc.fail_trace, step);
   if (sc.fail_update != LLONG_MAX) return report_update(h, out, sc.fail_update, step, dt);
   return 0;
 }
 
+// update_partials (solver.cpp:331-404) on every slab: out = base - flux of set
+// 0 (fractions slot 0) [and set 1 (slot 1)].
+void update_partials_all(lf_handle* h, double* SlabState::*base, double* SlabState::*out,
+                         bool two, double dt) {
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    const FluxArr fx1 = s.fluxx(1), fy1 = s.fluxy(1), ux1 = s.ustx(1), uy1 = s.usty(1);
+    const Field y1 = s.field(s.Y[1]);
+    launch_update_partials(s.field(s.*base), s.fluxx(0), s.fluxy(0), s.ustx(0), s.usty(0),
+                           s.field(s.Y[0]), two ? &fx1 : nullptr, two ? &fy1 : nullptr,
+                           two ? &ux1 : nullptr, two ? &uy1 : nullptr, two ? &y1 : nullptr,
+                           s.field(s.*out), s.L, h->mc.n, dt, h->d.dx, h->d.dy, h->dim2,
+                           s.stream);
+  }
+  CK(cudaGetLastError());
+}
+
+// solver.cpp:519-538: min over interior cells of e_int / sum_k y_k/(gamma_k - 1)
+double material_min_p(lf_handle* h) {
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    reset_scalars(&s.scal[3], s.stream);
+    launch_mat_min_p(s.field(s.U), s.field(s.P), s.L, h->mc, &s.scal[3], s.stream);
+  }
+  const unsigned long long key = combined_scalars(h, 3).min_p_key;
+  if (key == ~0ull) return std::numeric_limits<double>::infinity();  // min_p's initial value
+  const unsigned long long b = (key >> 63) ? (key & 0x7fffffffffffffffull) : ~key;
+  return bits_to_double(b);
+}
+
 int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t step,
                 double* outflow, lf_step_out* out) {
+  const bool mat = h->mc.n > 0;
+  if (mat && !h->partials_ready)
+    return set_err(h, LF_ERR_CONFIG, "multimaterial step needs material storage");
   for (auto& s : h->slabs) alloc_staged(s);
+  // fill_all_ghosts(state.field, mat, 0) then compute_dt (solver.cpp:491-492)
   fill_all(h, &SlabState::U);
-  launch_rate_all(h, &SlabState::U);
+  if (mat) fill_partials(h, &SlabState::P);
+  launch_rate_all(h, &SlabState::U, mat ? &SlabState::P : nullptr);
+  const Scalars s0 = combined_scalars(h, 0);
+  if (s0.fail_frac != LLONG_MAX) return report_frac(h, s0.fail_frac);
   double dt = 0.0;
-  int rc = finish_dt(h, combined_scalars(h, 0), cfl, time, limit, &dt);
+  int rc = finish_dt(h, s0, cfl, time, limit, &dt);
   if (rc) return rc;
   const bool hits = time + dt >= limit;
 
@@ -471,24 +581,29 @@ int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t ste
   const Scalars s1 = combined_scalars(h, 1);
   rc = check_stage(h, s1, &SlabState::U, &SlabState::Us, step, dt);
   if (rc) return rc;
+  if (mat) update_partials_all(h, &SlabState::P, &SlabState::Ps, false, dt);  // :501
   double min_rho = bits_to_double(s1.min_rho_bits), min_eint = bits_to_double(s1.min_eint_bits);
   double acc[4] = {0, 0, 0, 0};
   if (outflow) std::memcpy(acc, outflow, sizeof acc);
 
   if (h->d.time_order >= 2) {
     // corrector: Us -> U2 from U^n with 0.5*(F1 + F2) (solver.cpp:503-509)
-    staged_stage(h, &SlabState::Us, &SlabState::U, &SlabState::U2, 1, true, dt, 2);
+    staged_stage(h, &SlabState::Us, &SlabState::U, &SlabState::U2, 1, true, dt, 2,
+                 mat ? &SlabState::Ps : nullptr, 1);
     const Scalars s2 = combined_scalars(h, 2);
-    if (s2.fail_prim != LLONG_MAX) return report_prim(h, &SlabState::Us, s2.fail_prim, step);
+    if (s2.fail_frac != LLONG_MAX) return report_frac(h, s2.fail_frac);
+    if (s2.fail_prim != LLONG_MAX) return report_prim(h, &SlabState::Us, s2.fail_prim, step, 1);
     if (s2.fail_trace != LLONG_MAX) return report_trace(h, s2.fail_trace, step);
     // the reference writes the corrector in place before it throws
     swap_state(h, &SlabState::U, &SlabState::U2);
     if (s2.fail_update != LLONG_MAX) return report_update(h, &SlabState::U, s2.fail_update, step, dt);
+    if (mat) update_partials_all(h, &SlabState::P, &SlabState::P, true, dt);  // :508, in place
     min_rho = bits_to_double(s2.min_rho_bits);
     min_eint = bits_to_double(s2.min_eint_bits);
     boundary_outflow(h, true, dt, acc);
   } else {
     swap_state(h, &SlabState::U, &SlabState::Us);  // std::swap(state.field.comp, predictor_.comp)
+    if (mat) swap_state(h, &SlabState::P, &SlabState::Ps);
     boundary_outflow(h, false, dt, acc);
   }
   h->rate_valid = false;
@@ -500,13 +615,13 @@ int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t ste
     out->time = hits ? limit : time + dt;
     out->step = step + 1;
     out->min_rho = min_rho;
-    out->min_p = (h->d.gamma - 1.0) * min_eint;
+    out->min_p = mat ? material_min_p(h) : (h->d.gamma - 1.0) * min_eint;
   }
   return 0;
 }
 
 bool use_fused(lf_handle* h) {
-  if (h->path == LF_PATH_STAGED) return false;
+  if (h->path == LF_PATH_STAGED || h->mc.n > 0) return false;  // materials: stage-wise kernels
   return fused_supported(h);
 }
 
@@ -688,6 +803,88 @@ int lf_upload(lf_handle* h, double* const field[4], int64_t ld) {
   });
 }
 
+// ---- multimaterial (multimat.hpp; solver.cpp:61-88 MaterialSet argument) ----
+int lf_set_materials(lf_handle* h, int n, const double* gammas) {
+  return guarded(h, [&] {
+    // make_material_set, multimat.cpp:7-15
+    if (n < 1) return set_err(h, LF_ERR_CONFIG, "material set needs at least one material");
+    if (n > MAX_MATERIALS) return set_err(h, LF_ERR_CONFIG, "at most 16 materials are supported");
+    if (!gammas) return set_err(h, LF_ERR_ARGUMENT, "gammas is null");
+    for (int k = 0; k < n; ++k)
+      if (!(gammas[k] > 1.0) || !(gammas[k] <= 3.0))
+        return set_err(h, LF_ERR_CONFIG, "material adiabatic index must lie in (1, 3], got %s",
+                       fmt_f(gammas[k]).c_str());
+    if (h->mc.n) return set_err(h, LF_ERR_CONFIG, "the material set is fixed at construction");
+    h->mc.n = n;
+    for (int k = 0; k < n; ++k) h->mc.gamma[k] = gammas[k];
+    for (auto& s : h->slabs) {
+      alloc_staged(s);
+      CK(cudaSetDevice(s.device));
+      const size_t kb = ((size_t)n * s.L.fstride + s.L.pitch) * sizeof(double);
+      const size_t gb = ((size_t)s.L.fstride + s.L.pitch) * sizeof(double);
+      CK(cudaMalloc(&s.P, kb));
+      CK(cudaMalloc(&s.Ps, kb));
+      CK(cudaMemsetAsync(s.P, 0, kb, s.stream));
+      CK(cudaMemsetAsync(s.Ps, 0, kb, s.stream));
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaMalloc(&s.Y[k], kb));
+        CK(cudaMemsetAsync(s.Y[k], 0, kb, s.stream));
+        // gamma_[s].assign(cells, eos.gamma) (solver.cpp:81)
+        CK(cudaMalloc(&s.GC[k], gb));
+        fill_value(s.GC[k], (int64_t)(gb / sizeof(double)), h->d.gamma, s.stream);
+        CK(cudaMalloc(&s.USX[k], (size_t)s.fx_stride * sizeof(double)));
+        CK(cudaMalloc(&s.USY[k], (size_t)s.fy_stride * sizeof(double)));
+        CK(cudaMemsetAsync(s.USX[k], 0, (size_t)s.fx_stride * sizeof(double), s.stream));
+        CK(cudaMemsetAsync(s.USY[k], 0, (size_t)s.fy_stride * sizeof(double), s.stream));
+      }
+    }
+    sync_all(h);
+    fused_invalidate(h);
+    return 0;
+  });
+}
+
+int lf_upload_partials(lf_handle* h, double* const* partials, int64_t ld) {
+  return guarded(h, [&] {
+    if (!h->mc.n) return set_err(h, LF_ERR_CONFIG, "no material set (lf_set_materials)");
+    if (!partials || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad partials or ld");
+    const int gy = h->dim2 ? 2 : 0;
+    for (auto& s : h->slabs) {
+      CK(cudaSetDevice(s.device));
+      for (int k = 0; k < h->mc.n; ++k) {
+        const double* src = partials[k] + (int64_t)(s.sl.y0 + gy) * ld + 2;
+        double* dst = s.P + s.L.origin() + k * s.L.fstride;
+        CK(cudaMemcpy2DAsync(dst, s.L.pitch * sizeof(double), src, ld * sizeof(double),
+                             (size_t)s.L.nx * sizeof(double), (size_t)s.L.ny, cudaMemcpyDefault,
+                             s.stream));
+      }
+    }
+    sync_all(h);
+    h->partials_ready = 1;
+    return 0;
+  });
+}
+
+int lf_download_partials(lf_handle* h, double* const* partials, int64_t ld) {
+  return guarded(h, [&] {
+    if (!h->mc.n) return set_err(h, LF_ERR_CONFIG, "no material set (lf_set_materials)");
+    if (!partials || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad partials or ld");
+    const int gy = h->dim2 ? 2 : 0;
+    for (auto& s : h->slabs) {
+      CK(cudaSetDevice(s.device));
+      for (int k = 0; k < h->mc.n; ++k) {
+        double* dst = partials[k] + (int64_t)(s.sl.y0 + gy) * ld + 2;
+        const double* src = s.P + s.L.origin() + k * s.L.fstride;
+        CK(cudaMemcpy2DAsync(dst, ld * sizeof(double), src, s.L.pitch * sizeof(double),
+                             (size_t)s.L.nx * sizeof(double), (size_t)s.L.ny, cudaMemcpyDefault,
+                             s.stream));
+      }
+    }
+    sync_all(h);
+    return 0;
+  });
+}
+
 int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghosts) {
   return guarded(h, [&] {
     if (!field || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad field or ld");
@@ -854,6 +1051,9 @@ int lf_device_bytes(lf_handle* h, int64_t* bytes) {
   for (auto& s : h->slabs) {
     b += 2 * s.L.alloc * 8;
     if (s.Us) b += 2 * s.L.alloc * 8 + 2 * 4 * (s.fx_stride + s.fy_stride) * 8;
+    if (s.P)
+      b += (4 * ((int64_t)h->mc.n * s.L.fstride + s.L.pitch) + 2 * (s.L.fstride + s.L.pitch) +
+            2 * (s.fx_stride + s.fy_stride)) * 8;
   }
   *bytes = b + fused_bytes(h);
   return 0;

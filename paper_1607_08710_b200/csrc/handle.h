@@ -34,10 +34,19 @@ struct SlabState {
   Scalars* scal_host = nullptr;      // pinned mirror
   unsigned long long* aux = nullptr; // device scratch (Fourier maxima)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // multimaterial (lf_set_materials; same Layout strides, n_mat components)
+  double* P = nullptr;               // partial densities of U
+  double* Ps = nullptr;              // partial densities of U* (predictor_mat_)
+  double* Y[2] = {nullptr, nullptr}; // clamped fractions per slot (frac_)
+  double* GC[2] = {nullptr, nullptr};  // mixed-cell gamma per slot (gamma_), 1 component
+  double* USX[2] = {nullptr, nullptr}; // u* of the x faces of flux set k (ustar_x)
+  double* USY[2] = {nullptr, nullptr}; // u* of the y faces (ustar_y)
 
   Field field(double* p) const { return Field{p + L.origin(), L.pitch, L.fstride}; }
   FluxArr fluxx(int k) const { return FluxArr{FX[k], L.pitch, fx_stride}; }
   FluxArr fluxy(int k) const { return FluxArr{FY[k], L.pitch, fy_stride}; }
+  FluxArr ustx(int k) const { return FluxArr{USX[k], L.pitch, fx_stride}; }
+  FluxArr usty(int k) const { return FluxArr{USY[k], L.pitch, fy_stride}; }
 };
 
 struct Nccl;  // nccl.cpp
@@ -56,6 +65,9 @@ struct lf_handle {
   bool rate_valid = false;           // scal[0].rate_bits holds the rate of the current U
   void* fused = nullptr;             // lfb::FusedState (fused_step.cu)
   lf_error err{};
+  // multimaterial: material table and whether partial densities were uploaded
+  lfb::MatConsts mc{};
+  int partials_ready = 0;
 };
 
 namespace lfb {

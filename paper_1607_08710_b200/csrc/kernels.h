@@ -25,7 +25,8 @@ struct Scalars {
   double time;                       // state time after the step (device-resident runs)
   int hits;                          // time + dt >= limit
   int status;                        // 0 ok, else an LF_ERR_* kind detected in this step
-  double pad[2];
+  long long fail_frac;               // smallest failing ghosted index in the fraction closure
+  unsigned long long min_p_key;      // multimaterial min p (order-preserving key of a double)
 };
 
 // Slab geometry: local rows [0, ny) are global rows [y0, y0+ny) of ny_global.
@@ -52,9 +53,12 @@ void reset_scalars(Scalars* s, cudaStream_t st);
 
 // ghost fill (grid.cpp:72-114), 4 layers: x sides over interior rows, then
 // (after any halo exchange) y sides over every column at the domain edges.
-void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_t st);
+// ncomp components; component odd_x flips sign in a reflective x image,
+// odd_y in a y image (a conserved field: 1 and 2; partial densities: none, -1).
+void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_t st,
+                   int ncomp = 4, int odd_x = 1);
 void launch_fill_y_only(const Field& f, const Layout& L, const int bc[4], const Slab& sl,
-                        cudaStream_t st);
+                        cudaStream_t st, int ncomp = 4, int odd_y = 2);
 
 // Boundary-face fluxes for accumulate_boundary_outflow (solver.cpp:406-432):
 // out = [left 4 x ny | right 4 x ny | bottom 4 x nx | top 4 x nx], Heun-averaged when two.
@@ -84,5 +88,41 @@ void launch_fourier_raw(const Field& f, const Layout& L, const double* tx, const
 void launch_absmax(const Field& f, const Layout& L, unsigned long long* out4, cudaStream_t st);
 void launch_fourier_finish(const Field& f, const Layout& L, const unsigned long long* max4,
                            double gamma, cudaStream_t st);
+
+// ---------------------------------------------------------------- multimaterial
+// (solver.cpp:90-129, 331-404, 519-540; csrc/material_kernels.cu)
+constexpr int MAX_MATERIALS = 16;
+struct MatConsts {
+  int n;
+  double gamma[MAX_MATERIALS];
+};
+
+// fill_all_ghosts' closure over the reference's ghosted cells: clamped
+// fractions y_k = partial_k / rho into y (n comps) and the mixed-cell gamma
+// into gcell (1 comp); failures -> s->fail_frac.
+void launch_mat_fractions(const Field& u, const Field& part, const Field& y, const Field& gcell,
+                          const Layout& L, const Slab& sl, const MatConsts& mc, int dim2,
+                          Scalars* s, cudaStream_t st);
+// compute_dt / build_primitives / compute_fluxes with the per-cell gamma;
+// the fluxes also store u* per face (us.p: component 0 of a FluxArr).
+void launch_rate_g(const Field& u, const Field& gcell, const Layout& L, const Slab& sl,
+                   const Consts& k, int dim2, Scalars* s, cudaStream_t st);
+void launch_prims_g(const Field& u, const Field& w, const Field& gcell, const Layout& L,
+                    const Slab& sl, int dim2, Scalars* s, cudaStream_t st);
+void launch_fluxes_g(const Field& w, const Field& gcell, const FluxArr& fx, const FluxArr& fy,
+                     const FluxArr& usx, const FluxArr& usy, const Layout& L, const Slab& sl,
+                     const Consts& k, int muscl, int dim2, Scalars* s, cudaStream_t st);
+// update_partials: out_k = base_k - lam (per-material face fluxes of set a
+// [and b]); fractions of the upwind cells from ya [yb].
+void launch_update_partials(const Field& base, const FluxArr& fxa, const FluxArr& fya,
+                            const FluxArr& usxa, const FluxArr& usya, const Field& ya,
+                            const FluxArr* fxb, const FluxArr* fyb, const FluxArr* usxb,
+                            const FluxArr* usyb, const Field* yb, const Field& out,
+                            const Layout& L, int n_mat, double dt, double dx, double dy,
+                            int dim2, cudaStream_t st);
+// solver.cpp:522-538: min over interior cells of e_int / sum_k (y_k / (gamma_k - 1))
+void launch_mat_min_p(const Field& u, const Field& part, const Layout& L, const MatConsts& mc,
+                      Scalars* s, cudaStream_t st);
+void fill_value(double* p, int64_t n, double v, cudaStream_t st);
 
 }  // namespace lfb

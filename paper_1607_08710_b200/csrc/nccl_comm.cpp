@@ -121,7 +121,7 @@ void nccl_destroy(lf_handle* h) {
 // ring (both neighbours are the same peer): A sends the bottom NG rows down and
 // receives the top halo from above; B sends the top rows up and receives the
 // bottom halo from below.  Rows are whole padded rows (x ghosts included).
-void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf) {
+void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf, int ncomp) {
   SlabState& s = h->slabs[0];
   const bool periodic = h->d.bc[2] == LF_PERIODIC;
   const int R = h->nranks, r = h->rank;
@@ -131,11 +131,11 @@ void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf) {
   double* base = (s.*buf) + s.L.origin() - XPAD;  // row 0, allocation column 0
   auto rows = [&](int c, int row) { return base + c * s.L.fstride + (int64_t)row * s.L.pitch; };
   nck(g_api.GroupStart(), "ncclGroupStart");
-  for (int c = 0; c < 4; ++c) {  // phase A
+  for (int c = 0; c < ncomp; ++c) {  // phase A
     if (lo >= 0) nck(g_api.Send(rows(c, 0), n, ncclFloat64, lo, h->nccl->comm, s.stream), "ncclSend");
     if (hi >= 0) nck(g_api.Recv(rows(c, s.L.ny), n, ncclFloat64, hi, h->nccl->comm, s.stream), "ncclRecv");
   }
-  for (int c = 0; c < 4; ++c) {  // phase B
+  for (int c = 0; c < ncomp; ++c) {  // phase B
     if (hi >= 0)
       nck(g_api.Send(rows(c, s.L.ny - NG), n, ncclFloat64, hi, h->nccl->comm, s.stream), "ncclSend");
     if (lo >= 0) nck(g_api.Recv(rows(c, -NG), n, ncclFloat64, lo, h->nccl->comm, s.stream), "ncclRecv");
@@ -145,15 +145,17 @@ void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf) {
 
 void nccl_combine_scalars(lf_handle* h, Scalars* sc) {
   SlabState& s = h->slabs[0];
-  unsigned long long v[7] = {~sc->rate_bits,
+  unsigned long long v[9] = {~sc->rate_bits,
                              (unsigned long long)sc->fail_dt,
                              (unsigned long long)sc->fail_prim,
                              (unsigned long long)sc->fail_trace,
                              (unsigned long long)sc->fail_update,
                              sc->min_rho_bits,
-                             sc->min_eint_bits};
+                             sc->min_eint_bits,
+                             (unsigned long long)sc->fail_frac,
+                             sc->min_p_key};
   cck(cudaMemcpyAsync(h->nccl->dbuf, v, sizeof v, cudaMemcpyHostToDevice, s.stream), "copy");
-  nck(g_api.AllReduce(h->nccl->dbuf, h->nccl->dbuf, 7, ncclUint64, ncclMin, h->nccl->comm, s.stream),
+  nck(g_api.AllReduce(h->nccl->dbuf, h->nccl->dbuf, 9, ncclUint64, ncclMin, h->nccl->comm, s.stream),
       "ncclAllReduce");
   cck(cudaMemcpyAsync(v, h->nccl->dbuf, sizeof v, cudaMemcpyDeviceToHost, s.stream), "copy");
   cck(cudaStreamSynchronize(s.stream), "sync");
@@ -164,6 +166,8 @@ void nccl_combine_scalars(lf_handle* h, Scalars* sc) {
   sc->fail_update = (long long)v[4];
   sc->min_rho_bits = v[5];
   sc->min_eint_bits = v[6];
+  sc->fail_frac = (long long)v[7];
+  sc->min_p_key = v[8];
 }
 
 void nccl_max_u64(lf_handle* h, unsigned long long* v, int n) {

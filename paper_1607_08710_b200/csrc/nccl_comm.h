@@ -14,7 +14,7 @@ namespace lfb {
 int nccl_unique_id(void* id128);
 int nccl_init(lf_handle* h, const void* id128);
 void nccl_destroy(lf_handle* h);
-void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf);
+void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf, int ncomp = 4);
 void nccl_combine_scalars(lf_handle* h, Scalars* s);
 void nccl_max_u64(lf_handle* h, unsigned long long* v, int n);
 // fused step: max-reduce n u64 step accumulators and sum-reduce the boundary

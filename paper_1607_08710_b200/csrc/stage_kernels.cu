@@ -45,11 +45,11 @@ __device__ __forceinline__ long long warp_min_i64(long long v) {
 // grid.cpp:81-96: x sides over interior rows; each thread owns one
 // (component, row) and runs the reference's sequential l loop (l = 1..NG, the
 // first two layers are exactly the reference's, layers 3-4 extend the rule).
-__global__ void k_fill_x(Field f, int nx, int ny, int bc_lo, int bc_hi) {
+__global__ void k_fill_x(Field f, int nx, int ny, int bc_lo, int bc_hi, int odd_x) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (j >= ny) return;
-  const double sx = c == 1 ? -1.0 : 1.0;
+  const double sx = c == odd_x ? -1.0 : 1.0;
   double* row = f.comp(c) + (int64_t)j * f.pitch;
   for (int l = 1; l <= NG; ++l) {
     const int lo = -l;
@@ -68,11 +68,12 @@ __global__ void k_fill_x(Field f, int nx, int ny, int bc_lo, int bc_hi) {
 }
 
 // grid.cpp:98-113: y sides over every column (corners pick up the x ghosts).
-__global__ void k_fill_y(Field f, int nx, int ny, int bc_lo, int bc_hi, int do_lo, int do_hi) {
+__global__ void k_fill_y(Field f, int nx, int ny, int bc_lo, int bc_hi, int do_lo, int do_hi,
+                         int odd_y) {
   const int i = (int)(blockIdx.x * blockDim.x + threadIdx.x) - NG;
   const int c = blockIdx.y;
   if (i >= nx + NG) return;
-  const double sy = c == 2 ? -1.0 : 1.0;
+  const double sy = c == odd_y ? -1.0 : 1.0;
   double* col = f.comp(c) + i;
   const int64_t P = f.pitch;
   for (int l = 1; l <= NG; ++l) {
@@ -303,6 +304,8 @@ __global__ void k_reset(Scalars* s) {
   s->min_rho_bits = 0x7ff0000000000000ull;   // +inf
   s->min_eint_bits = 0x7ff0000000000000ull;
   s->status = 0;
+  s->fail_frac = LLONG_MAX;
+  s->min_p_key = ~0ull;
 }
 
 // ---------------------------------------------------------------- Fourier IC
@@ -368,14 +371,15 @@ void reset_scalars(Scalars* s, cudaStream_t st) {
   count_launch(), k_reset<<<1, 1, 0, st>>>(s);
 }
 
-void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_t st) {
-  count_launch(), k_fill_x<<<dim3(cdiv(L.ny, 128), 4), 128, 0, st>>>(f, L.nx, L.ny, bc[0], bc[1]);
+void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_t st, int ncomp,
+                   int odd_x) {
+  count_launch(), k_fill_x<<<dim3(cdiv(L.ny, 128), ncomp), 128, 0, st>>>(f, L.nx, L.ny, bc[0], bc[1], odd_x);
 }
 
 void launch_fill_y_only(const Field& f, const Layout& L, const int bc[4], const Slab& sl,
-                        cudaStream_t st) {
-  count_launch(), k_fill_y<<<dim3(cdiv(L.nx + 2 * NG, 128), 4), 128, 0, st>>>(f, L.nx, L.ny, bc[2], bc[3],
-                                                             sl.fill_lo, sl.fill_hi);
+                        cudaStream_t st, int ncomp, int odd_y) {
+  count_launch(), k_fill_y<<<dim3(cdiv(L.nx + 2 * NG, 128), ncomp), 128, 0, st>>>(
+      f, L.nx, L.ny, bc[2], bc[3], sl.fill_lo, sl.fill_hi, odd_y);
 }
 
 void launch_gather_boundary(const FluxArr& fxa, const FluxArr& fya, const FluxArr& fxb,

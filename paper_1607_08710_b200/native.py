@@ -8,12 +8,15 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import numpy as np
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liblagflux_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "lagflux_b200.h")
 
 LF_OK, LF_ERR_CONFIG, LF_ERR_DT_STATE, LF_ERR_DT_NONPOS = 0, 1, 2, 3
 LF_ERR_PRIMITIVE, LF_ERR_TRACE, LF_ERR_POSITIVITY, LF_ERR_DEVICE, LF_ERR_ARGUMENT = 4, 5, 6, 7, 8
+LF_ERR_FRACTION = 9
 LF_PATH_AUTO, LF_PATH_FUSED, LF_PATH_STAGED, LF_PATH_TWOPASS = 0, 1, 2, 3
 
 
@@ -50,6 +53,9 @@ SIGNATURES = [
     ("lf_local_rows", C.c_int, [H, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("lf_upload", C.c_int, [H, P4, C.c_int64]),
     ("lf_download", C.c_int, [H, P4, C.c_int64, C.c_int]),
+    ("lf_set_materials", C.c_int, [H, C.c_int, C.POINTER(C.c_double)]),
+    ("lf_upload_partials", C.c_int, [H, C.c_void_p, C.c_int64]),
+    ("lf_download_partials", C.c_int, [H, C.c_void_p, C.c_int64]),
     ("lf_init_fourier", C.c_int, [H, C.c_uint64]),
     ("lf_compute_dt", C.c_int, [H, C.c_double, C.c_double, C.c_double, DP]),
     ("lf_euler_stage", C.c_int, [H, C.c_double, C.c_int64]),
@@ -89,6 +95,13 @@ def lib():
             raise ImportError("liblagflux_b200.so ABI version mismatch")
         _lib = l
     return _lib
+
+
+def partial_ptrs(partial):
+    """double*[n] of the n contiguous (nyt, nxt) arrays of a partial-density stack."""
+    assert partial.dtype == np.float64 and partial.flags.c_contiguous and partial.ndim == 3
+    DPT = C.POINTER(C.c_double)
+    return (DPT * partial.shape[0])(*[partial[k].ctypes.data_as(DPT) for k in range(partial.shape[0])])
 
 
 def field_ptrs(field):

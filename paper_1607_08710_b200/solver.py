@@ -24,7 +24,7 @@ def _raise(e: N.lf_error):
         raise G.PositivityError(msg, e.i, e.j, e.step, e.dt)
     if e.kind == N.LF_ERR_CONFIG:
         raise G.ConfigError(msg)
-    if e.kind in (N.LF_ERR_DT_STATE, N.LF_ERR_PRIMITIVE, N.LF_ERR_TRACE):
+    if e.kind in (N.LF_ERR_DT_STATE, N.LF_ERR_PRIMITIVE, N.LF_ERR_TRACE, N.LF_ERR_FRACTION):
         raise G.InvalidStateError(msg)
     if e.kind == N.LF_ERR_DT_NONPOS:
         raise G.Error(msg)
@@ -45,11 +45,13 @@ class LagfluxSolver:
     devices: one entry per y-slab driven from this process (repeats allowed).
     dist:    (rank, nranks, device, nccl_id_bytes) for one-process-per-GPU slabs.
     path:    "auto" | "twopass" | "fused" | "staged" (Heun step implementation;
-             all produce identical results)."""
+             all produce identical results).
+    materials: a multimat.MaterialSet (the constructor's `const MaterialSet*`,
+             solver.cpp:61-88); heun_step then takes the MaterialCells."""
 
     def __init__(self, g: G.CartesianGrid, bc: G.BoundaryCondition, gamma: float = 1.4,
                  params: G.SchemeParams = G.SchemeParams(), threads: int = 1,
-                 devices: Sequence[int] = (0,), path: str = "auto", dist=None):
+                 materials=None, devices: Sequence[int] = (0,), path: str = "auto", dist=None):
         # constructor checks of solver.cpp:66-69
         if g.nx < 1 or g.ny < 1:
             raise G.ConfigError("grid has no interior cells")
@@ -76,6 +78,11 @@ class LagfluxSolver:
             _raise(err)
         self.set_path(path)
         self._resident = None  # SolverState whose field is on the device
+        self._resident_mat = None  # MaterialCells whose partials are on the device
+        self.materials = materials
+        if materials is not None:
+            gs = (C.c_double * materials.count())(*materials.gammas)
+            self._check(self._lib.lf_set_materials(self._h, materials.count(), gs))
 
     # ------------------------------------------------------------ plumbing
     def _error(self) -> N.lf_error:
@@ -138,10 +145,26 @@ class LagfluxSolver:
         self.upload(state.field)
         self._resident = state
 
-    def sync_to_host(self, state: G.SolverState, fill_ghosts: bool = False):
+    def sync_to_host(self, state: G.SolverState, fill_ghosts: bool = False, mat=None):
+        """Copy the device-resident state (and the MaterialCells' interior) back."""
         if self._resident is not state:
             raise G.Error("state is not resident on this solver")
         self.download(state.field, fill_ghosts)
+        if mat is not None:
+            if self._resident_mat is not mat:
+                raise G.Error("material cells are not resident on this solver")
+            self._check(self._lib.lf_download_partials(self._h, N.partial_ptrs(mat.partial),
+                                                       self._grid.nxt))
+
+    def _attach_mat(self, mat):
+        if self.materials is None:
+            return
+        if mat is None:
+            raise G.ConfigError("multimaterial step needs material storage")
+        if self._resident_mat is not mat:
+            self._check(self._lib.lf_upload_partials(self._h, N.partial_ptrs(mat.partial),
+                                                     self._grid.nxt))
+            self._resident_mat = mat
 
     def init_fourier(self, state: G.SolverState, seed: int):
         """Device-side seeded smooth-flow initial state (cases.fourier_*)."""
@@ -165,10 +188,13 @@ class LagfluxSolver:
         self.download(field_out)
 
     def heun_step(self, state: G.SolverState, controls: G.TimeControls,
-                  limit_time: float) -> float:
-        """LagfluxSolver::heun_step (solver.cpp:489-546) on the device-resident state."""
+                  limit_time: float, mat=None) -> float:
+        """LagfluxSolver::heun_step (solver.cpp:489-546) on the device-resident state;
+        with a material set, `mat` (multimat.MaterialCells) is advected too and stays
+        resident like the field (sync_to_host(state, mat=mat) copies it back)."""
         if self._resident is not state:
             self.attach(state)
+        self._attach_mat(mat)
         out = N.lf_step_out()
         acc = (C.c_double * 4)(*state.boundary_outflow)
         rc = self._lib.lf_heun_step(self._h, controls.cfl, state.time, limit_time, state.step,
@@ -183,10 +209,12 @@ class LagfluxSolver:
                                                    out.min_p))
         return out.dt
 
-    def advance(self, state: G.SolverState, controls: G.TimeControls, nsteps: int) -> int:
+    def advance(self, state: G.SolverState, controls: G.TimeControls, nsteps: int,
+                mat=None) -> int:
         """Up to nsteps heun_steps while time < t_final, with dt on the device (run.cpp:180-210)."""
         if self._resident is not state:
             self.attach(state)
+        self._attach_mat(mat)
         n = int(min(nsteps, max(0, controls.max_steps - state.step)))
         if n <= 0:
             return 0

@@ -58,3 +58,16 @@ def test_sm100a_cubin_only():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", N.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_partial_pointer_marshalling():
+    """n_mat partial-density arrays -> double*[n] (host only)."""
+    import ctypes as C
+    import numpy as np
+    from paper_1607_08710_b200 import native as N
+    p = np.arange(3 * 4 * 5, dtype=np.float64).reshape(3, 4, 5)
+    ptrs = N.partial_ptrs(p)
+    assert len(ptrs) == 3
+    for k in range(3):
+        assert C.cast(ptrs[k], C.c_void_p).value == p[k].ctypes.data
+        assert ptrs[k][7] == p[k].ravel()[7]
