@@ -14,12 +14,15 @@
 // interior back to state.field, exactly like the reference; a driver that only
 // reads the field at dumps calls set_auto_sync(false) and sync_to_host(state)
 // before each dump (one line in run.cpp's dump lambda) to avoid the copies.
+// MaterialCells (multimaterial runs) follow the same rule: uploaded on their
+// first step, copied back with the field.
 #pragma once
 
 #include <cstdint>
 #include <string>
 
 #include "lagflux/error.hpp"
+#include "lagflux/multimat.hpp"
 #include "lagflux/solver.hpp"
 #include "lagflux_b200.h"
 
@@ -36,8 +39,6 @@ class LagfluxSolver {
     if (g.gx < 2 || (g.dim == 2 && g.gy < 2))
       throw ConfigError("MUSCL stencils need at least two ghost layers");
     validate_boundary(bc, g.dim);
-    if (materials != nullptr)
-      throw ConfigError("multimaterial transport is not available on the B200 path");
     if (g.gx != 2 || g.gy != (g.dim == 2 ? 2 : 0))
       throw ConfigError("the B200 path uses the reference's ghost width 2");
     lf_desc d{};
@@ -56,7 +57,11 @@ class LagfluxSolver {
     d.bc[1] = kind(bc.x_high);
     d.bc[2] = kind(bc.y_low);
     d.bc[3] = kind(bc.y_high);
-    const int rc = lf_create(&d, &device, 1, &h_);
+    int rc = lf_create(&d, &device, 1, &h_);
+    if (rc == 0 && materials != nullptr) {
+      rc = lf_set_materials(h_, materials->count(), materials->gammas.data());
+      n_mat_ = materials->count();
+    }
     if (rc) {
       const std::string msg = error_text();
       lf_destroy(h_);
@@ -80,11 +85,16 @@ class LagfluxSolver {
   // solver.cpp:489-546
   double heun_step(SolverState& state, const TimeControls& controls, double limit_time,
                    MaterialCells* materials = nullptr) {
-    if (materials != nullptr)
-      throw ConfigError("multimaterial transport is not available on the B200 path");
+    if (n_mat_ == 0) materials = nullptr;  // solver.cpp:490
+    if (n_mat_ > 0 && materials == nullptr)
+      throw ConfigError("multimaterial step needs material storage");
     if (resident_ != &state) {
       upload(state.field);
       resident_ = &state;
+    }
+    if (materials != nullptr && resident_mat_ != materials) {
+      check(lf_upload_partials(h_, partial_ptrs(*materials).p, grid_.nxt()));
+      resident_mat_ = materials;
     }
     lf_step_out o{};
     const int rc = lf_heun_step(h_, controls.cfl, state.time, limit_time, state.step,
@@ -96,7 +106,10 @@ class LagfluxSolver {
     state.time = o.time;
     state.step = o.step;
     state.diagnostics.push_back({o.step, o.time, o.dt, o.min_rho, o.min_p});
-    if (auto_sync_) download(state.field);
+    if (auto_sync_) {
+      download(state.field);
+      if (materials != nullptr) check(lf_download_partials(h_, partial_ptrs(*materials).p, grid_.nxt()));
+    }
     return o.dt;
   }
 
@@ -115,9 +128,13 @@ class LagfluxSolver {
 
   // residency control (see the header comment)
   void set_auto_sync(bool on) { auto_sync_ = on; }
-  void sync_to_host(SolverState& state) const {
+  void sync_to_host(SolverState& state, MaterialCells* materials = nullptr) const {
     if (resident_ != &state) throw Error("state is not resident on this solver");
     download(state.field);
+    if (materials != nullptr) {
+      if (resident_mat_ != materials) throw Error("material cells are not resident on this solver");
+      check(lf_download_partials(h_, partial_ptrs(*materials).p, grid_.nxt()));
+    }
   }
   lf_handle* handle() const { return h_; }
 
@@ -140,7 +157,8 @@ class LagfluxSolver {
       case LF_ERR_CONFIG: throw ConfigError(e.message);
       case LF_ERR_DT_STATE:
       case LF_ERR_PRIMITIVE:
-      case LF_ERR_TRACE: throw InvalidStateError(e.message);
+      case LF_ERR_TRACE:
+      case LF_ERR_FRACTION: throw InvalidStateError(e.message);
       default: throw Error(e.message);
     }
   }
@@ -148,6 +166,14 @@ class LagfluxSolver {
     double* p[4] = {const_cast<double*>(f.comp[0].data()), const_cast<double*>(f.comp[1].data()),
                     const_cast<double*>(f.comp[2].data()), const_cast<double*>(f.comp[3].data())};
     check(lf_upload(h_, p, grid_.nxt()));
+  }
+  struct PartialPtrs {
+    double* p[16];
+  };
+  static PartialPtrs partial_ptrs(MaterialCells& m) {
+    PartialPtrs r{};
+    for (int k = 0; k < m.count() && k < 16; ++k) r.p[k] = m.partial[std::size_t(k)].data();
+    return r;
   }
   void download(CellField& f) const {
     double* p[4] = {f.comp[0].data(), f.comp[1].data(), f.comp[2].data(), f.comp[3].data()};
@@ -158,6 +184,8 @@ class LagfluxSolver {
   int threads_;
   lf_handle* h_ = nullptr;
   mutable const SolverState* resident_ = nullptr;
+  const MaterialCells* resident_mat_ = nullptr;
+  int n_mat_ = 0;
   bool auto_sync_ = true;
 };
 

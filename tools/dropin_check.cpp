@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "lagflux/error.hpp"
+#include "lagflux/multimat.hpp"
 #include "lagflux/solver.hpp"
 #include "lagflux_b200.hpp"
 
@@ -100,6 +101,61 @@ void run_pair(const char* name, const CartesianGrid& g, const BoundaryCondition&
   std::printf("%s: %zu steps compared\n", name, a.diagnostics.size());
 }
 
+// The triple-point regions (cases/triple_point.case) on a small mesh: three
+// materials, each cell's energy from its own material's gamma (run.cpp:29-78).
+void run_multimaterial(int nx, int ny, int steps, bool auto_sync) {
+  const CartesianGrid g = make_grid_2d(nx, ny, 0.0, 7.0, 0.0, 3.0);
+  const BoundaryCondition bc{BcKind::reflective, BcKind::reflective, BcKind::reflective,
+                             BcKind::reflective};
+  const MaterialSet set = make_material_set({1.5, 1.4, 1.5});
+  CellField f(g);
+  MaterialCells m(g, 3);
+  for (int j = g.gy; j < g.gy + g.ny; ++j)
+    for (int i = g.gx; i < g.gx + g.nx; ++i) {
+      const double x = g.xc(i), y = g.yc(j);
+      const int mat = x < 1.0 ? 0 : (y >= 1.5 ? 1 : 2);
+      const PrimitiveState w = mat == 0 ? PrimitiveState{1.0, 0.0, 0.0, 1.0}
+                               : mat == 1 ? PrimitiveState{0.125, 0.0, 0.0, 0.1}
+                                          : PrimitiveState{1.0, 0.0, 0.0, 0.1};
+      f.set_state(g, i, j, conserved_from_primitive(w, PerfectGasEos{set.gammas[size_t(mat)]}));
+      m.partial[size_t(mat)][size_t(g.idx(i, j))] = w.rho;
+    }
+  const SchemeParams params{};
+  const TimeControls controls{0.25, 1e30, 1 << 30};
+  LagfluxSolver ref(g, bc, PerfectGasEos{1.4}, params, 1, &set);
+  b200::LagfluxSolver gpu(g, bc, PerfectGasEos{1.4}, params, 1, &set);
+  gpu.set_auto_sync(auto_sync);
+  SolverState a, b;
+  a.field = f;
+  b.field = f;
+  MaterialCells ma = m, mb = m;
+  for (int s = 0; s < steps; ++s) {
+    const double da = ref.heun_step(a, controls, 1e30, &ma);
+    const double db = gpu.heun_step(b, controls, 1e30, &mb);
+    if (da != db) {
+      expect(false, "multimaterial: dt of step " + std::to_string(s));
+      return;
+    }
+  }
+  if (!auto_sync) gpu.sync_to_host(b, &mb);
+  expect(same_interior(g, a.field, b.field), "multimaterial: final field");
+  bool parts = true;
+  for (int k = 0; k < 3; ++k)
+    for (int j = g.gy; j < g.gy + g.ny; ++j)
+      for (int i = g.gx; i < g.gx + g.nx; ++i)
+        parts = parts && ma.partial[size_t(k)][size_t(g.idx(i, j))] ==
+                             mb.partial[size_t(k)][size_t(g.idx(i, j))];
+  expect(parts, "multimaterial: partial densities");
+  for (size_t k = 0; k < a.diagnostics.size(); ++k)
+    if (!(a.diagnostics[k].min_p == b.diagnostics[k].min_p &&
+          a.diagnostics[k].min_rho == b.diagnostics[k].min_rho)) {
+      expect(false, "multimaterial: diagnostics " + std::to_string(k));
+      break;
+    }
+  std::printf("multimaterial%s: %zu steps compared\n", auto_sync ? "" : "-resident",
+              a.diagnostics.size());
+}
+
 }  // namespace
 
 int main() {
@@ -149,6 +205,8 @@ int main() {
     }
     expect(!ea.empty() && ea == eb, "PositivityError text: '" + ea + "' vs '" + eb + "'");
   }
+  run_multimaterial(70, 30, 40, true);
+  run_multimaterial(70, 30, 40, false);
   std::printf("%s (%d mismatches)\n", failures ? "FAIL" : "OK", failures);
   return failures ? 1 : 0;
 }
