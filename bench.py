@@ -319,6 +319,106 @@ def run_ours(args):
     return 0
 
 
+def run_ours_mat(args):
+    """--workload triple_point: the multimaterial partial-density transport (SURVEY.md
+    §8f row 1) on cases/triple_point.case at its reference resolution, one GPU."""
+    torch, dist, world, rank, local = dist_setup(args)
+    from paper_1607_08710_b200 import cases as CS
+    from paper_1607_08710_b200 import grid as G
+    from paper_1607_08710_b200 import multimat as MM
+    from paper_1607_08710_b200.solver import LagfluxSolver
+
+    c = CS.triple_point(2048, 878)
+    g = c.grid
+    n_mat = len(c.material_gammas)
+    ms = MM.make_material_set(c.material_gammas)
+    f0, m0 = CS.regions_field(c)
+    solver = LagfluxSolver(g, c.bc, c.gamma, c.params, materials=ms, devices=(local,))
+    stream = torch.cuda.current_stream()
+    solver.set_stream(stream.cuda_stream)
+    state = G.SolverState(field=f0.copy())
+    mat = m0.copy()
+    controls = G.TimeControls(c.cfl, c.t_final, G.INT64_MAX)
+    solver.advance(state, controls, args.warmup, mat)
+    torch.cuda.synchronize()
+    launches0 = solver.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        taken = solver.advance(state, controls, args.steps, mat)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_step = ev0.elapsed_time(ev1) / max(taken, 1)
+    launches = solver.launch_count() - launches0
+    value = g.nx * g.ny / (ms_step / 1e3)
+    bytes_per = BYTES_PER_CELL_UPDATE + 40 * n_mat   # + read P^n twice, write P*, read P*, write P^{n+1}
+    hbm, hbm_src = measured_hbm()
+    achieved = bytes_per * g.nx * g.ny / (ms_step / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": hbm_src,
+                "algorithmic_bytes_per_cell_update": bytes_per,
+                "kernel": "whole stage-wise multimaterial step (no single dominant kernel)",
+                "kernel_ms_per_launch": ms_step, "kernel_share_of_step": 1.0, "traffic": None}
+
+    e2e = None
+    if not args.no_e2e:
+        hf = torch.empty((4, g.nyt, g.nxt), dtype=torch.float64, pin_memory=True).numpy()
+        hp = torch.empty((n_mat, g.nyt, g.nxt), dtype=torch.float64, pin_memory=True).numpy()
+        hf[...] = f0
+        hp[...] = m0.partial
+        st2 = G.SolverState(field=hf)
+        mat2 = MM.MaterialCells.__new__(MM.MaterialCells)
+        mat2.partial = hp
+        s2 = LagfluxSolver(g, c.bc, c.gamma, c.params, materials=ms, devices=(local,))
+        s2.set_stream(stream.cuda_stream)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s2.attach(st2)
+        k2 = s2.advance(st2, controls, args.steps, mat2)
+        s2.sync_to_host(st2, mat=mat2)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        nbytes = (4 + n_mat) * 8 * g.nx * g.ny
+        e2e = {"value": g.nx * g.ny * k2 / wall, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes / max(k2, 1),
+               "d2h_bytes_per_step": (nbytes + 48 * k2) / max(k2, 1),
+               "what": f"upload of field + {n_mat} partial densities from pinned memory, {k2} "
+                       f"steps (records to the host), download of both"}
+        s2.close()
+
+    cpu_baseline = None
+    if not args.no_cpu:
+        from oracle import oracle as O
+        if O.ref_available():
+            threads = os.cpu_count() or 1
+            r = O.RefSolver(g, c.bc, c.gamma, c.params, threads=threads, materials=ms)
+            r.set_state(f0)
+            r.set_partials(m0.partial)
+            r.heun_steps(1, c.cfl, c.t_final)
+            nsteps = 5
+            t0 = time.perf_counter()
+            r.heun_steps(nsteps, c.cfl, c.t_final)
+            wall = time.perf_counter() - t0
+            cpu_baseline = {"value": g.nx * g.ny * nsteps / wall, "unit": UNIT, "cores": threads,
+                            "kind": "reference",
+                            "sample": f"the same triple point {g.nx}x{g.ny}, {nsteps} heun_step "
+                                      f"calls with MaterialCells after 1 warm-up ({wall:.1f} s), "
+                                      f"OpenMP {threads} threads"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": taken,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (cases/triple_point.case regions)",
+            "config": {"workload": f"triple_point {g.nx}x{g.ny}, {n_mat} materials "
+                                   f"(gammas {list(c.material_gammas)}), reflective",
+                       "nx": g.nx, "ny": g.ny, "cfl": c.cfl, "path": "staged (multimaterial)",
+                       "l2": "state %.2f GB (field + partials)" % ((4 + n_mat) * 8 * g.nx * g.ny / 1e9)},
+            "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks.summary()}
+    print(json.dumps(line))
+    solver.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -329,11 +429,16 @@ def main():
     ap.add_argument("--path", choices=["auto", "twopass", "fused", "staged"], default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", choices=["smooth", "triple_point"], default="smooth",
+                    help="smooth: BASELINE config 4/5 (the headline); triple_point: the "
+                         "multimaterial transport (one GPU)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "triple_point":
+        return run_ours_mat(args)
     return run_ours(args)
 
 
