@@ -3,12 +3,12 @@
 // The reference's fp64 evaluation order throughout (compiled with
 // --fmad=false); divisions and square roots through fastmath.cuh, whose
 // results equal the IEEE operators bit for bit (up to the sign of a zero
-// quotient) whenever the range checks hold.  A failed range check -- possible
-// only for magnitudes beyond 2^+-960, i.e. never for physical data -- is
-// reported through `ok`; the kernels turn it into a failure flag, and the host
-// then recomputes the step with the stage-wise IEEE kernels.  Keeping the
-// IEEE slow paths out of these kernels keeps CALLs (and the registers they pin)
-// out of the hot loops.  Shared by fused_kernel.cu and twopass_kernel.cu.
+// quotient) on their fast paths.  The face solves never evaluate the range
+// checks: the cell box below proves them.  The per-cell epilogue still reports
+// its checks through `ok`; the kernels turn any failure into a flag, and the
+// host then recomputes the step with the stage-wise IEEE kernels, so no IEEE
+// slow path (CALL, pinned registers) sits in the hot loops.  Shared by
+// fused_kernel.cu and twopass_kernel.cu.
 #pragma once
 
 #include "fastmath.cuh"
@@ -156,18 +156,25 @@ __device__ __forceinline__ void prim_fast(double r, double mx, double my, double
   w[3] = gm1 * (e - (0.5 * (mx * mx + my * my)) * inv);
 }
 
-// CFL rate (solver.cpp:457-468) on the fast paths; false for a non-physical
-// cell; ok &= range checks.
-__device__ __forceinline__ bool rate_fast(const double v[4], const FK& c, double& rr, bool& ok) {
-  if (!(v[0] > 0.0)) return false;
-  const double inv = div1_fast(1.0, v[0], ok);
+// Epilogue of an updated cell, branch-free: the positivity test's internal
+// energy (solver.cpp:300-302) and the CFL rate of the new state
+// (solver.cpp:457-469) share 1/v0's reciprocal and the kinetic term
+// kin = 0.5 (v1^2 + v2^2), which both reference expressions contain verbatim
+// (kin / v0 and kin * inv).  ok_e / ok_r &= the range checks of each part;
+// rate_ok is false for a non-physical cell (the reference's compute_dt failure).
+__device__ __forceinline__ void cell_epilogue(const double v[4], const FK& c, double& eint,
+                                              bool& ok_e, double& rr, bool& rate_ok,
+                                              bool& ok_r) {
+  const Recip r0 = recip_of(v[0]);
+  const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
+  eint = v[3] - div_fast(kin, r0, ok_e);
+  const double inv = div_fast(1.0, r0, ok_r);
   const double uu = v[1] * inv, vv = v[2] * inv;
-  const double p = c.gm1 * (v[3] - 0.5 * (v[1] * v[1] + v[2] * v[2]) * inv);
-  if (!(p > 0.0)) return false;
-  const double cs = sqrt_fast(c.gamma * p * inv, ok);
-  rr = div_fast(abs_bits(uu) + cs, c.rdx, ok);
-  rr += div_fast(abs_bits(vv) + cs, c.rdy, ok);
-  return true;
+  const double p = c.gm1 * (v[3] - kin * inv);
+  rate_ok = (v[0] > 0.0) && (p > 0.0);
+  const double cs = sqrt_fast(c.gamma * p * inv, ok_r);
+  rr = div_fast(abs_bits(uu) + cs, c.rdx, ok_r);
+  rr += div_fast(abs_bits(vv) + cs, c.rdy, ok_r);
 }
 
 #endif  // __CUDACC__

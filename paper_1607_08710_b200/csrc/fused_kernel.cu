@@ -429,9 +429,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           a.un[q * a.fstride + o] = val;
         }
         // positivity (solver.cpp:300-307) and the diagnostics minima
-        bool ok = true;
-        const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
-        const double eint = v[3] - div1_fast(kin, v[0], ok);
+        // and the CFL rate of U^{n+1} for the next step's dt (solver.cpp:457-469)
+        bool ok = true, okr = true, rate_ok;
+        double eint, rr;
+        cell_epilogue(v, C, eint, ok, rr, rate_ok, okr);
         if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
           fail = 1;
         } else {
@@ -439,18 +440,15 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           nmin_r = kr > nmin_r ? kr : nmin_r;
           nmin_e = ke > nmin_e ? ke : nmin_e;
         }
-        // CFL rate of U^{n+1} for the next step's dt (solver.cpp:457-469)
-        double rr;
-        bool okr = true;
-        if (rate_fast(v, C, rr, okr)) {
+        if (rate_ok) {
           if (rr == rr) {
             const unsigned long long b = pos_bits(rr);
             rate_key = b > rate_key ? b : rate_key;
           }
+          if (!okr) fail = 1;
         } else {
           dtfail = 1;
         }
-        if (!okr) fail = 1;
         // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
         const int jg = j + a.y0g;
         if (c == 0)

@@ -233,9 +233,9 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
           const double lhs = v[3] * v[0];
           if (!(v[0] > 0.0) || !(lhs > kin * (1.0 + 0x1p-48)) || !(lhs >= 0x1p-960)) fail = 1;
         } else {
-          bool ok = true;
-          const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
-          const double eint = v[3] - div1_fast(kin, v[0], ok);
+          bool ok = true, okr = true, rate_ok;
+          double eint, rr;
+          cell_epilogue(v, C, eint, ok, rr, rate_ok, okr);
           if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
             fail = 1;
           } else {
@@ -243,17 +243,15 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
             nmin_r = kr > nmin_r ? kr : nmin_r;
             nmin_e = ke > nmin_e ? ke : nmin_e;
           }
-          double rr;
-          bool okr = true;
-          if (rate_fast(v, C, rr, okr)) {
+          if (rate_ok) {
             if (rr == rr) {
               const unsigned long long b = pos_bits(rr);
               rate_key = b > rate_key ? b : rate_key;
             }
+            if (!okr) fail = 1;
           } else {
             dtfail = 1;
           }
-          if (!okr) fail = 1;
           // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
           const int jg = row + a.y0g;
           if (c == 0)

@@ -23,11 +23,10 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # name -> (extra nvcc flags, LF_PATH_*); "base_*" variants build the same path
 # from the committed sources (git HEAD) for an A/B against the working tree
 VARIANTS = {
+    "base_fused": ("", 1),
+    "fused": ("", 1),
+    "base_tp": ("", 3),
     "tp": ("", 3),
-    "tp_smem": ("-DLF_TP_SMEM=1", 3),
-    "tp_smem_mb4": ("-DLF_TP_SMEM=1 -DLF_TP_MINBLOCKS=4", 3),
-    "tp_smem_mb4_late": ("-DLF_TP_SMEM=1 -DLF_TP_MINBLOCKS=4 -DLF_TP_LATELOAD=1", 3),
-    "tp_smem_late": ("-DLF_TP_SMEM=1 -DLF_TP_LATELOAD=1", 3),
 }
 
 
