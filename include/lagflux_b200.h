@@ -21,6 +21,7 @@
  *                                  time / diagnostics kept on the device
  *   lf_init_fourier                (new) on-device seeded smooth-flow IC (BASELINE 4-5)
  *   lf_last_error                  the exception object (what(), PositivityError fields)
+ *   lf_write_field_csv             field_csv + write_text_file   csv.cpp:26-83, run.cpp:162-168
  *   lf_set_materials               the constructor's `const MaterialSet*` (solver.cpp:61-88)
  *                                  with make_material_set's checks (multimat.cpp:7-15)
  *   lf_upload_partials /           MaterialCells::partial host <-> device
@@ -140,6 +141,16 @@ int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghost
 int lf_set_materials(lf_handle* h, int n, const double* gammas);
 int lf_upload_partials(lf_handle* h, double* const* partials, int64_t ld);
 int lf_download_partials(lf_handle* h, double* const* partials, int64_t ld);
+
+/* field_csv (csv.cpp:26-83) of the current state written to `path` (run.cpp's
+ * dump, write_text_file): "# config <digest hex> time <t>", the column line, then
+ * x[,y],rho,u[,v],p,e_internal[,y1..yn] per interior cell, %.17g, row-major.
+ * The per-cell quantities are derived on the device with the reference's
+ * expressions; `threads` host threads format rows in parallel (0: all cores).
+ * A mass fraction beyond round-off fails with LF_ERR_FRACTION (clamped_fraction's
+ * text) and writes nothing.  A distributed handle writes its own rows only. */
+int lf_write_field_csv(lf_handle* h, const char* path, uint64_t digest, double time,
+                       int threads);
 
 /* Seeded smooth-perturbation initial state (BASELINE configs 4-5), generated on the device. */
 int lf_init_fourier(lf_handle* h, uint64_t seed);

@@ -160,6 +160,9 @@ def ref_lib():
     lib.lfr_mixed_cell_gamma.restype = C.c_double
     lib.lfr_mixed_cell_gamma.argtypes = [C.c_int, DP, DP]
     lib.lfr_mass_fraction_fluxes.argtypes = [C.c_double, C.c_int, DP, DP]
+    lib.lfr_field_csv.restype = C.c_int64
+    lib.lfr_field_csv.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_char_p, C.c_int64,
+                                  C.POINTER(lfo_error)]
     return lib
 
 
@@ -232,6 +235,16 @@ class RefSolver:
                                          threads, self.n_mat, gs.ctypes.data_as(DP), C.byref(err))
         if not self.h:
             raise_error(err)
+
+    def field_csv(self, digest: int, time: float) -> bytes:
+        """The reference's field_csv (csv.cpp:26-83) of the current state."""
+        err = lfo_error()
+        n = self.lib.lfr_field_csv(self.h, digest, time, None, 0, C.byref(err))
+        if n < 0:
+            raise_error(err)
+        buf = C.create_string_buffer(n)
+        self.lib.lfr_field_csv(self.h, digest, time, buf, n, C.byref(err))
+        return buf.raw[:n]
 
     def set_partials(self, partial: np.ndarray) -> None:
         self.lib.lfr_set_partials(self.h, _kptrs(np.ascontiguousarray(partial)))

@@ -16,6 +16,7 @@
 #include <omp.h>
 #endif
 
+#include "lagflux/csv.hpp"
 #include "lagflux/error.hpp"
 #include "lagflux/multimat.hpp"
 #include "lagflux/solver.hpp"
@@ -188,6 +189,24 @@ double lfr_mixed_cell_gamma(int n, const double* gammas, const double* fractions
 void lfr_mass_fraction_fluxes(double mass_flux, int n, const double* y_upwind, double* out) {
   mass_fraction_fluxes(mass_flux, std::span<const double>(y_upwind, size_t(n)),
                        std::span<double>(out, size_t(n)));
+}
+
+// field_csv (csv.cpp:26-83) of the internal state (and material cells): returns
+// the length; copies min(len, cap) bytes into buf when buf != NULL.  -1 and the
+// error record when field_csv throws.
+int64_t lfr_field_csv(lfr_solver* r, uint64_t digest, double time, char* buf, int64_t cap,
+                      lfo_error* err) {
+  clear(err);
+  try {
+    const bool mm = r->mat.count() > 0;
+    const std::string s = field_csv(r->g, r->state.field, r->eos, mm ? &r->materials : nullptr,
+                                    mm ? &r->mat : nullptr, digest, time);
+    if (buf) std::memcpy(buf, s.data(), size_t(std::min<int64_t>(cap, int64_t(s.size()))));
+    return int64_t(s.size());
+  } catch (...) {
+    map_exception(err, LFO_ERR_PRIMITIVE);
+    return -1;
+  }
 }
 
 void lfr_destroy(lfr_solver* r) {

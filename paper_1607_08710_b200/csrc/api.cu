@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <charconv>
 #include <cinttypes>
 #include <climits>
 #include <cmath>
@@ -17,6 +18,8 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "fused.h"
 #include "handle.h"
@@ -881,6 +884,135 @@ int lf_download_partials(lf_handle* h, double* const* partials, int64_t ld) {
       }
     }
     sync_all(h);
+    return 0;
+  });
+}
+
+// ---- field dumps: field_csv (csv.cpp:26-83) + write_text_file (run.cpp:162-168) ----
+namespace {
+// format_g17 (csv.cpp:8-12): "%.17g".  std::to_chars(general, 17) is specified
+// as printf's %.17g in the C locale (and is several times faster); tests compare
+// the bytes against the reference's own field_csv.
+inline void put_g17(std::string& out, double v) {
+  char buf[32];
+  const auto r = std::to_chars(buf, buf + sizeof buf, v, std::chars_format::general, 17);
+  out.append(buf, (size_t)(r.ptr - buf));
+}
+}  // namespace
+
+int lf_write_field_csv(lf_handle* h, const char* path, uint64_t digest, double time,
+                       int threads) {
+  return guarded(h, [&] {
+    if (!path) return set_err(h, LF_ERR_ARGUMENT, "path is null");
+    if (h->mc.n && !h->partials_ready)
+      return set_err(h, LF_ERR_CONFIG, "multimaterial dump needs material storage");
+    const int nx = h->d.nx, nyg = h->d.ny, n_mat = h->mc.n;
+    const int ncols = 5 + n_mat;
+    // this process's rows (a distributed handle writes its slab rows only)
+    const int row0 = h->slabs.front().sl.y0;
+    const int rows = h->slabs.back().sl.y0 + h->slabs.back().L.ny - row0;
+    std::vector<double> cols((size_t)ncols * nx * rows);
+    unsigned long long fail_host = ~0ull;
+    for (auto& s : h->slabs) {
+      CK(cudaSetDevice(s.device));
+      const size_t plane = (size_t)nx * s.L.ny;
+      double* dbuf = nullptr;
+      unsigned long long* dfail = nullptr;
+      CK(cudaMalloc(&dbuf, ncols * plane * sizeof(double)));
+      CK(cudaMalloc(&dfail, sizeof(unsigned long long)));
+      CK(cudaMemsetAsync(dfail, 0xff, sizeof(unsigned long long), s.stream));
+      launch_csv_derive(s.field(s.U), s.field(n_mat ? s.P : s.U), s.L, s.sl, h->d.gamma, h->mc,
+                        dbuf, dfail, s.stream);
+      unsigned long long f;
+      for (int c = 0; c < ncols; ++c)
+        CK(cudaMemcpyAsync(&cols[((size_t)c * rows + (s.sl.y0 - row0)) * nx], dbuf + c * plane,
+                           plane * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaMemcpyAsync(&f, dfail, sizeof f, cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      fail_host = std::min(fail_host, f);
+      cudaFree(dbuf);
+      cudaFree(dfail);
+    }
+    if (fail_host != ~0ull) {
+      // clamped_fraction's message for the first failing (cell, material), csv.cpp:49
+      const int i = (int)(fail_host % (unsigned long long)nx);
+      const int jl = (int)(fail_host / (unsigned long long)nx) - row0;
+      const double rho = cols[(size_t)jl * nx + i];
+      double y = 0.0;
+      for (int k = 0; k < n_mat; ++k) {
+        double pk = 0.0;
+        for (auto& s : h->slabs) {
+          const int jj = jl + row0 - s.sl.y0;
+          if (jj < 0 || jj >= s.L.ny) continue;
+          CK(cudaSetDevice(s.device));
+          CK(cudaMemcpy(&pk, s.P + s.L.origin() + k * s.L.fstride + (int64_t)jj * s.L.pitch + i,
+                        sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        y = pk / rho;
+        if (!(y >= 0.0 && y <= 1.0) && (y < -1e-11 || y > 1.0 + 1e-11)) break;
+      }
+      return set_err(h, LF_ERR_FRACTION, "mass fraction out of [0,1] beyond round-off = %s",
+                     fmt_f(y).c_str());
+    }
+    // header and column names (csv.cpp:15-23, 33-36)
+    std::string head;
+    char hb[64];
+    std::snprintf(hb, sizeof hb, "# config %016llx time ", (unsigned long long)digest);
+    head += hb;
+    put_g17(head, time);
+    head += '\n';
+    head += h->dim2 ? "x,y,rho,u,v,p,e_internal" : "x,rho,u,p,e_internal";
+    for (int k = 1; k <= n_mat; ++k) head += ",y" + std::to_string(k);
+    head += '\n';
+    // rows formatted in parallel (row order kept), then written in order
+    int nt = threads > 0 ? threads : (int)std::thread::hardware_concurrency();
+    nt = std::max(1, std::min(nt, rows));
+    std::vector<std::string> parts((size_t)nt);
+    const size_t plane = (size_t)nx * rows;
+    auto work = [&](int t) {
+      const int j0 = (int)((int64_t)rows * t / nt), j1 = (int)((int64_t)rows * (t + 1) / nt);
+      std::string& out = parts[(size_t)t];
+      out.reserve((size_t)(j1 - j0) * nx * (size_t)(ncols + 2) * 24);
+      for (int jl = j0; jl < j1; ++jl) {
+        const double y = h->d.y0 + ((jl + row0) + 0.5) * h->d.dy;  // CartesianGrid::yc
+        for (int i = 0; i < nx; ++i) {
+          const size_t c = (size_t)jl * nx + i;
+          put_g17(out, h->d.x0 + (i + 0.5) * h->d.dx);               // CartesianGrid::xc
+          if (h->dim2) {
+            out += ',';
+            put_g17(out, y);
+          }
+          out += ',';
+          put_g17(out, cols[c]);
+          out += ',';
+          put_g17(out, cols[plane + c]);
+          if (h->dim2) {
+            out += ',';
+            put_g17(out, cols[2 * plane + c]);
+          }
+          out += ',';
+          put_g17(out, cols[3 * plane + c]);
+          out += ',';
+          put_g17(out, cols[4 * plane + c]);
+          for (int k = 0; k < n_mat; ++k) {
+            out += ',';
+            put_g17(out, cols[(5 + k) * plane + c]);
+          }
+          out += '\n';
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    FILE* fp = std::fopen(path, "wb");
+    if (!fp) return set_err(h, LF_ERR_ARGUMENT, "cannot open %s for writing", path);
+    bool ok = std::fwrite(head.data(), 1, head.size(), fp) == head.size();
+    for (auto& p : parts) ok = ok && std::fwrite(p.data(), 1, p.size(), fp) == p.size();
+    ok = (std::fclose(fp) == 0) && ok;
+    if (!ok) return set_err(h, LF_ERR_ARGUMENT, "short write to %s", path);
+    (void)nyg;
     return 0;
   });
 }

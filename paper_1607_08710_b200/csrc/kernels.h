@@ -124,5 +124,10 @@ void launch_update_partials(const Field& base, const FluxArr& fxa, const FluxArr
 void launch_mat_min_p(const Field& u, const Field& part, const Layout& L, const MatConsts& mc,
                       Scalars* s, cudaStream_t st);
 void fill_value(double* p, int64_t n, double v, cudaStream_t st);
+// field_csv's per-cell columns (csv.cpp:40-57): rho, u, v, p, e_internal, y_1..y_n as
+// planes of nx*ny; clamp failures -> atomicMin(fail, row-major global interior index)
+void launch_csv_derive(const Field& u, const Field& part, const Layout& L, const Slab& sl,
+                       double gamma0, const MatConsts& mc, double* out, unsigned long long* fail,
+                       cudaStream_t st);
 
 }  // namespace lfb

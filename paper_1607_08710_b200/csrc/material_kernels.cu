@@ -457,4 +457,68 @@ void fill_value(double* p, int64_t n, double v, cudaStream_t st) {
   count_launch(), k_fill_value<<<blocks, 256, 0, st>>>(p, n, v);
 }
 
+
+// ---------------------------------------------------------------- field dumps
+// field_csv's per-cell quantities (csv.cpp:40-57), in its expression order:
+//   u = mx / rho, v = my / rho, eint = E - 0.5 (mx^2 + my^2) / rho,
+//   p = (gamma - 1) eint, e = eint / rho, y_k = clamped_fraction(partial_k, rho),
+//   gamma = mixed_cell_gamma(y) (pure cells exact) or the eos gamma.
+// out: ncols planes of nx * ny (row-major, local rows); the smallest failing
+// interior index of the clamp (and its fraction value) -> fail / fail_val.
+namespace {
+__global__ void k_csv_derive(Field u, Field part, int nx, int ny, int y0, double gamma0,
+                             MatConsts mc, double* out, unsigned long long* fail) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= nx || j >= ny) return;
+  const int64_t o = (int64_t)j * u.pitch + i;
+  const int64_t plane = (int64_t)nx * ny, c = (int64_t)j * nx + i;
+  const double rho = u.p[o], mx = u.p[u.fstride + o], my = u.p[2 * u.fstride + o];
+  const double uu = mx / rho;
+  const double vv = my / rho;
+  double gamma = gamma0;
+  if (mc.n > 0) {
+    double s = 0.0;
+    int pure = -1;
+    for (int k = 0; k < mc.n; ++k) {
+      const double y = part.p[k * part.fstride + o] / rho;
+      double yk = y;
+      if (!(y >= 0.0 && y <= 1.0)) {
+        if (y < -1e-11 || y > 1.0 + 1e-11) {
+          // the first failing cell in field_csv's row-major order; the host
+          // recomputes its fraction for the message
+          atomicMin(fail, (unsigned long long)((int64_t)(j + y0) * nx + i));
+          yk = 0.0;
+        } else {
+          yk = y < 0.0 ? 0.0 : 1.0;
+        }
+      }
+      out[(5 + k) * plane + c] = yk;
+      // mixed_cell_gamma (multimat.cpp:25-32): the first pure material returns
+      if (pure < 0) {
+        if (yk == 1.0)
+          pure = k;
+        else
+          s += yk / (mc.gamma[k] - 1.0);
+      }
+    }
+    gamma = pure >= 0 ? mc.gamma[pure] : 1.0 + 1.0 / s;
+  }
+  const double eint = u.p[3 * u.fstride + o] - 0.5 * (mx * mx + my * my) / rho;
+  out[c] = rho;
+  out[plane + c] = uu;
+  out[2 * plane + c] = vv;
+  out[3 * plane + c] = (gamma - 1.0) * eint;
+  out[4 * plane + c] = eint / rho;
+}
+}  // namespace
+
+void launch_csv_derive(const Field& u, const Field& part, const Layout& L, const Slab& sl,
+                       double gamma0, const MatConsts& mc, double* out, unsigned long long* fail,
+                       cudaStream_t st) {
+  dim3 blk(32, 8);
+  dim3 grd(cdiv(L.nx, 32), cdiv(L.ny, 8));
+  count_launch(), k_csv_derive<<<grd, blk, 0, st>>>(u, part, L.nx, L.ny, sl.y0, gamma0, mc, out, fail);
+}
+
 }  // namespace lfb

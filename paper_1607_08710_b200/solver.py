@@ -166,6 +166,11 @@ class LagfluxSolver:
                                                      self._grid.nxt))
             self._resident_mat = mat
 
+    def write_field_csv(self, path: str, digest: int, time: float, threads: int = 0):
+        """run.cpp's dump: field_csv (csv.cpp:26-83) of the resident state (and its
+        material fractions) to `path`, formatted on `threads` host threads."""
+        self._check(self._lib.lf_write_field_csv(self._h, path.encode(), digest, time, threads))
+
     def init_fourier(self, state: G.SolverState, seed: int):
         """Device-side seeded smooth-flow initial state (cases.fourier_*)."""
         self._check(self._lib.lf_init_fourier(self._h, seed))

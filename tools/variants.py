@@ -25,7 +25,7 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 VARIANTS = {
     "base_fused": ("", 1),
     "fused": ("", 1),
-    "base_tp": ("", 3),
+    "fused_epip": ("-DLF_EPI_P=1", 1),
     "tp": ("", 3),
 }
 
