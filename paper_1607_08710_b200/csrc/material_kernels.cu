@@ -22,6 +22,7 @@
 #include <climits>
 
 #include "kernels.h"
+#include "reduce.cuh"
 
 namespace lfb {
 
@@ -33,20 +34,6 @@ __device__ __forceinline__ long long warp_min_i64(long long v) {
   for (int o = 16; o > 0; o >>= 1) {
     const long long w = __shfl_xor_sync(FULL, v, o);
     v = w < v ? w : v;
-  }
-  return v;
-}
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(FULL, v, o);
-    v = w < v ? w : v;
-  }
-  return v;
-}
-__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(FULL, v, o);
-    v = w > v ? w : v;
   }
   return v;
 }
@@ -132,9 +119,9 @@ __global__ void k_rate_g(Field u, Field gcell, int nx, int ny, int y0, Consts k,
       fail = gidx < fail ? gidx : fail;
     }
   }
-  best = warp_max_u64(best);
-  fail = warp_min_i64(fail);
-  if ((threadIdx.x & 31) == 0) {
+  best = block_reduce(best, MaxOp(), 0ull);
+  fail = block_reduce(fail, MinOp(), (long long)LLONG_MAX);
+  if (threadIdx.x == 0) {
     if (best) atomicMax(&s->rate_bits, best);
     if (fail != LLONG_MAX) atomicMin(&s->fail_dt, fail);
   }
@@ -359,8 +346,8 @@ __global__ void k_mat_min_p(Field u, Field part, int nx, int ny, MatConsts mc, S
       best = key < best ? key : best;
     }
   }
-  best = warp_min_u64(best);
-  if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(&s->min_p_key, best);
+  best = block_reduce(best, MinOp(), ~0ull);
+  if (threadIdx.x == 0 && best != ~0ull) atomicMin(&s->min_p_key, best);
 }
 
 __global__ void k_fill_value(double* p, int64_t n, double v) {
@@ -385,7 +372,7 @@ void launch_mat_fractions(const Field& u, const Field& part, const Field& y, con
 void launch_rate_g(const Field& u, const Field& gcell, const Layout& L, const Slab& sl,
                    const Consts& k, int dim2, Scalars* s, cudaStream_t st) {
   const int64_t n = (int64_t)L.nx * L.ny;
-  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 16);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8);
   if (dim2)
     count_launch(), k_rate_g<true><<<blocks, 256, 0, st>>>(u, gcell, L.nx, L.ny, sl.y0, k, s);
   else
@@ -448,7 +435,7 @@ void launch_update_partials(const Field& base, const FluxArr& fxa, const FluxArr
 void launch_mat_min_p(const Field& u, const Field& part, const Layout& L, const MatConsts& mc,
                       Scalars* s, cudaStream_t st) {
   const int64_t n = (int64_t)L.nx * L.ny;
-  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 16);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8);
   count_launch(), k_mat_min_p<<<blocks, 256, 0, st>>>(u, part, L.nx, L.ny, mc, s);
 }
 

@@ -12,6 +12,7 @@
 #include <climits>
 
 #include "kernels.h"
+#include "reduce.cuh"
 
 namespace lfb {
 
@@ -23,13 +24,6 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
   for (int o = 16; o > 0; o >>= 1) {
     unsigned long long w = __shfl_xor_sync(FULL, v, o);
     v = w > v ? w : v;
-  }
-  return v;
-}
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
-  for (int o = 16; o > 0; o >>= 1) {
-    unsigned long long w = __shfl_xor_sync(FULL, v, o);
-    v = w < v ? w : v;
   }
   return v;
 }
@@ -120,9 +114,9 @@ __global__ void k_rate(Field u, int nx, int ny, int y0, Consts k, Scalars* s) {
       fail = g < fail ? g : fail;
     }
   }
-  best = warp_max_u64(best);
-  fail = warp_min_i64(fail);
-  if ((threadIdx.x & 31) == 0) {
+  best = block_reduce(best, MaxOp(), 0ull);
+  fail = block_reduce(fail, MinOp(), (long long)LLONG_MAX);
+  if (threadIdx.x == 0) {
     if (best) atomicMax(&s->rate_bits, best);
     if (fail != LLONG_MAX) atomicMin(&s->fail_dt, fail);
   }
@@ -220,10 +214,10 @@ __global__ void k_update(Field base, FluxArr fxa, FluxArr fya, FluxArr fxb, Flux
                          Field out, int nx, int ny, int y0, double lam_x, double lam_y,
                          Scalars* s) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
   long long fail = LLONG_MAX;
   unsigned long long mr = ~0ull, me = ~0ull;
-  if (i < nx && j < ny) {
+  for (int j = blockIdx.y * blockDim.y + threadIdx.y; i < nx && j < ny;
+       j += gridDim.y * blockDim.y) {
     const int64_t o = (int64_t)j * base.pitch + i;
     const int64_t ex = (int64_t)j * fxa.pitch + i;
     const int64_t ey = (int64_t)j * fya.pitch + i;
@@ -260,16 +254,18 @@ __global__ void k_update(Field base, FluxArr fxa, FluxArr fya, FluxArr fxb, Flux
     for (int c = 0; c < 4; ++c) out.p[c * out.fstride + o] = vals[c];
     const double eint = internal_energy(vals[0], vals[1], vals[2], vals[3]);
     if (!(vals[0] > 0.0) || !(eint > 0.0)) {
-      fail = (long long)(j + y0) * nx + i;
+      const long long g = (long long)(j + y0) * nx + i;
+      fail = g < fail ? g : fail;
     } else {
-      mr = pos_bits(vals[0]);
-      me = pos_bits(eint);
+      const unsigned long long r = pos_bits(vals[0]), e = pos_bits(eint);
+      mr = r < mr ? r : mr;
+      me = e < me ? e : me;
     }
   }
-  fail = warp_min_i64(fail);
-  mr = warp_min_u64(mr);
-  me = warp_min_u64(me);
-  if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0) {
+  fail = block_reduce(fail, MinOp(), (long long)LLONG_MAX);
+  mr = block_reduce(mr, MinOp(), ~0ull);
+  me = block_reduce(me, MinOp(), ~0ull);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
     if (fail != LLONG_MAX) atomicMin(&s->fail_update, fail);
     if (mr != ~0ull) atomicMin(&s->min_rho_bits, mr);
     if (me != ~0ull) atomicMin(&s->min_eint_bits, me);
@@ -393,7 +389,7 @@ void launch_gather_boundary(const FluxArr& fxa, const FluxArr& fya, const FluxAr
 void launch_rate(const Field& u, const Layout& L, const Slab& sl, const Consts& k, int dim2,
                  Scalars* s, cudaStream_t st) {
   const int64_t n = (int64_t)L.nx * L.ny;
-  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 16);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8);
   if (dim2)
     count_launch(), k_rate<true><<<blocks, 256, 0, st>>>(u, L.nx, L.ny, sl.y0, k, s);
   else
@@ -432,7 +428,9 @@ void launch_update(const Field& base, const FluxArr& fxa, const FluxArr& fya,
   const double lam_x = dt / dx;  // solver.cpp:262-263 (divisions, not reciprocals)
   const double lam_y = dt / dy;
   dim3 blk(32, 8);
-  dim3 grd(cdiv(L.nx, 32), cdiv(L.ny, 8));
+  // a few blocks per SM, each looping over rows (one atomic per block per scalar)
+  const unsigned gx = cdiv(L.nx, 32);
+  dim3 grd(gx, std::max(1u, std::min(cdiv(L.ny, 8), cdiv(148 * 8, gx))));
   const FluxArr xb = fxb ? *fxb : fxa, yb = fyb ? *fyb : fya;
   if (fxb) {
     if (dim2)
