@@ -20,6 +20,7 @@
  *   lf_advance                     the run.cpp:180-210 step loop with the dt /
  *                                  time / diagnostics kept on the device
  *   lf_init_fourier                (new) on-device seeded smooth-flow IC (BASELINE 4-5)
+ *   lf_init_regions                initialize_hydro, InitKind::regions  run.cpp:29-78
  *   lf_last_error                  the exception object (what(), PositivityError fields)
  *   lf_write_field_csv             field_csv + write_text_file   csv.cpp:26-83, run.cpp:162-168
  *   lf_set_materials               the constructor's `const MaterialSet*` (solver.cpp:61-88)
@@ -151,6 +152,14 @@ int lf_download_partials(lf_handle* h, double* const* partials, int64_t ld);
  * text) and writes nothing.  A distributed handle writes its own rows only. */
 int lf_write_field_csv(lf_handle* h, const char* path, uint64_t digest, double time,
                        int threads);
+
+/* Region initial state generated on the device (initialize_hydro, run.cpp:29-78,
+ * InitKind::regions): regions = nreg x {x_min, x_max, y_min, y_max, rho, u, v, p,
+ * material (1-based)}; every interior cell centre must lie in exactly one region
+ * (LF_ERR_CONFIG with run.cpp's message otherwise).  Energy from the material's
+ * gamma (the eos gamma without a material set); with materials the partial
+ * densities are set too (rho in the cell's material, 0 elsewhere). */
+int lf_init_regions(lf_handle* h, const double* regions, int nreg);
 
 /* Seeded smooth-perturbation initial state (BASELINE configs 4-5), generated on the device. */
 int lf_init_fourier(lf_handle* h, uint64_t seed);

@@ -1088,6 +1088,63 @@ int lf_init_fourier(lf_handle* h, uint64_t seed) {
   });
 }
 
+int lf_init_regions(lf_handle* h, const double* regions, int nreg) {
+  return guarded(h, [&] {
+    if (!regions || nreg < 1) return set_err(h, LF_ERR_ARGUMENT, "no regions");
+    for (int r = 0; r < nreg; ++r) {
+      const double* R = regions + 9 * r;
+      const int m = (int)R[8];
+      if (!(R[4] > 0.0) || !(R[7] > 0.0))  // conserved_from_primitive's checks (euler.hpp:89-90)
+        return set_err(h, LF_ERR_PRIMITIVE, "%s = %s",
+                       !(R[4] > 0.0) ? "non-positive density" : "non-positive pressure",
+                       fmt_f(!(R[4] > 0.0) ? R[4] : R[7]).c_str());
+      if (h->mc.n && (m < 1 || m > h->mc.n))
+        return set_err(h, LF_ERR_CONFIG, "region material %d outside the material set", m);
+    }
+    unsigned long long fail = ~0ull;
+    for (auto& s : h->slabs) {
+      CK(cudaSetDevice(s.device));
+      double* dreg = nullptr;
+      unsigned long long* dfail = nullptr;
+      CK(cudaMalloc(&dreg, 9 * (size_t)nreg * sizeof(double)));
+      CK(cudaMalloc(&dfail, sizeof(unsigned long long)));
+      CK(cudaMemcpyAsync(dreg, regions, 9 * (size_t)nreg * sizeof(double), cudaMemcpyHostToDevice,
+                         s.stream));
+      CK(cudaMemsetAsync(dfail, 0xff, sizeof(unsigned long long), s.stream));
+      launch_init_regions(s.field(s.U), s.field(h->mc.n ? s.P : s.U), s.L, s.sl, h->d.x0, h->d.y0,
+                          h->d.dx, h->d.dy, h->dim2, dreg, nreg, h->mc, h->d.gamma, dfail, s.stream);
+      unsigned long long f;
+      CK(cudaMemcpyAsync(&f, dfail, sizeof f, cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      fail = std::min(fail, f);
+      cudaFree(dreg);
+      cudaFree(dfail);
+    }
+    if (h->nccl) {  // min over ranks as max of the complement
+      unsigned long long nf = ~fail;
+      nccl_max_u64(h, &nf, 1);
+      fail = ~nf;
+    }
+    if (fail != ~0ull) {
+      // run.cpp:61-64 (the coordinate and the hit count of the first bad cell)
+      const int i = (int)(fail % (unsigned long long)h->d.nx), j = (int)(fail / (unsigned long long)h->d.nx);
+      const double x = h->d.x0 + (i + 0.5) * h->d.dx, y = h->d.y0 + (j + 0.5) * h->d.dy;
+      int hits = 0;
+      for (int r = 0; r < nreg; ++r) {
+        const double* R = regions + 9 * r;
+        hits += (x >= R[0] && x < R[1]) && (!h->dim2 || (y >= R[2] && y < R[3]));
+      }
+      return set_err(h, LF_ERR_CONFIG,
+                     "cell center (%s,%s) is covered by %d regions; regions must tile the domain exactly",
+                     fmt_f(x).c_str(), fmt_f(y).c_str(), hits);
+    }
+    if (h->mc.n) h->partials_ready = 1;
+    h->rate_valid = false;
+    fused_invalidate(h);
+    return 0;
+  });
+}
+
 int lf_compute_dt(lf_handle* h, double cfl, double time, double limit_time, double* dt) {
   return guarded(h, [&] {
     launch_rate_all(h, &SlabState::U);

@@ -124,6 +124,12 @@ void launch_update_partials(const Field& base, const FluxArr& fxa, const FluxArr
 void launch_mat_min_p(const Field& u, const Field& part, const Layout& L, const MatConsts& mc,
                       Scalars* s, cudaStream_t st);
 void fill_value(double* p, int64_t n, double v, cudaStream_t st);
+// initialize_hydro for InitKind::regions (run.cpp:29-78): reg = nreg x {x_min,
+// x_max, y_min, y_max, rho, u, v, p, material}; failures -> atomicMin(fail, index)
+void launch_init_regions(const Field& u, const Field& part, const Layout& L, const Slab& sl,
+                         double x0, double y0, double dx, double dy, int dim2, const double* reg,
+                         int nreg, const MatConsts& mc, double gamma0, unsigned long long* fail,
+                         cudaStream_t st);
 // field_csv's per-cell columns (csv.cpp:40-57): rho, u, v, p, e_internal, y_1..y_n as
 // planes of nx*ny; clamp failures -> atomicMin(fail, row-major global interior index)
 void launch_csv_derive(const Field& u, const Field& part, const Layout& L, const Slab& sl,

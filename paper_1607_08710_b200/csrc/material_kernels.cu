@@ -509,3 +509,62 @@ void launch_csv_derive(const Field& u, const Field& part, const Layout& L, const
 }
 
 }  // namespace lfb
+
+// ---------------------------------------------------------------- region ICs
+// initialize_hydro for InitKind::regions (run.cpp:29-78): each interior cell
+// centre (CartesianGrid::xc/yc) must lie in exactly one region; the cell gets the
+// region's primitive state converted with its material's gamma
+// (conserved_from_primitive, euler.hpp:87-97) and, with materials, partial
+// density rho in its material and 0 elsewhere.  Failures (not exactly one
+// region) -> smallest row-major interior index in *fail.
+namespace lfb {
+namespace {
+__global__ void k_init_regions(Field u, Field part, int nx, int ny, int y0g, double x0,
+                               double yo, double dx, double dy, int dim2, const double* __restrict__ reg,
+                               int nreg, MatConsts mc, double gamma0,
+                               unsigned long long* fail) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= nx || j >= ny) return;
+  const double x = x0 + (i + 0.5) * dx;
+  const double y = yo + ((j + y0g) + 0.5) * dy;
+  int hits = 0, material = 0;
+  double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+  for (int r = 0; r < nreg; ++r) {
+    const double* R = reg + 9 * r;  // x_min x_max y_min y_max rho u v p material(1-based)
+    const bool in_x = x >= R[0] && x < R[1];
+    const bool in_y = !dim2 || (y >= R[2] && y < R[3]);
+    if (in_x && in_y) {
+      ++hits;
+      w0 = R[4];
+      w1 = R[5];
+      w2 = R[6];
+      w3 = R[7];
+      material = (int)R[8] - 1;
+    }
+  }
+  if (hits != 1) {
+    atomicMin(fail, (unsigned long long)((int64_t)(j + y0g) * nx + i));
+    return;
+  }
+  const double gamma = mc.n > 0 ? mc.gamma[material] : gamma0;
+  const int64_t o = (int64_t)j * u.pitch + i;
+  u.p[o] = w0;
+  u.p[u.fstride + o] = w0 * w1;
+  u.p[2 * u.fstride + o] = w0 * w2;
+  u.p[3 * u.fstride + o] = w3 / (gamma - 1.0) + 0.5 * w0 * (w1 * w1 + w2 * w2);
+  for (int k = 0; k < mc.n; ++k) part.p[k * part.fstride + o] = k == material ? w0 : 0.0;
+}
+}  // namespace
+
+void launch_init_regions(const Field& u, const Field& part, const Layout& L, const Slab& sl,
+                         double x0, double y0, double dx, double dy, int dim2, const double* reg,
+                         int nreg, const MatConsts& mc, double gamma0, unsigned long long* fail,
+                         cudaStream_t st) {
+  dim3 blk(32, 8);
+  dim3 grd((unsigned)((L.nx + 31) / 32), (unsigned)((L.ny + 7) / 8));
+  count_launch(), k_init_regions<<<grd, blk, 0, st>>>(u, part, L.nx, L.ny, sl.y0, x0, y0, dx, dy,
+                                                     dim2, reg, nreg, mc, gamma0, fail);
+}
+
+}  // namespace lfb

@@ -55,6 +55,7 @@ SIGNATURES = [
     ("lf_download", C.c_int, [H, P4, C.c_int64, C.c_int]),
     ("lf_set_materials", C.c_int, [H, C.c_int, C.POINTER(C.c_double)]),
     ("lf_write_field_csv", C.c_int, [H, C.c_char_p, C.c_uint64, C.c_double, C.c_int]),
+    ("lf_init_regions", C.c_int, [H, C.POINTER(C.c_double), C.c_int]),
     ("lf_upload_partials", C.c_int, [H, C.c_void_p, C.c_int64]),
     ("lf_download_partials", C.c_int, [H, C.c_void_p, C.c_int64]),
     ("lf_init_fourier", C.c_int, [H, C.c_uint64]),

@@ -171,6 +171,19 @@ class LagfluxSolver:
         material fractions) to `path`, formatted on `threads` host threads."""
         self._check(self._lib.lf_write_field_csv(self._h, path.encode(), digest, time, threads))
 
+    def init_regions(self, state: G.SolverState, regions, mat=None):
+        """Device-side initialize_hydro for region cases (cases.Region list); with a
+        material set, `mat` becomes the resident MaterialCells (download with
+        sync_to_host(state, mat=mat))."""
+        flat = []
+        for r in regions:
+            flat += [r.x_min, r.x_max, r.y_min, r.y_max, r.rho, r.u, r.v, r.p, float(r.material)]
+        arr = (C.c_double * len(flat))(*flat)
+        self._check(self._lib.lf_init_regions(self._h, arr, len(regions)))
+        self._resident = state
+        if self.materials is not None:
+            self._resident_mat = mat
+
     def init_fourier(self, state: G.SolverState, seed: int):
         """Device-side seeded smooth-flow initial state (cases.fourier_*)."""
         self._check(self._lib.lf_init_fourier(self._h, seed))

@@ -138,3 +138,44 @@ def test_unequal_gammas_stay_positive(cuda):
     state, _ = run_gpu_mat(CS.material_contact_1d(64, (1.5, 1.4), 1.5, 50))
     for d in state.diagnostics:
         assert d.min_rho > 0.0 and d.min_p > 0.0
+
+
+@pytest.mark.parametrize("name", ["mm_triple_70x30", "mm_quadrant_48x40", "mm_contact_unequal_64"])
+@pytest.mark.parametrize("devices", [(0,), (0, 0, 0)])
+def test_device_region_init_equals_host(cuda, name, devices):
+    """lf_init_regions == initialize_hydro on the host (regions_field), field and
+    partials, and the steps from it equal the golden run."""
+    c = MAT_CASES[name]
+    if c.grid.dim == 1 and len(devices) > 1:
+        pytest.skip("y-slabs need a 2D grid")
+    f0, m0 = CS.regions_field(c)
+    s = LagfluxSolver(c.grid, c.bc, c.gamma, c.params,
+                      materials=MM.make_material_set(c.material_gammas), devices=devices)
+    state = G.SolverState(field=G.new_field(c.grid))
+    mat = MM.MaterialCells(c.grid, len(c.material_gammas))
+    s.init_regions(state, c.regions, mat)
+    s.sync_to_host(state, mat=mat)
+    g = c.grid
+    assert_fields_equal(g.interior(state.field), g.interior(f0), "field")
+    assert_fields_equal(g.interior(mat.partial), g.interior(m0.partial), "partials")
+    for _ in range(c.max_steps):
+        s.heun_step(state, G.TimeControls(c.cfl, c.t_final), c.t_final, mat)
+    s.sync_to_host(state, mat=mat)
+    gold = load_golden(name)
+    assert_fields_equal(g.interior(state.field), gold["final"], name)
+    assert_fields_equal(g.interior(mat.partial), gold["final_partial"], name)
+
+
+def test_device_region_init_errors(cuda):
+    c = MAT_CASES["mm_triple_70x30"]
+    s = LagfluxSolver(c.grid, c.bc, c.gamma, c.params,
+                      materials=MM.make_material_set(c.material_gammas))
+    state = G.SolverState(field=G.new_field(c.grid))
+    bad = list(c.regions)
+    bad[1] = CS.Region(0.5, 7.0, 1.5, 3.0, 0.125, 0.0, 0.0, 0.1, 2)   # overlaps region 1
+    with pytest.raises(G.ConfigError) as e1:
+        s.init_regions(state, bad)
+    with pytest.raises(G.ConfigError) as e2:
+        CS.regions_field(CS.MatCase(c.name, c.grid, c.bc, c.gamma, c.material_gammas, tuple(bad),
+                                    c.params, c.cfl, c.t_final, c.max_steps))
+    assert str(e1.value) == str(e2.value)
