@@ -103,3 +103,49 @@ def test_slabs_thinner_than_the_halo_are_rejected(cuda):
     g = G.make_grid_2d(16, 6, 0.0, 1.0, 0.0, 1.0)
     with pytest.raises(G.ConfigError, match="at least 4 rows"):
         LagfluxSolver(g, G.BoundaryCondition(), devices=(0, 0))
+
+
+def draw_stress(seed):
+    """Cases built to fail: CFL far past stability and extreme contrasts, so the
+    positivity / trace / primitive / fraction checks and their texts are compared."""
+    case, path, nslabs, mat = draw(10_000 + seed)
+    rng = np.random.default_rng(77 + seed)
+    regions = tuple(CS.Region(r.x_min, r.x_max, r.y_min, r.y_max,
+                              float(10 ** rng.uniform(-3, 1)), float(rng.uniform(-3, 3)),
+                              float(rng.uniform(-3, 3)) if case.grid.dim == 2 else 0.0,
+                              float(10 ** rng.uniform(-4, 1)), r.material)
+                    for r in case.regions)
+    case = CS.MatCase(case.name, case.grid, case.bc, case.gamma, case.material_gammas, regions,
+                      case.params, float(rng.uniform(0.9, 3.0)), case.t_final, 8)
+    return case, path, nslabs, mat
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_failing_case_equals_oracle(cuda, seed):
+    case, path, nslabs, mat = draw_stress(seed)
+    f0, m0 = CS.regions_field(case)
+    ms = MM.make_material_set(case.material_gammas) if mat else None
+    o = O.OracleSolver(case.grid, case.bc, case.gamma, case.params, materials=ms)
+    ostate, omat, oerr = G.SolverState(field=f0.copy()), (m0.copy() if mat else None), None
+    try:
+        for _ in range(case.max_steps):
+            o.heun_step(ostate, case.cfl, case.t_final, omat)
+    except G.Error as e:
+        oerr = e
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, materials=ms,
+                      devices=(0,) * nslabs, path=path)
+    state, gmat, gerr = G.SolverState(field=f0.copy()), (m0.copy() if mat else None), None
+    try:
+        for _ in range(case.max_steps):
+            s.heun_step(state, G.TimeControls(case.cfl, case.t_final), case.t_final, gmat)
+    except G.Error as e:
+        gerr = e
+    s.sync_to_host(state, mat=gmat)
+    what = f"stress {seed}: path={path} slabs={nslabs} mat={mat} cfl={case.cfl:.2f}"
+    assert type(oerr) is type(gerr), what + f": {oerr!r} vs {gerr!r}"
+    assert str(oerr) == str(gerr), what
+    g = case.grid
+    # the corrector writes in place before it throws (solver.cpp:507): same state
+    assert_fields_equal(g.interior(state.field), g.interior(ostate.field), what)
+    rec = lambda st: [(d.step, d.time, d.dt, d.min_rho, d.min_p) for d in st.diagnostics]  # noqa: E731
+    assert rec(state) == rec(ostate), what
