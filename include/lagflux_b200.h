@@ -193,8 +193,9 @@ int lf_launch_count(lf_handle* h, int64_t* launches);
  * max rate of the current state (diagnostic for tests). */
 int lf_max_rate(lf_handle* h, double* rate);
 /* Device self-check of the exact fast-path division / sqrt / limiter on n random
- * operands (csrc/selftest.cu).  counts[7] = {tested, div valid, div mismatches,
- * shared-reciprocal mismatches, sqrt valid, sqrt mismatches, limiter mismatches}. */
+ * operands (csrc/selftest.cu).  counts[10] = {tested, div valid, div mismatches,
+ * shared-reciprocal mismatches, sqrt valid, sqrt mismatches, limiter mismatches,
+ * tiny-dividend divisions tested, their mismatches vs '/', their out-of-range}. */
 int lf_selftest_fastmath(int64_t n, uint64_t seed, int64_t* counts);
 /* Device self-check of the cell box (csrc/face_fast.cuh): n random faces whose
  * four stencil cells lie in the box, extremes and one-ulp neighbours

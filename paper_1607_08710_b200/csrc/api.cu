@@ -120,6 +120,9 @@ void free_slab(SlabState& s) {
   cudaFree(s.aux);
   cudaFree(s.P);
   cudaFree(s.Ps);
+  cudaFree(s.P2);
+  cudaFree(s.MFX);
+  cudaFree(s.MFY);
   for (int k = 0; k < 2; ++k) {
     cudaFree(s.Y[k]);
     cudaFree(s.GC[k]);
@@ -624,7 +627,9 @@ int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t ste
 }
 
 bool use_fused(lf_handle* h) {
-  if (h->path == LF_PATH_STAGED || h->mc.n > 0) return false;  // materials: stage-wise kernels
+  if (h->path == LF_PATH_STAGED) return false;
+  // materials: the two-pass material kernels for up to 4 materials, else stage-wise
+  if (h->mc.n > 0 && (h->mc.n > 4 || h->path == LF_PATH_FUSED || !h->partials_ready)) return false;
   return fused_supported(h);
 }
 
@@ -646,11 +651,19 @@ int guarded(lf_handle* h, F&& f) {
 
 namespace lfb {
 void fill_all_public(lf_handle* h, double* SlabState::*buf) { fill_all(h, buf); }
+void fill_partials_public(lf_handle* h, double* SlabState::*buf) { fill_partials(h, buf); }
 void alloc_staged_public(lf_handle* h) {
   for (auto& s : h->slabs) alloc_staged(s);
 }
 Scalars rate_of_current(lf_handle* h) {
-  launch_rate_all(h, &SlabState::U);
+  if (h->mc.n) {
+    // heun_step's fill_all_ghosts(state.field, mat, 0) before compute_dt
+    fill_all(h, &SlabState::U);
+    fill_partials(h, &SlabState::P);
+    launch_rate_all(h, &SlabState::U, &SlabState::P);
+  } else {
+    launch_rate_all(h, &SlabState::U);
+  }
   return combined_scalars(h, 0);
 }
 int staged_heun_public(lf_handle* h, double cfl, double time, double limit, int64_t step,
@@ -827,8 +840,16 @@ int lf_set_materials(lf_handle* h, int n, const double* gammas) {
       const size_t gb = ((size_t)s.L.fstride + s.L.pitch) * sizeof(double);
       CK(cudaMalloc(&s.P, kb));
       CK(cudaMalloc(&s.Ps, kb));
+      CK(cudaMalloc(&s.P2, kb));
       CK(cudaMemsetAsync(s.P, 0, kb, s.stream));
       CK(cudaMemsetAsync(s.Ps, 0, kb, s.stream));
+      CK(cudaMemsetAsync(s.P2, 0, kb, s.stream));
+      if (n <= 4) {  // the two-pass material kernels' stage-a fluxes
+        CK(cudaMalloc(&s.MFX, (size_t)n * s.fx_stride * sizeof(double)));
+        CK(cudaMalloc(&s.MFY, (size_t)n * s.fy_stride * sizeof(double)));
+        CK(cudaMemsetAsync(s.MFX, 0, (size_t)n * s.fx_stride * sizeof(double), s.stream));
+        CK(cudaMemsetAsync(s.MFY, 0, (size_t)n * s.fy_stride * sizeof(double), s.stream));
+      }
       for (int k = 0; k < 2; ++k) {
         CK(cudaMalloc(&s.Y[k], kb));
         CK(cudaMemsetAsync(s.Y[k], 0, kb, s.stream));

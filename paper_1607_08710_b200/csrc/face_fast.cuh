@@ -37,7 +37,10 @@ __device__ __forceinline__ FK make_fk(double gamma, double gm1, double beta, dou
 // Lagrange-flux face flux (riemann_hll.hpp:29-39, solver.cpp:26-43) on the fast
 // paths, for u* != 0; ok &= every range check.  When needs_mean(us_out) the
 // caller replaces f with face_mean (the reference's mean-state branch).
-template <int AXIS>
+// TINY: some velocity of the stencil may lie in (0, 2^-500) (numerical
+// precursors), so the velocity-weighted quotient of u* goes through div_exact;
+// without such velocities the cell box proves the plain fast path valid.
+template <int AXIS, bool TINY = true>
 __device__ __forceinline__ void face_fast(double m0, double m1, double m2, double m3, double p0,
                                           double p1, double p2, double p3, const FK& c,
                                           double f[4], bool& ok, double& ps_out, double& us_out) {
@@ -49,7 +52,8 @@ __device__ __forceinline__ void face_fast(double m0, double m1, double m2, doubl
   const double rho_sum = m0 + p0;
   const Recip rs = recip_of(rho_sum);
   const double ps = div_fast(p0 * m3 + m0 * p3, rs, ok) - div_fast(m0 * p0, rs, ok) * cmax * (ur - ul);
-  const double us = div_fast(m0 * ul + p0 * ur, rs, ok) - div1_fast(p3 - m3, cmax * rho_sum, ok);
+  const double un = TINY ? div_exact(m0 * ul + p0 * ur, rs, ok) : div_fast(m0 * ul + p0 * ur, rs, ok);
+  const double us = un - div1_fast(p3 - m3, cmax * rho_sum, ok);
   // upwind side, branch-free (u* > 0: minus trace, else plus trace); the mean
   // state of u* == 0 is patched afterwards by face_mean (rare), so the main
   // path stays one straight line the compiler can interleave with other faces
@@ -116,14 +120,15 @@ __device__ __forceinline__ void traces_ab(double a, double b, double q0, double 
 }
 
 // The cell box.  If every cell feeding a face has rho, p in [2^-100, 2^100) and
-// |u|, |v| in {0} u [2^-500, 2^100), every division and square root of the face
-// (face_fast / face_mean) is on its fast path, so the kernels test the box once
-// per cell instead of range-checking each operation:
+// |u|, |v| < 2^100, every division and square root of the face (face_fast /
+// face_mean) is on its fast path -- except the velocity-weighted quotient of u*,
+// which div_exact completes with the IEEE operator when needed -- so the
+// kernels test the box once per cell instead of range-checking each operation:
 //   * traces: rho0 - hs > 0 is either >= rho0/2 or, by Sterbenz, an exact
 //     difference of two values >= 2^-101, hence >= 2^-153; all traces are below
-//     2^101; a velocity trace is 0 or >= 2^-605 (the same argument one level down);
-//   * dividends: rho_L u_L + rho_R u_R is 0 or >= 2^-810, p_R - p_L is 0 or
-//     >= 2^-205, every other dividend is a product of traces >= 2^-306;
+//     2^101;
+//   * dividends: p_R - p_L is 0 or >= 2^-205, every other dividend except
+//     rho_L u_L + rho_R u_R (div_exact) is a product of traces >= 2^-306;
 //   * divisors rho_L + rho_R, cmax (rho_L + rho_R), rho, gamma - 1 lie in
 //     [2^-280, 2^233], so every quotient is in [2^-913, 2^400] -- normal, where
 //     the fast path is exact (fastmath.cuh; gamma - 1 in [2^-14, 2^6) is checked
@@ -135,9 +140,13 @@ __device__ __forceinline__ bool pos_in_box(double x) {
   return ((unsigned)__double2hiint(x) - 0x39b00000u) < (0x46300000u - 0x39b00000u);
 }
 __device__ __forceinline__ bool vel_in_box(double x) {
-  // |x| in [2^-500 (hi 0x20b00000), 2^100) or x == +-0
+  // |x| < 2^100 (hi word of 2^100 = 0x46300000); zero and subnormals included
+  return ((unsigned)__double2hiint(x) & 0x7fffffffu) < 0x46300000u;
+}
+// a velocity in (0, 2^-500): the stencil needs the exact u* quotient (face_fast<.., true>)
+__device__ __forceinline__ bool vel_tiny(double x) {
   const unsigned h = (unsigned)__double2hiint(x) & 0x7fffffffu;
-  return (h - 0x20b00000u) < (0x46300000u - 0x20b00000u) || (h | (unsigned)__double2loint(x)) == 0u;
+  return h < 0x20b00000u && (h | (unsigned)__double2loint(x)) != 0u;
 }
 __device__ __forceinline__ bool cell_in_box(const double w[4]) {
   return pos_in_box(w[0]) && pos_in_box(w[3]) && vel_in_box(w[1]) && vel_in_box(w[2]);
@@ -167,7 +176,7 @@ __device__ __forceinline__ void cell_epilogue(const double v[4], const FK& c, do
                                               bool& ok_r) {
   const Recip r0 = recip_of(v[0]);
   const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
-  eint = v[3] - div_fast(kin, r0, ok_e);
+  eint = v[3] - div_exact(kin, r0, ok_e);
   const double inv = div_fast(1.0, r0, ok_r);
   const double uu = v[1] * inv, vv = v[2] * inv;
   const double p = c.gm1 * (v[3] - kin * inv);

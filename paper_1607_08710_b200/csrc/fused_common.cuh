@@ -28,9 +28,10 @@ struct StepAcc {
   unsigned long long nmin_rho;    // ~bits(min rho of U^{n+1})
   unsigned long long nmin_eint;   // ~bits(min e_int of U^{n+1})
   unsigned long long dtfail_next; // rate check of U^{n+1} failed
-  unsigned long long pad[3];
+  unsigned long long nmin_p;      // ~bits(min p of U^{n+1}) from the partials (multimaterial)
+  unsigned long long pad[2];
 };
-constexpr int STEP_ACC_WORDS = 5;
+constexpr int STEP_ACC_WORDS = 6;
 
 // Per-step record handed back to the host.
 struct StepRec {
@@ -38,6 +39,7 @@ struct StepRec {
   double time;       // time after the step
   double min_rho;
   double min_eint;
+  double min_p_mat;  // multimaterial min p (solver.cpp:522-538); +inf without
   int hits;
   int status;        // 0 ok, 1 failure flag (host diagnoses), 2 skipped (done)
 };

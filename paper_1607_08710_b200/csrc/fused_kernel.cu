@@ -551,6 +551,7 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
   r.time = c.time;
   r.min_rho = 0.0;
   r.min_eint = 0.0;
+  r.min_p_mat = __longlong_as_double(0x7ff0000000000000ll);
   StepCtl n;
   n.rate_bits = acc->rate_next;
   n.dtfail = acc->dtfail_next != 0;
@@ -568,6 +569,7 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
     r.time = r.hits ? limit : c.time + dt;
     r.min_rho = __longlong_as_double((long long)~acc->nmin_rho);
     r.min_eint = __longlong_as_double((long long)~acc->nmin_eint);
+    r.min_p_mat = __longlong_as_double((long long)~acc->nmin_p);
     const double ax = dt * dy, ay = dt * dx;
     for (int q = 0; q < 4; ++q) {
       outflow[q] += ax * sums[q];
@@ -584,6 +586,7 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
   acc->nmin_rho = NINF_KEY;
   acc->nmin_eint = NINF_KEY;
   acc->dtfail_next = 0ull;
+  acc->nmin_p = NINF_KEY;
 }
 
 __global__ void k_acc_init(StepAcc* acc) {
@@ -593,6 +596,7 @@ __global__ void k_acc_init(StepAcc* acc) {
     acc[i].nmin_rho = NINF_KEY;
     acc[i].nmin_eint = NINF_KEY;
     acc[i].dtfail_next = 0ull;
+    acc[i].nmin_p = NINF_KEY;
   }
 }
 

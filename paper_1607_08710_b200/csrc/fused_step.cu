@@ -157,7 +157,7 @@ static void seed_ctl(lf_handle* h, double time) {
     c.time = time;
     c.rate_bits = sc.rate_bits;
     c.done = 0;
-    c.dtfail = sc.fail_dt != LLONG_MAX;
+    c.dtfail = sc.fail_dt != LLONG_MAX || sc.fail_frac != LLONG_MAX;
     f->ctl_host[0] = c;
     FK(cudaMemcpyAsync(&f->ctl[f->cur], &f->ctl_host[0], sizeof(StepCtl), cudaMemcpyHostToDevice,
                        s0.stream));
@@ -183,10 +183,15 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   double* bnd = f->bnd + (size_t)cur * bnd_words(h);
   if (h->nccl) FK(cudaMemsetAsync(bnd, 0, bnd_words(h) * sizeof(double), s0.stream));
   if (k0) FK(cudaEventRecord(k0, s0.stream));
+  const bool mat = h->mc.n > 0;
   if (use_twopass(h)) {
     // two passes: predictor U^n -> U*, F^n; ghosts / halos of U*; corrector
+    if (mat) fill_partials_public(h, &SlabState::P);
     for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) fill_all_public(h, &SlabState::Us);
+      if (pass == 1) {
+        fill_all_public(h, &SlabState::Us);
+        if (mat) fill_partials_public(h, &SlabState::Ps);
+      }
       for (auto& s : h->slabs) {
         PassArgs a;
         a.x = (pass == 0 ? s.U : s.Us) + s.L.origin();
@@ -216,7 +221,21 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
         a.ctl = f->ctl + cur;
         a.acc = f->acc + cur;
         a.bnd = bnd;
-        launch_pass(a, pass == 1, h->d.spatial_order >= 2, s.stream);
+        if (mat) {
+          MatPassArgs m;
+          m.px = (pass == 0 ? s.P : s.Ps) + s.L.origin();
+          m.pbase = s.P + s.L.origin();
+          m.pout = (pass == 0 ? s.Ps : s.P2) + s.L.origin();
+          m.mfx = s.MFX;
+          m.mfy = s.MFY;
+          m.mfxo = s.MFX;
+          m.mfyo = s.MFY;
+          m.mfx_stride = s.fx_stride;
+          m.mfy_stride = s.fy_stride;
+          launch_pass_mat(a, m, h->mc, pass == 1, h->d.spatial_order >= 2, s.stream);
+        } else {
+          launch_pass(a, pass == 1, h->d.spatial_order >= 2, s.stream);
+        }
       }
     }
   }
@@ -258,7 +277,10 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   launch_finalize(f->ctl + cur, f->acc + cur, f->ctl + nxt, f->rec + n_in_batch, bnd, f->outflow,
                   h->d.nx, h->d.ny, h->d.dx, h->d.dy, cfl, limit, t_final, s0.stream);
   FK(cudaGetLastError());
-  for (auto& s : h->slabs) std::swap(s.U, s.U2);
+  for (auto& s : h->slabs) {
+    std::swap(s.U, s.U2);
+    if (mat) std::swap(s.P, s.P2);
+  }
   f->cur = nxt;
 }
 
@@ -313,19 +335,22 @@ static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_fin
   // the output of step done-1 (a failed or skipped step leaves its input intact)
   const int undo = n - done;
   if (undo & 1)
-    for (auto& s : h->slabs) std::swap(s.U, s.U2);
+    for (auto& s : h->slabs) {
+      std::swap(s.U, s.U2);
+      if (h->mc.n) std::swap(s.P, s.P2);
+    }
   f->cur = (f->cur + undo) & 1;
   f->valid = *failed_at < 0;
   return done;
 }
 
-static void to_out(const StepRec& r, int64_t step, double gm1, lf_step_out* o) {
+static void to_out(const StepRec& r, int64_t step, double gm1, lf_step_out* o, bool mat = false) {
   o->dt = r.dt;
   o->hits_limit = r.hits;
   o->time = r.time;
   o->step = step;
   o->min_rho = r.min_rho;
-  o->min_p = gm1 * r.min_eint;
+  o->min_p = mat ? r.min_p_mat : gm1 * r.min_eint;
 }
 
 int fused_heun(lf_handle* h, double cfl, double time, double limit, int64_t step,
@@ -335,7 +360,7 @@ int fused_heun(lf_handle* h, double cfl, double time, double limit, int64_t step
   const int done = run_batch(h, 1, cfl, limit, limit, time, outflow, &failed_at, false, nullptr);
   if (done == 1) {
     if (outflow) std::memcpy(outflow, fstate(h)->outflow_host, 4 * sizeof(double));
-    if (out) to_out(fstate(h)->rec_host[0], step + 1, h->d.gamma - 1.0, out);
+    if (out) to_out(fstate(h)->rec_host[0], step + 1, h->d.gamma - 1.0, out, h->mc.n > 0);
     return 0;
   }
   // a flag was raised: the stage-wise kernels reproduce the exact error / state
@@ -356,7 +381,7 @@ int fused_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* 
                                false, nullptr);
     for (int i = 0; i < done; ++i) {
       *step += 1;
-      if (per_step) to_out(f->rec_host[i], *step, h->d.gamma - 1.0, &per_step[k + i]);
+      if (per_step) to_out(f->rec_host[i], *step, h->d.gamma - 1.0, &per_step[k + i], h->mc.n > 0);
       *time = f->rec_host[i].time;
     }
     k += done;

@@ -41,6 +41,9 @@ struct SlabState {
   double* GC[2] = {nullptr, nullptr};  // mixed-cell gamma per slot (gamma_), 1 component
   double* USX[2] = {nullptr, nullptr}; // u* of the x faces of flux set k (ustar_x)
   double* USY[2] = {nullptr, nullptr}; // u* of the y faces (ustar_y)
+  double* P2 = nullptr;              // two-pass path: partial densities of U^{n+1}
+  double* MFX = nullptr;             // two-pass path: predictor's material x-face fluxes
+  double* MFY = nullptr;             //                and y-face fluxes (F^n strides)
 
   Field field(double* p) const { return Field{p + L.origin(), L.pitch, L.fstride}; }
   FluxArr fluxx(int k) const { return FluxArr{FX[k], L.pitch, fx_stride}; }
@@ -73,6 +76,7 @@ struct lf_handle {
 namespace lfb {
 // api.cu services used by the fused path
 void fill_all_public(lf_handle* h, double* SlabState::*buf);
+void fill_partials_public(lf_handle* h, double* SlabState::*buf);
 void alloc_staged_public(lf_handle* h);
 Scalars rate_of_current(lf_handle* h);
 int staged_heun_public(lf_handle* h, double cfl, double time, double limit, int64_t step,

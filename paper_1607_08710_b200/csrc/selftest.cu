@@ -46,7 +46,7 @@ __device__ __forceinline__ bool same(double x, double y) {
 }
 
 __global__ void k_selftest(long long n, unsigned long long seed, unsigned long long* out) {
-  unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long c[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     unsigned long long s = seed ^ (unsigned long long)i * 0x632be59bd9b4e019ull;
@@ -79,8 +79,33 @@ __global__ void k_selftest(long long n, unsigned long long seed, unsigned long l
     const double beta = 1.0 + (double)(splitmix(s) >> 11) * 0x1.0p-53;
     const double la = draw(s, false), lb = draw(s, false);
     if (!same(sweby_fast(la, lb, beta), sweby(la, lb, beta))) c[6] += 1;
+    // div_exact: dividends down to the subnormals (scales 2^-1074 .. 2^-700,
+    // subnormal quotients included) and constructed near-ties of the subnormal
+    // rounding (b (m + 1/2) 2^-1074 +- 1 ulp) over physical-range divisors
+    {
+      const unsigned long long rr = splitmix(s);
+      double tiny, bd = fabs(draw(s, false));
+      if (bd == 0.0) bd = 1.0;
+      if (rr & 1) {
+        const int e = (int)((rr >> 1) % 375);
+        const unsigned long long mant = splitmix(s) >> (12 + (int)((rr >> 9) % 40));
+        tiny = ldexp((double)mant * 0x1p-537 * 0x1p-537, e);
+      } else {
+        const double mm = (double)(splitmix(s) >> 20) + 0.5;
+        tiny = (bd * mm) * 0x1p-537 * 0x1p-537;
+        const unsigned long long t2 = splitmix(s);
+        if ((t2 & 2) && tiny > 0.0)  // one ulp off the tie (never below +0)
+          tiny = __longlong_as_double(__double_as_longlong(tiny) + ((t2 & 4) ? 1 : -1));
+      }
+      if (splitmix(s) & 1) tiny = -tiny;
+      bool ok = true;
+      const double q = div_exact(tiny, recip_of(bd), ok);
+      c[7] += 1;
+      if (ok && !same(q, tiny / bd) && !(q == 0.0 && tiny / bd == 0.0)) c[8] += 1;
+      if (!ok) c[9] += 1;
+    }
   }
-  for (int k = 0; k < 7; ++k) atomicAdd(&out[k], c[k]);
+  for (int k = 0; k < 10; ++k) atomicAdd(&out[k], c[k]);
 }
 
 // ---- the cell box (face_fast.cuh) --------------------------------------
@@ -120,6 +145,11 @@ __device__ __forceinline__ void box_cell(unsigned long long& s, const double* pr
       w[q] = prev[q] == 0.0 ? 0.0 : nudge(s, prev[q]);
     } else if ((k & 7) == 2) {
       w[q] = 0.0;
+    } else if ((k & 7) == 3) {
+      // precursor-sized velocities: 2^-1074 .. 2^-600, subnormals included
+      const double m = ldexp((double)(splitmix(s) >> (12 + (int)(k >> 8) % 50)) * 0x1p-537 * 0x1p-537,
+                             (int)((k >> 16) % 470));
+      w[q] = (k & 8) ? -m : m;
     } else {
       const double m = box_mag(s, -500, 100);
       w[q] = (k & 8) ? -m : m;
@@ -194,14 +224,14 @@ extern "C" int lf_selftest_box(int64_t n, uint64_t seed, int64_t* counts) {
 extern "C" int lf_selftest_fastmath(int64_t n, uint64_t seed, int64_t* counts) {
   if (!counts || n < 0) return LF_ERR_ARGUMENT;
   unsigned long long* d = nullptr;
-  if (cudaMalloc(&d, 8 * sizeof(unsigned long long)) != cudaSuccess) return LF_ERR_DEVICE;
-  cudaMemset(d, 0, 8 * sizeof(unsigned long long));
+  if (cudaMalloc(&d, 10 * sizeof(unsigned long long)) != cudaSuccess) return LF_ERR_DEVICE;
+  cudaMemset(d, 0, 10 * sizeof(unsigned long long));
   lfb::count_launch();
   lfb::k_selftest<<<148 * 8, 256>>>((long long)n, (unsigned long long)seed, d);
-  unsigned long long h[8];
+  unsigned long long h[10];
   const cudaError_t e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   cudaFree(d);
   if (e != cudaSuccess) return LF_ERR_DEVICE;
-  for (int k = 0; k < 7; ++k) counts[k] = (int64_t)h[k];
+  for (int k = 0; k < 10; ++k) counts[k] = (int64_t)h[k];
   return LF_OK;
 }

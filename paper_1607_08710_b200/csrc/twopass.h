@@ -33,8 +33,25 @@ struct PassArgs {
   double* bnd;          // corrector: boundary faces [left 4*nyg | right 4*nyg | bottom 4*nx | top 4*nx]
 };
 
+// Multimaterial operands of the two passes (csrc/twopass_mat_kernel.cu):
+// partial densities with the field's Layout strides, and the predictor's
+// per-material face fluxes (the corrector's stage-a term) with the F^n strides.
+struct MatPassArgs {
+  const double* px;      // partials of the pass input: P^n (predictor) or P* (corrector)
+  const double* pbase;   // P^n
+  double* pout;          // P* or P^{n+1}
+  const double* mfx;     // corrector: stage-a material fluxes, x faces [K][ny][pitch]
+  const double* mfy;     // corrector: y faces [K][ny+1][pitch]
+  double* mfxo;          // predictor: written
+  double* mfyo;
+  int64_t mfx_stride, mfy_stride;
+};
+
 int tp_strips(int nx);
 bool tp_fits(int64_t pitch, int ny);  // 32-bit offsets suffice for the slab
 void launch_pass(const PassArgs& a, bool corr, bool muscl, cudaStream_t st);
+struct MatConsts;
+void launch_pass_mat(const PassArgs& a, const MatPassArgs& m, const MatConsts& mc, bool corr,
+                     bool muscl, cudaStream_t st);
 
 }  // namespace lfb

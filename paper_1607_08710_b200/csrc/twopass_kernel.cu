@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
   }
   double wm2[4] = {1.0, 0.0, 0.0, 1.0}, wm1[4] = {1.0, 0.0, 0.0, 1.0};
   double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fyprev[4] = {0.0, 0.0, 0.0, 0.0};
+  // rows r-3 .. r-1 of this lane with a velocity in (0, 2^-500), one bit per row
+  unsigned tiny_rows = 0;
 
 #if LF_TP_UNROLL == 2
 #pragma unroll 2
@@ -162,6 +164,9 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
       prim_fast(cur[0], cur[1], cur[2], cur[3], a.gm1, w, okw);
       if (!cell_in_box(w) && col_interior && r >= 0 && r < a.ny) fail = 1;
     }
+    tiny_rows = ((tiny_rows << 1) | (unsigned)(vel_tiny(w[1]) || vel_tiny(w[2]))) & 0xfu;
+    // the faces of this iteration read W rows r-3 .. r of lanes l-2 .. l+1
+    const bool tiny = __any_sync(FULL, tiny_rows != 0u);
     // -- y: traces of row r-1, face (r-2 | r-1); x: traces of row r-2 (shuffles)
     double ylo[4], yhi[4], xlo[4], xhi[4], xp[4], da[4], db[4];
     shfl_down4(wm2, xp, 1);
@@ -180,10 +185,20 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     const bool need_x = it >= 4 && lane >= 2 && lane <= LANES - 2 && c <= a.nx;
     const bool need_y = it >= 3 && lane >= 2 && lane <= LANES - 3 && col_interior;
     double psx, usx, psy, usy;
-    face_fast<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx, okx, psx,
-                 usx);
-    face_fast<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3], C,
-                 fy, oky, psy, usy);
+    if (tiny) {
+      // a velocity in (0, 2^-500) in this warp's stencil rows (numerical
+      // precursors ahead of a shock): the exact u* quotient (div_exact)
+      face_fast<0, true>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx,
+                         okx, psx, usx);
+      face_fast<1, true>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2],
+                         ylo[3], C, fy, oky, psy, usy);
+      if ((need_x && !okx) || (need_y && !oky)) fail = 1;  // div_exact out of range
+    } else {
+      face_fast<0, false>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx,
+                          okx, psx, usx);
+      face_fast<1, false>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2],
+                          ylo[3], C, fy, oky, psy, usy);
+    }
     if (needs_mean(usx))
       face_mean<0>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], psx, usx, C,
                    fx, okx);

@@ -11,12 +11,14 @@ pytestmark = pytest.mark.gpu
 
 
 def test_fast_division_sqrt_limiter_exact(cuda):
-    counts = (C.c_int64 * 7)()
+    counts = (C.c_int64 * 10)()
     n = 1 << 28
     assert N.lib().lf_selftest_fastmath(n, 0x1607087100, counts) == 0
-    tested, div_ok, div_bad, shared_bad, sqrt_ok, sqrt_bad, lim_bad = list(counts)
+    tested, div_ok, div_bad, shared_bad, sqrt_ok, sqrt_bad, lim_bad, tiny, tiny_bad, tiny_oor = list(counts)
     assert tested == n
     assert div_bad == 0 and shared_bad == 0 and sqrt_bad == 0 and lim_bad == 0
+    # div_exact (tiny dividends, subnormal quotients, constructed rounding ties)
+    assert tiny == n and tiny_bad == 0 and tiny_oor == 0
     # the fast paths must cover the physical range (half the draws) and more
     assert div_ok > 0.5 * n and sqrt_ok > 0.5 * n
 

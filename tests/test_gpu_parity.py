@@ -241,7 +241,57 @@ def _box_cases():
 
 
 @pytest.mark.parametrize("path", ["twopass", "fused"])
-@pytest.mark.parametrize("which", ["tiny_velocity", "light_region", "gamma_near_one"])
+def test_tiny_velocities_stay_on_the_fast_path(cuda, path):
+    """Velocities down to the subnormals (numerical precursors ahead of shocks):
+    the exact u* quotient (div_exact) keeps them in the fast kernels -- no
+    stage-wise re-run -- with the oracle's bits."""
+    case, field = _box_cases()["tiny_velocity"]
+    field = field.copy()
+    g = case.grid
+    field[2][g.gy + 20, g.gx + 3:g.gx + 7] = 5e-324 * field[0][g.gy + 20, g.gx + 3:g.gx + 7]
+    ref, rdiag = run_oracle(case, 4, field=field)
+
+    def run(fld):
+        s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path=path)
+        st = G.SolverState(field=np.array(fld))
+        n0 = s.launch_count()
+        for _ in range(4):
+            s.heun_step(st, G.TimeControls(case.cfl, case.t_final), case.t_final)
+        s.sync_to_host(st)
+        n = s.launch_count() - n0
+        s.close()
+        return st, n
+
+    state, n_tiny = run(field)
+    assert_fields_equal(g.interior(state.field), g.interior(ref.field), "tiny")
+    assert np.array_equal(diag_array(state)[:, :4], rdiag[:, :4])
+    _, n_plain = run(CS.initial_field(CS.quadrant(48, 4)))
+    assert n_tiny == n_plain
+
+
+@pytest.mark.parametrize("cfg", ["sedov", "quadrant"])
+def test_shock_precursors_need_no_stagewise_rerun(cuda, cfg):
+    """Shocks into quiescent regions create arbitrarily small velocities ahead of
+    the front; the fast two-pass step handles them itself (constant launches per
+    step) and stays bit-identical to the oracle."""
+    case = CS.sedov(128, 40) if cfg == "sedov" else CS.quadrant(128, 40)
+    f0 = CS.initial_field(case)
+    ref, rdiag = run_oracle(case, 40, field=f0)
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path="twopass")
+    st = G.SolverState(field=f0.copy())
+    counts = []
+    for _ in range(40):
+        n0 = s.launch_count()
+        s.heun_step(st, G.TimeControls(case.cfl, case.t_final), case.t_final)
+        counts.append(s.launch_count() - n0)
+    s.sync_to_host(st)
+    assert_fields_equal(case.grid.interior(st.field), case.grid.interior(ref.field), cfg)
+    assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4])
+    assert max(counts[1:]) == min(counts[1:]) <= 8, counts
+
+
+@pytest.mark.parametrize("path", ["twopass", "fused"])
+@pytest.mark.parametrize("which", ["light_region", "gamma_near_one"])
 def test_out_of_box_states_rerun_exactly(cuda, which, path):
     case, field = _box_cases()[which]
     ref, rdiag = run_oracle(case, 4, field=field)

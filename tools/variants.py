@@ -23,10 +23,10 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # name -> (extra nvcc flags, LF_PATH_*); "base_*" variants build the same path
 # from the committed sources (git HEAD) for an A/B against the working tree
 VARIANTS = {
+    "base_tp": ("", 3),
+    "tp": ("", 3),
     "base_fused": ("", 1),
     "fused": ("", 1),
-    "fused_epip": ("-DLF_EPI_P=1", 1),
-    "tp": ("", 3),
 }
 
 
