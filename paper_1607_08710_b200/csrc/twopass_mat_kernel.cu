@@ -18,9 +18,11 @@
 // The predictor stores P* and its per-material face fluxes (the corrector's
 // stage-a term); the corrector writes P^{n+1}, min p and the next step's CFL
 // rate with the mixed-cell gamma of U^{n+1} (the next step's fill closure).
-// Range checks stay on every fast division here (the cell box of face_fast.cuh
-// assumes one gamma); a clamp beyond round-off or any failed check flags the
-// step and the stage-wise kernels recompute it exactly (errors included).
+// The cell box of face_fast.cuh (with every cell's gamma checked as well) proves
+// the face solves' fast divisions valid; the velocity-weighted u* quotient and
+// the fraction quotients go through div_exact.  A clamp beyond round-off or a
+// failed check flags the step and the stage-wise kernels recompute it exactly
+// (errors included).
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -59,38 +61,55 @@ struct MatK {
   double gamma[4];
 };
 
-// fill_all_ghosts' closure for one cell (solver.cpp:100-121); bad: a fraction
-// beyond round-off.  Partial densities diffuse into arbitrarily small values
-// (fronts decay geometrically), so these quotients use the IEEE operator --
-// exact for every operand, its slow path taken only for such tiny values --
-// instead of the fast path's range check, which would flag those steps.
+struct MatR {
+  Recip rg[4];   // 1 / (gamma_k - 1.0), shared by every cell
+};
+
+// fill_all_ghosts' closure for one cell (solver.cpp:100-121) from the raw
+// fractions raw_k = P_k / rho and their quotients q_k = raw_k / (gamma_k - 1);
+// bad: a fraction beyond round-off.  The quotients go through div_exact:
+// partial densities diffuse into arbitrarily small values (fronts decay
+// geometrically) and the quotient must stay exact there.
 template <int K>
-__device__ __forceinline__ double closure(const double* p, double rho, const MatK& m, double y[K],
-                                          bool& bad, bool& ok) {
+__device__ __forceinline__ double closure_q(const double raw[K], const double q[K], const MatK& m,
+                                            const MatR& mr, double y[K], bool& bad, bool& ok) {
   double ysum = 0.0;
   int pure = -1;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const double raw = p[k] / rho;
-    double yk = raw;
+    double yk = raw[k];
+    double qk = q[k];
     if (yk < 0.0 || yk > 1.0) {
-      if (raw < -1e-11 || raw > 1.0 + 1e-11) {
+      if (raw[k] < -1e-11 || raw[k] > 1.0 + 1e-11) {
         bad = true;
         yk = 0.0;
       } else {
-        yk = raw < 0.0 ? 0.0 : 1.0;
+        yk = raw[k] < 0.0 ? 0.0 : 1.0;
       }
+      qk = div_exact(yk, mr.rg[k], ok);
     }
     y[k] = yk;
     if (yk == 1.0) pure = k;
-    ysum += yk / (m.gamma[k] - 1.0);
+    ysum += qk;
   }
   double gp = 0.0;
 #pragma unroll
   for (int k = 0; k < K; ++k)
     if (pure == k) gp = m.gamma[k];
-  (void)ok;
-  return pure >= 0 ? gp : 1.0 + 1.0 / ysum;
+  return pure >= 0 ? gp : 1.0 + div1_fast(1.0, ysum, ok);
+}
+
+template <int K>
+__device__ __forceinline__ double closure(const double* p, double rho, const MatK& m,
+                                          const MatR& mr, double y[K], bool& bad, bool& ok) {
+  const Recip rr = recip_of(rho);
+  double raw[K], q[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    raw[k] = div_exact(p[k], rr, ok);
+    q[k] = div_exact(raw[k], mr.rg[k], ok);
+  }
+  return closure_q<K>(raw, q, m, mr, y, bad, ok);
 }
 
 __device__ __forceinline__ bool gamma_in_box(double g) {
@@ -99,45 +118,53 @@ __device__ __forceinline__ bool gamma_in_box(double g) {
 }
 
 // face_fast with each side's own gamma (lagrangian_hll(wm, wp, n, el, er) and
-// conserved_from_primitive with that side's EOS, riemann_hll.hpp:29-39)
+// conserved_from_primitive with that side's EOS, riemann_hll.hpp:29-39).  The
+// cell box of face_fast.cuh holds with per-side gammas too (every cell's gamma
+// is checked: gamma - 1 in [2^-14, 2^6)), so only the velocity-weighted u*
+// quotient needs div_exact; ok reports its range.  u* == 0: face_mean_g.
 template <int AXIS>
 __device__ __forceinline__ void face_g(const double m[4], const double p[4], double gl, double gr,
                                        double f[4], bool& ok, double& ps_out, double& us_out) {
+  bool unused = true;
   const double ul = AXIS == 0 ? m[1] : m[2];
   const double ur = AXIS == 0 ? p[1] : p[2];
-  const double cl = sqrt_fast(div1_fast(gl * m[3], m[0], ok), ok);
-  const double cr = sqrt_fast(div1_fast(gr * p[3], p[0], ok), ok);
+  const double cl = sqrt_fast(div1_fast(gl * m[3], m[0], unused), unused);
+  const double cr = sqrt_fast(div1_fast(gr * p[3], p[0], unused), unused);
   const double cmax = pmax(cl, cr);
   const double rho_sum = m[0] + p[0];
   const Recip rs = recip_of(rho_sum);
-  const double ps =
-      div_fast(p[0] * m[3] + m[0] * p[3], rs, ok) - div_fast(m[0] * p[0], rs, ok) * cmax * (ur - ul);
-  const double us = div_exact(m[0] * ul + p[0] * ur, rs, ok) - div1_fast(p[3] - m[3], cmax * rho_sum, ok);
-  if (us > 0.0 || us < 0.0) {
-    const bool pos = us > 0.0;
-    const double s0 = pos ? m[0] : p[0], s1 = pos ? m[1] : p[1], s2 = pos ? m[2] : p[2];
-    const double s3 = pos ? m[3] : p[3], gs = pos ? gl : gr;
-    const double a1 = s0 * s1, a2 = s0 * s2;
-    const double a3 = div1_fast(s3, gs - 1.0, ok) + 0.5 * s0 * (s1 * s1 + s2 * s2);
-    f[0] = s0 * us;
-    f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
-    f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
-    f[3] = a3 * us + ps * us;
-  } else {
-    // solver.cpp:33-36 mean state (u* == 0 or NaN)
-    const double m3c = div1_fast(m[3], gl - 1.0, ok) + 0.5 * m[0] * (m[1] * m[1] + m[2] * m[2]);
-    const double p3c = div1_fast(p[3], gr - 1.0, ok) + 0.5 * p[0] * (p[1] * p[1] + p[2] * p[2]);
-    const double a0 = 0.5 * (m[0] + p[0]);
-    const double a1 = 0.5 * (m[0] * m[1] + p[0] * p[1]);
-    const double a2 = 0.5 * (m[0] * m[2] + p[0] * p[2]);
-    const double a3 = 0.5 * (m3c + p3c);
-    f[0] = a0 * us;
-    f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
-    f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
-    f[3] = a3 * us + ps * us;
-  }
+  const double ps = div_fast(p[0] * m[3] + m[0] * p[3], rs, unused) -
+                    div_fast(m[0] * p[0], rs, unused) * cmax * (ur - ul);
+  const double us =
+      div_exact(m[0] * ul + p[0] * ur, rs, ok) - div1_fast(p[3] - m[3], cmax * rho_sum, unused);
+  const bool pos = us > 0.0;
+  const double s0 = pos ? m[0] : p[0], s1 = pos ? m[1] : p[1], s2 = pos ? m[2] : p[2];
+  const double s3 = pos ? m[3] : p[3], gs = pos ? gl : gr;
+  const double a1 = s0 * s1, a2 = s0 * s2;
+  const double a3 = div1_fast(s3, gs - 1.0, unused) + 0.5 * s0 * (s1 * s1 + s2 * s2);
+  f[0] = s0 * us;
+  f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
+  f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
+  f[3] = a3 * us + ps * us;
   ps_out = ps;
   us_out = us;
+}
+
+// solver.cpp:33-41 mean state (u* == 0 or NaN) with each side's EOS
+template <int AXIS>
+__device__ __forceinline__ void face_mean_g(const double m[4], const double p[4], double gl,
+                                            double gr, double ps, double us, double f[4]) {
+  bool unused = true;
+  const double m3c = div1_fast(m[3], gl - 1.0, unused) + 0.5 * m[0] * (m[1] * m[1] + m[2] * m[2]);
+  const double p3c = div1_fast(p[3], gr - 1.0, unused) + 0.5 * p[0] * (p[1] * p[1] + p[2] * p[2]);
+  const double a0 = 0.5 * (m[0] + p[0]);
+  const double a1 = 0.5 * (m[0] * m[1] + p[0] * p[1]);
+  const double a2 = 0.5 * (m[0] * m[2] + p[0] * p[2]);
+  const double a3 = 0.5 * (m3c + p3c);
+  f[0] = a0 * us;
+  f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
+  f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
+  f[3] = a3 * us + ps * us;
 }
 
 // edge_material_flux (solver.cpp:345-357) from the face's mass flux and u* and
@@ -159,6 +186,9 @@ __device__ __forceinline__ void mat_face(double mass, double us, const double yl
 
 template <bool CORR, bool MUSCL, int K>
 __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassArgs m, MatK mk) {
+  MatR mr;
+#pragma unroll
+  for (int k = 0; k < K; ++k) mr.rg[k] = recip_of(mk.gamma[k] - 1.0);
   const StepCtl ctl = *a.ctl;
   if (ctl.done) return;
   if (ctl.dtfail) {
@@ -197,6 +227,16 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
 
   const int P = (int)a.pitch;
   int o_in = (y0 - 2) * P + c;
+  // the next input row (U and partials), loaded one iteration ahead
+  double nxt[4] = {1.0, 0.0, 0.0, 1.0}, pnx[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) pnx[k] = k == 0 ? 1.0 : 0.0;
+  if (col_in_mem) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) nxt[q] = __ldg(a.x + q * a.fstride + o_in);
+#pragma unroll
+    for (int k = 0; k < K; ++k) pnx[k] = __ldg(m.px + k * a.fstride + o_in);
+  }
   // windows: W rows r-2, r-1; gamma rows r-2, r-1; fractions rows r-2, r-1
   double wm2[4] = {1.0, 0.0, 0.0, 1.0}, wm1[4] = {1.0, 0.0, 0.0, 1.0};
   double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fyprev[4] = {0.0, 0.0, 0.0, 0.0};
@@ -213,14 +253,46 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
     double w[4] = {1.0, 0.0, 0.0, 1.0}, yr[K], gr = mk.gamma[0];
 #pragma unroll
     for (int k = 0; k < K; ++k) yr[k] = 0.0;
+    double cur[4], pc[K];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+#pragma unroll
+    for (int k = 0; k < K; ++k) pc[k] = pnx[k];
+    if (it + 1 < nit && col_in_mem) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nxt[q] = __ldg(a.x + q * a.fstride + o_in + P);
+#pragma unroll
+      for (int k = 0; k < K; ++k) pnx[k] = __ldg(m.px + k * a.fstride + o_in + P);
+    }
+    // this iteration's update operands, issued early (their latency hides
+    // behind the closure, traces and face solves)
+    double bse[4] = {0.0, 0.0, 0.0, 0.0}, pbs[K];
+    double fnx[4] = {0.0, 0.0, 0.0, 0.0}, fny[4] = {0.0, 0.0, 0.0, 0.0}, max_[K], may_[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) pbs[k] = max_[k] = may_[k] = 0.0;
+    if (it >= 4 && upd) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bse[q] = __ldg(a.base + q * a.fstride + o_row);
+#pragma unroll
+      for (int k = 0; k < K; ++k) pbs[k] = __ldg(m.pbase + k * a.fstride + o_row);
+    }
+    if (CORR) {
+      if (it >= 4 && col_in_mem && c >= 0 && c <= a.nx) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fnx[q] = __ldg(a.fx + q * a.fx_stride + o_row);
+#pragma unroll
+        for (int k = 0; k < K; ++k) max_[k] = __ldg(m.mfx + k * m.mfx_stride + o_row);
+      }
+      if (it >= 3 && col_interior) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fny[q] = __ldg(a.fy + q * a.fy_stride + (o_row + P));
+#pragma unroll
+        for (int k = 0; k < K; ++k) may_[k] = __ldg(m.mfy + k * m.mfy_stride + (o_row + P));
+      }
+    }
     if (col_in_mem) {
-      double cur[4], pc[K];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) cur[q] = __ldg(a.x + q * a.fstride + o_in);
-#pragma unroll
-      for (int k = 0; k < K; ++k) pc[k] = __ldg(m.px + k * a.fstride + o_in);
       bool bad = false, ok = true;
-      gr = closure<K>(pc, cur[0], mk, yr, bad, ok);
+      gr = closure<K>(pc, cur[0], mk, mr, yr, bad, ok);
       prim_fast(cur[0], cur[1], cur[2], cur[3], gr - 1.0, w, ok);
       // the fill's closure covers the reference's ghosted cells; the state
       // checks the interior (ghosts are images of interior cells)
@@ -251,6 +323,8 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
     bool okx = true, oky = true;
     face_g<0>(xmh, xlo, gl_x, gm2, fx, okx, psx, usx);
     face_g<1>(hiprev, ylo, gm2, gm1c, fy, oky, psy, usy);
+    if (needs_mean(usx)) face_mean_g<0>(xmh, xlo, gl_x, gm2, psx, usx, fx);
+    if (needs_mean(usy)) face_mean_g<1>(hiprev, ylo, gm2, gm1c, psy, usy, fy);
     const bool need_x = it >= 4 && lane >= 2 && lane <= LANES - 2 && c <= a.nx;
     const bool need_y = it >= 3 && lane >= 2 && lane <= LANES - 3 && col_interior;
     if ((need_x && !okx) || (need_y && !oky)) MFAIL(5);
@@ -267,22 +341,6 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
     // -- stage-a operands (corrector) and the Heun averages
     double fxa[4], fya[4];
     if (CORR) {
-      double fnx[4] = {0.0, 0.0, 0.0, 0.0}, fny[4] = {0.0, 0.0, 0.0, 0.0};
-      double max_[K], may_[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) max_[k] = may_[k] = 0.0;
-      if (it >= 4 && col_in_mem && c >= 0 && c <= a.nx) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) fnx[q] = __ldg(a.fx + q * a.fx_stride + o_row);
-#pragma unroll
-        for (int k = 0; k < K; ++k) max_[k] = __ldg(m.mfx + k * m.mfx_stride + o_row);
-      }
-      if (it >= 3 && col_interior) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) fny[q] = __ldg(a.fy + q * a.fy_stride + (o_row + P));
-#pragma unroll
-        for (int k = 0; k < K; ++k) may_[k] = __ldg(m.mfy + k * m.mfy_stride + (o_row + P));
-      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         fxa[q] = 0.5 * (fnx[q] + fx[q]);
@@ -326,7 +384,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
         double v[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          double val = __ldg(a.base + q * a.fstride + o_row) - lam_x * (fxr[q] - fxa[q]);
+          double val = bse[q] - lam_x * (fxr[q] - fxa[q]);
           val -= lam_y * (fya[q] - fyprev[q]);
           v[q] = val;
           a.out[q * a.fstride + o_row] = val;
@@ -339,7 +397,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
           const double fr = CORR ? mfxr[k] : 0.0 + mfxr[k];
           const double fb = CORR ? myprev[k] : 0.0 + myprev[k];
           const double ft = CORR ? mfy_s[k] : 0.0 + mfy_s[k];
-          double val = __ldg(m.pbase + k * a.fstride + o_row) - lam_x * (fr - fl);
+          double val = pbs[k] - lam_x * (fr - fl);
           val -= lam_y * (ft - fb);
           pn[k] = val;
           m.pout[k * a.fstride + o_row] = val;
@@ -354,17 +412,25 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
           const Recip r0 = recip_of(v[0]);
           const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
           const double eint = v[3] - div_exact(kin, r0, ok);
+          double rawn[K], qn[K];
+          bool have_q = false;
           if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
             MFAIL(9);
           } else {
             const unsigned long long kr = ~pos_bits(v[0]), ke = ~pos_bits(eint);
             nmin_r = kr > nmin_r ? kr : nmin_r;
             nmin_e = ke > nmin_e ? ke : nmin_e;
-            // min p from the fresh partials (solver.cpp:526-536): no clamp here
+            // min p from the fresh partials (solver.cpp:526-536): no clamp here;
+            // its quotients are the next step's closure quotients too
             double s = 0.0;
 #pragma unroll
-            for (int k = 0; k < K; ++k) s += (pn[k] / v[0]) / (mk.gamma[k] - 1.0);
-            const double pmin = eint / s;
+            for (int k = 0; k < K; ++k) {
+              rawn[k] = div_exact(pn[k], r0, ok);
+              qn[k] = div_exact(rawn[k], mr.rg[k], ok);
+              s += qn[k];
+            }
+            have_q = true;
+            const double pmin = div_exact(eint, recip_of(s), ok);
             if (!ok) MFAIL(10);
             if (pmin == pmin) {
               if (pmin > 0.0) {
@@ -378,7 +444,14 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
           // the next step's CFL rate with its fill closure (solver.cpp:441-469)
           double yn[K];
           bool bad = false, okg = true;
-          const double g = closure<K>(pn, v[0], mk, yn, bad, okg);
+          if (!have_q) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              rawn[k] = div_exact(pn[k], r0, okg);
+              qn[k] = div_exact(rawn[k], mr.rg[k], okg);
+            }
+          }
+          const double g = closure_q<K>(rawn, qn, mk, mr, yn, bad, okg);
           const double inv = div_fast(1.0, r0, okg);
           const double uu = v[1] * inv, vv = v[2] * inv;
           const double pp = (g - 1.0) * (v[3] - kin * inv);

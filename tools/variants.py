@@ -25,8 +25,7 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 VARIANTS = {
     "base_tp": ("", 3),
     "tp": ("", 3),
-    "base_fused": ("", 1),
-    "fused": ("", 1),
+    "tp_nb": ("-DLF_DIVTINY_MODE=4", 3),
 }
 
 
