@@ -357,7 +357,8 @@ def run_ours_mat(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "peak_source": hbm_src,
                 "algorithmic_bytes_per_cell_update": bytes_per,
-                "kernel": "whole stage-wise multimaterial step (no single dominant kernel)",
+                "kernel": "whole multimaterial step (two-pass material kernels lfb::k_pass_mat "
+                          "+ ghost fills + finalize)",
                 "kernel_ms_per_launch": ms_step, "kernel_share_of_step": 1.0, "traffic": None}
 
     e2e = None
@@ -410,7 +411,8 @@ def run_ours_mat(args):
             "data": "synthetic (cases/triple_point.case regions)",
             "config": {"workload": f"triple_point {g.nx}x{g.ny}, {n_mat} materials "
                                    f"(gammas {list(c.material_gammas)}), reflective",
-                       "nx": g.nx, "ny": g.ny, "cfl": c.cfl, "path": "staged (multimaterial)",
+                       "nx": g.nx, "ny": g.ny, "cfl": c.cfl,
+                       "path": "two-pass material kernels (csrc/twopass_mat_kernel.cu)",
                        "l2": "state %.2f GB (field + partials)" % ((4 + n_mat) * 8 * g.nx * g.ny / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary()}
