@@ -1,0 +1,66 @@
+"""BASELINE configs 2 and 3 at full size: GPU time and bitwise parity against the
+reference compiled from its own sources (oracle/_ref), on this box.
+
+    python tools/bench_configs.py [out.json]
+
+Config 2: four-quadrant 1024^2, transmissive, CFL 0.45, 200 steps.
+Config 3: Sedov 4096^2, reflective, CFL 0.4, 100 steps (the reference needs ~5 GB
+          and tens of seconds on all host cores).
+For each: device-resident steps through lf_advance (CUDA-event timed), then the
+final field and every step's dt / time / min rho / min p compared with the
+reference run (==).
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+from paper_1607_08710_b200 import cases as CS  # noqa: E402
+from paper_1607_08710_b200 import grid as G  # noqa: E402
+from paper_1607_08710_b200.solver import LagfluxSolver  # noqa: E402
+
+out = {}
+for name, case in (("config2_quadrant_1024", CS.quadrant(1024, 200)),
+                   ("config3_sedov_4096", CS.sedov(4096, 100))):
+    g = case.grid
+    f0 = CS.initial_field(case)
+    s = LagfluxSolver(g, case.bc, case.gamma, case.params)
+    stream = torch.cuda.current_stream()
+    s.set_stream(stream.cuda_stream)
+    st = G.SolverState(field=f0.copy())
+    ctl = G.TimeControls(case.cfl, case.t_final, case.max_steps)
+    s.attach(st)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    n = s.advance(st, ctl, case.max_steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    s.sync_to_host(st)
+    rec = {"steps": n, "gpu_ms_per_step": ms / n, "gpu_cell_updates_per_s": g.nx * g.ny * n / (ms / 1e3)}
+    if O.ref_available():
+        threads = os.cpu_count() or 1
+        r = O.RefSolver(g, case.bc, case.gamma, case.params, threads=threads)
+        r.set_state(f0)
+        t0 = time.perf_counter()
+        diag = r.heun_steps(n, case.cfl, case.t_final)
+        wall = time.perf_counter() - t0
+        rf = r.get_state()[0]
+        d = np.array([[x.dt, x.time, x.min_rho, x.min_p] for x in st.diagnostics])
+        rec.update({"reference_s_per_step": wall / n, "reference_threads": threads,
+                    "reference_cell_updates_per_s": g.nx * g.ny * n / wall,
+                    "field_equal": bool(np.all(g.interior(st.field) == g.interior(rf))),
+                    "diagnostics_equal": bool(np.array_equal(d, diag[:, :4])),
+                    "dt_first_last": [float(d[0, 0]), float(d[-1, 0])]})
+    out[name] = rec
+    print(name, json.dumps(rec), flush=True)
+    s.close()
+if len(sys.argv) > 1:
+    with open(sys.argv[1], "w") as f:
+        json.dump(out, f, indent=1)
