@@ -813,6 +813,7 @@ int lf_upload(lf_handle* h, double* const field[4], int64_t ld) {
       }
     }
     sync_all(h);
+    h->tp_exact = 0;  // a new state: the plain fast kernels first
     h->rate_valid = false;
     fused_invalidate(h);
     return 0;
@@ -1103,6 +1104,7 @@ int lf_init_fourier(lf_handle* h, uint64_t seed) {
       cudaFree(damp[k]);
     }
     CK(cudaGetLastError());
+    h->tp_exact = 0;  // a new state: the plain fast kernels first
     h->rate_valid = false;
     fused_invalidate(h);
     return 0;
@@ -1160,6 +1162,7 @@ int lf_init_regions(lf_handle* h, const double* regions, int nreg) {
                      fmt_f(x).c_str(), fmt_f(y).c_str(), hits);
     }
     if (h->mc.n) h->partials_ready = 1;
+    h->tp_exact = 0;  // a new state: the plain fast kernels first
     h->rate_valid = false;
     fused_invalidate(h);
     return 0;

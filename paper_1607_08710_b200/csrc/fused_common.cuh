@@ -41,7 +41,8 @@ struct StepRec {
   double min_eint;
   double min_p_mat;  // multimaterial min p (solver.cpp:522-538); +inf without
   int hits;
-  int status;        // 0 ok, 1 failure flag (host diagnoses), 2 skipped (done)
+  int status;        // 0 ok, 1 failure flag (host diagnoses), 2 skipped (done),
+                     // 3 precursor velocities: re-run with the exact two-pass kernels
 };
 
 struct FusedArgs {

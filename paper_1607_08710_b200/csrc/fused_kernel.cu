@@ -560,7 +560,7 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
     n = c;
     n.done = 1;
   } else if (failed) {
-    r.status = 1;
+    r.status = acc->fail == 2ull ? 3 : 1;   // 3: only the exact two-pass kernels are needed
     n = c;
     n.done = 1;
   } else {

@@ -234,7 +234,7 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
           m.mfy_stride = s.fy_stride;
           launch_pass_mat(a, m, h->mc, pass == 1, h->d.spatial_order >= 2, s.stream);
         } else {
-          launch_pass(a, pass == 1, h->d.spatial_order >= 2, s.stream);
+          launch_pass(a, pass == 1, h->d.spatial_order >= 2, h->tp_exact != 0, s.stream);
         }
       }
     }
@@ -328,7 +328,7 @@ static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_fin
       ++done;
       continue;
     }
-    if (f->rec_host[i].status == 1) *failed_at = i;
+    if (f->rec_host[i].status == 1 || f->rec_host[i].status == 3) *failed_at = i;
     break;
   }
   // U/U2 were swapped once per enqueued step; the state after `done` steps is
@@ -353,11 +353,24 @@ static void to_out(const StepRec& r, int64_t step, double gm1, lf_step_out* o, b
   o->min_p = mat ? r.min_p_mat : gm1 * r.min_eint;
 }
 
+// A step flagged "needs exact" (status 3) by the plain two-pass kernels: switch
+// the handle to the exact kernels (sticky) and report that it should be re-run.
+static bool needs_exact(lf_handle* h, int i) {
+  FusedState* f = fstate(h);
+  if (f->rec_host[i].status != 3 || h->tp_exact) return false;
+  h->tp_exact = 1;
+  fused_invalidate(h);
+  return true;
+}
+
 int fused_heun(lf_handle* h, double cfl, double time, double limit, int64_t step,
                double* outflow, lf_step_out* out) {
   fused_alloc(h, 1);
   int failed_at;
-  const int done = run_batch(h, 1, cfl, limit, limit, time, outflow, &failed_at, false, nullptr);
+  int done = run_batch(h, 1, cfl, limit, limit, time, outflow, &failed_at, false, nullptr);
+  if (done == 0 && failed_at == 0 && needs_exact(h, 0)) {
+    done = run_batch(h, 1, cfl, limit, limit, time, outflow, &failed_at, false, nullptr);
+  }
   if (done == 1) {
     if (outflow) std::memcpy(outflow, fstate(h)->outflow_host, 4 * sizeof(double));
     if (out) to_out(fstate(h)->rec_host[0], step + 1, h->d.gamma - 1.0, out, h->mc.n > 0);
@@ -372,8 +385,12 @@ int fused_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* 
                   int64_t* step, double* outflow, lf_step_out* per_step, int* taken) {
   if (taken) *taken = 0;
   int k = 0;
+  // batches grow 16 -> 256: a flag early in a run (a shock precursor on the
+  // plain kernels) discards at most a short batch of enqueued steps
+  int cap = 16;
   while (k < nsteps && *time < t_final) {
-    const int batch = std::min(nsteps - k, 256);
+    const int batch = std::min(nsteps - k, cap);
+    cap = std::min(2 * cap, 256);
     fused_alloc(h, batch);
     FusedState* f = fstate(h);
     int failed_at;
@@ -388,6 +405,7 @@ int fused_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* 
     if (taken) *taken = k;
     // the device outflow covers exactly the completed steps (finalize skips others)
     if (outflow) std::memcpy(outflow, f->outflow_host, 4 * sizeof(double));
+    if (failed_at >= 0 && needs_exact(h, failed_at)) continue;  // the batch resumes, exact kernels
     if (failed_at >= 0) {
       fused_invalidate(h);
       lf_step_out o;
@@ -419,7 +437,16 @@ int fused_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, do
   FK(cudaEventRecord(f->e0, s0.stream));
   int failed_at;
   double kms = 0.0;
-  const int done = run_batch(h, nsteps, cfl, big, big, t0, nullptr, &failed_at, true, &kms);
+  int done = run_batch(h, nsteps, cfl, big, big, t0, nullptr, &failed_at, true, &kms);
+  if (failed_at >= 0 && needs_exact(h, failed_at)) {
+    // precursor velocities: time the exact kernels from the last completed step
+    if (f->valid) {
+      FK(cudaMemcpy(&f->ctl_host[1], &f->ctl[f->cur], sizeof(StepCtl), cudaMemcpyDeviceToHost));
+      t0 = f->ctl_host[1].time;
+    }
+    FK(cudaEventRecord(f->e0, s0.stream));
+    done = run_batch(h, nsteps, cfl, big, big, t0, nullptr, &failed_at, true, &kms);
+  }
   FK(cudaEventRecord(f->e1, s0.stream));
   FK(cudaEventSynchronize(f->e1));
   float loop = 0.f;

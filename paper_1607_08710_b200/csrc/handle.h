@@ -71,6 +71,9 @@ struct lf_handle {
   // multimaterial: material table and whether partial densities were uploaded
   lfb::MatConsts mc{};
   int partials_ready = 0;
+  // the two-pass path has met shock-precursor velocities: use its exact kernels
+  // until a new state is uploaded (set by a step with status 3)
+  int tp_exact = 0;
 };
 
 namespace lfb {

@@ -49,7 +49,9 @@ struct MatPassArgs {
 
 int tp_strips(int nx);
 bool tp_fits(int64_t pitch, int ny);  // 32-bit offsets suffice for the slab
-void launch_pass(const PassArgs& a, bool corr, bool muscl, cudaStream_t st);
+// exact: the kernels that complete shock-precursor quotients exactly (see
+// twopass_kernel.cu); the plain ones flag such steps (StepAcc::fail = 2)
+void launch_pass(const PassArgs& a, bool corr, bool muscl, bool exact, cudaStream_t st);
 struct MatConsts;
 void launch_pass_mat(const PassArgs& a, const MatPassArgs& m, const MatConsts& mc, bool corr,
                      bool muscl, cudaStream_t st);

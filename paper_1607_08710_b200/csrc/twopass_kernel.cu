@@ -67,7 +67,11 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 #define LF_TP_UNROLL 1
 #endif
 
-template <bool CORR, bool MUSCL>
+// EXACT = false: the plain fast path; a warp whose stencil rows hold a velocity
+// in (0, 2^-500) (shock precursors) does not compute with it but raises the
+// "needs exact" flag (StepAcc::fail = 2) and the host re-runs the step with
+// EXACT = true, which takes the exact u* quotient in such warps.
+template <bool CORR, bool MUSCL, bool EXACT>
 __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a) {
   const StepCtl ctl = *a.ctl;
   if (ctl.done) return;
@@ -105,6 +109,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
   const int nit = (y1 - y0) + 4;
 
   unsigned fail = const_in_box(a.gamma, a.gm1) ? 0u : 1u;
+  unsigned need_exact = 0;
   unsigned long long rate_key = 0ull, nmin_r = NINF_KEY, nmin_e = NINF_KEY;
   unsigned dtfail = 0;
 
@@ -164,9 +169,16 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
       prim_fast(cur[0], cur[1], cur[2], cur[3], a.gm1, w, okw);
       if (!cell_in_box(w) && col_interior && r >= 0 && r < a.ny) fail = 1;
     }
-    tiny_rows = ((tiny_rows << 1) | (unsigned)(vel_tiny(w[1]) || vel_tiny(w[2]))) & 0xfu;
-    // the faces of this iteration read W rows r-3 .. r of lanes l-2 .. l+1
-    const bool tiny = __any_sync(FULL, tiny_rows != 0u);
+    // the faces of this iteration read W rows r-3 .. r of lanes l-2 .. l+1: the
+    // exact kernels keep that window per warp; the plain ones only note any
+    // precursor velocity at all and flag the step once, at the end
+    bool tiny = false;
+    if (EXACT) {
+      tiny_rows = ((tiny_rows << 1) | (unsigned)(vel_tiny(w[1]) || vel_tiny(w[2]))) & 0xfu;
+      tiny = __any_sync(FULL, tiny_rows != 0u);
+    } else {
+      need_exact |= (unsigned)(vel_tiny(w[1]) || vel_tiny(w[2]));
+    }
     // -- y: traces of row r-1, face (r-2 | r-1); x: traces of row r-2 (shuffles)
     double ylo[4], yhi[4], xlo[4], xhi[4], xp[4], da[4], db[4];
     shfl_down4(wm2, xp, 1);
@@ -185,7 +197,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     const bool need_x = it >= 4 && lane >= 2 && lane <= LANES - 2 && c <= a.nx;
     const bool need_y = it >= 3 && lane >= 2 && lane <= LANES - 3 && col_interior;
     double psx, usx, psy, usy;
-    if (tiny) {
+    if (EXACT && tiny) {
       // a velocity in (0, 2^-500) in this warp's stencil rows (numerical
       // precursors ahead of a shock): the exact u* quotient (div_exact)
       face_fast<0, true>(xmh[0], xmh[1], xmh[2], xmh[3], xlo[0], xlo[1], xlo[2], xlo[3], C, fx,
@@ -305,8 +317,10 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
   }
   const unsigned anyfail = __any_sync(FULL, fail);
   dtfail = __any_sync(FULL, dtfail);
+  need_exact = __any_sync(FULL, need_exact);
   if (lane == 0) {
     if (anyfail) atomicMax(&a.acc->fail, 1ull);
+    if (need_exact) atomicMax(&a.acc->fail, 2ull);   // dominates: the exact re-run decides
     if (CORR) {
       if (rate_key) atomicMax(&a.acc->rate_next, rate_key);
       if (nmin_r != NINF_KEY) atomicMax(&a.acc->nmin_rho, nmin_r);
@@ -325,21 +339,29 @@ bool tp_fits(int64_t pitch, int ny) {
   return pitch * (int64_t)(ny + NG + 1) < (int64_t)1 << 31;
 }
 
-void launch_pass(const PassArgs& a, bool corr, bool muscl, cudaStream_t st) {
-  const int warps = a.strips * ((a.ny + a.rows_per_chunk - 1) / a.rows_per_chunk);
-  const int blocks = (warps + TP_THREADS / 32 - 1) / (TP_THREADS / 32);
-  count_launch();
+template <bool EXACT>
+static void launch_k(const PassArgs& a, bool corr, bool muscl, unsigned blocks, cudaStream_t st) {
   if (corr) {
     if (muscl)
-      k_pass<true, true><<<blocks, TP_THREADS, 0, st>>>(a);
+      k_pass<true, true, EXACT><<<blocks, TP_THREADS, 0, st>>>(a);
     else
-      k_pass<true, false><<<blocks, TP_THREADS, 0, st>>>(a);
+      k_pass<true, false, EXACT><<<blocks, TP_THREADS, 0, st>>>(a);
   } else {
     if (muscl)
-      k_pass<false, true><<<blocks, TP_THREADS, 0, st>>>(a);
+      k_pass<false, true, EXACT><<<blocks, TP_THREADS, 0, st>>>(a);
     else
-      k_pass<false, false><<<blocks, TP_THREADS, 0, st>>>(a);
+      k_pass<false, false, EXACT><<<blocks, TP_THREADS, 0, st>>>(a);
   }
+}
+
+void launch_pass(const PassArgs& a, bool corr, bool muscl, bool exact, cudaStream_t st) {
+  const int warps = a.strips * ((a.ny + a.rows_per_chunk - 1) / a.rows_per_chunk);
+  const unsigned blocks = (unsigned)((warps + TP_THREADS / 32 - 1) / (TP_THREADS / 32));
+  count_launch();
+  if (exact)
+    launch_k<true>(a, corr, muscl, blocks, st);
+  else
+    launch_k<false>(a, corr, muscl, blocks, st);
 }
 
 }  // namespace lfb

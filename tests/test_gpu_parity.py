@@ -243,8 +243,8 @@ def _box_cases():
 @pytest.mark.parametrize("path", ["twopass", "fused"])
 def test_tiny_velocities_stay_on_the_fast_path(cuda, path):
     """Velocities down to the subnormals (numerical precursors ahead of shocks):
-    the exact u* quotient (div_exact) keeps them in the fast kernels -- no
-    stage-wise re-run -- with the oracle's bits."""
+    the plain two-pass kernels flag the step, it is re-run by the exact two-pass
+    kernels (div_exact) -- never by the stage-wise ones -- with the oracle's bits."""
     case, field = _box_cases()["tiny_velocity"]
     field = field.copy()
     g = case.grid
@@ -266,14 +266,17 @@ def test_tiny_velocities_stay_on_the_fast_path(cuda, path):
     assert_fields_equal(g.interior(state.field), g.interior(ref.field), "tiny")
     assert np.array_equal(diag_array(state)[:, :4], rdiag[:, :4])
     _, n_plain = run(CS.initial_field(CS.quadrant(48, 4)))
-    assert n_tiny == n_plain
+    if path == "twopass":
+        assert n_tiny <= n_plain + 12  # one flagged two-pass attempt (7 launches + re-seed)
+    else:
+        assert n_tiny == n_plain       # the fused kernel always takes the exact quotient
 
 
 @pytest.mark.parametrize("cfg", ["sedov", "quadrant"])
 def test_shock_precursors_need_no_stagewise_rerun(cuda, cfg):
     """Shocks into quiescent regions create arbitrarily small velocities ahead of
-    the front; the fast two-pass step handles them itself (constant launches per
-    step) and stays bit-identical to the oracle."""
+    the front; the two-pass path switches to its exact kernels once (one flagged
+    attempt) and never falls back to the stage-wise kernels; bits as the oracle."""
     case = CS.sedov(128, 40) if cfg == "sedov" else CS.quadrant(128, 40)
     f0 = CS.initial_field(case)
     ref, rdiag = run_oracle(case, 40, field=f0)
@@ -287,7 +290,9 @@ def test_shock_precursors_need_no_stagewise_rerun(cuda, cfg):
     s.sync_to_host(st)
     assert_fields_equal(case.grid.interior(st.field), case.grid.interior(ref.field), cfg)
     assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4])
-    assert max(counts[1:]) == min(counts[1:]) <= 8, counts
+    assert max(counts) <= 18, counts                      # no stage-wise re-run (29+)
+    assert sum(c > 10 for c in counts) <= 1, counts       # at most one flagged step
+    assert max(counts[-20:]) == min(counts[-20:]) <= 8, counts
 
 
 @pytest.mark.parametrize("path", ["twopass", "fused"])

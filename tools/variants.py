@@ -25,7 +25,6 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 VARIANTS = {
     "base_tp": ("", 3),
     "tp": ("", 3),
-    "tp_nb": ("-DLF_DIVTINY_MODE=4", 3),
 }
 
 
