@@ -66,8 +66,9 @@ size_t fused_smem_bytes();
 void fused_configure();
 void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st);
 void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* rec,
-                     const double* bnd, double* outflow, int nx, int nyg, double dx, double dy,
-                     double cfl, double limit, double t_final, cudaStream_t st);
+                     const double* bnd, double* outflow, int nx, int nyg, bool sum_x, bool sum_y,
+                     double dx, double dy, double cfl, double limit, double t_final,
+                     cudaStream_t st);
 void launch_acc_init(StepAcc* acc, cudaStream_t st);
 
 }  // namespace lfb

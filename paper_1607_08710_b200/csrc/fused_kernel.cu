@@ -500,8 +500,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 // control record of the next step.
 __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCtl* nxt,
                            StepRec* rec, const double* __restrict__ bnd, double* outflow,
-                           int nx, int nyg, double dx, double dy, double cfl, double limit,
-                           double t_final) {
+                           int nx, int nyg, bool sum_x, bool sum_y, double dx, double dy,
+                           double cfl, double limit, double t_final) {
   constexpr int TILE = 512;
   __shared__ double sums[8];
   __shared__ double dif[8][TILE];
@@ -520,23 +520,27 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
     // order, then s += (top - bottom) over the columns in order.  The
     // differences are independent (all threads, one tile at a time); only the
     // accumulation is sequential (one thread per component and direction).
+    // A periodic axis skips its sums: both of its boundary faces are the same
+    // face, solved from the same inputs by the same code, so every difference
+    // is +0.0 and so is their ordered sum.
     double s = 0.0;
-    const int nmax = nyg > nx ? nyg : nx;
+    const int ex = sum_x ? nyg : 0, ey = sum_y ? nx : 0;
+    const int nmax = ex > ey ? ex : ey;
     for (int base = 0; base < nmax; base += TILE) {
       for (int k = tid; k < 8 * TILE; k += blockDim.x) {
         const int ch = k / TILE, e = base + k % TILE, q = ch & 3;
         double d = 0.0;
-        if (ch < 4 && e < nyg)
+        if (ch < 4 && e < ex)
           d = bnd[4 * (int64_t)nyg + (int64_t)q * nyg + e] - bnd[(int64_t)q * nyg + e];
-        else if (ch >= 4 && e < nx)
+        else if (ch >= 4 && e < ey)
           d = bnd[8 * (int64_t)nyg + 4 * (int64_t)nx + (int64_t)q * nx + e] -
               bnd[8 * (int64_t)nyg + (int64_t)q * nx + e];
         dif[ch][k % TILE] = d;
       }
       __syncthreads();
       if (tid < 8) {
-        const int n = (tid < 4 ? nyg : nx) - base;
-        const int m = n < TILE ? n : TILE;
+        const int n = (tid < 4 ? ex : ey) - base;
+        const int m = n < TILE ? (n > 0 ? n : 0) : TILE;
         for (int e = 0; e < m; ++e) s += dif[tid][e];
       }
       __syncthreads();
@@ -624,11 +628,12 @@ void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t s
 }
 
 void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* rec,
-                     const double* bnd, double* outflow, int nx, int nyg, double dx, double dy,
-                     double cfl, double limit, double t_final, cudaStream_t st) {
+                     const double* bnd, double* outflow, int nx, int nyg, bool sum_x, bool sum_y,
+                     double dx, double dy, double cfl, double limit, double t_final,
+                     cudaStream_t st) {
   count_launch();
-  k_finalize<<<1, 256, 0, st>>>(ctl, acc, nxt, rec, bnd, outflow, nx, nyg, dx, dy, cfl, limit,
-                               t_final);
+  k_finalize<<<1, 256, 0, st>>>(ctl, acc, nxt, rec, bnd, outflow, nx, nyg, sum_x, sum_y, dx, dy,
+                               cfl, limit, t_final);
 }
 
 void launch_acc_init(StepAcc* acc, cudaStream_t st) {

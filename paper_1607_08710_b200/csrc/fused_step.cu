@@ -275,7 +275,9 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   FK(cudaGetLastError());
   if (h->nccl) nccl_reduce_step(h, f->acc + cur, STEP_ACC_WORDS, bnd, bnd_words(h));
   launch_finalize(f->ctl + cur, f->acc + cur, f->ctl + nxt, f->rec + n_in_batch, bnd, f->outflow,
-                  h->d.nx, h->d.ny, h->d.dx, h->d.dy, cfl, limit, t_final, s0.stream);
+                  h->d.nx, h->d.ny, !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC),
+                  !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC), h->d.dx, h->d.dy,
+                  cfl, limit, t_final, s0.stream);
   FK(cudaGetLastError());
   for (auto& s : h->slabs) {
     std::swap(s.U, s.U2);
