@@ -21,6 +21,7 @@
  *                                  time / diagnostics kept on the device
  *   lf_init_fourier                (new) on-device seeded smooth-flow IC (BASELINE 4-5)
  *   lf_init_regions                initialize_hydro, InitKind::regions  run.cpp:29-78
+ *   lf_interior_totals             interior_totals(grid, state.field)  grid.cpp:122-133
  *   lf_last_error                  the exception object (what(), PositivityError fields)
  *   lf_write_field_csv             field_csv + write_text_file   csv.cpp:26-83, run.cpp:162-168
  *   lf_set_materials               the constructor's `const MaterialSet*` (solver.cpp:61-88)
@@ -176,6 +177,12 @@ int lf_heun_step(lf_handle* h, double cfl, double time, double limit_time, int64
  * (may be NULL).  *taken receives the steps executed. */
 int lf_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* time,
                int64_t* step, double* boundary_outflow, lf_step_out* per_step, int* taken);
+
+/* interior_totals (grid.cpp:122-133) of the device-resident state: per
+ * component, the row-major ordered sum over the interior times the cell volume,
+ * bit-equal to the reference.  A distributed handle chains the sums over the
+ * ranks in row order and returns the global totals on every rank (collective). */
+int lf_interior_totals(lf_handle* h, double tot[4]);
 
 int lf_last_error(lf_handle* h, lf_error* err);
 

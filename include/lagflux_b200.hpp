@@ -18,6 +18,7 @@
 // first step, copied back with the field.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <string>
 
@@ -121,6 +122,18 @@ class LagfluxSolver {
     double dt = 0.0;
     check(lf_compute_dt(h_, controls.cfl, time, limit_time, &dt));
     return dt;
+  }
+
+  // interior_totals(grid, state.field) (grid.cpp:122-133), summed on the device in
+  // the reference's order: the resident copy of `state`, else its host field
+  std::array<double, 4> interior_totals(const SolverState& state) const {
+    if (resident_ != &state) {
+      upload(state.field);
+      resident_ = nullptr;
+    }
+    std::array<double, 4> t{};
+    check(lf_interior_totals(h_, t.data()));
+    return t;
   }
 
   const CartesianGrid& grid() const { return grid_; }

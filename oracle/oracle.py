@@ -160,6 +160,7 @@ def ref_lib():
     lib.lfr_mixed_cell_gamma.restype = C.c_double
     lib.lfr_mixed_cell_gamma.argtypes = [C.c_int, DP, DP]
     lib.lfr_mass_fraction_fluxes.argtypes = [C.c_double, C.c_int, DP, DP]
+    lib.lfr_interior_totals.argtypes = [C.c_void_p, DP]
     lib.lfr_field_csv.restype = C.c_int64
     lib.lfr_field_csv.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_char_p, C.c_int64,
                                   C.POINTER(lfo_error)]
@@ -269,6 +270,12 @@ class RefSolver:
         self.lib.lfr_get_state(self.h, _ptrs(f), C.byref(t), C.byref(s), C.cast(acc, DP))
         return f, t.value, s.value, list(acc)
 
+    def interior_totals(self) -> List[float]:
+        """lagflux::interior_totals of the current state (grid.cpp:122-133)."""
+        t = np.zeros(4)
+        self.lib.lfr_interior_totals(self.h, t.ctypes.data_as(DP))
+        return [float(x) for x in t]
+
     def heun_steps(self, n: int, cfl: float, limit_time: float) -> np.ndarray:
         """n heun_step calls; returns (n, 5) rows {dt, time, min_rho, min_p, step}."""
         diag = np.zeros((max(n, 1), 5))
@@ -305,6 +312,14 @@ def oracle_run(g, bc, gamma, params, field, cfl, steps: int, limit: float = 1e30
             break
         s.heun_step(state, cfl, limit)
     return state.field, state.diagnostics, state.boundary_outflow
+
+
+def oracle_interior_totals(g: G.CartesianGrid, field: np.ndarray) -> List[float]:
+    """The oracle's restatement of interior_totals (grid.cpp:122-133)."""
+    f = np.ascontiguousarray(field)
+    t = np.zeros(4)
+    oracle_lib().lfo_interior_totals(C.byref(_cgrid(g)), _ptrs(f), t.ctypes.data_as(DP))
+    return [float(x) for x in t]
 
 
 def fourier_tables_oracle(seed: int, g: G.CartesianGrid):

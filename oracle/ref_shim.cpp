@@ -293,6 +293,12 @@ int lfr_euler_stage(lfr_solver* r, double dt, int64_t step, double* const out[4]
 }
 
 // Element functions for known-answer tests.
+// lagflux::interior_totals (grid.cpp:122-133) of the solver's current state.
+void lfr_interior_totals(lfr_solver* r, double tot[4]) {
+  const std::array<double, 4> t = interior_totals(r->g, r->state.field);
+  for (int c = 0; c < 4; ++c) tot[c] = t[size_t(c)];
+}
+
 void lfr_fill_ghosts(const lfo_grid* g, const int bc[4], int parity, double* f) {
   const CartesianGrid cg = to_grid(g);
   const BoundaryCondition b{bc_kind(bc[0]), bc_kind(bc[1]), bc_kind(bc[2]), bc_kind(bc[3])};

@@ -1176,6 +1176,42 @@ int lf_compute_dt(lf_handle* h, double cfl, double time, double limit_time, doub
   });
 }
 
+int lf_interior_totals(lf_handle* h, double tot[4]) {
+  return guarded(h, [&] {
+    if (!tot) return set_err(h, LF_ERR_ARGUMENT, "null totals");
+    // slabs in row order; each continues the running sums of the one below
+    std::vector<size_t> order(h->slabs.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = k;
+    std::sort(order.begin(), order.end(),
+              [&](size_t a, size_t b) { return h->slabs[a].sl.y0 < h->slabs[b].sl.y0; });
+    double run[4] = {0.0, 0.0, 0.0, 0.0};
+    for (size_t n = 0; n < order.size(); ++n) {
+      SlabState& s = h->slabs[order[n]];
+      CK(cudaSetDevice(s.device));
+      double* d = nullptr;  // {in[4], out[4]}
+      CK(cudaMalloc(&d, 8 * sizeof(double)));
+      CK(cudaMemcpyAsync(d, run, sizeof run, cudaMemcpyHostToDevice, s.stream));
+      if (h->nccl) nccl_recv_prev(h, d, 4);
+      launch_interior_sums(s.U + s.L.origin(), s.L.fstride, (int)s.L.pitch, s.L.nx, s.L.ny, d,
+                           d + 4, s.stream);
+      if (h->nccl) {
+        nccl_send_next(h, d + 4, 4);
+        // the last rank holds the totals: every other rank contributes +0.0,
+        // which leaves them unchanged (a running sum from +0.0 is never -0.0)
+        if (h->rank != h->nranks - 1) CK(cudaMemsetAsync(d + 4, 0, 4 * sizeof(double), s.stream));
+        nccl_sum_f64(h, d + 4, 4);
+      }
+      CK(cudaMemcpyAsync(run, d + 4, sizeof run, cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      cudaFree(d);
+      CK(cudaGetLastError());
+    }
+    const double vol = h->dim2 ? h->d.dx * h->d.dy : h->d.dx;
+    for (int c = 0; c < 4; ++c) tot[c] = run[c] * vol;
+    return 0;
+  });
+}
+
 int lf_max_rate(lf_handle* h, double* rate) {
   return guarded(h, [&] {
     launch_rate_all(h, &SlabState::U);

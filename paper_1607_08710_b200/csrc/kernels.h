@@ -132,6 +132,10 @@ void launch_init_regions(const Field& u, const Field& part, const Layout& L, con
                          cudaStream_t st);
 // field_csv's per-cell columns (csv.cpp:40-57): rho, u, v, p, e_internal, y_1..y_n as
 // planes of nx*ny; clamp failures -> atomicMin(fail, row-major global interior index)
+// interior_totals' ordered per-component sums (grid.cpp:122-133) over one slab,
+// starting from s_in[4] (NULL: 0.0); u at the interior origin
+void launch_interior_sums(const double* u, int64_t fstride, int pitch, int nx, int ny,
+                          const double* s_in, double* s_out, cudaStream_t st);
 void launch_csv_derive(const Field& u, const Field& part, const Layout& L, const Slab& sl,
                        double gamma0, const MatConsts& mc, double* out, unsigned long long* fail,
                        cudaStream_t st);

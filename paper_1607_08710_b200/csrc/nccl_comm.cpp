@@ -180,6 +180,23 @@ void nccl_max_u64(lf_handle* h, unsigned long long* v, int n) {
   cck(cudaStreamSynchronize(s.stream), "sync");
 }
 
+void nccl_recv_prev(lf_handle* h, double* d, int n) {
+  if (h->rank == 0) return;
+  nck(g_api.Recv(d, (size_t)n, ncclFloat64, h->rank - 1, h->nccl->comm, h->slabs[0].stream),
+      "ncclRecv");
+}
+
+void nccl_send_next(lf_handle* h, const double* d, int n) {
+  if (h->rank == h->nranks - 1) return;
+  nck(g_api.Send(d, (size_t)n, ncclFloat64, h->rank + 1, h->nccl->comm, h->slabs[0].stream),
+      "ncclSend");
+}
+
+void nccl_sum_f64(lf_handle* h, double* d, int n) {
+  nck(g_api.AllReduce(d, d, (size_t)n, ncclFloat64, ncclSum, h->nccl->comm, h->slabs[0].stream),
+      "ncclAllReduce");
+}
+
 void nccl_gather_boundary(lf_handle* h, double* left, double* right, double* bot, double* top) {
   SlabState& s = h->slabs[0];
   const size_t ny = (size_t)h->d.ny, nx = (size_t)h->d.nx;

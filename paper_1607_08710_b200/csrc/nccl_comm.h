@@ -20,6 +20,11 @@ void nccl_max_u64(lf_handle* h, unsigned long long* v, int n);
 // fused step: max-reduce n u64 step accumulators and sum-reduce the boundary
 // faces (nbnd doubles, each rank owns disjoint entries, zero elsewhere) in place
 void nccl_reduce_step(lf_handle* h, void* acc_u64, int n, double* bnd, size_t nbnd);
+// ordered chains over the ranks (interior totals): rank r-1 -> rank r, n doubles
+void nccl_recv_prev(lf_handle* h, double* d, int n);
+void nccl_send_next(lf_handle* h, const double* d, int n);
+// in-place sum of n device doubles over the ranks
+void nccl_sum_f64(lf_handle* h, double* d, int n);
 // sum-combine the boundary-face arrays (each rank owns disjoint entries)
 void nccl_gather_boundary(lf_handle* h, double* left, double* right, double* bot, double* top);
 

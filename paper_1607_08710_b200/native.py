@@ -71,6 +71,7 @@ SIGNATURES = [
     ("lf_time_steps", C.c_int, [H, C.c_int, C.c_double, DP, DP, C.POINTER(C.c_int)]),
     ("lf_device_bytes", C.c_int, [H, C.POINTER(C.c_int64)]),
     ("lf_max_rate", C.c_int, [H, DP]),
+    ("lf_interior_totals", C.c_int, [H, DP]),
     ("lf_launch_count", C.c_int, [H, C.POINTER(C.c_int64)]),
     ("lf_slab_partition", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("lf_selftest_fastmath", C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),

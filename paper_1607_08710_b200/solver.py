@@ -10,7 +10,7 @@ addition a run.cpp-style driver needs.
 from __future__ import annotations
 
 import ctypes as C
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -262,6 +262,13 @@ class LagfluxSolver:
         n = C.c_int64()
         self._check(self._lib.lf_launch_count(self._h, C.byref(n)))
         return n.value
+
+    def interior_totals(self) -> List[float]:
+        """interior_totals(grid, state.field) (grid.cpp:122-133) of the device-resident
+        state, bit-equal to the reference's ordered sums."""
+        t = (C.c_double * 4)()
+        self._check(self._lib.lf_interior_totals(self._h, C.cast(t, C.POINTER(C.c_double))))
+        return list(t)
 
     def max_rate(self) -> float:
         r = C.c_double()

@@ -98,6 +98,9 @@ void run_pair(const char* name, const CartesianGrid& g, const BoundaryCondition&
   for (int c = 0; c < 4; ++c)
     expect(a.boundary_outflow[size_t(c)] == b.boundary_outflow[size_t(c)],
            std::string(name) + ": boundary outflow");
+  // the conservation audit (grid.cpp:122-133), resident state summed on the device
+  const std::array<double, 4> ta = interior_totals(g, a.field), tb = gpu.interior_totals(b);
+  for (int c = 0; c < 4; ++c) expect(ta[size_t(c)] == tb[size_t(c)], std::string(name) + ": interior totals");
   std::printf("%s: %zu steps compared\n", name, a.diagnostics.size());
 }
 
