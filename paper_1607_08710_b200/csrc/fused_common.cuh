@@ -65,10 +65,14 @@ struct FusedArgs {
 size_t fused_smem_bytes();
 void fused_configure();
 void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st);
+// dt, time, diagnostics and the next control record of a step; outflow_zero:
+// every axis periodic, the outflow update is the += of +0.0 sums done here
 void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* rec,
-                     const double* bnd, double* outflow, int nx, int nyg, bool sum_x, bool sum_y,
-                     double dx, double dy, double cfl, double limit, double t_final,
-                     cudaStream_t st);
+                     double* outflow, bool outflow_zero, double dx, double dy, double cfl,
+                     double limit, double t_final, cudaStream_t st);
+// the boundary-outflow sums of the step recorded in `rec` (no-op unless it completed)
+void launch_outflow(const StepRec* rec, const double* bnd, double* outflow, int nx, int nyg,
+                    bool sum_x, bool sum_y, double dx, double dy, cudaStream_t st);
 void launch_acc_init(StepAcc* acc, cudaStream_t st);
 
 }  // namespace lfb

@@ -499,13 +499,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 // (solver.cpp:406-432, one thread per component and direction) and the
 // control record of the next step.
 __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCtl* nxt,
-                           StepRec* rec, const double* __restrict__ bnd, double* outflow,
-                           int nx, int nyg, bool sum_x, bool sum_y, double dx, double dy,
+                           StepRec* rec, double* outflow, bool outflow_zero, double dx, double dy,
                            double cfl, double limit, double t_final) {
-  constexpr int TILE = 512;
-  __shared__ double sums[8];
-  __shared__ double dif[8][TILE];
-  const int tid = threadIdx.x;
   const StepCtl c = *ctl;
   const bool skip = c.done != 0;
   double dt = 0.0;
@@ -515,40 +510,6 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
     if (c.time + dt > limit) dt = limit - c.time;
   }
   const bool failed = !skip && (acc->fail != 0 || c.dtfail || !(dt > 0.0));
-  if (!skip && !failed) {
-    // solver.cpp:412-430: per component, s += (right - left) over the rows in
-    // order, then s += (top - bottom) over the columns in order.  The
-    // differences are independent (all threads, one tile at a time); only the
-    // accumulation is sequential (one thread per component and direction).
-    // A periodic axis skips its sums: both of its boundary faces are the same
-    // face, solved from the same inputs by the same code, so every difference
-    // is +0.0 and so is their ordered sum.
-    double s = 0.0;
-    const int ex = sum_x ? nyg : 0, ey = sum_y ? nx : 0;
-    const int nmax = ex > ey ? ex : ey;
-    for (int base = 0; base < nmax; base += TILE) {
-      for (int k = tid; k < 8 * TILE; k += blockDim.x) {
-        const int ch = k / TILE, e = base + k % TILE, q = ch & 3;
-        double d = 0.0;
-        if (ch < 4 && e < ex)
-          d = bnd[4 * (int64_t)nyg + (int64_t)q * nyg + e] - bnd[(int64_t)q * nyg + e];
-        else if (ch >= 4 && e < ey)
-          d = bnd[8 * (int64_t)nyg + 4 * (int64_t)nx + (int64_t)q * nx + e] -
-              bnd[8 * (int64_t)nyg + (int64_t)q * nx + e];
-        dif[ch][k % TILE] = d;
-      }
-      __syncthreads();
-      if (tid < 8) {
-        const int n = (tid < 4 ? ex : ey) - base;
-        const int m = n < TILE ? (n > 0 ? n : 0) : TILE;
-        for (int e = 0; e < m; ++e) s += dif[tid][e];
-      }
-      __syncthreads();
-    }
-    if (tid < 8) sums[tid] = s;
-  }
-  __syncthreads();
-  if (tid != 0) return;
   StepRec r;
   r.dt = dt;
   r.hits = 0;
@@ -574,10 +535,13 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
     r.min_rho = __longlong_as_double((long long)~acc->nmin_rho);
     r.min_eint = __longlong_as_double((long long)~acc->nmin_eint);
     r.min_p_mat = __longlong_as_double((long long)~acc->nmin_p);
-    const double ax = dt * dy, ay = dt * dx;
-    for (int q = 0; q < 4; ++q) {
-      outflow[q] += ax * sums[q];
-      outflow[q] += ay * sums[4 + q];
+    if (outflow_zero) {
+      // every axis periodic: both face sums are +0.0 (k_outflow's comment)
+      const double ax = dt * dy, ay = dt * dx;
+      for (int q = 0; q < 4; ++q) {
+        outflow[q] += ax * 0.0;
+        outflow[q] += ay * 0.0;
+      }
     }
     n.time = r.time;
     n.done = !(r.time < t_final);
@@ -591,6 +555,65 @@ __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCt
   acc->nmin_eint = NINF_KEY;
   acc->dtfail_next = 0ull;
   acc->nmin_p = NINF_KEY;
+}
+
+// accumulate_boundary_outflow (solver.cpp:406-432) of a completed step: per
+// component, s += (right - left) over the rows in order, then s += (top -
+// bottom) over the columns in order, outflow += dt*dy*s_x, += dt*dx*s_y.  Only
+// the accumulation is sequential (lanes 0-7 of warp 0, one chain per component
+// and axis); the other warps stage the next tile of differences meanwhile.  A
+// periodic axis skips its sums: both of its boundary faces are the same face,
+// solved from the same inputs by the same code, so every difference is +0.0 and
+// so is their ordered sum.  Runs on a side stream, off the step's critical path.
+__global__ void __launch_bounds__(256)
+    k_outflow(const StepRec* __restrict__ rec, const double* __restrict__ bnd, double* outflow,
+              int nx, int nyg, bool sum_x, bool sum_y, double dx, double dy) {
+  constexpr int TILE = 256;
+  __shared__ double dif[2][TILE][9];  // [buffer][element][chain]; 9: conflict-free rows
+  const StepRec r = *rec;
+  if (r.status != 0) return;
+  const int tid = threadIdx.x;
+  const int ex = sum_x ? nyg : 0, ey = sum_y ? nx : 0;
+  const int ntiles = ((ex > ey ? ex : ey) + TILE - 1) / TILE;
+  auto stage = [&](int t, int buf) {
+    for (int k = tid - 32; k < 8 * TILE; k += blockDim.x - 32) {
+      const int ch = k / TILE, e = t * TILE + k % TILE, q = ch & 3;
+      double d = 0.0;
+      if (ch < 4 && e < ex)
+        d = bnd[4 * (int64_t)nyg + (int64_t)q * nyg + e] - bnd[(int64_t)q * nyg + e];
+      else if (ch >= 4 && e < ey)
+        d = bnd[8 * (int64_t)nyg + 4 * (int64_t)nx + (int64_t)q * nx + e] -
+            bnd[8 * (int64_t)nyg + (int64_t)q * nx + e];
+      dif[buf][k % TILE][ch] = d;
+    }
+  };
+  double s = 0.0;
+  if (tid >= 32 && ntiles > 0) stage(0, 0);
+  __syncthreads();
+  for (int t = 0; t < ntiles; ++t) {
+    if (tid >= 32) {
+      if (t + 1 < ntiles) stage(t + 1, (t + 1) & 1);
+    } else if (tid < 8) {
+      const int n = (tid < 4 ? ex : ey) - t * TILE;
+      const double(*d)[9] = dif[t & 1];
+      if (n >= TILE) {
+#pragma unroll 32
+        for (int e = 0; e < TILE; ++e) s += d[e][tid];
+      } else {
+        for (int e = 0; e < n; ++e) s += d[e][tid];
+      }
+    }
+    __syncthreads();
+  }
+  __shared__ double sums[8];
+  if (tid < 8) sums[tid] = s;
+  __syncthreads();
+  if (tid != 0) return;
+  const double ax = r.dt * dy, ay = r.dt * dx;
+  for (int q = 0; q < 4; ++q) {
+    outflow[q] += ax * sums[q];
+    outflow[q] += ay * sums[4 + q];
+  }
 }
 
 __global__ void k_acc_init(StepAcc* acc) {
@@ -628,12 +651,17 @@ void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t s
 }
 
 void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* rec,
-                     const double* bnd, double* outflow, int nx, int nyg, bool sum_x, bool sum_y,
-                     double dx, double dy, double cfl, double limit, double t_final,
-                     cudaStream_t st) {
+                     double* outflow, bool outflow_zero, double dx, double dy, double cfl,
+                     double limit, double t_final, cudaStream_t st) {
   count_launch();
-  k_finalize<<<1, 256, 0, st>>>(ctl, acc, nxt, rec, bnd, outflow, nx, nyg, sum_x, sum_y, dx, dy,
-                               cfl, limit, t_final);
+  k_finalize<<<1, 1, 0, st>>>(ctl, acc, nxt, rec, outflow, outflow_zero, dx, dy, cfl, limit,
+                             t_final);
+}
+
+void launch_outflow(const StepRec* rec, const double* bnd, double* outflow, int nx, int nyg,
+                    bool sum_x, bool sum_y, double dx, double dy, cudaStream_t st) {
+  count_launch();
+  k_outflow<<<1, 256, 0, st>>>(rec, bnd, outflow, nx, nyg, sum_x, sum_y, dx, dy);
 }
 
 void launch_acc_init(StepAcc* acc, cudaStream_t st) {

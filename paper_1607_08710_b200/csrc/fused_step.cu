@@ -52,6 +52,11 @@ struct FusedState {
   int rows_per_chunk = 0;          // fused kernel
   int tp_rows = 0;                 // two-pass kernels
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // boundary-outflow sums run on a low-priority side stream: ev_fin[b] = the
+  // finalize of a step using bnd slot b, ev_out[b] = its sums (slot b is
+  // rewritten two steps later, after ev_out[b])
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fin[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
 };
 
 static FusedState* fstate(lf_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
@@ -94,6 +99,13 @@ static void fused_alloc(lf_handle* h, int steps) {
     FK(cudaHostAlloc(&f->outflow_host, 4 * sizeof(double), cudaHostAllocDefault));
     FK(cudaEventCreate(&f->e0));
     FK(cudaEventCreate(&f->e1));
+    int lo = 0, hi = 0;
+    FK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FK(cudaStreamCreateWithPriority(&f->side, cudaStreamNonBlocking, lo));
+    for (int b = 0; b < 2; ++b) {
+      FK(cudaEventCreateWithFlags(&f->ev_fin[b], cudaEventDisableTiming));
+      FK(cudaEventCreateWithFlags(&f->ev_out[b], cudaEventDisableTiming));
+    }
     launch_acc_init(f->acc, s0.stream);
     fused_configure();
     // chunk rows: several waves of 2 blocks / SM, long marches (pipeline fill is 9 rows)
@@ -132,6 +144,14 @@ void fused_release(lf_handle* h) {
   cudaFreeHost(f->ctl_host);
   if (f->e0) cudaEventDestroy(f->e0);
   if (f->e1) cudaEventDestroy(f->e1);
+  if (f->side) {
+    cudaStreamSynchronize(f->side);
+    cudaStreamDestroy(f->side);
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (f->ev_fin[b]) cudaEventDestroy(f->ev_fin[b]);
+    if (f->ev_out[b]) cudaEventDestroy(f->ev_out[b]);
+  }
   delete f;
   h->fused = nullptr;
 }
@@ -178,8 +198,10 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
                          cudaEvent_t k0, cudaEvent_t k1) {
   FusedState* f = fstate(h);
   const int cur = f->cur, nxt = cur ^ 1;
-  fill_all_public(h, &SlabState::U);
   SlabState& s0 = h->slabs[0];
+  // bnd slot `cur` is free once the outflow sums of two steps ago have read it
+  FK(cudaStreamWaitEvent(s0.stream, f->ev_out[cur], 0));
+  fill_all_public(h, &SlabState::U);
   double* bnd = f->bnd + (size_t)cur * bnd_words(h);
   if (h->nccl) FK(cudaMemsetAsync(bnd, 0, bnd_words(h) * sizeof(double), s0.stream));
   if (k0) FK(cudaEventRecord(k0, s0.stream));
@@ -274,10 +296,17 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   if (k1) FK(cudaEventRecord(k1, s0.stream));
   FK(cudaGetLastError());
   if (h->nccl) nccl_reduce_step(h, f->acc + cur, STEP_ACC_WORDS, bnd, bnd_words(h));
-  launch_finalize(f->ctl + cur, f->acc + cur, f->ctl + nxt, f->rec + n_in_batch, bnd, f->outflow,
-                  h->d.nx, h->d.ny, !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC),
-                  !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC), h->d.dx, h->d.dy,
-                  cfl, limit, t_final, s0.stream);
+  const bool sum_x = !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC);
+  const bool sum_y = !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC);
+  launch_finalize(f->ctl + cur, f->acc + cur, f->ctl + nxt, f->rec + n_in_batch, f->outflow,
+                  !sum_x && !sum_y, h->d.dx, h->d.dy, cfl, limit, t_final, s0.stream);
+  if (sum_x || sum_y) {
+    FK(cudaEventRecord(f->ev_fin[cur], s0.stream));
+    FK(cudaStreamWaitEvent(f->side, f->ev_fin[cur], 0));
+    launch_outflow(f->rec + n_in_batch, bnd, f->outflow, h->d.nx, h->d.ny, sum_x, sum_y, h->d.dx,
+                   h->d.dy, f->side);
+    FK(cudaEventRecord(f->ev_out[cur], f->side));
+  }
   FK(cudaGetLastError());
   for (auto& s : h->slabs) {
     std::swap(s.U, s.U2);
@@ -305,6 +334,8 @@ static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_fin
   for (int i = 0; i < n; ++i)
     enqueue_step(h, i, cfl, limit, t_final, timing ? evs[2 * i] : nullptr,
                  timing ? evs[2 * i + 1] : nullptr);
+  // the side stream's last outflow sums (in-order) before the outflow comes back
+  FK(cudaStreamWaitEvent(s0.stream, f->ev_out[f->cur ^ 1], 0));
   FK(cudaMemcpyAsync(f->rec_host, f->rec, (size_t)n * sizeof(StepRec), cudaMemcpyDeviceToHost,
                      s0.stream));
   FK(cudaMemcpyAsync(f->outflow_host, f->outflow, 4 * sizeof(double), cudaMemcpyDeviceToHost,

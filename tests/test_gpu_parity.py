@@ -290,9 +290,11 @@ def test_shock_precursors_need_no_stagewise_rerun(cuda, cfg):
     s.sync_to_host(st)
     assert_fields_equal(case.grid.interior(st.field), case.grid.interior(ref.field), cfg)
     assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4])
-    assert max(counts) <= 18, counts                      # no stage-wise re-run (29+)
-    assert sum(c > 10 for c in counts) <= 1, counts       # at most one flagged step
-    assert max(counts[-20:]) == min(counts[-20:]) <= 8, counts
+    base = counts[-1]                                     # one step: 7 launches, +1 outflow sums
+    assert max(counts[-20:]) == min(counts[-20:]) == base <= 8, counts
+    assert max(counts) <= 2 * base + 3, counts            # no stage-wise re-run (29+)
+    assert sum(c > base + 3 for c in counts) <= 1, counts  # at most one flagged step (the
+    # first step also seeds the control record: rate, reset, accumulators)
 
 
 @pytest.mark.parametrize("path", ["twopass", "fused"])
