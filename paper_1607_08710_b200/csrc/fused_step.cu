@@ -51,6 +51,8 @@ struct FusedState {
   bool valid = false;              // ctl[cur].rate_bits is the rate of the current U
   int rows_per_chunk = 0;          // fused kernel
   int tp_rows = 0;                 // two-pass kernels
+  int tp_rows_nmat = -1;           // the material count tp_rows was sized for
+  int sms = 148;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   // boundary-outflow sums run on a low-priority side stream: ev_fin[b] = the
   // finalize of a step using bnd slot b, ev_out[b] = its sums (slot b is
@@ -117,10 +119,15 @@ static void fused_alloc(lf_handle* h, int steps) {
     const int target_blocks = 2 * sms * 6;
     const int chunks = std::max(1, (target_blocks + strips - 1) / strips);
     f->rows_per_chunk = std::max((ny_local + chunks - 1) / chunks, 64);
-    // two-pass: independent warps, ~3 waves of 16 resident warps per SM
-    const int tp_target = sms * 16 * 3;
-    const int tp_chunks = std::max(1, (tp_target + tp_strips(h->d.nx) - 1) / tp_strips(h->d.nx));
-    f->tp_rows = std::max((ny_local + tp_chunks - 1) / tp_chunks, 32);
+    f->sms = sms;
+  }
+  // two-pass chunking follows the resident warps of the kernel in use
+  const int nmat = std::min(h->mc.n, 4);
+  if (f->tp_rows_nmat != nmat) {
+    int ny_local = 0;
+    for (auto& s : h->slabs) ny_local = std::max(ny_local, s.L.ny);
+    f->tp_rows = tp_choose_rows(h->d.nx, ny_local, f->sms, tp_resident_warps(nmat));
+    f->tp_rows_nmat = nmat;
   }
   if (steps > f->cap) {
     cudaFree(f->rec);

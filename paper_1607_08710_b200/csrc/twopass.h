@@ -49,6 +49,11 @@ struct MatPassArgs {
 
 int tp_strips(int nx);
 bool tp_fits(int64_t pitch, int ny);  // 32-bit offsets suffice for the slab
+// resident warps per SM of the corrector kernel: k_pass (nmat 0) or k_pass_mat<nmat>
+int tp_resident_warps(int nmat);
+int tp_resident_warps_mat(int nmat);
+// rows per chunk for a slab of ny rows: whole waves of independent warps
+int tp_choose_rows(int nx, int ny, int sms, int warps_per_sm);
 // exact: the kernels that complete shock-precursor quotients exactly (see
 // twopass_kernel.cu); the plain ones flag such steps (StepAcc::fail = 2)
 void launch_pass(const PassArgs& a, bool corr, bool muscl, bool exact, cudaStream_t st);

@@ -20,6 +20,9 @@
 // it wins because it keeps every SM issuing instead of waiting at barriers.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdint>
+
 #include "../../include/lagflux_b200.h"
 #include "face_fast.cuh"
 #include "fused_common.cuh"
@@ -333,6 +336,45 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
 }  // namespace
 
 int tp_strips(int nx) { return (nx + TXW - 1) / TXW; }
+
+int tp_resident_warps(int nmat) {
+  if (nmat > 0) return tp_resident_warps_mat(nmat);
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass<true, true, false>, TP_THREADS, 0) !=
+          cudaSuccess ||
+      b < 1)
+    b = LF_TP_MINBLOCKS;
+  return b * (TP_THREADS / 32);
+}
+
+// Each warp marches one strip over one chunk of rows (plus ~4 rows of stencil
+// fill); the warps are independent, so the cost is about (waves) x (rows + fill)
+// where a wave is one warp per resident slot.  Chunk counts are chosen so the
+// warps fill whole waves (measured: 16384^2 at 13 chunks = 4.3 waves runs 4 %
+// slower than 12 chunks = 3.96 waves; 1024^2 at 22 rows = 0.98 wave 7.1 G/s,
+// 20 rows = 1.08 waves 5.5 G/s).  Four waves when the marches stay long (the
+// tail of a wave is the last warps' finish), else the cheapest of 1-3 waves.
+int tp_choose_rows(int nx, int ny, int sms, int warps_per_sm) {
+  const int64_t strips = tp_strips(nx), cap = (int64_t)sms * warps_per_sm;
+  auto rows_for = [&](int64_t k) {
+    const int64_t chunks = std::max<int64_t>(1, k * cap / strips);
+    return (int)std::max<int64_t>((ny + chunks - 1) / chunks, 16);
+  };
+  const int r4 = rows_for(4);
+  if (r4 >= 64) return r4;
+  int best = r4;
+  int64_t best_cost = INT64_MAX;
+  for (int k = 1; k <= 4; ++k) {
+    const int r = rows_for(k);
+    const int64_t warps = strips * ((ny + r - 1) / r);
+    const int64_t cost = ((warps + cap - 1) / cap) * (r + 8);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = r;
+    }
+  }
+  return best;
+}
 
 bool tp_fits(int64_t pitch, int ny) {
   // k_pass addresses (row, column) with 32-bit element offsets, rows -NG .. ny+NG

@@ -540,6 +540,19 @@ void launch_k(const PassArgs& a, const MatPassArgs& m, const MatK& mk, unsigned 
 
 }  // namespace
 
+int tp_resident_warps_mat(int nmat) {
+  int b = 0;
+  cudaError_t e;
+  switch (nmat) {
+    case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, 1>, TP_THREADS, 0); break;
+    case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, 2>, TP_THREADS, 0); break;
+    case 3: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, 3>, TP_THREADS, 0); break;
+    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, 4>, TP_THREADS, 0);
+  }
+  if (e != cudaSuccess || b < 1) b = 2;
+  return b * (TP_THREADS / 32);
+}
+
 void launch_pass_mat(const PassArgs& a, const MatPassArgs& m, const MatConsts& mc, bool corr,
                      bool muscl, cudaStream_t st) {
   MatK mk{};
