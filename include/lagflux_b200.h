@@ -194,6 +194,10 @@ int lf_set_path(lf_handle* h, int path);               /* LF_PATH_* */
 int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
                   int* kernel_launches);
 int lf_device_bytes(lf_handle* h, int64_t* bytes);
+/* The device's own ghost fill of the current state (the kernels' fill, not the
+ * host apply_boundary of lf_download), downloaded with the reference's two
+ * ghost layers (corners included) into the ghosted row-major layout. */
+int lf_download_ghosted(lf_handle* h, double* const field[4], int64_t ld);
 /* Kernels launched by this library in this process so far (all handles). */
 int lf_launch_count(lf_handle* h, int64_t* launches);
 /* One scalar per interior cell: the CFL rate field is not kept; this returns the

@@ -224,6 +224,22 @@ void exchange_local(lf_handle* h, double* SlabState::*buf, int ncomp = 4) {
 void fill_all(lf_handle* h, double* SlabState::*buf, int ncomp = 4, int odd_x = 1,
               int odd_y = 2) {
   const int xbc[4] = {h->d.bc[0], h->d.bc[1], h->d.bc[2], h->d.bc[3]};
+  bool one = true;  // the single-launch fill applies (every ghost source is interior)
+  for (auto& s : h->slabs) one = one && s.L.nx >= NG && (!h->dim2 || s.L.ny >= NG);
+  if (one) {
+    // the y sides read only their own slab's rows, so they precede the halo
+    // exchange (which carries the x ghosts of the neighbours' rows)
+    for (auto& s : h->slabs) {
+      CK(cudaSetDevice(s.device));
+      launch_fill_xy(s.field(s.*buf), s.L, xbc, s.sl, h->dim2, s.stream, ncomp, odd_x, odd_y);
+    }
+    if (h->nccl)
+      nccl_exchange_halos(h, buf, ncomp);
+    else
+      exchange_local(h, buf, ncomp);
+    CK(cudaGetLastError());
+    return;
+  }
   for (auto& s : h->slabs) {
     CK(cudaSetDevice(s.device));
     launch_fill_x(s.field(s.*buf), s.L, xbc, s.stream, ncomp, odd_x);
@@ -1055,6 +1071,30 @@ int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghost
     }
     sync_all(h);
     if (fill_ghosts) host_apply_boundary(h->d, field, ld);
+    return 0;
+  });
+}
+
+int lf_download_ghosted(lf_handle* h, double* const field[4], int64_t ld) {
+  return guarded(h, [&] {
+    if (!field || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad field or ld");
+    fill_all(h, &SlabState::U);
+    const int gy = h->dim2 ? 2 : 0;
+    for (auto& s : h->slabs) {
+      CK(cudaSetDevice(s.device));
+      // interior rows, plus the domain's y ghost rows on the edge slabs (filled
+      // there, or received as halos when y is periodic over several slabs)
+      const int r0 = h->dim2 && s.sl.y0 == 0 ? -2 : 0;
+      const int r1 = s.L.ny + (h->dim2 && s.sl.y0 + s.L.ny == h->d.ny ? 2 : 0);
+      for (int c = 0; c < 4; ++c) {
+        double* dst = field[c] + (int64_t)(s.sl.y0 + gy + r0) * ld;
+        const double* src = s.U + s.L.origin() + c * s.L.fstride + (int64_t)r0 * s.L.pitch - 2;
+        CK(cudaMemcpy2DAsync(dst, ld * sizeof(double), src, s.L.pitch * sizeof(double),
+                             (size_t)(s.L.nx + 4) * sizeof(double), (size_t)(r1 - r0),
+                             cudaMemcpyDefault, s.stream));
+      }
+    }
+    sync_all(h);
     return 0;
   });
 }

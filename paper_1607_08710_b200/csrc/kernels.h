@@ -57,6 +57,9 @@ void reset_scalars(Scalars* s, cudaStream_t st);
 // odd_y in a y image (a conserved field: 1 and 2; partial densities: none, -1).
 void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_t st,
                    int ncomp = 4, int odd_x = 1);
+// x and y sides in one launch; needs nx >= NG and (2D) ny >= NG
+void launch_fill_xy(const Field& f, const Layout& L, const int bc[4], const Slab& sl, bool dim2,
+                    cudaStream_t st, int ncomp, int odd_x, int odd_y);
 void launch_fill_y_only(const Field& f, const Layout& L, const int bc[4], const Slab& sl,
                         cudaStream_t st, int ncomp = 4, int odd_y = 2);
 

@@ -90,6 +90,59 @@ __global__ void k_fill_y(Field f, int nx, int ny, int bc_lo, int bc_hi, int do_l
   }
 }
 
+// Both sides in one launch (nx >= NG and, in 2D, ny >= NG: every source is an
+// interior cell).  x ghosts of the interior rows as k_fill_x; the y ghost rows
+// as k_fill_y, where a corner -- k_fill_y's copy of an x ghost -- is recomposed
+// from the interior cell both rules point at, with the same multiplications
+// (a reflective side multiplies by +-1: exact, so the composition is the
+// sequential x-then-y fill bit for bit).  Threads own disjoint ghost cells and
+// read interior cells only.
+__global__ void k_fill_xy(Field f, int nx, int ny, int bx_lo, int bx_hi, int by_lo, int by_hi,
+                          int do_lo, int do_hi, int odd_x, int odd_y) {
+  const int c = blockIdx.y;
+  const double sx = c == odd_x ? -1.0 : 1.0, sy = c == odd_y ? -1.0 : 1.0;
+  double* base = f.comp(c);
+  const int64_t P = f.pitch;
+  const int t = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  // column i of a row after the x fill
+  auto xval = [&](const double* row, int i) -> double {
+    if (i >= 0 && i < nx) return row[i];
+    const bool lo = i < 0;
+    const int l = lo ? -i : i - nx + 1;
+    switch (lo ? bx_lo : bx_hi) {
+      case 0: return row[lo ? 0 : nx - 1];
+      case 1: return sx * row[lo ? l - 1 : nx - l];
+      default: return row[lo ? ((nx - l) % nx + nx) % nx : (l - 1) % nx];
+    }
+  };
+  if (t < 2 * ny) {  // x sides: (row, side)
+    double* row = base + (int64_t)(t >> 1) * P;
+    const bool lo = (t & 1) == 0;
+    for (int l = 1; l <= NG; ++l) {
+      const int i = lo ? -l : nx - 1 + l;
+      row[i] = xval(row, i);
+    }
+    return;
+  }
+  const int u = t - 2 * ny;  // y sides: (column incl. x ghosts, side)
+  if (u >= 2 * (nx + 2 * NG)) return;
+  const int i = (u >> 1) - NG;
+  const bool lo = (u & 1) == 0;
+  if (lo ? !do_lo : !do_hi) return;
+  const int b = lo ? by_lo : by_hi;
+  for (int l = 1; l <= NG; ++l) {
+    const int jd = lo ? -l : ny - 1 + l;
+    int js;
+    switch (b) {
+      case 0: js = lo ? 0 : ny - 1; break;
+      case 1: js = lo ? l - 1 : ny - l; break;
+      default: js = lo ? ((ny - l) % ny + ny) % ny : (l - 1) % ny;
+    }
+    const double v = xval(base + (int64_t)js * P, i);
+    base[(int64_t)jd * P + i] = b == 1 ? sy * v : v;
+  }
+}
+
 // ---------------------------------------------------------------- CFL rate
 // solver.cpp:449-470: max over interior cells, exact (order independent).
 template <bool DIM2>
@@ -370,6 +423,14 @@ void reset_scalars(Scalars* s, cudaStream_t st) {
 void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_t st, int ncomp,
                    int odd_x) {
   count_launch(), k_fill_x<<<dim3(cdiv(L.ny, 128), ncomp), 128, 0, st>>>(f, L.nx, L.ny, bc[0], bc[1], odd_x);
+}
+
+void launch_fill_xy(const Field& f, const Layout& L, const int bc[4], const Slab& sl, bool dim2,
+                    cudaStream_t st, int ncomp, int odd_x, int odd_y) {
+  const int threads = 2 * L.ny + 2 * (L.nx + 2 * NG);
+  count_launch(), k_fill_xy<<<dim3(cdiv(threads, 128), ncomp), 128, 0, st>>>(
+      f, L.nx, L.ny, bc[0], bc[1], bc[2], bc[3], dim2 && sl.fill_lo, dim2 && sl.fill_hi, odd_x,
+      odd_y);
 }
 
 void launch_fill_y_only(const Field& f, const Layout& L, const int bc[4], const Slab& sl,

@@ -72,6 +72,7 @@ SIGNATURES = [
     ("lf_device_bytes", C.c_int, [H, C.POINTER(C.c_int64)]),
     ("lf_max_rate", C.c_int, [H, DP]),
     ("lf_interior_totals", C.c_int, [H, DP]),
+    ("lf_download_ghosted", C.c_int, [H, P4, C.c_int64]),
     ("lf_launch_count", C.c_int, [H, C.POINTER(C.c_int64)]),
     ("lf_slab_partition", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("lf_selftest_fastmath", C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),

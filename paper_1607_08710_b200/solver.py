@@ -140,6 +140,11 @@ class LagfluxSolver:
         self._check(self._lib.lf_download(self._h, N.field_ptrs(field), self._grid.nxt,
                                           1 if fill_ghosts else 0))
 
+    def download_ghosted(self, field: np.ndarray):
+        """The device kernels' own ghost fill of the current state, two layers
+        (corners included), into `field` (test hook: lf_download_ghosted)."""
+        self._check(self._lib.lf_download_ghosted(self._h, N.field_ptrs(field), self._grid.nxt))
+
     def attach(self, state: G.SolverState):
         """Make `state` the device-resident state (uploads its field)."""
         self.upload(state.field)

@@ -224,6 +224,40 @@ def test_download_fill_ghosts_matches_reference_fill(cuda):
         assert_fields_equal(out, ref, str(bcs))
 
 
+@pytest.mark.parametrize("shape,devices", [((20, 12), (0,)), ((4, 4), (0,)), ((33, 17), (0, 0)),
+                                          ((29, 24), (0, 0, 0)), ((37, 1), (0,)), ((3, 9), (0,))])
+def test_device_ghost_fill_matches_reference(cuda, shape, devices):
+    """The kernels' ghost fill (x and y sides in one launch when nx, ny >= 4; the
+    two-kernel fill otherwise), corners included, against apply_boundary
+    (grid.cpp:79-120) of the reference (the oracle's restatement without oracle/_ref)."""
+    nx, ny = shape
+    g = G.make_grid_1d(nx, 0.0, 1.0) if ny == 1 else G.make_grid_2d(nx, ny, 0.0, 1.0, 0.0, 0.7)
+    rng = np.random.default_rng(nx * 100 + ny)
+    f = G.new_field(g)
+    g.interior(f)[...] = rng.standard_normal(g.interior(f).shape)
+    g.interior(f)[1][..., 0] = 0.0                       # signed zeros through the flips
+    fill = O.ref_lib().lfr_fill_ghosts if O.ref_available() else O.oracle_lib().lfo_fill_ghosts
+    combos = [(a, b, c, d) for a in range(3) for b in range(3) for c in range(3) for d in range(3)
+              if (a == 2) == (b == 2) and (c == 2) == (d == 2)]
+    for bcs in combos:
+        if g.dim == 1 and bcs[2:] != (0, 0):
+            continue
+        if len(devices) > 1 and (bcs[2] == 2) != (bcs[3] == 2):
+            continue
+        s = LagfluxSolver(g, G.BoundaryCondition(*bcs), devices=devices)
+        s.upload(f)
+        out = np.full_like(f, np.nan)
+        s.download_ghosted(out)
+        s.close()
+        ref = f.copy()
+        for c, parity in enumerate((0, 1, 2, 0)):
+            arr = np.ascontiguousarray(ref[c])
+            fill(O.C.byref(O._cgrid(g)), (O.C.c_int * 4)(*bcs), parity, arr.ctypes.data_as(O.DP))
+            ref[c] = arr
+        assert np.array_equal(out, ref), (bcs, devices)
+        assert np.array_equal(np.signbit(out), np.signbit(ref)), (bcs, devices)
+
+
 def _box_cases():
     """States outside the fast kernels' cell box (face_fast.cuh): each must take
     the stage-wise IEEE re-run and still equal the oracle."""
