@@ -6,7 +6,8 @@ reference compiled from its own sources (oracle/_ref), on this box.
 Config 2: four-quadrant 1024^2, transmissive, CFL 0.45, 200 steps.
 Config 3: Sedov 4096^2, reflective, CFL 0.4, 100 steps (the reference needs ~5 GB
           and tens of seconds on all host cores).
-For each: device-resident steps through lf_advance (CUDA-event timed), then the
+For each: device-resident steps through lf_advance (CUDA-event timed, after an
+untimed 20-step run that makes the handle's one-time allocations), then the
 final field and every step's dt / time / min rho / min p compared with the
 reference run (==).
 """
@@ -32,8 +33,14 @@ for name, case in (("config2_quadrant_1024", CS.quadrant(1024, 200)),
     s = LagfluxSolver(g, case.bc, case.gamma, case.params)
     stream = torch.cuda.current_stream()
     s.set_stream(stream.cuda_stream)
-    st = G.SolverState(field=f0.copy())
     ctl = G.TimeControls(case.cfl, case.t_final, case.max_steps)
+    # one-time device allocations outside the timed region: a 20-step throwaway
+    # run; the timed run restarts from the initial state (the upload also resets
+    # the exact-kernel switch, so its first flagged batch is timed)
+    warm = G.SolverState(field=f0.copy())
+    s.attach(warm)
+    s.advance(warm, ctl, 20)
+    st = G.SolverState(field=f0.copy())
     s.attach(st)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
