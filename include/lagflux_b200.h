@@ -214,6 +214,11 @@ int lf_selftest_fastmath(int64_t n, uint64_t seed, int64_t* counts);
  * primitives must pass its fast-path range check.  counts[2] = {faces solved,
  * faces with a failed range check}. */
 int lf_selftest_box(int64_t n, uint64_t seed, int64_t* counts);
+/* Device self-check of the corrector epilogue's box (csrc/face_fast.cuh,
+ * cell_epilogue_box): n random updated cells at the box edges; counts[3] =
+ * {cells the box accepts, of those failing a per-operation check, of those
+ * whose rate or e_int differs}. */
+int lf_selftest_epilogue(int64_t n, uint64_t seed, int64_t* counts);
 
 #ifdef __cplusplus
 }

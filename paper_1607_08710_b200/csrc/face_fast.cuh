@@ -186,6 +186,34 @@ __device__ __forceinline__ void cell_epilogue(const double v[4], const FK& c, do
   rr += div_fast(abs_bits(vv) + cs, c.rdy, ok_r);
 }
 
+// cell_epilogue with its rate checks proved by a box instead of tested per
+// operation.  If rho in [2^-100, 2^100), |m_x|, |m_y| < 2^100, p in [2^-400,
+// 2^400) and dx, dy in [2^-100, 2^100) (dxy_box, once per launch): 1/rho is in
+// (2^-100, 2^100]; gamma p / rho (gamma in [1, 2^7)) lies in [2^-500, 2^507], so
+// the square root is on its fast path and cs in [2^-250, 2^254); |u| < 2^200;
+// the rate dividends |u| + cs lie in [2^-250, 2^255) and the quotients by dx, dy
+// in [2^-355, 2^355] -- all normal, where the fast paths are exact.  ok_r is
+// then the box itself; a cell outside it flags the step (stage-wise re-run).
+// The e_int quotient keeps div_exact and its own test (tiny kinetic energies).
+__device__ __forceinline__ void cell_epilogue_box(const double v[4], const FK& c, bool dxy_box,
+                                                  double& eint, bool& ok_e, double& rr,
+                                                  bool& rate_ok, bool& ok_r) {
+  const Recip r0 = recip_of(v[0]);
+  const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
+  eint = v[3] - div_exact(kin, r0, ok_e);
+  bool dead = true;  // proved by the box
+  const double inv = div_fast(1.0, r0, dead);
+  const double uu = v[1] * inv, vv = v[2] * inv;
+  const double p = c.gm1 * (v[3] - kin * inv);
+  rate_ok = (v[0] > 0.0) && (p > 0.0);
+  const double cs = sqrt_fast(c.gamma * p * inv, dead);
+  rr = div_fast(abs_bits(uu) + cs, c.rdx, dead);
+  rr += div_fast(abs_bits(vv) + cs, c.rdy, dead);
+  // hi words: 2^-400 = 0x26f00000, 2^400 = 0x58f00000
+  const bool p_box = ((unsigned)__double2hiint(p) - 0x26f00000u) < (0x58f00000u - 0x26f00000u);
+  ok_r = ok_r && dxy_box && pos_in_box(v[0]) && vel_in_box(v[1]) && vel_in_box(v[2]) && p_box;
+}
+
 #endif  // __CUDACC__
 
 }  // namespace lfb

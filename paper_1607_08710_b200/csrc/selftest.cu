@@ -202,9 +202,63 @@ __global__ void k_selftest_box(long long n, unsigned long long seed, unsigned lo
   for (int k = 0; k < 2; ++k) atomicAdd(&out[k], c[k]);
 }
 
+// cell_epilogue_box against cell_epilogue on updated cells drawn at the box
+// edges: counts {cells the box accepts, of those failing a per-operation check,
+// of those with a different rate or e_int}.
+__global__ void k_selftest_epilogue(long long n, unsigned long long seed, unsigned long long* out) {
+  unsigned long long c[3] = {0, 0, 0};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long s = seed ^ (unsigned long long)i * 0xd1b54a32d192ed03ull;
+    const double gm1 = box_mag(s, -14, 6);
+    const double gamma = 1.0 + gm1;
+    if (!const_in_box(gamma, gm1)) continue;
+    const double dx = box_mag(s, -100, 100), dy = box_mag(s, -100, 100);
+    const FK C = make_fk(gamma, gm1, 1.5, dx, dy);
+    double v[4];
+    v[0] = box_mag(s, -101, 101);
+    for (int q = 1; q <= 2; ++q) {
+      const unsigned long long k = splitmix(s);
+      double m = (k & 7) == 0 ? 0.0 : box_mag(s, (k & 8) ? -1074 + 60 : -300, 101);
+      if ((k & 7) == 1) m = __longlong_as_double((long long)(splitmix(s) & 0xfffffffffffffull));  // subnormal
+      v[q] = (k & 16) ? -m : m;
+    }
+    // E from a target pressure near the p box edges (the recomputed p differs by rounding)
+    const double pt = box_mag(s, -402, 402);
+    const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
+    v[3] = pt / gm1 + kin / v[0];
+    if (splitmix(s) & 1) v[3] = nudge(s, v[3]);
+    const bool dxy_box = pos_in_box(dx) && pos_in_box(dy);
+    double e1, r1, e2, r2;
+    bool oke1 = true, okr1 = true, rok1, oke2 = true, okr2 = true, rok2;
+    cell_epilogue(v, C, e1, oke1, r1, rok1, okr1);
+    cell_epilogue_box(v, C, dxy_box, e2, oke2, r2, rok2, okr2);
+    if (!(rok2 && okr2)) continue;
+    c[0] += 1;
+    if (!rok1 || !okr1) c[1] += 1;
+    if (!same(r1, r2) || !same(e1, e2) || oke1 != oke2) c[2] += 1;
+  }
+  for (int k = 0; k < 3; ++k) atomicAdd(&out[k], c[k]);
+}
+
 }  // namespace
 
 }  // namespace lfb
+
+extern "C" int lf_selftest_epilogue(int64_t n, uint64_t seed, int64_t* counts) {
+  if (!counts || n < 0) return LF_ERR_ARGUMENT;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 4 * sizeof(unsigned long long)) != cudaSuccess) return LF_ERR_DEVICE;
+  cudaMemset(d, 0, 4 * sizeof(unsigned long long));
+  lfb::count_launch();
+  lfb::k_selftest_epilogue<<<148 * 8, 256>>>((long long)n, (unsigned long long)seed, d);
+  unsigned long long h[4];
+  const cudaError_t e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return LF_ERR_DEVICE;
+  for (int k = 0; k < 3; ++k) counts[k] = (int64_t)h[k];
+  return LF_OK;
+}
 
 extern "C" int lf_selftest_box(int64_t n, uint64_t seed, int64_t* counts) {
   if (!counts || n < 0) return LF_ERR_ARGUMENT;

@@ -69,6 +69,9 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 #ifndef LF_TP_UNROLL
 #define LF_TP_UNROLL 1
 #endif
+#ifndef LF_EPI_BOX
+#define LF_EPI_BOX 1
+#endif
 
 // EXACT = false: the plain fast path; a warp whose stencil rows hold a velocity
 // in (0, 2^-500) (shock precursors) does not compute with it but raises the
@@ -93,6 +96,9 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
   const double lam_x = dt / a.dx;
   const double lam_y = dt / a.dy;
   const FK C = make_fk(a.gamma, a.gm1, a.beta, a.dx, a.dy);
+#if LF_EPI_BOX
+  const bool dxy_box = pos_in_box(a.dx) && pos_in_box(a.dy);
+#endif
 
   const int lane = threadIdx.x & 31;
   const int warp = blockIdx.x * (TP_THREADS / 32) + (threadIdx.x >> 5);
@@ -265,7 +271,11 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
         } else {
           bool ok = true, okr = true, rate_ok;
           double eint, rr;
+#if LF_EPI_BOX
+          cell_epilogue_box(v, C, dxy_box, eint, ok, rr, rate_ok, okr);
+#else
           cell_epilogue(v, C, eint, ok, rr, rate_ok, okr);
+#endif
           if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
             fail = 1;
           } else {

@@ -77,6 +77,7 @@ SIGNATURES = [
     ("lf_slab_partition", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("lf_selftest_fastmath", C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
     ("lf_selftest_box", C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
+    ("lf_selftest_epilogue", C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
 ]
 
 _lib = None

@@ -34,3 +34,15 @@ def test_cell_box_implies_fast_path_validity(cuda):
     solved, failed = list(counts)
     assert solved > n // 4
     assert failed == 0
+
+
+def test_epilogue_box_implies_fast_path_validity(cuda):
+    """The corrector's epilogue box (cell_epilogue_box): wherever it accepts an
+    updated cell, the per-operation checks pass and rate / e_int are identical."""
+    counts = (C.c_int64 * 3)()
+    n = 1 << 26
+    assert N.lib().lf_selftest_epilogue(n, 0x1607087102, counts) == 0
+    accepted, check_failed, differ = list(counts)
+    assert accepted > n // 8
+    assert check_failed == 0
+    assert differ == 0
