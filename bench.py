@@ -261,7 +261,9 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         row0, rows = solver.local_rows()
-        host = torch.empty((4, g.nyt, g.nxt), dtype=torch.float64, pin_memory=True)
+        # this rank's rows only (weak scaling: the global grid is N x 8.6 GB)
+        solver.local_host = True
+        host = torch.empty(solver.local_field_shape(), dtype=torch.float64, pin_memory=True)
         hf = host.numpy()
         solver.download(hf)  # the current state as this step's input (untimed)
         barrier()

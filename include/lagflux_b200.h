@@ -125,7 +125,9 @@ int lf_slab_partition(int ny, int nranks, int rank, int* row0, int* nrows);
 /* Host <-> device field transfer in the reference's ghosted layout:
  * component c of cell (i, j) (total indices, ghosts included) at field[c][j*ld + i],
  * ld >= nx + 4.  Distributed handles transfer their own slab rows only, at the
- * same global positions.  Download writes interior cells; fill_ghosts != 0
+ * same global positions; a rank that allocates only its own rows (total rows
+ * y0 .. y0 + rows + 3 in 2D) passes component pointers biased by -y0 * ld, and
+ * fill_ghosts = 0 (lf_local_rows gives y0, rows).  Download writes interior cells; fill_ghosts != 0
  * additionally applies the boundary conditions to the host ghosts
  * (apply_boundary, grid.cpp:116-121). */
 int lf_upload(lf_handle* h, double* const field[4], int64_t ld);

@@ -109,6 +109,18 @@ def partial_ptrs(partial):
     return (DPT * partial.shape[0])(*[partial[k].ctypes.data_as(DPT) for k in range(partial.shape[0])])
 
 
+def biased_field_ptrs(field, row_bias: int):
+    """P4 of a field that holds only the total rows row_bias .. row_bias + nyt_local - 1
+    of the global ghosted layout: each pointer is biased by -row_bias * ld so the
+    library's global row addressing (lf_upload / lf_download of a distributed
+    handle) lands inside the local buffer."""
+    base = field_ptrs(field)
+    if not row_bias:
+        return base
+    off = row_bias * field.shape[2] * 8
+    return P4(*[C.cast(C.c_void_p(C.cast(base[c], C.c_void_p).value - off), DP) for c in range(4)])
+
+
 def field_ptrs(field):
     """P4 of the four contiguous component arrays of a (4, nyt, nxt) float64 field."""
     assert field.dtype.name == "float64" and field.flags.c_contiguous and field.shape[0] == 4

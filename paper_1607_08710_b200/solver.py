@@ -78,6 +78,9 @@ class LagfluxSolver:
             _raise(err)
         self.set_path(path)
         self._resident = None  # SolverState whose field is on the device
+        # host fields hold only this rank's rows (distributed handles): see
+        # local_field_shape(); the ABI takes pointers biased by -y0 * ld
+        self.local_host = False
         self._resident_mat = None  # MaterialCells whose partials are on the device
         self.materials = materials
         if materials is not None:
@@ -126,6 +129,18 @@ class LagfluxSolver:
         self._check(self._lib.lf_local_rows(self._h, C.byref(r0), C.byref(n)))
         return r0.value, n.value
 
+    def local_field_shape(self):
+        """(4, rows + 2 gy, nxt): a host field holding this rank's slab rows and
+        their two ghost rows each side (total rows y0 .. y0 + rows + 2 gy - 1)."""
+        _, n = self.local_rows()
+        return (4, n + 2 * self._grid.gy, self._grid.nxt)
+
+    def _ptrs(self, field):
+        if not self.local_host:
+            return N.field_ptrs(field)
+        assert field.shape == self.local_field_shape(), (field.shape, self.local_field_shape())
+        return N.biased_field_ptrs(field, self.local_rows()[0])
+
     def device_bytes(self) -> int:
         b = C.c_int64()
         self._check(self._lib.lf_device_bytes(self._h, C.byref(b)))
@@ -133,17 +148,19 @@ class LagfluxSolver:
 
     # ------------------------------------------------------------ state transfer
     def upload(self, field: np.ndarray):
-        self._check(self._lib.lf_upload(self._h, N.field_ptrs(field), self._grid.nxt))
+        self._check(self._lib.lf_upload(self._h, self._ptrs(field), self._grid.nxt))
         self._resident = None
 
     def download(self, field: np.ndarray, fill_ghosts: bool = False):
-        self._check(self._lib.lf_download(self._h, N.field_ptrs(field), self._grid.nxt,
+        if fill_ghosts and self.local_host:
+            raise ValueError("fill_ghosts needs the whole grid on the host")
+        self._check(self._lib.lf_download(self._h, self._ptrs(field), self._grid.nxt,
                                           1 if fill_ghosts else 0))
 
     def download_ghosted(self, field: np.ndarray):
         """The device kernels' own ghost fill of the current state, two layers
         (corners included), into `field` (test hook: lf_download_ghosted)."""
-        self._check(self._lib.lf_download_ghosted(self._h, N.field_ptrs(field), self._grid.nxt))
+        self._check(self._lib.lf_download_ghosted(self._h, self._ptrs(field), self._grid.nxt))
 
     def attach(self, state: G.SolverState):
         """Make `state` the device-resident state (uploads its field)."""

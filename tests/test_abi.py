@@ -71,3 +71,19 @@ def test_partial_pointer_marshalling():
     for k in range(3):
         assert C.cast(ptrs[k], C.c_void_p).value == p[k].ctypes.data
         assert ptrs[k][7] == p[k].ravel()[7]
+
+
+def test_biased_field_pointers_address_the_local_rows():
+    """A distributed rank's host buffer holds total rows y0 .. y0 + rows + 3 only; the
+    library addresses row y0 + 2 + r of the global layout through biased pointers
+    (lf_upload / lf_download of a distributed handle, include/lagflux_b200.h)."""
+    import numpy as np
+    y0, rows, nxt = 37, 5, 11
+    local = np.zeros((4, rows + 4, nxt))
+    p = N.biased_field_ptrs(local, y0)
+    for c in range(4):
+        addr = ctypes.cast(p[c], ctypes.c_void_p).value
+        # global interior row r of this slab -> local buffer row 2 + r
+        for r in (0, rows - 1):
+            assert addr + ((y0 + 2 + r) * nxt + 2) * 8 == local[c, 2 + r, 2:].ctypes.data
+    assert N.biased_field_ptrs(local, 0)[1][0] == N.field_ptrs(local)[1][0]
