@@ -256,22 +256,28 @@ class LagfluxSolver:
             self.attach(state)
         self._attach_mat(mat)
         n = int(min(nsteps, max(0, controls.max_steps - state.step)))
-        if n <= 0:
-            return 0
-        rec = (N.lf_step_out * n)()
-        t, s = C.c_double(state.time), C.c_int64(state.step)
-        acc = (C.c_double * 4)(*state.boundary_outflow)
-        taken = C.c_int()
-        rc = self._lib.lf_advance(self._h, n, controls.cfl, controls.t_final, C.byref(t),
-                                  C.byref(s), C.cast(acc, N.DP), rec, C.byref(taken))
-        for k in range(taken.value):
-            o = rec[k]
-            state.diagnostics.append(G.StepDiagnostics(o.step, o.time, o.dt, o.min_rho, o.min_p))
-        state.time, state.step = t.value, s.value
-        state.boundary_outflow = list(acc)
-        if rc:
-            _raise(self._error())
-        return taken.value
+        done = 0
+        # records come back in bounded chunks (nsteps may be far more than the
+        # steps to t_final)
+        rec = (N.lf_step_out * min(max(n, 1), 4096))()
+        while done < n:
+            chunk = min(n - done, len(rec))
+            t, s = C.c_double(state.time), C.c_int64(state.step)
+            acc = (C.c_double * 4)(*state.boundary_outflow)
+            taken = C.c_int()
+            rc = self._lib.lf_advance(self._h, chunk, controls.cfl, controls.t_final, C.byref(t),
+                                      C.byref(s), C.cast(acc, N.DP), rec, C.byref(taken))
+            for k in range(taken.value):
+                o = rec[k]
+                state.diagnostics.append(G.StepDiagnostics(o.step, o.time, o.dt, o.min_rho, o.min_p))
+            state.time, state.step = t.value, s.value
+            state.boundary_outflow = list(acc)
+            done += taken.value
+            if rc:
+                _raise(self._error())
+            if taken.value < chunk:
+                break
+        return done
 
     def time_steps(self, nsteps: int, cfl: float):
         """Device-timed steps: (summed kernel ms, loop ms, kernel launches)."""
