@@ -3,6 +3,7 @@ reference compiled from its own sources (oracle/_ref), on this box.
 
     python tools/bench_configs.py [out.json]
 
+Config 1: Sod 400x4, reflective, CFL 0.5, to t = 0.2 (353 steps; launch-bound).
 Config 2: four-quadrant 1024^2, transmissive, CFL 0.45, 200 steps.
 Config 3: Sedov 4096^2, reflective, CFL 0.4, 100 steps (the reference needs ~5 GB
           and tens of seconds on all host cores).
@@ -26,7 +27,8 @@ from paper_1607_08710_b200 import grid as G  # noqa: E402
 from paper_1607_08710_b200.solver import LagfluxSolver  # noqa: E402
 
 out = {}
-for name, case in (("config2_quadrant_1024", CS.quadrant(1024, 200)),
+for name, case in (("config1_sod_400x4", CS.sod()),
+                   ("config2_quadrant_1024", CS.quadrant(1024, 200)),
                    ("config3_sedov_4096", CS.sedov(4096, 100))):
     g = case.grid
     f0 = CS.initial_field(case)
