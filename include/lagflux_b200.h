@@ -22,6 +22,8 @@
  *   lf_init_fourier                (new) on-device seeded smooth-flow IC (BASELINE 4-5)
  *   lf_init_regions                initialize_hydro, InitKind::regions  run.cpp:29-78
  *   lf_interior_totals             interior_totals(grid, state.field)  grid.cpp:122-133
+ *   lf_edge_flux                   edge_flux (free function)      solver.cpp:45-53,
+ *                                  solver.hpp:31-37 (batched, on the device)
  *   lf_last_error                  the exception object (what(), PositivityError fields)
  *   lf_write_field_csv             field_csv + write_text_file   csv.cpp:26-83, run.cpp:162-168
  *   lf_set_materials               the constructor's `const MaterialSet*` (solver.cpp:61-88)
@@ -185,6 +187,17 @@ int lf_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* tim
  * bit-equal to the reference.  A distributed handle chains the sums over the
  * ranks in row order and returns the global totals on every rank (collective). */
 int lf_interior_totals(lf_handle* h, double tot[4]);
+
+/* The reference's free edge_flux(w_minus, w_plus, n, eos_minus, eos_plus)
+ * (solver.cpp:45-53) for n faces on `device`: w_* = n x {rho, u, v, p},
+ * normals = n x {nx, ny}, gamma_* = n per-side gammas; flux = n x {mass, mom_x,
+ * mom_y, energy}; contact (may be NULL) = n x {p*, u*} of lagrangian_hll.
+ * Bit-equal to the reference (general normals, no axis specialisation).  A
+ * non-physical trace returns LF_ERR_PRIMITIVE with sound_speed's message for the
+ * smallest such face (err->i = face index; err may be NULL). */
+int lf_edge_flux(int64_t n, const double* w_minus, const double* w_plus, const double* normals,
+                 const double* gamma_minus, const double* gamma_plus, double* flux,
+                 double* contact, int device, lf_error* err);
 
 int lf_last_error(lf_handle* h, lf_error* err);
 

@@ -29,6 +29,26 @@
 
 namespace lagflux::b200 {
 
+// edge_flux (solver.cpp:45-53) evaluated on the device; throws InvalidStateError
+// like sound_speed for a non-physical trace.  One face per call: a device round
+// trip, for API parity -- batch faces through lf_edge_flux.
+inline EdgeFlux edge_flux(const PrimitiveState& w_minus, const PrimitiveState& w_plus, Vec2 n,
+                          PerfectGasEos eos_minus, PerfectGasEos eos_plus, int device = 0) {
+  const double wm[4] = {w_minus.rho, w_minus.u, w_minus.v, w_minus.p};
+  const double wp[4] = {w_plus.rho, w_plus.u, w_plus.v, w_plus.p};
+  const double nr[2] = {n.x, n.y};
+  double f[4];
+  lf_error e{};
+  const int rc = lf_edge_flux(1, wm, wp, nr, &eos_minus.gamma, &eos_plus.gamma, f, nullptr, device, &e);
+  if (rc == LF_ERR_PRIMITIVE) throw InvalidStateError(e.message);
+  if (rc) throw Error(e.message);
+  return EdgeFlux{f[0], f[1], f[2], f[3]};
+}
+inline EdgeFlux edge_flux(const PrimitiveState& w_minus, const PrimitiveState& w_plus, Vec2 n,
+                          PerfectGasEos eos) {
+  return b200::edge_flux(w_minus, w_plus, n, eos, eos, 0);
+}
+
 class LagfluxSolver {
  public:
   LagfluxSolver(const CartesianGrid& g, const BoundaryCondition& bc, PerfectGasEos eos,

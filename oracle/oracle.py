@@ -161,6 +161,8 @@ def ref_lib():
     lib.lfr_mixed_cell_gamma.argtypes = [C.c_int, DP, DP]
     lib.lfr_mass_fraction_fluxes.argtypes = [C.c_double, C.c_int, DP, DP]
     lib.lfr_interior_totals.argtypes = [C.c_void_p, DP]
+    lib.lfr_edge_flux2.argtypes = [DP, DP, C.c_double, C.c_double, C.c_double, C.c_double, DP, DP,
+                                   C.c_char_p, C.c_int]
     lib.lfr_field_csv.restype = C.c_int64
     lib.lfr_field_csv.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_char_p, C.c_int64,
                                   C.POINTER(lfo_error)]

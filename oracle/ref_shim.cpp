@@ -328,6 +328,27 @@ void lfr_edge_flux(const double wm[4], const double wp[4], double nx, double ny,
   f[3] = e.energy;
 }
 
+// edge_flux / lagrangian_hll with one EOS per side (solver.cpp:45-53,
+// riemann_hll.hpp:27-45); 0, or 1 with the exception's what() in msg.
+int lfr_edge_flux2(const double wm[4], const double wp[4], double nx, double ny, double gm,
+                   double gp, double f[4], double cs[2], char* msg, int cap) {
+  try {
+    const PrimitiveState a{wm[0], wm[1], wm[2], wm[3]}, b{wp[0], wp[1], wp[2], wp[3]};
+    const ContactSolution s = lagrangian_hll(a, b, Vec2{nx, ny}, PerfectGasEos{gm}, PerfectGasEos{gp});
+    const EdgeFlux e = edge_flux(a, b, Vec2{nx, ny}, PerfectGasEos{gm}, PerfectGasEos{gp});
+    f[0] = e.mass;
+    f[1] = e.mom_x;
+    f[2] = e.mom_y;
+    f[3] = e.energy;
+    cs[0] = s.p_star;
+    cs[1] = s.u_star;
+    return 0;
+  } catch (const std::exception& x) {
+    std::snprintf(msg, (size_t)cap, "%s", x.what());
+    return 1;
+  }
+}
+
 int lfr_omp_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -1216,6 +1216,60 @@ int lf_compute_dt(lf_handle* h, double cfl, double time, double limit_time, doub
   });
 }
 
+int lf_edge_flux(int64_t n, const double* w_minus, const double* w_plus, const double* normals,
+                 const double* gamma_minus, const double* gamma_plus, double* flux,
+                 double* contact, int device, lf_error* err) {
+  if (err) clear_err(err);
+  if (n < 0 || (n > 0 && (!w_minus || !w_plus || !normals || !gamma_minus || !gamma_plus || !flux)))
+    return LF_ERR_ARGUMENT;
+  if (n == 0) return 0;
+  std::vector<void*> bufs;
+  auto fail_dev = [&](const char* what) {
+    for (void* p : bufs) cudaFree(p);
+    if (err) {
+      err->kind = LF_ERR_DEVICE;
+      snprintf(err->message, sizeof err->message, "%s", what);
+    }
+    return LF_ERR_DEVICE;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return fail_dev("cudaSetDevice");
+  const size_t sz[8] = {4, 4, 2, 1, 1, 4, 2, 0};
+  double* d[7];
+  for (int k = 0; k < 7; ++k) {
+    if (cudaMalloc(&d[k], (size_t)n * sz[k] * sizeof(double)) != cudaSuccess) return fail_dev("cudaMalloc");
+    bufs.push_back(d[k]);
+  }
+  unsigned long long* dfail = nullptr;
+  if (cudaMalloc(&dfail, sizeof *dfail) != cudaSuccess) return fail_dev("cudaMalloc");
+  bufs.push_back(dfail);
+  const double* src[5] = {w_minus, w_plus, normals, gamma_minus, gamma_plus};
+  for (int k = 0; k < 5; ++k)
+    if (cudaMemcpy(d[k], src[k], (size_t)n * sz[k] * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail_dev("cudaMemcpy");
+  if (cudaMemset(dfail, 0xff, sizeof *dfail) != cudaSuccess) return fail_dev("cudaMemset");
+  launch_edge_flux(n, d[0], d[1], d[2], d[3], d[4], d[5], contact ? d[6] : nullptr, dfail, 0);
+  unsigned long long f = 0;
+  if (cudaMemcpy(&f, dfail, sizeof f, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(flux, d[5], (size_t)n * 4 * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      (contact && cudaMemcpy(contact, d[6], (size_t)n * 2 * sizeof(double), cudaMemcpyDeviceToHost) !=
+                      cudaSuccess))
+    return fail_dev("edge_flux kernel");
+  for (void* p : bufs) cudaFree(p);
+  if (f == ~0ull) return 0;
+  // sound_speed's throw (euler.hpp:99-104) for the smallest failing face
+  const int64_t i = (int64_t)(f / 4);
+  const int which = (int)(f % 4);
+  const double v = (which < 2 ? w_minus : w_plus)[4 * i + (which % 2 ? 3 : 0)];
+  if (err) {
+    err->kind = LF_ERR_PRIMITIVE;
+    err->i = i;
+    err->value = v;
+    snprintf(err->message, sizeof err->message, "%s = %s",
+             which % 2 ? "non-positive pressure" : "non-positive density", fmt_f(v).c_str());
+  }
+  return LF_ERR_PRIMITIVE;
+}
+
 int lf_interior_totals(lf_handle* h, double tot[4]) {
   return guarded(h, [&] {
     if (!tot) return set_err(h, LF_ERR_ARGUMENT, "null totals");

@@ -135,6 +135,12 @@ void launch_init_regions(const Field& u, const Field& part, const Layout& L, con
                          cudaStream_t st);
 // field_csv's per-cell columns (csv.cpp:40-57): rho, u, v, p, e_internal, y_1..y_n as
 // planes of nx*ny; clamp failures -> atomicMin(fail, row-major global interior index)
+// edge_flux (solver.cpp:45-53) of n faces: w = n x {rho, u, v, p}, nrm = n x {nx, ny},
+// one gamma per side and face; flux n x 4, contact n x {p*, u*} (may be NULL);
+// fail: min over failing faces of 4 i + check (init ~0)
+void launch_edge_flux(int64_t n, const double* wm, const double* wp, const double* nrm,
+                      const double* gm, const double* gp, double* flux, double* contact,
+                      unsigned long long* fail, cudaStream_t st);
 // interior_totals' ordered per-component sums (grid.cpp:122-133) over one slab,
 // starting from s_in[4] (NULL: 0.0); u at the interior origin
 void launch_interior_sums(const double* u, int64_t fstride, int pitch, int nx, int ny,

@@ -72,6 +72,7 @@ SIGNATURES = [
     ("lf_device_bytes", C.c_int, [H, C.POINTER(C.c_int64)]),
     ("lf_max_rate", C.c_int, [H, DP]),
     ("lf_interior_totals", C.c_int, [H, DP]),
+    ("lf_edge_flux", C.c_int, [C.c_int64, DP, DP, DP, DP, DP, DP, DP, C.c_int, C.POINTER(lf_error)]),
     ("lf_download_ghosted", C.c_int, [H, P4, C.c_int64]),
     ("lf_launch_count", C.c_int, [H, C.POINTER(C.c_int64)]),
     ("lf_slab_partition", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),

@@ -304,6 +304,30 @@ class LagfluxSolver:
         return r.value
 
 
+def edge_flux(w_minus, w_plus, normals, gamma_minus, gamma_plus=None, device: int = 0):
+    """The reference's free edge_flux (solver.cpp:45-53) for a batch of faces on the
+    device: w_* (n, 4) primitive traces {rho, u, v, p}, normals (n, 2), one gamma
+    per side (scalars or (n,) arrays).  Returns (flux (n, 4), contact (n, 2) =
+    lagrangian_hll's {p*, u*}); a non-physical trace raises InvalidStateError with
+    sound_speed's message for the smallest such face."""
+    wm = np.ascontiguousarray(w_minus, dtype=np.float64).reshape(-1, 4)
+    wp = np.ascontiguousarray(w_plus, dtype=np.float64).reshape(-1, 4)
+    n = wm.shape[0]
+    nr = np.ascontiguousarray(np.broadcast_to(np.asarray(normals, dtype=np.float64), (n, 2)))
+    gm = np.ascontiguousarray(np.broadcast_to(np.asarray(gamma_minus, dtype=np.float64), (n,)))
+    gp = np.ascontiguousarray(np.broadcast_to(np.asarray(
+        gamma_minus if gamma_plus is None else gamma_plus, dtype=np.float64), (n,)))
+    flux = np.empty((n, 4))
+    contact = np.empty((n, 2))
+    err = N.lf_error()
+    p = lambda a: a.ctypes.data_as(N.DP)  # noqa: E731
+    rc = N.lib().lf_edge_flux(n, p(wm), p(wp), p(nr), p(gm), p(gp), p(flux), p(contact), device,
+                              C.byref(err))
+    if rc:
+        _raise(err)
+    return flux, contact
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     rc = N.lib().lf_nccl_unique_id(buf)

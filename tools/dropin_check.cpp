@@ -8,6 +8,7 @@
 // boundary outflow and error text agrees.
 #include <cmath>
 #include <cstdio>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -161,8 +162,39 @@ void run_multimaterial(int nx, int ny, int steps, bool auto_sync) {
 
 }  // namespace
 
+// The free edge_flux (solver.cpp:45-53): general normals, two EOS, the u* == 0
+// mean branch, and sound_speed's throw.
+void edge_flux_pair() {
+  const PrimitiveState a{1.0, 0.3, -0.2, 1.0}, b{0.125, -0.1, 0.4, 0.1}, c{1.0, 0.0, 0.0, 1.0};
+  const Vec2 normals[3] = {{1.0, 0.0}, {0.0, 1.0}, {0.6, 0.8}};
+  for (const Vec2& n : normals)
+    for (const auto& pr : {std::make_pair(a, b), std::make_pair(b, a), std::make_pair(c, c)}) {
+      const EdgeFlux x = edge_flux(pr.first, pr.second, n, PerfectGasEos{1.4}, PerfectGasEos{1.6});
+      const EdgeFlux y = b200::edge_flux(pr.first, pr.second, n, PerfectGasEos{1.4}, PerfectGasEos{1.6});
+      expect(x.mass == y.mass && x.mom_x == y.mom_x && x.mom_y == y.mom_y && x.energy == y.energy &&
+                 std::signbit(x.mom_x) == std::signbit(y.mom_x) &&
+                 std::signbit(x.mom_y) == std::signbit(y.mom_y),
+             "edge_flux");
+    }
+  std::string ref_what, gpu_what;
+  const PrimitiveState bad{1.0, 0.0, 0.0, -2.5};
+  try {
+    edge_flux(a, bad, Vec2{1.0, 0.0}, PerfectGasEos{1.4});
+  } catch (const InvalidStateError& e) {
+    ref_what = e.what();
+  }
+  try {
+    b200::edge_flux(a, bad, Vec2{1.0, 0.0}, PerfectGasEos{1.4});
+  } catch (const InvalidStateError& e) {
+    gpu_what = e.what();
+  }
+  expect(!ref_what.empty() && ref_what == gpu_what, "edge_flux error: " + ref_what + " | " + gpu_what);
+  std::printf("edge_flux: compared\n");
+}
+
 int main() {
   const PerfectGasEos eos{1.4};
+  edge_flux_pair();
   {
     const CartesianGrid g = make_grid_2d(64, 48, 0.0, 1.0, 0.0, 0.75);
     run_pair("smooth-periodic", g, {BcKind::periodic, BcKind::periodic, BcKind::periodic, BcKind::periodic},
