@@ -222,4 +222,13 @@ class LagfluxSolver {
   bool auto_sync_ = true;
 };
 
+// The free compute_dt (solver.cpp:55-59): a solver with default boundaries and
+// scheme parameters evaluates compute_dt of `field` on the device.
+inline double compute_dt(const CartesianGrid& g, const CellField& field, PerfectGasEos eos,
+                         const TimeControls& controls, double time, double limit_time,
+                         int device = 0) {
+  LagfluxSolver solver(g, BoundaryCondition{}, eos, SchemeParams{}, 1, nullptr, device);
+  return solver.compute_dt(field, controls, time, limit_time);
+}
+
 }  // namespace lagflux::b200

@@ -328,6 +328,17 @@ def edge_flux(w_minus, w_plus, normals, gamma_minus, gamma_plus=None, device: in
     return flux, contact
 
 
+def compute_dt(g: G.CartesianGrid, field: np.ndarray, gamma: float, controls: G.TimeControls,
+               time: float, limit_time: float, device: int = 0) -> float:
+    """The free compute_dt (solver.cpp:55-59): default boundaries and scheme
+    parameters, evaluated on the device."""
+    s = LagfluxSolver(g, G.BoundaryCondition(), gamma, G.SchemeParams(), devices=(device,))
+    try:
+        return s.compute_dt(field, controls, time, limit_time)
+    finally:
+        s.close()
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     rc = N.lib().lf_nccl_unique_id(buf)

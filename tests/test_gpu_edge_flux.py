@@ -67,3 +67,16 @@ def test_edge_flux_error_is_sound_speeds(cuda):
         assert O.ref_lib().lfr_edge_flux2(wm[12].ctypes.data_as(O.DP), wp[12].ctypes.data_as(O.DP), 1.0, 0.0,
                                           1.4, 1.4, f.ctypes.data_as(O.DP), c.ctypes.data_as(O.DP), msg, 320) == 1
         assert msg.value.decode() == "non-positive density = -1.000000"
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_free_compute_dt_equals_reference(cuda):
+    """The free compute_dt (solver.cpp:55-59) on the device equals the reference's."""
+    from paper_1607_08710_b200 import cases as CS
+    case = CS.quadrant(96, 1)
+    f = CS.initial_field(case)
+    ctl = G.TimeControls(0.45, 1e30)
+    for t, limit in ((0.0, 1e30), (0.25, 0.25 + 1e-6)):
+        r = O.RefSolver(case.grid, G.BoundaryCondition(), 1.4)
+        r.set_state(f)
+        assert S.compute_dt(case.grid, f, 1.4, ctl, t, limit) == r.compute_dt(0.45, t, limit)

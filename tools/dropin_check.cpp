@@ -190,6 +190,13 @@ void edge_flux_pair() {
   }
   expect(!ref_what.empty() && ref_what == gpu_what, "edge_flux error: " + ref_what + " | " + gpu_what);
   std::printf("edge_flux: compared\n");
+  // the free compute_dt (solver.cpp:55-59)
+  const CartesianGrid g = make_grid_2d(40, 30, 0.0, 1.0, 0.0, 0.75);
+  const CellField f = smooth_field(g, PerfectGasEos{1.4});
+  const TimeControls tc{0.45, 1e30, 1 << 30};
+  expect(compute_dt(g, f, PerfectGasEos{1.4}, tc, 0.0, 1e30) ==
+             b200::compute_dt(g, f, PerfectGasEos{1.4}, tc, 0.0, 1e30),
+         "free compute_dt");
 }
 
 int main() {
