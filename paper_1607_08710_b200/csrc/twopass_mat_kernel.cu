@@ -184,6 +184,25 @@ __device__ __forceinline__ void mat_face(double mass, double us, const double yl
   out[K - 1] = zero ? 0.0 : rest;
 }
 
+// The update operands of a row (U^n, P^n and, in the corrector, the stage-a
+// faces F^n and material fluxes) are staged one row ahead in shared memory with
+// cp.async: at 8 warps/SM the loads issued at the top of their own iteration
+// did not return before their use (ncu: long_scoreboard 25 % of the corrector),
+// and in registers they would add 42 live registers to a 255-register kernel.
+// Each lane copies and reads only its own elements, so the per-thread
+// cp.async.wait_group orders them; absent operands are zero-filled (src-size 0).
+#ifndef LF_MAT_ASYNC
+#define LF_MAT_ASYNC 1
+#endif
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gsrc),
+               "r"(pred ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
 template <bool CORR, bool MUSCL, int K>
 __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassArgs m, MatK mk) {
   MatR mr;
@@ -227,6 +246,37 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
 
   const int P = (int)a.pitch;
   int o_in = (y0 - 2) * P + c;
+#if LF_MAT_ASYNC
+  // [warp][buffer][operand][lane]: bse 0-3, pbs 4.., fnx, fny, max_, may_
+  constexpr int NOP = CORR ? 12 + 3 * K : 4 + K;
+  __shared__ double stage[TP_THREADS / 32][2][NOP][32];
+  double(*const st)[NOP][32] = stage[threadIdx.x >> 5];
+  auto issue = [&](int itn, int orow, int buf) {
+    const bool pu = itn >= 4 && upd;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      cp_async8(&st[buf][q][lane], pu ? a.base + q * a.fstride + orow : a.base, pu);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      cp_async8(&st[buf][4 + k][lane], pu ? m.pbase + k * a.fstride + orow : m.pbase, pu);
+    if (CORR) {
+      const bool px = itn >= 4 && col_in_mem && c >= 0 && c <= a.nx;
+      const bool py = itn >= 3 && col_interior;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cp_async8(&st[buf][4 + K + q][lane], px ? a.fx + q * a.fx_stride + orow : a.fx, px);
+        cp_async8(&st[buf][8 + K + q][lane], py ? a.fy + q * a.fy_stride + (orow + P) : a.fy, py);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        cp_async8(&st[buf][12 + K + k][lane], px ? m.mfx + k * m.mfx_stride + orow : m.mfx, px);
+        cp_async8(&st[buf][12 + 2 * K + k][lane], py ? m.mfy + k * m.mfy_stride + (orow + P) : m.mfy, py);
+      }
+    }
+    cp_commit();
+  };
+  issue(0, o_in - 2 * P, 0);
+#endif
   // the next input row (U and partials), loaded one iteration ahead
   double nxt[4] = {1.0, 0.0, 0.0, 1.0}, pnx[K];
 #pragma unroll
@@ -264,12 +314,17 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
 #pragma unroll
       for (int k = 0; k < K; ++k) pnx[k] = __ldg(m.px + k * a.fstride + o_in + P);
     }
-    // this iteration's update operands, issued early (their latency hides
-    // behind the closure, traces and face solves)
     double bse[4] = {0.0, 0.0, 0.0, 0.0}, pbs[K];
     double fnx[4] = {0.0, 0.0, 0.0, 0.0}, fny[4] = {0.0, 0.0, 0.0, 0.0}, max_[K], may_[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) pbs[k] = max_[k] = may_[k] = 0.0;
+#if LF_MAT_ASYNC
+    // the next row's operands in flight during this row's work
+    if (it + 1 < nit) issue(it + 1, o_row + P, (it + 1) & 1);
+    else cp_commit();
+#else
+    // this iteration's update operands, issued early (their latency hides
+    // behind the closure, traces and face solves)
     if (it >= 4 && upd) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) bse[q] = __ldg(a.base + q * a.fstride + o_row);
@@ -290,6 +345,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
         for (int k = 0; k < K; ++k) may_[k] = __ldg(m.mfy + k * m.mfy_stride + (o_row + P));
       }
     }
+#endif
     if (col_in_mem) {
       bool bad = false, ok = true;
       gr = closure<K>(pc, cur[0], mk, mr, yr, bad, ok);
@@ -339,6 +395,28 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
     mat_face<K>(fx[0], usx, ylx, ym2, mfx_s);
     mat_face<K>(fy[0], usy, ym2, ym1, mfy_s);
     // -- stage-a operands (corrector) and the Heun averages
+#if LF_MAT_ASYNC
+    cp_wait1();  // this row's group (the next row's may still be in flight)
+    {
+      const double(*const sb)[32] = st[it & 1];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bse[q] = sb[q][lane];
+#pragma unroll
+      for (int k = 0; k < K; ++k) pbs[k] = sb[4 + k][lane];
+      if (CORR) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          fnx[q] = sb[4 + K + q][lane];
+          fny[q] = sb[8 + K + q][lane];
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          max_[k] = sb[12 + K + k][lane];
+          may_[k] = sb[12 + 2 * K + k][lane];
+        }
+      }
+    }
+#endif
     double fxa[4], fya[4];
     if (CORR) {
 #pragma unroll
