@@ -25,6 +25,7 @@
 #include "handle.h"
 #include "host_util.h"
 #include "nccl_comm.h"
+#include "twopass.h"
 
 using namespace lfb;
 
@@ -221,8 +222,10 @@ void exchange_local(lf_handle* h, double* SlabState::*buf, int ncomp = 4) {
 // Ghost cells of `buf` on every slab: x sides, halo rows, then y sides at the
 // domain edges (grid.cpp:79-113 order).  A conserved field by default; the
 // partial densities are ncomp = n_mat even-parity components (odd = -1).
+// buf2 (optional): ncomp2 even-parity components (partial densities) filled in
+// the same launch when the single-launch fill applies.
 void fill_all(lf_handle* h, double* SlabState::*buf, int ncomp = 4, int odd_x = 1,
-              int odd_y = 2) {
+              int odd_y = 2, double* SlabState::*buf2 = nullptr, int ncomp2 = 0) {
   const int xbc[4] = {h->d.bc[0], h->d.bc[1], h->d.bc[2], h->d.bc[3]};
   bool one = true;  // the single-launch fill applies (every ghost source is interior)
   for (auto& s : h->slabs) one = one && s.L.nx >= NG && (!h->dim2 || s.L.ny >= NG);
@@ -231,13 +234,23 @@ void fill_all(lf_handle* h, double* SlabState::*buf, int ncomp = 4, int odd_x = 
     // exchange (which carries the x ghosts of the neighbours' rows)
     for (auto& s : h->slabs) {
       CK(cudaSetDevice(s.device));
-      launch_fill_xy(s.field(s.*buf), s.L, xbc, s.sl, h->dim2, s.stream, ncomp, odd_x, odd_y);
+      const Field f2 = buf2 ? s.field(s.*buf2) : Field{};
+      launch_fill_xy(s.field(s.*buf), s.L, xbc, s.sl, h->dim2, s.stream, ncomp, odd_x, odd_y,
+                     buf2 ? &f2 : nullptr, ncomp2);
     }
-    if (h->nccl)
+    if (h->nccl) {
       nccl_exchange_halos(h, buf, ncomp);
-    else
+      if (buf2) nccl_exchange_halos(h, buf2, ncomp2);
+    } else {
       exchange_local(h, buf, ncomp);
+      if (buf2) exchange_local(h, buf2, ncomp2);
+    }
     CK(cudaGetLastError());
+    return;
+  }
+  if (buf2) {
+    fill_all(h, buf, ncomp, odd_x, odd_y);
+    fill_all(h, buf2, ncomp2, -1, -1);
     return;
   }
   for (auto& s : h->slabs) {
@@ -646,6 +659,11 @@ bool use_fused(lf_handle* h) {
   if (h->path == LF_PATH_STAGED) return false;
   // materials: the two-pass material kernels for up to 4 materials, else stage-wise
   if (h->mc.n > 0 && (h->mc.n > 4 || h->path == LF_PATH_FUSED || !h->partials_ready)) return false;
+  // (the fused one-kernel step has no material transport: a slab beyond the
+  // two-pass kernels' 32-bit offsets goes stage-wise)
+  if (h->mc.n > 0)
+    for (auto& s : h->slabs)
+      if (!tp_fits(s.L.pitch, s.L.ny)) return false;
   return fused_supported(h);
 }
 
@@ -668,6 +686,9 @@ int guarded(lf_handle* h, F&& f) {
 namespace lfb {
 void fill_all_public(lf_handle* h, double* SlabState::*buf) { fill_all(h, buf); }
 void fill_partials_public(lf_handle* h, double* SlabState::*buf) { fill_partials(h, buf); }
+void fill_state_public(lf_handle* h, double* SlabState::*ubuf, double* SlabState::*pbuf) {
+  fill_all(h, ubuf, 4, 1, 2, pbuf, h->mc.n);
+}
 void alloc_staged_public(lf_handle* h) {
   for (auto& s : h->slabs) alloc_staged(s);
 }

@@ -208,18 +208,22 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   SlabState& s0 = h->slabs[0];
   // bnd slot `cur` is free once the outflow sums of two steps ago have read it
   FK(cudaStreamWaitEvent(s0.stream, f->ev_out[cur], 0));
-  fill_all_public(h, &SlabState::U);
+  const bool mat = h->mc.n > 0;   // (materials run on the two-pass kernels only)
+  if (mat)
+    fill_state_public(h, &SlabState::U, &SlabState::P);
+  else
+    fill_all_public(h, &SlabState::U);
   double* bnd = f->bnd + (size_t)cur * bnd_words(h);
   if (h->nccl) FK(cudaMemsetAsync(bnd, 0, bnd_words(h) * sizeof(double), s0.stream));
   if (k0) FK(cudaEventRecord(k0, s0.stream));
-  const bool mat = h->mc.n > 0;
   if (use_twopass(h)) {
     // two passes: predictor U^n -> U*, F^n; ghosts / halos of U*; corrector
-    if (mat) fill_partials_public(h, &SlabState::P);
     for (int pass = 0; pass < 2; ++pass) {
       if (pass == 1) {
-        fill_all_public(h, &SlabState::Us);
-        if (mat) fill_partials_public(h, &SlabState::Ps);
+        if (mat)
+          fill_state_public(h, &SlabState::Us, &SlabState::Ps);
+        else
+          fill_all_public(h, &SlabState::Us);
       }
       for (auto& s : h->slabs) {
         PassArgs a;

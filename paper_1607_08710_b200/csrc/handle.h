@@ -80,6 +80,8 @@ namespace lfb {
 // api.cu services used by the fused path
 void fill_all_public(lf_handle* h, double* SlabState::*buf);
 void fill_partials_public(lf_handle* h, double* SlabState::*buf);
+// conserved field and partial densities together (one fill launch per slab)
+void fill_state_public(lf_handle* h, double* SlabState::*ubuf, double* SlabState::*pbuf);
 void alloc_staged_public(lf_handle* h);
 Scalars rate_of_current(lf_handle* h);
 int staged_heun_public(lf_handle* h, double cfl, double time, double limit, int64_t step,

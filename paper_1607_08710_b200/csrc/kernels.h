@@ -58,8 +58,10 @@ void reset_scalars(Scalars* s, cudaStream_t st);
 void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_t st,
                    int ncomp = 4, int odd_x = 1);
 // x and y sides in one launch; needs nx >= NG and (2D) ny >= NG
+// f2 (may be NULL): ncomp2 more components of even parity in the same launch
 void launch_fill_xy(const Field& f, const Layout& L, const int bc[4], const Slab& sl, bool dim2,
-                    cudaStream_t st, int ncomp, int odd_x, int odd_y);
+                    cudaStream_t st, int ncomp, int odd_x, int odd_y, const Field* f2 = nullptr,
+                    int ncomp2 = 0);
 void launch_fill_y_only(const Field& f, const Layout& L, const int bc[4], const Slab& sl,
                         cudaStream_t st, int ncomp = 4, int odd_y = 2);
 
