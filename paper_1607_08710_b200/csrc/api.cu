@@ -25,6 +25,7 @@
 #include "handle.h"
 #include "host_util.h"
 #include "nccl_comm.h"
+#include "trace.h"
 #include "twopass.h"
 
 using namespace lfb;
@@ -596,6 +597,7 @@ double material_min_p(lf_handle* h) {
 
 int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t step,
                 double* outflow, lf_step_out* out) {
+  LF_TRACE("stage-wise heun step");
   const bool mat = h->mc.n > 0;
   if (mat && !h->partials_ready)
     return set_err(h, LF_ERR_CONFIG, "multimaterial step needs material storage");
@@ -836,6 +838,7 @@ int lf_local_rows(lf_handle* h, int* row0, int* nrows) {
 }
 
 int lf_upload(lf_handle* h, double* const field[4], int64_t ld) {
+  LF_TRACE("lf_upload");
   return guarded(h, [&] {
     if (!field || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad field or ld");
     const int gy = h->dim2 ? 2 : 0;
@@ -907,6 +910,7 @@ int lf_set_materials(lf_handle* h, int n, const double* gammas) {
 }
 
 int lf_upload_partials(lf_handle* h, double* const* partials, int64_t ld) {
+  LF_TRACE("lf_upload_partials");
   return guarded(h, [&] {
     if (!h->mc.n) return set_err(h, LF_ERR_CONFIG, "no material set (lf_set_materials)");
     if (!partials || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad partials or ld");
@@ -928,6 +932,7 @@ int lf_upload_partials(lf_handle* h, double* const* partials, int64_t ld) {
 }
 
 int lf_download_partials(lf_handle* h, double* const* partials, int64_t ld) {
+  LF_TRACE("lf_download_partials");
   return guarded(h, [&] {
     if (!h->mc.n) return set_err(h, LF_ERR_CONFIG, "no material set (lf_set_materials)");
     if (!partials || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad partials or ld");
@@ -961,6 +966,7 @@ inline void put_g17(std::string& out, double v) {
 
 int lf_write_field_csv(lf_handle* h, const char* path, uint64_t digest, double time,
                        int threads) {
+  LF_TRACE("lf_write_field_csv");
   return guarded(h, [&] {
     if (!path) return set_err(h, LF_ERR_ARGUMENT, "path is null");
     if (h->mc.n && !h->partials_ready)
@@ -1077,6 +1083,7 @@ int lf_write_field_csv(lf_handle* h, const char* path, uint64_t digest, double t
 }
 
 int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghosts) {
+  LF_TRACE("lf_download");
   return guarded(h, [&] {
     if (!field || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad field or ld");
     const int gy = h->dim2 ? 2 : 0;
@@ -1097,6 +1104,7 @@ int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghost
 }
 
 int lf_download_ghosted(lf_handle* h, double* const field[4], int64_t ld) {
+  LF_TRACE("lf_download_ghosted");
   return guarded(h, [&] {
     if (!field || ld < h->d.nx + 4) return set_err(h, LF_ERR_ARGUMENT, "bad field or ld");
     fill_all(h, &SlabState::U);
@@ -1121,6 +1129,7 @@ int lf_download_ghosted(lf_handle* h, double* const field[4], int64_t ld) {
 }
 
 int lf_init_fourier(lf_handle* h, uint64_t seed) {
+  LF_TRACE("lf_init_fourier");
   return guarded(h, [&] {
     if (!h->dim2) return set_err(h, LF_ERR_CONFIG, "the Fourier initial state is 2D");
     std::vector<double> tx, ty, amp;
@@ -1173,6 +1182,7 @@ int lf_init_fourier(lf_handle* h, uint64_t seed) {
 }
 
 int lf_init_regions(lf_handle* h, const double* regions, int nreg) {
+  LF_TRACE("lf_init_regions");
   return guarded(h, [&] {
     if (!regions || nreg < 1) return set_err(h, LF_ERR_ARGUMENT, "no regions");
     for (int r = 0; r < nreg; ++r) {
@@ -1231,6 +1241,7 @@ int lf_init_regions(lf_handle* h, const double* regions, int nreg) {
 }
 
 int lf_compute_dt(lf_handle* h, double cfl, double time, double limit_time, double* dt) {
+  LF_TRACE("lf_compute_dt");
   return guarded(h, [&] {
     launch_rate_all(h, &SlabState::U);
     return finish_dt(h, combined_scalars(h, 0), cfl, time, limit_time, dt);
@@ -1240,6 +1251,7 @@ int lf_compute_dt(lf_handle* h, double cfl, double time, double limit_time, doub
 int lf_edge_flux(int64_t n, const double* w_minus, const double* w_plus, const double* normals,
                  const double* gamma_minus, const double* gamma_plus, double* flux,
                  double* contact, int device, lf_error* err) {
+  LF_TRACE("lf_edge_flux");
   if (err) clear_err(err);
   if (n < 0 || (n > 0 && (!w_minus || !w_plus || !normals || !gamma_minus || !gamma_plus || !flux)))
     return LF_ERR_ARGUMENT;
@@ -1292,6 +1304,7 @@ int lf_edge_flux(int64_t n, const double* w_minus, const double* w_plus, const d
 }
 
 int lf_interior_totals(lf_handle* h, double tot[4]) {
+  LF_TRACE("lf_interior_totals");
   return guarded(h, [&] {
     if (!tot) return set_err(h, LF_ERR_ARGUMENT, "null totals");
     // slabs in row order; each continues the running sums of the one below
@@ -1336,6 +1349,7 @@ int lf_max_rate(lf_handle* h, double* rate) {
 }
 
 int lf_euler_stage(lf_handle* h, double dt, int64_t step) {
+  LF_TRACE("lf_euler_stage");
   return guarded(h, [&] {
     for (auto& s : h->slabs) alloc_staged(s);
     staged_stage(h, &SlabState::U, &SlabState::U, &SlabState::Us, 0, false, dt, 1);
@@ -1351,6 +1365,7 @@ int lf_euler_stage(lf_handle* h, double dt, int64_t step) {
 
 int lf_heun_step(lf_handle* h, double cfl, double time, double limit_time, int64_t step,
                  double* boundary_outflow, lf_step_out* out) {
+  LF_TRACE("lf_heun_step");
   return guarded(h, [&] {
     if (h->d.time_order >= 2 && use_fused(h))
       return fused_heun(h, cfl, time, limit_time, step, boundary_outflow, out);
@@ -1360,6 +1375,7 @@ int lf_heun_step(lf_handle* h, double cfl, double time, double limit_time, int64
 
 int lf_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* time,
                int64_t* step, double* outflow, lf_step_out* per_step, int* taken) {
+  LF_TRACE("lf_advance");
   return guarded(h, [&] {
     if (h->d.time_order >= 2 && use_fused(h))
       return fused_advance(h, nsteps, cfl, t_final, time, step, outflow, per_step, taken);
@@ -1402,6 +1418,7 @@ int lf_set_path(lf_handle* h, int path) {
 
 int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
                   int* kernel_launches) {
+  LF_TRACE("lf_time_steps");
   return guarded(h, [&] {
     if (!use_fused(h) || h->d.time_order < 2)
       return set_err(h, LF_ERR_ARGUMENT, "lf_time_steps times the fused Heun path");

@@ -19,6 +19,7 @@
 #include "fused_common.cuh"
 #include "twopass.h"
 #include "nccl_comm.h"
+#include "trace.h"
 
 namespace lfb {
 
@@ -203,6 +204,7 @@ static void seed_ctl(lf_handle* h, double time) {
 // Enqueue one fused step on every slab.
 static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit, double t_final,
                          cudaEvent_t k0, cudaEvent_t k1) {
+  LF_TRACE("enqueue heun step");
   FusedState* f = fstate(h);
   const int cur = f->cur, nxt = cur ^ 1;
   SlabState& s0 = h->slabs[0];
@@ -330,6 +332,7 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
 // in f->rec_host) and the index of a failed step (-1 if none).
 static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_final, double time,
                      const double* outflow_in, int* failed_at, bool timing, double* kernel_ms) {
+  LF_TRACE("step batch");
   FusedState* f = fstate(h);
   SlabState& s0 = h->slabs[0];
   seed_ctl(h, time);
