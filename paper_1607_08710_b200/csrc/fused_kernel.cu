@@ -30,6 +30,7 @@
 #include "../../include/lagflux_b200.h"
 #include "fastmath.cuh"
 #include "fused_common.cuh"
+#include "pdl.cuh"
 #include "kernels.h"
 #include "face_fast.cuh"
 #include "lagflux_device.cuh"
@@ -501,6 +502,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 __global__ void k_finalize(const StepCtl* __restrict__ ctl, StepAcc* acc, StepCtl* nxt,
                            StepRec* rec, double* outflow, bool outflow_zero, double dx, double dy,
                            double cfl, double limit, double t_final) {
+  pdl_wait();
   const StepCtl c = *ctl;
   const bool skip = c.done != 0;
   double dt = 0.0;
@@ -654,8 +656,8 @@ void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* re
                      double* outflow, bool outflow_zero, double dx, double dy, double cfl,
                      double limit, double t_final, cudaStream_t st) {
   count_launch();
-  k_finalize<<<1, 1, 0, st>>>(ctl, acc, nxt, rec, outflow, outflow_zero, dx, dy, cfl, limit,
-                             t_final);
+  launch_chain(k_finalize, dim3(1), dim3(1), 0, st, ctl, acc, nxt, rec, outflow, outflow_zero, dx,
+               dy, cfl, limit, t_final);
 }
 
 void launch_outflow(const StepRec* rec, const double* bnd, double* outflow, int nx, int nyg,

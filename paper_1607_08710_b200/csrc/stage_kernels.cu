@@ -12,6 +12,7 @@
 #include <climits>
 
 #include "kernels.h"
+#include "pdl.cuh"
 #include "reduce.cuh"
 
 namespace lfb {
@@ -101,6 +102,7 @@ __global__ void k_fill_y(Field f, int nx, int ny, int bc_lo, int bc_hi, int do_l
 // even parity), so a multimaterial state fills in one launch.
 __global__ void k_fill_xy(Field f, Field f2, int n1, int nx, int ny, int bx_lo, int bx_hi,
                           int by_lo, int by_hi, int do_lo, int do_hi, int odd_x, int odd_y) {
+  pdl_wait();
   const int c = blockIdx.y;
   const double sx = c == odd_x ? -1.0 : 1.0, sy = c == odd_y ? -1.0 : 1.0;
   double* base = c < n1 ? f.comp(c) : f2.comp(c - n1);
@@ -430,9 +432,10 @@ void launch_fill_x(const Field& f, const Layout& L, const int bc[4], cudaStream_
 void launch_fill_xy(const Field& f, const Layout& L, const int bc[4], const Slab& sl, bool dim2,
                     cudaStream_t st, int ncomp, int odd_x, int odd_y, const Field* f2, int ncomp2) {
   const int threads = 2 * L.ny + 2 * (L.nx + 2 * NG);
-  count_launch(), k_fill_xy<<<dim3(cdiv(threads, 128), ncomp + (f2 ? ncomp2 : 0)), 128, 0, st>>>(
-      f, f2 ? *f2 : f, ncomp, L.nx, L.ny, bc[0], bc[1], bc[2], bc[3], dim2 && sl.fill_lo,
-      dim2 && sl.fill_hi, odd_x, odd_y);
+  count_launch();
+  launch_chain(k_fill_xy, dim3(cdiv(threads, 128), ncomp + (f2 ? ncomp2 : 0)), dim3(128), 0, st,
+               f, f2 ? *f2 : f, ncomp, L.nx, L.ny, bc[0], bc[1], bc[2], bc[3],
+               (int)(dim2 && sl.fill_lo), (int)(dim2 && sl.fill_hi), odd_x, odd_y);
 }
 
 void launch_fill_y_only(const Field& f, const Layout& L, const int bc[4], const Slab& sl,

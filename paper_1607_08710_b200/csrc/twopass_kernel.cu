@@ -28,6 +28,7 @@
 #include "fused_common.cuh"
 #include "kernels.h"
 #include "twopass.h"
+#include "pdl.cuh"
 
 namespace lfb {
 
@@ -93,6 +94,7 @@ __device__ __forceinline__ void tp_cp_async8(double* sdst, const double* gsrc, b
 // EXACT = true, which takes the exact u* quotient in such warps.
 template <bool CORR, bool MUSCL, bool EXACT>
 __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a) {
+  pdl_wait();  // the previous kernel of the step chain (pdl.cuh)
   const StepCtl ctl = *a.ctl;
   if (ctl.done) return;
   if (ctl.dtfail) {
@@ -444,14 +446,14 @@ template <bool EXACT>
 static void launch_k(const PassArgs& a, bool corr, bool muscl, unsigned blocks, cudaStream_t st) {
   if (corr) {
     if (muscl)
-      k_pass<true, true, EXACT><<<blocks, TP_THREADS, 0, st>>>(a);
+      launch_chain(k_pass<true, true, EXACT>, dim3(blocks), dim3(TP_THREADS), 0, st, a);
     else
-      k_pass<true, false, EXACT><<<blocks, TP_THREADS, 0, st>>>(a);
+      launch_chain(k_pass<true, false, EXACT>, dim3(blocks), dim3(TP_THREADS), 0, st, a);
   } else {
     if (muscl)
-      k_pass<false, true, EXACT><<<blocks, TP_THREADS, 0, st>>>(a);
+      launch_chain(k_pass<false, true, EXACT>, dim3(blocks), dim3(TP_THREADS), 0, st, a);
     else
-      k_pass<false, false, EXACT><<<blocks, TP_THREADS, 0, st>>>(a);
+      launch_chain(k_pass<false, false, EXACT>, dim3(blocks), dim3(TP_THREADS), 0, st, a);
   }
 }
 

@@ -32,6 +32,7 @@
 #include "fused_common.cuh"
 #include "kernels.h"
 #include "twopass.h"
+#include "pdl.cuh"
 
 #ifdef LF_MAT_DEBUG
 #define MFAIL(code)                                                                    \
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
   MatR mr;
 #pragma unroll
   for (int k = 0; k < K; ++k) mr.rg[k] = recip_of(mk.gamma[k] - 1.0);
+  pdl_wait();  // the previous kernel of the step chain (pdl.cuh)
   const StepCtl ctl = *a.ctl;
   if (ctl.done) return;
   if (ctl.dtfail) {
@@ -609,10 +611,10 @@ template <bool CORR, bool MUSCL>
 void launch_k(const PassArgs& a, const MatPassArgs& m, const MatK& mk, unsigned blocks,
               cudaStream_t st) {
   switch (mk.n) {
-    case 1: k_pass_mat<CORR, MUSCL, 1><<<blocks, TP_THREADS, 0, st>>>(a, m, mk); break;
-    case 2: k_pass_mat<CORR, MUSCL, 2><<<blocks, TP_THREADS, 0, st>>>(a, m, mk); break;
-    case 3: k_pass_mat<CORR, MUSCL, 3><<<blocks, TP_THREADS, 0, st>>>(a, m, mk); break;
-    default: k_pass_mat<CORR, MUSCL, 4><<<blocks, TP_THREADS, 0, st>>>(a, m, mk); break;
+    case 1: launch_chain(k_pass_mat<CORR, MUSCL, 1>, dim3(blocks), dim3(TP_THREADS), 0, st, a, m, mk); break;
+    case 2: launch_chain(k_pass_mat<CORR, MUSCL, 2>, dim3(blocks), dim3(TP_THREADS), 0, st, a, m, mk); break;
+    case 3: launch_chain(k_pass_mat<CORR, MUSCL, 3>, dim3(blocks), dim3(TP_THREADS), 0, st, a, m, mk); break;
+    default: launch_chain(k_pass_mat<CORR, MUSCL, 4>, dim3(blocks), dim3(TP_THREADS), 0, st, a, m, mk); break;
   }
 }
 
