@@ -6,6 +6,7 @@
 
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -38,10 +39,14 @@ struct NcclFail : std::runtime_error {
 
 bool load_api() {
   if (g_api.lib) return true;
+  // LF_NCCL_LIB: another implementation of the same entry points (the tests'
+  // thread-rank stand-in, tests/fake_nccl)
+  const char* over = std::getenv("LF_NCCL_LIB");
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  if (over && over[0]) g_api.lib = dlopen(over, RTLD_NOW | RTLD_LOCAL);
   for (const char* n : names) {
-    g_api.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
     if (g_api.lib) break;
+    g_api.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
   }
   if (!g_api.lib) return false;
 #define SYM(field, name) g_api.field = reinterpret_cast<decltype(g_api.field)>(dlsym(g_api.lib, name))
