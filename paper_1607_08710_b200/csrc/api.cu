@@ -1367,7 +1367,7 @@ int lf_heun_step(lf_handle* h, double cfl, double time, double limit_time, int64
                  double* boundary_outflow, lf_step_out* out) {
   LF_TRACE("lf_heun_step");
   return guarded(h, [&] {
-    if (h->d.time_order >= 2 && use_fused(h))
+    if (use_fused(h))
       return fused_heun(h, cfl, time, limit_time, step, boundary_outflow, out);
     return staged_heun(h, cfl, time, limit_time, step, boundary_outflow, out);
   });
@@ -1377,7 +1377,7 @@ int lf_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* tim
                int64_t* step, double* outflow, lf_step_out* per_step, int* taken) {
   LF_TRACE("lf_advance");
   return guarded(h, [&] {
-    if (h->d.time_order >= 2 && use_fused(h))
+    if (use_fused(h))
       return fused_advance(h, nsteps, cfl, t_final, time, step, outflow, per_step, taken);
     // stage-wise fallback keeps the run.cpp loop on the host
     int k = 0;
@@ -1420,8 +1420,8 @@ int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, doubl
                   int* kernel_launches) {
   LF_TRACE("lf_time_steps");
   return guarded(h, [&] {
-    if (!use_fused(h) || h->d.time_order < 2)
-      return set_err(h, LF_ERR_ARGUMENT, "lf_time_steps times the fused Heun path");
+    if (!use_fused(h))
+      return set_err(h, LF_ERR_ARGUMENT, "lf_time_steps times the fused / two-pass path");
     return fused_time_steps(h, nsteps, cfl, kernel_ms, step_ms, kernel_launches);
   });
 }

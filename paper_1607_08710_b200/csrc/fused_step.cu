@@ -66,8 +66,12 @@ static FusedState* fstate(lf_handle* h) { return reinterpret_cast<FusedState*>(h
 
 static size_t bnd_words(lf_handle* h) { return 8 * (size_t)h->d.ny + 8 * (size_t)h->d.nx; }
 
+static bool use_twopass(lf_handle* h);
+
 bool fused_supported(lf_handle* h) {
-  if (!h->dim2 || h->d.time_order < 2) return false;
+  if (!h->dim2) return false;
+  // time_order 1 runs on the two-pass kernels only (the fused step is Heun)
+  if (h->d.time_order < 2 && !use_twopass(h)) return false;
   if (h->d.nx < 4) return false;
   for (auto& s : h->slabs) {
     if (s.L.ny < 4) return false;
@@ -219,9 +223,12 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   if (h->nccl) FK(cudaMemsetAsync(bnd, 0, bnd_words(h) * sizeof(double), s0.stream));
   if (k0) FK(cudaEventRecord(k0, s0.stream));
   if (use_twopass(h)) {
-    // two passes: predictor U^n -> U*, F^n; ghosts / halos of U*; corrector
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) {
+    // two passes: predictor U^n -> U*, F^n; ghosts / halos of U*; corrector.
+    // time_order 1: one pass, the corrector kernels as the single forward-Euler
+    // stage (input and base U^n, no Heun average; solver.cpp:510-514)
+    const bool heun = h->d.time_order >= 2;
+    for (int pass = heun ? 0 : 1; pass < 2; ++pass) {
+      if (pass == 1 && heun) {
         if (mat)
           fill_state_public(h, &SlabState::Us, &SlabState::Ps);
         else
@@ -229,7 +236,7 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
       }
       for (auto& s : h->slabs) {
         PassArgs a;
-        a.x = (pass == 0 ? s.U : s.Us) + s.L.origin();
+        a.x = (pass == 0 || !heun ? s.U : s.Us) + s.L.origin();
         a.base = s.U + s.L.origin();
         a.out = (pass == 0 ? s.Us : s.U2) + s.L.origin();
         a.fx = s.FX[0];
@@ -256,9 +263,10 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
         a.ctl = f->ctl + cur;
         a.acc = f->acc + cur;
         a.bnd = bnd;
+        a.heun = heun ? 1 : 0;
         if (mat) {
           MatPassArgs m;
-          m.px = (pass == 0 ? s.P : s.Ps) + s.L.origin();
+          m.px = (pass == 0 || !heun ? s.P : s.Ps) + s.L.origin();
           m.pbase = s.P + s.L.origin();
           m.pout = (pass == 0 ? s.Ps : s.P2) + s.L.origin();
           m.mfx = s.MFX;

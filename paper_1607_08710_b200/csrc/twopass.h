@@ -31,6 +31,9 @@ struct PassArgs {
   const StepCtl* ctl;
   StepAcc* acc;
   double* bnd;          // corrector: boundary faces [left 4*nyg | right 4*nyg | bottom 4*nx | top 4*nx]
+  int heun;             // corrector: 1 the Heun average with the stage-a faces; 0 the single
+                        // forward-Euler stage of time_order 1 (x = base = U^n, F alone,
+                        // solver.cpp:510-514)
 };
 
 // Multimaterial operands of the two passes (csrc/twopass_mat_kernel.cu):

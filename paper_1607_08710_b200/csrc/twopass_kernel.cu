@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
 #pragma unroll
     for (int q = 0; q < 4; ++q) tp_cp_async8(&st[buf][q][lane], pb ? a.base + q * a.fstride + orow : a.base, pb);
     if (CORR) {
-      const bool px = pb && c >= 0 && c <= a.nx, py = itn >= 3 && col_interior;
+      const bool px = a.heun && pb && c >= 0 && c <= a.nx, py = a.heun && itn >= 3 && col_interior;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         tp_cp_async8(&st[buf][4 + q][lane], px ? a.fx + q * a.fx_stride + orow : a.fx, px);
@@ -193,12 +193,12 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     if (it >= 4 && col_in_mem) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) base[q] = __ldg(a.base + q * a.fstride + o_row);
-      if (CORR && c >= 0 && c <= a.nx) {
+      if (CORR && a.heun && c >= 0 && c <= a.nx) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) fnx[q] = __ldg(a.fx + q * a.fx_stride + o_row);
       }
     }
-    if (CORR && it >= 3 && col_interior) {
+    if (CORR && a.heun && it >= 3 && col_interior) {
       // face (row | row+1); at it == 3 this is the chunk's first face (y0-1 | y0)
 #pragma unroll
       for (int q = 0; q < 4; ++q) fny[q] = __ldg(a.fy + q * a.fy_stride + (o_row + P));
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
       fail = 1;
     if (need_y && !traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && r - 1 >= 0 && r - 1 <= a.ny)
       fail = 1;
-    if (CORR) {
+    if (CORR && a.heun) {
       // Heun average 0.5 (F^n + F*) per face (solver.cpp:284-289)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {

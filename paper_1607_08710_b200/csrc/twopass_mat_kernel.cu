@@ -262,8 +262,8 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
     for (int k = 0; k < K; ++k)
       cp_async8(&st[buf][4 + k][lane], pu ? m.pbase + k * a.fstride + orow : m.pbase, pu);
     if (CORR) {
-      const bool px = itn >= 4 && col_in_mem && c >= 0 && c <= a.nx;
-      const bool py = itn >= 3 && col_interior;
+      const bool px = a.heun && itn >= 4 && col_in_mem && c >= 0 && c <= a.nx;
+      const bool py = a.heun && itn >= 3 && col_interior;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         cp_async8(&st[buf][4 + K + q][lane], px ? a.fx + q * a.fx_stride + orow : a.fx, px);
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
 #pragma unroll
       for (int k = 0; k < K; ++k) pbs[k] = __ldg(m.pbase + k * a.fstride + o_row);
     }
-    if (CORR) {
+    if (CORR && a.heun) {
       if (it >= 4 && col_in_mem && c >= 0 && c <= a.nx) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) fnx[q] = __ldg(a.fx + q * a.fx_stride + o_row);
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
     }
 #endif
     double fxa[4], fya[4];
-    if (CORR) {
+    if (CORR && a.heun) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         fxa[q] = 0.5 * (fnx[q] + fx[q]);

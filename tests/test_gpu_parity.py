@@ -355,3 +355,28 @@ def test_out_of_box_states_rerun_exactly(cuda, which, path):
     inbox = CS.quadrant(48, 4)
     _, n_in = run(inbox, CS.initial_field(inbox))
     assert n_out > n_in
+
+
+@pytest.mark.parametrize("spatial_order", [1, 2])
+@pytest.mark.parametrize("cfg", ["sod", "quadrant", "smooth"])
+def test_time_order_1_on_the_two_pass_kernels(cuda, cfg, spatial_order):
+    """time_order 1 (solver.cpp:510-514: one forward-Euler stage, F alone in the
+    update and the outflow) runs as one corrector-kernel pass -- not stage-wise --
+    and equals the oracle bit for bit."""
+    import dataclasses
+    base = {"sod": CS.sod(96, 8), "quadrant": CS.quadrant(80, 30),
+            "smooth": CS.smooth(64, 30, ny=40, y_extent=40 / 64)}[cfg]
+    case = dataclasses.replace(base, params=G.SchemeParams(spatial_order=spatial_order, time_order=1))
+    ref, rdiag = run_oracle(case, 30)
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path="twopass")
+    st = G.SolverState(field=CS.initial_field(case))
+    s.advance(st, G.TimeControls(case.cfl, case.t_final), 3)
+    n0 = s.launch_count()
+    s.advance(st, G.TimeControls(case.cfl, case.t_final), 27)
+    per_step = (s.launch_count() - n0) / 27
+    s.sync_to_host(st)
+    s.close()
+    assert_fields_equal(case.grid.interior(st.field), case.grid.interior(ref.field), cfg)
+    assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4])
+    assert list(st.boundary_outflow) == list(ref.boundary_outflow)
+    assert per_step <= 5, per_step     # fill, pass, finalize (+ outflow sums): not stage-wise
