@@ -80,3 +80,53 @@ def test_free_compute_dt_equals_reference(cuda):
         r = O.RefSolver(case.grid, G.BoundaryCondition(), 1.4)
         r.set_state(f)
         assert S.compute_dt(case.grid, f, 1.4, ctl, t, limit) == r.compute_dt(0.45, t, limit)
+
+
+def test_known_answers_on_the_device(cuda):
+    """test_solver.cpp:114-137 and test_riemann.cpp:19-43, through lf_edge_flux."""
+    wm = np.array([[1.0, 2.0, 0.0, 1.0], [1.0, 1.0, 0.0, 1.0], [1.0, 1.0, 0.0, 1.0],
+                   [1.0, 0.0, 0.0, 1.0], [0.7, 1.3, 0.0, 2.1]])
+    wp = np.array([[1.0, 2.0, 0.0, 1.0], [1.0, -1.0, 0.0, 1.0], [0.5, 0.8, 0.0, 0.9],
+                   [0.125, 0.0, 0.0, 0.1], [0.7, 1.3, 0.0, 2.1]])
+    f, c = S.edge_flux(wm, wp, [1.0, 0.0], 1.4)
+    assert f[0, 0] == pytest.approx(2.0, rel=1e-14) and f[0, 1] == pytest.approx(5.0, rel=1e-14)
+    assert f[0, 2] == 0.0 and f[0, 3] == pytest.approx(11.0, rel=1e-14)
+    assert f[1, 0] == 0.0 and f[1, 3] == 0.0 and f[1, 1] == pytest.approx(1.0 + math.sqrt(1.4), rel=1e-14)
+    assert c[2, 1] > 0.0 and f[2, 0] == 1.0 * c[2, 1]
+    assert c[3, 0] == pytest.approx(0.2, rel=1e-14) and c[3, 1] == pytest.approx(0.8 / math.sqrt(1.4), rel=1e-14)
+    assert c[4, 0] == pytest.approx(2.1, rel=1e-15) and c[4, 1] == pytest.approx(1.3, rel=1e-15)
+
+
+def _state_gen(n, seed):
+    """testing::StateGen (test_util.hpp:12-36): log-uniform rho in [0.1, 10], p in
+    [0.01, 10], u, v uniform in [-5, 5]."""
+    rng = np.random.default_rng(seed)
+    rho = np.exp(rng.uniform(np.log(0.1), np.log(10.0), n))
+    p = np.exp(rng.uniform(np.log(0.01), np.log(10.0), n))
+    return np.stack([rho, rng.uniform(-5, 5, n), rng.uniform(-5, 5, n), p], axis=1)
+
+
+def test_flux_consistency_and_symmetries_on_the_device(cuda):
+    """test_solver.cpp:139-159 (consistency: equal traces give the exact Euler flux
+    F(U).n, 4 normals, 1e-14) and test_riemann.cpp:45-67 (mirror symmetry of the
+    contact solution), 1000 states each, on lf_edge_flux."""
+    n = 1000
+    w = _state_gen(n, 0xF1)
+    g = 1.4
+    for nrm in ((1.0, 0.0), (0.0, 1.0), (-1.0, 0.0), (0.6, 0.8)):
+        f, c = S.edge_flux(w, w, nrm, g)
+        rho, u, v, p = w.T
+        un = u * nrm[0] + v * nrm[1]
+        E = p / (g - 1.0) + 0.5 * rho * (u * u + v * v)
+        exact = np.stack([rho * un, rho * u * un + p * nrm[0], rho * v * un + p * nrm[1], (E + p) * un], axis=1)
+        scale = 1.0 + np.abs(exact)
+        assert np.all(np.abs(f - exact) <= 1e-14 * scale * 8), nrm
+        assert np.allclose(c[:, 0], p, rtol=1e-14) and np.allclose(c[:, 1], un, rtol=1e-14, atol=1e-14)
+    # mirror: swapping the sides and flipping the normal velocity mirrors (p*, u*)
+    wl, wr = _state_gen(n, 0x411), _state_gen(n, 0x412)
+    ml, mr = wr.copy(), wl.copy()
+    ml[:, 1] *= -1.0
+    mr[:, 1] *= -1.0
+    _, c1 = S.edge_flux(wl, wr, (1.0, 0.0), g)
+    _, c2 = S.edge_flux(ml, mr, (1.0, 0.0), g)
+    assert np.allclose(c1[:, 0], c2[:, 0], rtol=1e-13) and np.allclose(c1[:, 1], -c2[:, 1], rtol=1e-13, atol=1e-13)
