@@ -55,7 +55,6 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 
 // Build-time tuning knobs (tools/variants.py sweeps them):
 //   LF_TP_MINBLOCKS  resident blocks per SM requested from ptxas (register budget)
-//   LF_TP_PAIR       1: x- and y-face Riemann solves in one straight line
 //   LF_TP_LATELOAD   1: load the update operands after the face solves
 //   LF_TP_UNROLL     2: unroll the row loop twice (state rotation by renaming)
 //   LF_TP_ASYNC      1: update operands staged one row ahead in shared memory
@@ -63,9 +62,6 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 //                    12 warps/SM), +20-32 % in the 8-warp material kernel
 #ifndef LF_TP_MINBLOCKS
 #define LF_TP_MINBLOCKS 3
-#endif
-#ifndef LF_TP_PAIR
-#define LF_TP_PAIR 1
 #endif
 #ifndef LF_TP_LATELOAD
 #define LF_TP_LATELOAD 0
