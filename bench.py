@@ -65,6 +65,25 @@ def ncu_traffic():
         return None
 
 
+def ncu_compute_bound():
+    """The pass kernels' real bound from the committed ncu --set full capture
+    (profiles/r01_ncu_16k.json): fp64-pipe and issue utilisation per kernel."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_16k.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        ks = d["twopass"]["kernels"]
+        return {"bound": "fp64 pipe / issue latency (not HBM)",
+                "kernels": {k["kernel"].split("(")[0].split("::")[-1]:
+                            {"fp64_pipe_pct": round(k["fp64_pipe_pct"], 1),
+                             "issue_active_pct": round(k["issue_active_pct"], 1),
+                             "top_stall": max(k["top_stalls_pct"], key=k["top_stalls_pct"].get)}
+                            for k in ks},
+                "source": "profiles/r01_ncu_16k.json (ncu --set full, 16384^2)"}
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -255,7 +274,8 @@ def run_ours(args):
                 "kernel_share_of_step": kernel_ms / loop_ms if loop_ms > 0 else None,
                 "frac_of_nominal_8TBs": achieved / 8000.0,
                 "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                "traffic_source": traffic.get("source") if traffic else None}
+                "traffic_source": traffic.get("source") if traffic else None,
+                "compute": ncu_compute_bound()}
 
     # e2e through the public API with host buffers (rank-local slab)
     e2e = None
