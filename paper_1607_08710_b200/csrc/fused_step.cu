@@ -1,11 +1,15 @@
-// fused_step.cu -- host driver of the fused Heun step (kernels in fused_kernel.cu).
+// fused_step.cu -- host driver of the device-resident Heun step: the two-pass
+// kernels (twopass_kernel.cu / twopass_mat_kernel.cu, the default) or the
+// one-kernel step (fused_kernel.cu).
 //
-// Per step, on the slab streams: ghost fill of U^n (x sides, halo rows, y sides)
-// -> k_fused_step (U^n -> U^{n+1}, diagnostics and the next CFL rate) ->
-// [NCCL max of the step accumulators and sum of the boundary faces across
-// ranks] -> k_finalize (dt, time, outflow, next step's control record).  dt and
-// time stay on the device, so lf_advance enqueues whole batches of steps
-// without a host round trip; records come back once per batch.
+// Per step, on the slab stream: ghost fill of U^n (one launch, then halo rows)
+// -> predictor -> fill of U* -> corrector (or k_fused_step) -> [NCCL max of the
+// step accumulators and sum of the boundary faces across ranks] -> k_finalize
+// (dt, time, diagnostics, next step's control record); the chain is launched
+// with programmatic dependent launch (pdl.cuh).  The ordered boundary-outflow
+// sums (k_outflow) run on a low-priority side stream.  dt and time stay on the
+// device, so lf_advance enqueues whole batches of steps without a host round
+// trip; records come back once per batch.
 #include <cuda_runtime.h>
 
 #include <algorithm>
