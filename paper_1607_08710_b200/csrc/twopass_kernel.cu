@@ -77,6 +77,9 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 #ifndef LF_TP_ASYNC
 #define LF_TP_ASYNC 0
 #endif
+#ifndef LF_TP_EDGE1
+#define LF_TP_EDGE1 1
+#endif
 __device__ __forceinline__ void tp_cp_async8(double* sdst, const double* gsrc, bool pred) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gsrc),
@@ -128,6 +131,10 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
   // the domain's last face nx by whichever lane holds column nx
   const bool store_fx = (lane >= 2 && lane <= LANES - 3 && c <= a.nx) || (lane == LANES - 2 && c == a.nx);
   const int nit = (y1 - y0) + 4;
+#if LF_TP_EDGE1
+  // this warp's strip holds the domain's first or last column
+  const bool x_edge_warp = x0 - 2 <= 0 || x0 - 2 + LANES > a.nx - 1;
+#endif
 
   unsigned fail = const_in_box(a.gamma, a.gm1) ? 0u : 1u;
   unsigned need_exact = 0;
@@ -339,8 +346,12 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
           } else {
             dtfail = 1;
           }
-          // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
+          // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432);
+          // one warp-uniform test skips all four in the interior of the domain
           const int jg = row + a.y0g;
+#if LF_TP_EDGE1
+          if (x_edge_warp || jg == 0 || jg == a.nyg - 1) {
+#endif
           if (c == 0)
             for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = fx[q];
           if (c == a.nx - 1)
@@ -350,6 +361,9 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
           if (jg == a.nyg - 1)
             for (int q = 0; q < 4; ++q)
               a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fy[q];
+#if LF_TP_EDGE1
+          }
+#endif
         }
       }
     } else if (!CORR && it == 3 && y0 == 0 && upd) {
