@@ -241,6 +241,8 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
   const bool upd = lane >= 2 && lane <= LANES - 3 && col_interior;
   const bool store_fx = (lane >= 2 && lane <= LANES - 3 && c <= a.nx) || (lane == LANES - 2 && c == a.nx);
   const int nit = (y1 - y0) + 4;
+  // this warp's strip holds the domain's first or last column
+  const bool x_edge_warp = x0 - 2 <= 0 || x0 - 2 + LANES > a.nx - 1;
 
   unsigned fail = 0;
   unsigned long long rate_key = 0ull, nmin_r = NINF_KEY, nmin_e = NINF_KEY, nmin_p = NINF_KEY;
@@ -547,17 +549,20 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
               rate_key = b > rate_key ? b : rate_key;
             }
           }
-          // boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
+          // boundary faces for accumulate_boundary_outflow (solver.cpp:406-432);
+          // one warp-uniform test skips all four in the interior of the domain
           const int jg = row + a.y0g;
-          if (c == 0)
-            for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = fxa[q];
-          if (c == a.nx - 1)
-            for (int q = 0; q < 4; ++q) a.bnd[4 * (int64_t)a.nyg + (int64_t)q * a.nyg + jg] = fxr[q];
-          if (jg == 0)
-            for (int q = 0; q < 4; ++q) a.bnd[8 * (int64_t)a.nyg + (int64_t)q * a.nx + c] = fyprev[q];
-          if (jg == a.nyg - 1)
-            for (int q = 0; q < 4; ++q)
-              a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fya[q];
+          if (x_edge_warp || jg == 0 || jg == a.nyg - 1) {
+            if (c == 0)
+              for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = fxa[q];
+            if (c == a.nx - 1)
+              for (int q = 0; q < 4; ++q) a.bnd[4 * (int64_t)a.nyg + (int64_t)q * a.nyg + jg] = fxr[q];
+            if (jg == 0)
+              for (int q = 0; q < 4; ++q) a.bnd[8 * (int64_t)a.nyg + (int64_t)q * a.nx + c] = fyprev[q];
+            if (jg == a.nyg - 1)
+              for (int q = 0; q < 4; ++q)
+                a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fya[q];
+          }
         }
       }
     } else if (!CORR && it == 3 && y0 == 0 && upd) {
