@@ -18,6 +18,7 @@ namespace lfb {
 
 #ifdef __CUDACC__
 
+
 struct FK {
   double gamma, gm1, beta;
   Recip rgm1, rdx, rdy;  // shared reciprocals of the constant divisors
@@ -52,7 +53,7 @@ __device__ __forceinline__ void face_fast(double m0, double m1, double m2, doubl
   const double rho_sum = m0 + p0;
   const Recip rs = recip_of(rho_sum);
   const double ps = div_fast(p0 * m3 + m0 * p3, rs, ok) - div_fast(m0 * p0, rs, ok) * cmax * (ur - ul);
-  const double un = TINY ? div_exact(m0 * ul + p0 * ur, rs, ok) : div_fast(m0 * ul + p0 * ur, rs, ok);
+  const double un = TINY ? div_exact_ol(m0 * ul + p0 * ur, rs, ok) : div_fast(m0 * ul + p0 * ur, rs, ok);
   const double us = un - div1_fast(p3 - m3, cmax * rho_sum, ok);
   // upwind side, branch-free (u* > 0: minus trace, else plus trace); the mean
   // state of u* == 0 is patched afterwards by face_mean (rare), so the main
@@ -195,12 +196,15 @@ __device__ __forceinline__ void cell_epilogue(const double v[4], const FK& c, do
 // in [2^-355, 2^355] -- all normal, where the fast paths are exact.  ok_r is
 // then the box itself; a cell outside it flags the step (stage-wise re-run).
 // The e_int quotient keeps div_exact and its own test (tiny kinetic energies).
+// OL: the e_int quotient's tiny-dividend completion out of line (the exact
+// kernels: smaller code, no spill; inline in the plain kernels, -1 % otherwise).
+template <bool OL = false>
 __device__ __forceinline__ void cell_epilogue_box(const double v[4], const FK& c, bool dxy_box,
                                                   double& eint, bool& ok_e, double& rr,
                                                   bool& rate_ok, bool& ok_r) {
   const Recip r0 = recip_of(v[0]);
   const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
-  eint = v[3] - div_exact(kin, r0, ok_e);
+  eint = v[3] - (OL ? div_exact_ol(kin, r0, ok_e) : div_exact(kin, r0, ok_e));
   bool dead = true;  // proved by the box
   const double inv = div_fast(1.0, r0, dead);
   const double uu = v[1] * inv, vv = v[2] * inv;

@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
           bool ok = true, okr = true, rate_ok;
           double eint, rr;
 #if LF_EPI_BOX
-          cell_epilogue_box(v, C, dxy_box, eint, ok, rr, rate_ok, okr);
+          cell_epilogue_box<EXACT>(v, C, dxy_box, eint, ok, rr, rate_ok, okr);
 #else
           cell_epilogue(v, C, eint, ok, rr, rate_ok, okr);
 #endif

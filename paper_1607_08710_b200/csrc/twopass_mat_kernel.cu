@@ -34,6 +34,16 @@
 #include "twopass.h"
 #include "pdl.cuh"
 
+// the multimaterial passes call div_exact at many sites: outline its cold path
+#ifndef LF_MAT_DIV_OUTLINE
+#define LF_MAT_DIV_OUTLINE 1
+#endif
+#if LF_MAT_DIV_OUTLINE
+#define LF_MAT_DIV_EXACT div_exact_ol
+#else
+#define LF_MAT_DIV_EXACT div_exact
+#endif
+
 #ifdef LF_MAT_DEBUG
 #define MFAIL(code)                                                                    \
   do {                                                                                 \
@@ -87,7 +97,7 @@ __device__ __forceinline__ double closure_q(const double raw[K], const double q[
       } else {
         yk = raw[k] < 0.0 ? 0.0 : 1.0;
       }
-      qk = div_exact(yk, mr.rg[k], ok);
+      qk = LF_MAT_DIV_EXACT(yk, mr.rg[k], ok);
     }
     y[k] = yk;
     if (yk == 1.0) pure = k;
@@ -107,8 +117,8 @@ __device__ __forceinline__ double closure(const double* p, double rho, const Mat
   double raw[K], q[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    raw[k] = div_exact(p[k], rr, ok);
-    q[k] = div_exact(raw[k], mr.rg[k], ok);
+    raw[k] = LF_MAT_DIV_EXACT(p[k], rr, ok);
+    q[k] = LF_MAT_DIV_EXACT(raw[k], mr.rg[k], ok);
   }
   return closure_q<K>(raw, q, m, mr, y, bad, ok);
 }
@@ -137,7 +147,7 @@ __device__ __forceinline__ void face_g(const double m[4], const double p[4], dou
   const double ps = div_fast(p[0] * m[3] + m[0] * p[3], rs, unused) -
                     div_fast(m[0] * p[0], rs, unused) * cmax * (ur - ul);
   const double us =
-      div_exact(m[0] * ul + p[0] * ur, rs, ok) - div1_fast(p[3] - m[3], cmax * rho_sum, unused);
+      LF_MAT_DIV_EXACT(m[0] * ul + p[0] * ur, rs, ok) - div1_fast(p[3] - m[3], cmax * rho_sum, unused);
   const bool pos = us > 0.0;
   const double s0 = pos ? m[0] : p[0], s1 = pos ? m[1] : p[1], s2 = pos ? m[2] : p[2];
   const double s3 = pos ? m[3] : p[3], gs = pos ? gl : gr;
@@ -493,7 +503,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
           bool ok = true;
           const Recip r0 = recip_of(v[0]);
           const double kin = 0.5 * (v[1] * v[1] + v[2] * v[2]);
-          const double eint = v[3] - div_exact(kin, r0, ok);
+          const double eint = v[3] - LF_MAT_DIV_EXACT(kin, r0, ok);
           double rawn[K], qn[K];
           bool have_q = false;
           if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
@@ -507,12 +517,12 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
             double s = 0.0;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-              rawn[k] = div_exact(pn[k], r0, ok);
-              qn[k] = div_exact(rawn[k], mr.rg[k], ok);
+              rawn[k] = LF_MAT_DIV_EXACT(pn[k], r0, ok);
+              qn[k] = LF_MAT_DIV_EXACT(rawn[k], mr.rg[k], ok);
               s += qn[k];
             }
             have_q = true;
-            const double pmin = div_exact(eint, recip_of(s), ok);
+            const double pmin = LF_MAT_DIV_EXACT(eint, recip_of(s), ok);
             if (!ok) MFAIL(10);
             if (pmin == pmin) {
               if (pmin > 0.0) {
@@ -529,8 +539,8 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
           if (!have_q) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-              rawn[k] = div_exact(pn[k], r0, okg);
-              qn[k] = div_exact(rawn[k], mr.rg[k], okg);
+              rawn[k] = LF_MAT_DIV_EXACT(pn[k], r0, okg);
+              qn[k] = LF_MAT_DIV_EXACT(rawn[k], mr.rg[k], okg);
             }
           }
           const double g = closure_q<K>(rawn, qn, mk, mr, yn, bad, okg);
