@@ -220,7 +220,7 @@ def run_ours(args):
         dist.broadcast_object_list(nid, src=0)
         dist_arg = (rank, world, local, nid[0])
     solver = LagfluxSolver(g, case.bc, case.gamma, case.params, devices=(local,), path=args.path,
-                           dist=dist_arg)
+                           dist=dist_arg, math=args.math)
     stream = torch.cuda.current_stream()
     solver.set_stream(stream.cuda_stream)
     state = G.SolverState(field=np.zeros((4, 1, 1)))  # device-resident; host copy not needed
@@ -277,6 +277,34 @@ def run_ours(args):
                 "traffic_source": traffic.get("source") if traffic else None,
                 "compute": ncu_compute_bound()}
 
+    # the same workload in the tolerance arithmetic (LF_MATH_CONTRACT), device-resident
+    contract = None
+    if args.math == "exact" and not args.no_contract and args.path in ("auto", "twopass"):
+        solver.set_math("contract")
+        cstate = G.SolverState(field=np.zeros((4, 1, 1)))
+        solver.init_fourier(cstate, case.seed)
+        solver.advance(cstate, controls, args.warmup)
+        barrier()
+        with ClockSampler(local) as cclocks:
+            ev0.record(stream)
+            ctaken = solver.advance(cstate, controls, args.steps)
+            ev1.record(stream)
+            barrier()
+        t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        cvalue = cells_total * ctaken / (float(t.item()) / 1e3)
+        ck_ms, _, ck_n = solver.time_steps(max(5, min(args.steps, 20)), case.cfl)
+        cach = BYTES_PER_CELL_UPDATE * cells_local / (ck_ms / max(ck_n, 1) / 1e3) / 1e9
+        contract = {"value": cvalue, "unit": UNIT, "ms_per_step": float(t.item()) / max(ctaken, 1),
+                    "roofline_frac": cach / hbm, "clocks": cclocks.summary(),
+                    "what": "the same steps with lf_set_math(LF_MATH_CONTRACT): FMA contraction and "
+                            "reciprocal products in the two-pass kernels; within the north-star "
+                            "tolerance of the reference (relative L1 <= 1e-10 per field, dt to "
+                            "1e-12; tests/test_gpu_contract.py), not bit-identical"}
+        solver.set_math("exact")
+        solver.init_fourier(state, case.seed)   # the e2e leg below starts from a fresh state
+
     # e2e through the public API with host buffers (rank-local slab)
     e2e = None
     if not args.no_e2e:
@@ -329,11 +357,13 @@ def run_ours(args):
                 "config": {"workload": f"config{4 if world == 1 else 5}-smooth "
                                        f"{g.nx}x{g.ny} periodic, y-slabs={world}",
                            "nx": g.nx, "ny": g.ny, "cfl": case.cfl, "seed": case.seed,
-                           "parallelism": f"y-slab x{world}", "path": args.path,
+                           "parallelism": f"y-slab x{world}", "path": args.path, "math": args.math,
                            "l2": "inputs larger than L2 (state %.1f GB per GPU)" % (
                                4 * 8 * g.nx * solver.local_rows()[1] / 1e9)},
                 "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clock_summary}
+        if contract is not None:
+            line["math_contract"] = contract
         print(json.dumps(line))
     solver.close()
     if world > 1:
@@ -451,7 +481,12 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="cells per side per GPU")
     ap.add_argument("--path", choices=["auto", "twopass", "fused", "staged"], default="auto")
+    ap.add_argument("--math", choices=["exact", "contract"], default="exact",
+                    help="exact: bit-identical to the reference; contract: FMA contraction and "
+                         "reciprocal products in the two-pass kernels (north-star tolerance)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-contract", action="store_true",
+                    help="skip the extra LF_MATH_CONTRACT measurement of the headline workload")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", choices=["smooth", "triple_point"], default="smooth",
                     help="smooth: BASELINE config 4/5 (the headline); triple_point: the "

@@ -67,6 +67,14 @@ enum {
  *            exact diagnosis path for every failure)
  *   TWOPASS  predictor and corrector as two warp-independent streaming kernels */
 enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2, LF_PATH_TWOPASS = 3 };
+/* Arithmetic of the two-pass kernels (the default path).  LF_MATH_EXACT: the
+ * reference's operation order without contraction, bit-identical to it.
+ * LF_MATH_CONTRACT: FMA contraction and quotients as products by a refined
+ * reciprocal -- fewer fp64 instructions, results within the north star's
+ * tolerance of the reference (relative L1 <= 1e-10 per conserved field, dt to
+ * 1e-12), not bit-identical.  The stage-wise and fused kernels (and every step
+ * the fast kernels flag) always compute in LF_MATH_EXACT. */
+enum { LF_MATH_EXACT = 0, LF_MATH_CONTRACT = 1 };
 
 typedef struct lf_desc {
   int dim;              /* 1 or 2 (CartesianGrid::dim) */
@@ -204,6 +212,7 @@ int lf_last_error(lf_handle* h, lf_error* err);
 /* ---- measurement / tuning hooks (used by bench.py; no reference counterpart) ---- */
 int lf_set_stream(lf_handle* h, void* cuda_stream);   /* NULL: the handle's own stream */
 int lf_set_path(lf_handle* h, int path);               /* LF_PATH_* */
+int lf_set_math(lf_handle* h, int math);               /* LF_MATH_* (default EXACT) */
 /* Time n device-resident steps with CUDA events around each launch of the
  * dominant kernel.  kernel_ms: summed kernel time; step_ms: whole-loop time. */
 int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,

@@ -1416,6 +1416,12 @@ int lf_set_path(lf_handle* h, int path) {
   return 0;
 }
 
+int lf_set_math(lf_handle* h, int math) {
+  if (!h || (math != LF_MATH_EXACT && math != LF_MATH_CONTRACT)) return LF_ERR_ARGUMENT;
+  h->math = math;
+  return 0;
+}
+
 int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
                   int* kernel_launches) {
   LF_TRACE("lf_time_steps");

@@ -65,6 +65,9 @@ struct FusedArgs {
 size_t fused_smem_bytes();
 void fused_configure();
 void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st);
+// LF_MATH_CONTRACT (fused_contract.cu)
+void fused_configure_contract();
+void launch_fused_step_contract(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st);
 // dt, time, diagnostics and the next control record of a step; outflow_zero:
 // every axis periodic, the outflow update is the += of +0.0 sums done here
 void launch_finalize(const StepCtl* ctl, StepAcc* acc, StepCtl* nxt, StepRec* rec,

@@ -38,6 +38,10 @@
 // Build-time tuning knobs (tools/variants.py sweeps them):
 //   LF_MINBLOCKS  resident blocks per SM requested from ptxas (register budget)
 
+#if LF_CONTRACT
+#define k_fused_step k_fused_step_contract   // distinct kernel names for ncu filters
+#endif
+
 namespace lfb {
 
 namespace {
@@ -495,6 +499,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
   if (__any_sync(FULL, fail) && (threadIdx.x & 31) == 0) atomicMax(&a.acc->fail, 1ull);
 }
 
+#if !LF_CONTRACT
 // After the step's kernel (and the cross-rank all-reduce of acc): dt / time
 // bookkeeping (solver.cpp:494,542-544), the ordered boundary-outflow sums
 // (solver.cpp:406-432, one thread per component and direction) and the
@@ -629,12 +634,31 @@ __global__ void k_acc_init(StepAcc* acc) {
   }
 }
 
+#endif  // !LF_CONTRACT
+
 constexpr size_t SMEM_BYTES =
     (size_t)(URING * 4 + 4 + 4 + 16 + 16 + 8 + 4 + 4 + 4 + 4) * NC * sizeof(double) +
     URING * sizeof(unsigned long long);
 
 }  // namespace
 
+#if LF_CONTRACT
+// fused_contract.cu: the one-kernel step in the tolerance arithmetic (LF_MATH_CONTRACT)
+void fused_configure_contract() {
+  cudaFuncSetAttribute(k_fused_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)SMEM_BYTES);
+  cudaFuncSetAttribute(k_fused_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)SMEM_BYTES);
+}
+
+void launch_fused_step_contract(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st) {
+  count_launch();
+  if (muscl)
+    k_fused_step<true><<<grid, FUSED_THREADS, SMEM_BYTES, st>>>(a);
+  else
+    k_fused_step<false><<<grid, FUSED_THREADS, SMEM_BYTES, st>>>(a);
+}
+#else
 size_t fused_smem_bytes() { return SMEM_BYTES; }
 
 void fused_configure() {
@@ -670,5 +694,6 @@ void launch_acc_init(StepAcc* acc, cudaStream_t st) {
   count_launch();
   k_acc_init<<<1, 1, 0, st>>>(acc);
 }
+#endif  // LF_CONTRACT
 
 }  // namespace lfb

@@ -119,6 +119,7 @@ static void fused_alloc(lf_handle* h, int steps) {
     }
     launch_acc_init(f->acc, s0.stream);
     fused_configure();
+    fused_configure_contract();
     // chunk rows: several waves of 2 blocks / SM, long marches (pipeline fill is 9 rows)
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s0.device);
@@ -281,7 +282,10 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
           m.mfy_stride = s.fy_stride;
           launch_pass_mat(a, m, h->mc, pass == 1, h->d.spatial_order >= 2, s.stream);
         } else {
-          launch_pass(a, pass == 1, h->d.spatial_order >= 2, h->tp_exact != 0, s.stream);
+          if (h->math == LF_MATH_CONTRACT)
+            launch_pass_contract(a, pass == 1, h->d.spatial_order >= 2, s.stream);
+          else
+            launch_pass(a, pass == 1, h->d.spatial_order >= 2, h->tp_exact != 0, s.stream);
         }
       }
     }
@@ -316,7 +320,10 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
     a.bnd = bnd;
     dim3 grid((h->d.nx + FUSED_TXO - 1) / FUSED_TXO,
               (s.L.ny + f->rows_per_chunk - 1) / f->rows_per_chunk);
-    launch_fused_step(a, h->d.spatial_order >= 2, grid, s.stream);
+    if (h->math == LF_MATH_CONTRACT)
+      launch_fused_step_contract(a, h->d.spatial_order >= 2, grid, s.stream);
+    else
+      launch_fused_step(a, h->d.spatial_order >= 2, grid, s.stream);
   }
   if (k1) FK(cudaEventRecord(k1, s0.stream));
   FK(cudaGetLastError());

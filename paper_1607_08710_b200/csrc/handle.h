@@ -61,6 +61,7 @@ struct lf_handle {
   lfb::Consts k{};
   int dim2 = 1;
   int path = LF_PATH_AUTO;
+  int math = LF_MATH_EXACT;   // arithmetic of the two-pass kernels (lf_set_math)
   std::vector<lfb::SlabState> slabs;
   // distributed (one slab per process)
   int rank = 0, nranks = 1;

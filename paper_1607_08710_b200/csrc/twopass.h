@@ -60,6 +60,9 @@ int tp_choose_rows(int nx, int ny, int sms, int warps_per_sm);
 // exact: the kernels that complete shock-precursor quotients exactly (see
 // twopass_kernel.cu); the plain ones flag such steps (StepAcc::fail = 2)
 void launch_pass(const PassArgs& a, bool corr, bool muscl, bool exact, cudaStream_t st);
+// LF_MATH_CONTRACT: the same kernels built with FMA contraction and reciprocal
+// multiplication (twopass_contract.cu); held to the north-star tolerance
+void launch_pass_contract(const PassArgs& a, bool corr, bool muscl, cudaStream_t st);
 struct MatConsts;
 void launch_pass_mat(const PassArgs& a, const MatPassArgs& m, const MatConsts& mc, bool corr,
                      bool muscl, cudaStream_t st);

@@ -30,6 +30,10 @@
 #include "twopass.h"
 #include "pdl.cuh"
 
+#if LF_CONTRACT
+#define k_pass k_pass_contract   // distinct kernel names in launch lists and ncu filters
+#endif
+
 namespace lfb {
 
 namespace {
@@ -229,7 +233,8 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
       tiny_rows = ((tiny_rows << 1) | (unsigned)(vel_tiny(w[1]) || vel_tiny(w[2]))) & 0xfu;
       tiny = __any_sync(FULL, tiny_rows != 0u);
     } else {
-      need_exact |= (unsigned)(vel_tiny(w[1]) || vel_tiny(w[2]));
+      // the contract arithmetic multiplies by reciprocals: tiny dividends need nothing
+      if (!LF_CONTRACT) need_exact |= (unsigned)(vel_tiny(w[1]) || vel_tiny(w[2]));
     }
     // -- y: traces of row r-1, face (r-2 | r-1); x: traces of row r-2 (shuffles)
     double ylo[4], yhi[4], xlo[4], xhi[4], xp[4], da[4], db[4];
@@ -406,6 +411,25 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
 
 }  // namespace
 
+#if LF_CONTRACT
+// twopass_contract.cu: the same kernels in the tolerance arithmetic (fastmath.cuh)
+void launch_pass_contract(const PassArgs& a, bool corr, bool muscl, cudaStream_t st) {
+  const int warps = a.strips * ((a.ny + a.rows_per_chunk - 1) / a.rows_per_chunk);
+  const unsigned blocks = (unsigned)((warps + TP_THREADS / 32 - 1) / (TP_THREADS / 32));
+  count_launch();
+  if (corr) {
+    if (muscl)
+      launch_chain(k_pass<true, true, false>, dim3(blocks), dim3(TP_THREADS), 0, st, a);
+    else
+      launch_chain(k_pass<true, false, false>, dim3(blocks), dim3(TP_THREADS), 0, st, a);
+  } else {
+    if (muscl)
+      launch_chain(k_pass<false, true, false>, dim3(blocks), dim3(TP_THREADS), 0, st, a);
+    else
+      launch_chain(k_pass<false, false, false>, dim3(blocks), dim3(TP_THREADS), 0, st, a);
+  }
+}
+#else
 int tp_strips(int nx) { return (nx + TXW - 1) / TXW; }
 
 int tp_resident_warps(int nmat) {
@@ -476,5 +500,6 @@ void launch_pass(const PassArgs& a, bool corr, bool muscl, bool exact, cudaStrea
   else
     launch_k<false>(a, corr, muscl, blocks, st);
 }
+#endif  // LF_CONTRACT
 
 }  // namespace lfb

@@ -18,6 +18,7 @@ LF_OK, LF_ERR_CONFIG, LF_ERR_DT_STATE, LF_ERR_DT_NONPOS = 0, 1, 2, 3
 LF_ERR_PRIMITIVE, LF_ERR_TRACE, LF_ERR_POSITIVITY, LF_ERR_DEVICE, LF_ERR_ARGUMENT = 4, 5, 6, 7, 8
 LF_ERR_FRACTION = 9
 LF_PATH_AUTO, LF_PATH_FUSED, LF_PATH_STAGED, LF_PATH_TWOPASS = 0, 1, 2, 3
+LF_MATH_EXACT, LF_MATH_CONTRACT = 0, 1
 
 
 class lf_desc(C.Structure):
@@ -68,6 +69,7 @@ SIGNATURES = [
     ("lf_last_error", C.c_int, [H, C.POINTER(lf_error)]),
     ("lf_set_stream", C.c_int, [H, C.c_void_p]),
     ("lf_set_path", C.c_int, [H, C.c_int]),
+    ("lf_set_math", C.c_int, [H, C.c_int]),
     ("lf_time_steps", C.c_int, [H, C.c_int, C.c_double, DP, DP, C.POINTER(C.c_int)]),
     ("lf_device_bytes", C.c_int, [H, C.POINTER(C.c_int64)]),
     ("lf_max_rate", C.c_int, [H, DP]),

@@ -51,7 +51,8 @@ class LagfluxSolver:
 
     def __init__(self, g: G.CartesianGrid, bc: G.BoundaryCondition, gamma: float = 1.4,
                  params: G.SchemeParams = G.SchemeParams(), threads: int = 1,
-                 materials=None, devices: Sequence[int] = (0,), path: str = "auto", dist=None):
+                 materials=None, devices: Sequence[int] = (0,), path: str = "auto", dist=None,
+                 math: str = "exact"):
         # constructor checks of solver.cpp:66-69
         if g.nx < 1 or g.ny < 1:
             raise G.ConfigError("grid has no interior cells")
@@ -77,6 +78,7 @@ class LagfluxSolver:
             self.close()
             _raise(err)
         self.set_path(path)
+        self.set_math(math)
         self._resident = None  # SolverState whose field is on the device
         # host fields hold only this rank's rows (distributed handles): see
         # local_field_shape(); the ABI takes pointers biased by -y0 * ld
@@ -120,6 +122,14 @@ class LagfluxSolver:
         code = {"auto": N.LF_PATH_AUTO, "fused": N.LF_PATH_FUSED, "staged": N.LF_PATH_STAGED,
                 "twopass": N.LF_PATH_TWOPASS}[path]
         self._check(self._lib.lf_set_path(self._h, code))
+
+    def set_math(self, math: str):
+        """'exact' (default): bit-identical to the reference.  'contract': the two-pass
+        kernels with FMA contraction and reciprocal products, within the north star's
+        tolerance (relative L1 <= 1e-10 per field, dt to 1e-12), not bit-identical."""
+        code = {"exact": N.LF_MATH_EXACT, "contract": N.LF_MATH_CONTRACT}[math]
+        self._check(self._lib.lf_set_math(self._h, code))
+        self.math = math
 
     def set_stream(self, stream_ptr: Optional[int]):
         self._check(self._lib.lf_set_stream(self._h, stream_ptr))

@@ -22,9 +22,16 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 
 # name -> (extra nvcc flags, LF_PATH_*); "base_*" variants build the same path
 # from the committed sources (git HEAD) for an A/B against the working tree
+# (a third element selects LF_MATH_*: 1 = contract; bit equality is checked
+# against the first variant of the same arithmetic)
 VARIANTS = {
-    "base_tp": ("", 3),
     "tp": ("", 3),
+    "c_tp": ("", 3, 1),
+    "c_async": ("-DLF_TP_ASYNC=1", 3, 1),
+    "c_late": ("-DLF_TP_LATELOAD=1", 3, 1),
+    "c_mb4": ("-DLF_TP_MINBLOCKS=4", 3, 1),
+    "c_mb2": ("-DLF_TP_MINBLOCKS=2", 3, 1),
+    "c_fused": ("", 1, 1),
 }
 
 
@@ -42,7 +49,7 @@ def build(names=None):
     os.makedirs(OUT, exist_ok=True)
     head = None
     procs = []
-    for name, (flags, _path) in VARIANTS.items():
+    for name, (flags, _path, *_m) in VARIANTS.items():
         if names and name not in names:
             continue
         src = CSRC
@@ -65,7 +72,7 @@ def run(n=8192, steps=10):
     from paper_1607_08710_b200.solver import make_desc
     case = CS.smooth(n, steps)
     g = case.grid
-    ref = None
+    refs = {}
     results = {}
     names = list(VARIANTS)
     for name in names:
@@ -80,6 +87,8 @@ def run(n=8192, steps=10):
         h = C.c_void_p()
         assert lib.lf_create(C.byref(desc), (C.c_int * 1)(0), 1, C.byref(h)) == 0
         assert lib.lf_set_path(h, VARIANTS[name][1]) == 0
+        math = VARIANTS[name][2] if len(VARIANTS[name]) > 2 else 0
+        assert lib.lf_set_math(h, math) == 0
         assert lib.lf_init_fourier(h, case.seed) == 0
         km, lm, nl = C.c_double(), C.c_double(), C.c_int()
         assert lib.lf_time_steps(h, 3, case.cfl, C.byref(km), C.byref(lm), C.byref(nl)) == 0
@@ -89,8 +98,9 @@ def run(n=8192, steps=10):
         lib.lf_destroy(h)
         per = km.value / nl.value
         same = None
+        ref = refs.get(math)
         if ref is None:
-            ref = f
+            refs[math] = f
         else:
             same = bool(np.array_equal(g.interior(f) == g.interior(ref), np.ones_like(g.interior(f), bool)))
         results[name] = {"kernel_ms": per, "gcells_s": g.nx * g.ny / per / 1e6, "same_as_first": same}
