@@ -233,6 +233,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    resolved = solver.resolved_path()   # auto: two-pass unless its scratch does not fit
     # warm-up
     solver.advance(state, controls, args.warmup)
     barrier()
@@ -256,7 +257,7 @@ def run_ours(args):
     # dominant kernel: per-launch CUDA events around the fused step kernel
     try:
         kernel_ms, loop_ms, k_launches = solver.time_steps(max(5, min(args.steps, 20)), case.cfl)
-        kernel_name = ("one-kernel Heun step (lfb::k_fused_step)" if args.path == "fused" else
+        kernel_name = ("one-kernel Heun step (lfb::k_fused_step)" if resolved == "fused" else
                        "two-pass Heun step (lfb::k_pass predictor + corrector, one launch pair)")
     except ValueError:  # stage-wise path: no single dominant kernel, use the whole step
         kernel_ms, loop_ms, k_launches = ms_max, ms_max, max(taken, 1)
@@ -279,7 +280,7 @@ def run_ours(args):
 
     # the same workload in the tolerance arithmetic (LF_MATH_CONTRACT), device-resident
     contract = None
-    if args.math == "exact" and not args.no_contract and args.path in ("auto", "twopass"):
+    if args.math == "exact" and not args.no_contract and resolved != "staged":
         solver.set_math("contract")
         cstate = G.SolverState(field=np.zeros((4, 1, 1)))
         solver.init_fourier(cstate, case.seed)
@@ -299,7 +300,7 @@ def run_ours(args):
         contract = {"value": cvalue, "unit": UNIT, "ms_per_step": float(t.item()) / max(ctaken, 1),
                     "roofline_frac": cach / hbm, "clocks": cclocks.summary(),
                     "what": "the same steps with lf_set_math(LF_MATH_CONTRACT): FMA contraction and "
-                            "reciprocal products in the two-pass kernels; within the north-star "
+                            "reciprocal products in the same kernels; within the north-star "
                             "tolerance of the reference (relative L1 <= 1e-10 per field, dt to "
                             "1e-12; tests/test_gpu_contract.py), not bit-identical"}
         solver.set_math("exact")
@@ -354,10 +355,11 @@ def run_ours(args):
                 "steps": taken, "warmup": args.warmup, "ms_per_step": ms_max / max(taken, 1),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (seeded 8-mode Fourier flow, BASELINE config 4/5)",
-                "config": {"workload": f"config{4 if world == 1 else 5}-smooth "
+                "config": {"workload": f"config{4 if world == 1 and g.nx < 32768 else 5}-smooth "
                                        f"{g.nx}x{g.ny} periodic, y-slabs={world}",
                            "nx": g.nx, "ny": g.ny, "cfl": case.cfl, "seed": case.seed,
-                           "parallelism": f"y-slab x{world}", "path": args.path, "math": args.math,
+                           "parallelism": f"y-slab x{world}", "path": args.path, "resolved_path": resolved,
+                           "math": args.math,
                            "l2": "inputs larger than L2 (state %.1f GB per GPU)" % (
                                4 * 8 * g.nx * solver.local_rows()[1] / 1e9)},
                 "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,

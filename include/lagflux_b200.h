@@ -213,6 +213,10 @@ int lf_last_error(lf_handle* h, lf_error* err);
 int lf_set_stream(lf_handle* h, void* cuda_stream);   /* NULL: the handle's own stream */
 int lf_set_path(lf_handle* h, int path);               /* LF_PATH_* */
 int lf_set_math(lf_handle* h, int math);               /* LF_MATH_* (default EXACT) */
+/* The path the next step takes: LF_PATH_TWOPASS, LF_PATH_FUSED or LF_PATH_STAGED.
+ * LF_PATH_AUTO runs the two-pass kernels when their scratch (four more states'
+ * worth) fits in device memory, else the one-kernel step (e.g. 32768^2 on one GPU). */
+int lf_resolved_path(lf_handle* h, int* path);
 /* Time n device-resident steps with CUDA events around each launch of the
  * dominant kernel.  kernel_ms: summed kernel time; step_ms: whole-loop time. */
 int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,

@@ -161,6 +161,11 @@ class LagfluxSolver {
 
   // residency control (see the header comment)
   void set_auto_sync(bool on) { auto_sync_ = on; }
+  // opt-in tolerance arithmetic (lf_set_math): contract = true trades bit equality
+  // with the reference for the north star's tolerance (relative L1 <= 1e-10, dt to 1e-12)
+  void set_contract_math(bool contract) {
+    check(lf_set_math(h_, contract ? LF_MATH_CONTRACT : LF_MATH_EXACT));
+  }
   void sync_to_host(SolverState& state, MaterialCells* materials = nullptr) const {
     if (resident_ != &state) throw Error("state is not resident on this solver");
     download(state.field);

@@ -1416,6 +1416,14 @@ int lf_set_path(lf_handle* h, int path) {
   return 0;
 }
 
+int lf_resolved_path(lf_handle* h, int* path) {
+  if (!h || !path) return LF_ERR_ARGUMENT;
+  return guarded(h, [&] {
+    *path = !use_fused(h) ? LF_PATH_STAGED : twopass_selected(h) ? LF_PATH_TWOPASS : LF_PATH_FUSED;
+    return 0;
+  });
+}
+
 int lf_set_math(lf_handle* h, int math) {
   if (!h || (math != LF_MATH_EXACT && math != LF_MATH_CONTRACT)) return LF_ERR_ARGUMENT;
   h->math = math;

@@ -13,6 +13,8 @@ int fused_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* 
 int fused_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
                      int* launches);
 void fused_release(lf_handle* h);
+// a fast-path step of this handle runs the two-pass kernels (else the one-kernel step)
+bool twopass_selected(lf_handle* h);
 int64_t fused_bytes(lf_handle* h);
 
 }  // namespace lfb

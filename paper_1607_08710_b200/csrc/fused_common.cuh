@@ -64,6 +64,7 @@ struct FusedArgs {
 
 size_t fused_smem_bytes();
 void fused_configure();
+int fused_blocks_per_sm();   // resident blocks of k_fused_step (after fused_configure)
 void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st);
 // LF_MATH_CONTRACT (fused_contract.cu)
 void fused_configure_contract();

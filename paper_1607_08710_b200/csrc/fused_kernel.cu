@@ -661,6 +661,14 @@ void launch_fused_step_contract(const FusedArgs& a, bool muscl, dim3 grid, cudaS
 #else
 size_t fused_smem_bytes() { return SMEM_BYTES; }
 
+int fused_blocks_per_sm() {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused_step<true>, FUSED_THREADS,
+                                                    SMEM_BYTES) != cudaSuccess || b < 1)
+    b = LF_MINBLOCKS;
+  return b;
+}
+
 void fused_configure() {
   cudaFuncSetAttribute(k_fused_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)SMEM_BYTES);

@@ -90,8 +90,27 @@ static bool use_twopass(lf_handle* h) {
   if (h->path == LF_PATH_FUSED) return false;
   for (auto& s : h->slabs)
     if (!tp_fits(s.L.pitch, s.L.ny)) return false;
-  return true;
+  if (h->path == LF_PATH_AUTO && h->tp_mem_ok < 0) {
+    // the two passes need U*, W and two F face sets beside U^n / U^{n+1}: six more
+    // state-sized arrays (32768^2: 206 GB in all).  Decided once, before they are
+    // allocated; a slab that does not fit runs the one-kernel step (two states).
+    h->tp_mem_ok = 1;
+    for (auto& s : h->slabs) {
+      double need = 0.0;   // all slabs of this device (in-process slabs share one)
+      for (auto& o : h->slabs)
+        if (o.device == s.device && !o.Us)
+          need += 8.0 * ((double)o.L.alloc * 2 +
+                         2.0 * 4 * ((double)o.L.pitch * o.L.ny * 2 + o.L.pitch));
+      size_t free_b = 0, total_b = 0;
+      FK(cudaSetDevice(s.device));
+      FK(cudaMemGetInfo(&free_b, &total_b));
+      if (need + (double)(1ull << 30) > (double)free_b) h->tp_mem_ok = 0;
+    }
+  }
+  return h->path != LF_PATH_AUTO || h->tp_mem_ok != 0;
 }
+
+bool twopass_selected(lf_handle* h) { return use_twopass(h); }
 
 static void fused_alloc(lf_handle* h, int steps) {
   FusedState* f = fstate(h);
@@ -120,15 +139,30 @@ static void fused_alloc(lf_handle* h, int steps) {
     launch_acc_init(f->acc, s0.stream);
     fused_configure();
     fused_configure_contract();
-    // chunk rows: several waves of 2 blocks / SM, long marches (pipeline fill is 9 rows)
+    // chunk rows: the blocks are independent and equally long, so a step costs about
+    // (waves) x (rows + 9 rows of pipeline fill); pick the chunk count that minimises
+    // it (16384^2: 15 chunks = 6.94 waves instead of 13 = 6.02, i.e. 7 waves either way;
+    // 32768^2: 14 chunks = 12.96 waves instead of 7 = 6.48)
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s0.device);
     const int strips = (h->d.nx + FUSED_TXO - 1) / FUSED_TXO;
     int ny_local = 0;
     for (auto& s : h->slabs) ny_local = std::max(ny_local, s.L.ny);
-    const int target_blocks = 2 * sms * 6;
-    const int chunks = std::max(1, (target_blocks + strips - 1) / strips);
-    f->rows_per_chunk = std::max((ny_local + chunks - 1) / chunks, 64);
+    const int64_t cap = (int64_t)sms * fused_blocks_per_sm();
+    const int64_t nslab = (int64_t)h->slabs.size();   // in-process slabs share the device
+    int best_rows = std::max(ny_local, 1);
+    int64_t best_cost = INT64_MAX;
+    for (int chunks = 1; chunks <= 512; ++chunks) {
+      const int rows = (ny_local + chunks - 1) / chunks;
+      if (rows < 64 && chunks > 1) break;
+      const int64_t blocks = nslab * strips * ((ny_local + rows - 1) / rows);
+      const int64_t cost = ((blocks + cap - 1) / cap) * (rows + 9);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best_rows = rows;
+      }
+    }
+    f->rows_per_chunk = best_rows;
     f->sms = sms;
   }
   // two-pass chunking follows the resident warps of the kernel in use

@@ -75,6 +75,9 @@ struct lf_handle {
   // the two-pass path has met shock-precursor velocities: use its exact kernels
   // until a new state is uploaded (set by a step with status 3)
   int tp_exact = 0;
+  // LF_PATH_AUTO: -1 undecided, 1 the two-pass scratch fits in device memory, 0 it
+  // does not (then the one-kernel step, which needs two states, runs instead)
+  int tp_mem_ok = -1;
 };
 
 namespace lfb {

@@ -70,6 +70,7 @@ SIGNATURES = [
     ("lf_set_stream", C.c_int, [H, C.c_void_p]),
     ("lf_set_path", C.c_int, [H, C.c_int]),
     ("lf_set_math", C.c_int, [H, C.c_int]),
+    ("lf_resolved_path", C.c_int, [H, C.POINTER(C.c_int)]),
     ("lf_time_steps", C.c_int, [H, C.c_int, C.c_double, DP, DP, C.POINTER(C.c_int)]),
     ("lf_device_bytes", C.c_int, [H, C.POINTER(C.c_int64)]),
     ("lf_max_rate", C.c_int, [H, DP]),

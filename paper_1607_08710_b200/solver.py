@@ -131,6 +131,13 @@ class LagfluxSolver:
         self._check(self._lib.lf_set_math(self._h, code))
         self.math = math
 
+    def resolved_path(self) -> str:
+        """The path the next step takes ('twopass', 'fused' or 'staged')."""
+        p = C.c_int()
+        self._check(self._lib.lf_resolved_path(self._h, C.byref(p)))
+        return {N.LF_PATH_TWOPASS: "twopass", N.LF_PATH_FUSED: "fused",
+                N.LF_PATH_STAGED: "staged"}[p.value]
+
     def set_stream(self, stream_ptr: Optional[int]):
         self._check(self._lib.lf_set_stream(self._h, stream_ptr))
 

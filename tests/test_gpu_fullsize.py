@@ -109,3 +109,28 @@ def test_baseline_configs_full_size_equal_reference(cuda, cfg):
     assert np.all(g.interior(st.field) == g.interior(rf))
     d = np.array([[x.dt, x.time, x.min_rho, x.min_p] for x in st.diagnostics])
     assert np.array_equal(d, diag[:, :4])
+
+
+def test_auto_path_by_device_memory(cuda):
+    """LF_PATH_AUTO: the two-pass kernels at 16384^2; at BASELINE config 5's 32768^2 their
+    scratch (206 GB) does not fit one B200, so the one-kernel step (two states, 69 GB)
+    runs -- periodic boundaries conserve mass and energy over its steps."""
+    case = CS.smooth(16384, 1)
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params)
+    s.init_fourier(G.SolverState(field=None), case.seed)
+    assert s.resolved_path() == "twopass"
+    s.close()
+    case = CS.smooth(32768, 3)
+    g = case.grid
+    s = LagfluxSolver(g, case.bc, case.gamma, case.params)
+    st = G.SolverState(field=None)
+    s.init_fourier(st, case.seed)
+    assert s.resolved_path() == "fused"
+    t0 = s.interior_totals()
+    assert s.advance(st, G.TimeControls(case.cfl, case.t_final, 3), 3) == 3
+    t1 = s.interior_totals()
+    s.close()
+    for c in (0, 3):
+        assert abs(t1[c] - t0[c]) <= 1e-12 * abs(t0[c])
+    for c in (1, 2):
+        assert abs(t1[c] - t0[c]) <= 1e-12 * (abs(t0[0]) + abs(t0[3]))
