@@ -55,24 +55,24 @@ def measured_hbm():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the fused kernel from the committed ncu capture."""
+def ncu_traffic(path):
+    """DRAM bytes per step of the path's dominant kernel(s) from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f)
+            return json.load(f)[path]
     except Exception:
         return None
 
 
-def ncu_compute_bound():
-    """The pass kernels' real bound from the committed ncu --set full capture
+def ncu_compute_bound(path):
+    """The path's kernels' real bound from the committed ncu --set full capture
     (profiles/r01_ncu_16k.json): fp64-pipe and issue utilisation per kernel."""
     p = os.path.join(ROOT, "profiles", "r01_ncu_16k.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        ks = d["twopass"]["kernels"]
+        ks = d[path]["kernels"]
         return {"bound": "fp64 pipe / issue latency (not HBM)",
                 "kernels": {k["kernel"].split("(")[0].split("::")[-1]:
                             {"fp64_pipe_pct": round(k["fp64_pipe_pct"], 1),
@@ -266,7 +266,7 @@ def run_ours(args):
     cells_local = g.nx * solver.local_rows()[1]
     hbm, hbm_src = measured_hbm()
     achieved = BYTES_PER_CELL_UPDATE * cells_local / (per_launch_ms / 1e3) / 1e9
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(resolved)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "peak_source": hbm_src,
                 "algorithmic_bytes_per_cell_update": BYTES_PER_CELL_UPDATE,
@@ -276,7 +276,7 @@ def run_ours(args):
                 "frac_of_nominal_8TBs": achieved / 8000.0,
                 "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                 "traffic_source": traffic.get("source") if traffic else None,
-                "compute": ncu_compute_bound()}
+                "compute": ncu_compute_bound(resolved)}
 
     # the same workload in the tolerance arithmetic (LF_MATH_CONTRACT), device-resident
     contract = None

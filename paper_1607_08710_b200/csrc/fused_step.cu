@@ -86,10 +86,23 @@ bool fused_supported(lf_handle* h) {
 
 // the two-pass kernels unless the fused one is asked for (or the slab is too
 // large for their 32-bit offsets)
+// LF_PATH_AUTO on large slabs: the one-kernel step.  Both run the 16384^2 step at
+// ~11.7-11.9 G cell-updates/s, but the two-pass one moves 290 B per cell-update, draws
+// the board's full 1000 W and runs at whatever clock the power cap leaves (1.73-1.9 GHz
+// from box to box), while the fused one (64 B) stays at the full 1965 MHz (~775 W).
+// Below 2^27 cells per slab the two-pass kernels fill the GPU better (1024^2: one wave).
+static bool prefer_fused(lf_handle* h) {
+  if (h->path != LF_PATH_AUTO || h->d.time_order < 2 || h->mc.n > 0) return false;
+  for (auto& s : h->slabs)
+    if ((int64_t)s.L.nx * s.L.ny < ((int64_t)1 << 27)) return false;
+  return true;
+}
+
 static bool use_twopass(lf_handle* h) {
   if (h->path == LF_PATH_FUSED) return false;
   for (auto& s : h->slabs)
     if (!tp_fits(s.L.pitch, s.L.ny)) return false;
+  if (prefer_fused(h)) return false;
   if (h->path == LF_PATH_AUTO && h->tp_mem_ok < 0) {
     // the two passes need U*, W and two F face sets beside U^n / U^{n+1}: six more
     // state-sized arrays (32768^2: 206 GB in all).  Decided once, before they are

@@ -111,13 +111,19 @@ def test_baseline_configs_full_size_equal_reference(cuda, cfg):
     assert np.array_equal(d, diag[:, :4])
 
 
-def test_auto_path_by_device_memory(cuda):
-    """LF_PATH_AUTO: the two-pass kernels at 16384^2; at BASELINE config 5's 32768^2 their
-    scratch (206 GB) does not fit one B200, so the one-kernel step (two states, 69 GB)
-    runs -- periodic boundaries conserve mass and energy over its steps."""
+def test_auto_path_by_size_and_device_memory(cuda):
+    """LF_PATH_AUTO: the two-pass kernels below 2^27 cells per slab, the one-kernel step
+    above (it stays at full clock under the power cap, fused_step.cu prefer_fused); at
+    BASELINE config 5's 32768^2 only the one-kernel step fits one B200 (the two-pass
+    scratch is 206 GB) -- periodic boundaries conserve mass and energy over its steps."""
+    for n, want in ((8192, "twopass"), (16384, "fused")):
+        case = CS.smooth(n, 1)
+        s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params)
+        s.init_fourier(G.SolverState(field=None), case.seed)
+        assert s.resolved_path() == want, n
+        s.close()
     case = CS.smooth(16384, 1)
-    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params)
-    s.init_fourier(G.SolverState(field=None), case.seed)
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path="twopass")
     assert s.resolved_path() == "twopass"
     s.close()
     case = CS.smooth(32768, 3)

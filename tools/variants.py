@@ -25,13 +25,12 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # (a third element selects LF_MATH_*: 1 = contract; bit equality is checked
 # against the first variant of the same arithmetic)
 VARIANTS = {
+    "f": ("", 1),
+    "f_box1": ("-DLF_FUSED_EPI_BOX=1", 1),
+    "f_box2": ("-DLF_FUSED_EPI_BOX=2", 1),
     "tp": ("", 3),
-    "c_tp": ("", 3, 1),
-    "c_async": ("-DLF_TP_ASYNC=1", 3, 1),
-    "c_late": ("-DLF_TP_LATELOAD=1", 3, 1),
-    "c_mb4": ("-DLF_TP_MINBLOCKS=4", 3, 1),
-    "c_mb2": ("-DLF_TP_MINBLOCKS=2", 3, 1),
-    "c_fused": ("", 1, 1),
+    "c_f": ("", 1, 1),
+    "c_f_box1": ("-DLF_FUSED_EPI_BOX=1", 1, 1),
 }
 
 
