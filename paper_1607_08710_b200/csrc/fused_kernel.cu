@@ -102,6 +102,14 @@ constexpr int PREFETCH = 2;
 #define LF_FUSED_EPI_BOX 1
 #endif
 #endif
+// LF_FUSED_EDGEROWS: the corrector's ghost-row images behind one block-uniform branch
+#ifndef LF_FUSED_EDGEROWS
+#define LF_FUSED_EDGEROWS 1
+#endif
+// LF_FUSED_EDGE1: the boundary-face stores behind one block-uniform test
+#ifndef LF_FUSED_EDGE1
+#define LF_FUSED_EDGE1 1
+#endif
 #ifndef LF_MINBLOCKS
 #define LF_MINBLOCKS 2
 #endif
@@ -322,6 +330,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
     }
     const bool has_ws = t >= 2 && t <= NC - 3 && src_t >= 2 && src_t <= NC - 3;
     const bool dox = t >= 4 && t <= NC - 4 && c <= a.nx;  // x-faces of output cells
+#if LF_FUSED_EDGE1
+    const bool x_edge_blk = x0 - 4 <= 0 || x0 - 4 + NC > a.nx - 1;   // holds column 0 or nx-1
+#endif
     for (int k = 0; k < nit; ++k) {
       const int aa = y0 - 7 + k;   // W* row consumed this iteration
       const int j = aa - 2;        // U^{n+1} row finished this iteration
@@ -340,6 +351,11 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           w[3] = ws[3 * NC];
           if (flip_u) w[1] = -w[1];
         }
+#if LF_FUSED_EDGEROWS
+        // the ghost-row images below are block-uniform and rare: one branch around them
+        // instead of predicated selects on every row
+        if ((bottom_edge && aa <= 1) || (top_edge && aa >= a.ny)) {
+#endif
         if (bottom_edge && aa == 0) {
           // W*(-1) = image of W*(0)
 #pragma unroll
@@ -372,6 +388,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 #pragma unroll
           for (int q = 0; q < 4; ++q) w[q] = sStash[q * NC + t];
         }
+#if LF_FUSED_EDGEROWS
+        }
+#endif
         if (k >= 7) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -471,6 +490,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         }
         // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
         const int jg = j + a.y0g;
+#if LF_FUSED_EDGE1
+        // one block-uniform test skips all four in the interior of the domain
+        if (x_edge_blk || jg == 0 || jg == a.nyg - 1) {
+#endif
         if (c == 0)
           for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = sFc[q * NC + t];
         if (c == a.nx - 1)
@@ -480,6 +503,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         if (jg == a.nyg - 1)
           for (int q = 0; q < 4; ++q)
             a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fc[q];
+#if LF_FUSED_EDGE1
+        }
+#endif
       }
       if (c_active && k >= 8) {
 #pragma unroll

@@ -26,11 +26,9 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # against the first variant of the same arithmetic)
 VARIANTS = {
     "f": ("", 1),
-    "f_box1": ("-DLF_FUSED_EPI_BOX=1", 1),
-    "f_box2": ("-DLF_FUSED_EPI_BOX=2", 1),
-    "tp": ("", 3),
+    "f_norows": ("-DLF_FUSED_EDGEROWS=0", 1),
     "c_f": ("", 1, 1),
-    "c_f_box1": ("-DLF_FUSED_EPI_BOX=1", 1, 1),
+    "c_f_norows": ("-DLF_FUSED_EDGEROWS=0", 1, 1),
 }
 
 
