@@ -106,6 +106,11 @@ constexpr int PREFETCH = 2;
 #ifndef LF_FUSED_EDGEROWS
 #define LF_FUSED_EDGEROWS 1
 #endif
+// LF_FUSED_DONTCARE: corrector lanes whose values are never kept load clamped
+// neighbours instead of selecting defaults (fewer selects in the critical warps)
+#ifndef LF_FUSED_DONTCARE
+#define LF_FUSED_DONTCARE 1
+#endif
 // LF_FUSED_EDGE1: the boundary-face stores behind one block-uniform test
 #ifndef LF_FUSED_EDGE1
 #define LF_FUSED_EDGE1 1
@@ -329,6 +334,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       flip_u = a.bc_xhi == LF_REFLECTIVE;
     }
     const bool has_ws = t >= 2 && t <= NC - 3 && src_t >= 2 && src_t <= NC - 3;
+#if LF_FUSED_DONTCARE
+    // lanes without a W* column (t < 2, t > NC-3) feed no face or cell that is kept:
+    // they read a clamped column instead of selecting a default state
+    const int src_c = min(max(src_t, 2), NC - 3);
+    const unsigned long long flip_bits = flip_u ? 0x8000000000000000ull : 0ull;
+#endif
     const bool dox = t >= 4 && t <= NC - 4 && c <= a.nx;  // x-faces of output cells
 #if LF_FUSED_EDGE1
     const bool x_edge_blk = x0 - 4 <= 0 || x0 - 4 + NC > a.nx - 1;   // holds column 0 or nx-1
@@ -343,7 +354,19 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         // -- W*(aa) with the boundary images of the reference's ghost fill of
         //    predictor_ (grid.cpp:72-114); a reflective image negates the normal
         //    velocity exactly as it negates the normal momentum
+#if LF_FUSED_DONTCARE
+        {
+          const double* ws = sWs + ((k + 1) & 1) * 4 * NC + src_c;
+          w[0] = ws[0];
+          w[1] = __longlong_as_double(__double_as_longlong(ws[NC]) ^ flip_bits);
+          w[2] = ws[2 * NC];
+          w[3] = ws[3 * NC];
+          (void)has_ws;
+        }
+        if (false) {
+#else
         if (has_ws) {
+#endif
           const double* ws = sWs + ((k + 1) & 1) * 4 * NC + src_t;
           w[0] = ws[0];
           w[1] = ws[NC];
@@ -414,10 +437,19 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       double fc[4] = {0.0, 0.0, 0.0, 0.0};
       if (c_active && k >= 7) {
         const bool dx_ = dox && k >= 9;
+#if LF_FUSED_DONTCARE
+        // a lane without a kept x-face reads its left neighbour's trace anyway (unused)
+        const int tm = t > 0 ? t - 1 : t;
+#else
         const int tm = dx_ ? t - 1 : t;
+#endif
         double mx[4];
 #pragma unroll
+#if LF_FUSED_DONTCARE
+        for (int q = 0; q < 4; ++q) mx[q] = sTc[q * NC + tm];
+#else
         for (int q = 0; q < 4; ++q) mx[q] = dx_ ? sTc[q * NC + tm] : xlo[q];
+#endif
         double fx[4], fs[4];
         bool okx = true, oky = true;  // implied by the cell box (face_fast.cuh): unused
         double psx, usx, psy, usy;
