@@ -26,9 +26,9 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # against the first variant of the same arithmetic)
 VARIANTS = {
     "f": ("", 1),
-    "f_nodc": ("-DLF_FUSED_DONTCARE=0", 1),
+    "f_nodcp": ("-DLF_FUSED_DONTCARE_P=0", 1),
     "c_f": ("", 1, 1),
-    "c_f_nodc": ("-DLF_FUSED_DONTCARE=0", 1, 1),
+    "c_f_nodcp": ("-DLF_FUSED_DONTCARE_P=0", 1, 1),
 }
 
 
