@@ -7,14 +7,20 @@ N > 1.  A step is one LagfluxSolver::heun_step (both stages + dt, solver.cpp:489
 one cell-update advances one interior cell by one step (bench.cpp:104,107).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scaling weak|strong]
 
 ours:       value = cells x K / device time of K device-resident steps (CUDA events on
             the launching stream, barrier + synchronize around, max over ranks).
             e2e   = the same through the public API with HOST buffers: upload of the
             initial state from pinned memory, K steps, download of the final state,
             all inside the timed region.
+            --scaling strong: config 5's 32768^2 grid split over the N ranks (total
+            work fixed), with a final-state digest checked against one handle
+            holding the whole grid (the reference's scaling_sweep determinism check,
+            bench.cpp:96-99,113-135).
 reference:  the reference's own LagfluxSolver (oracle/_ref, compiled from its sources)
-            on all host cores, on a bounded strip of the same workload.
+            on all host cores on the same 16384^2 config-4 grid, with the same
+            --steps / --warmup, timed like bench.cpp:70-76.
 """
 from __future__ import annotations
 
@@ -36,7 +42,7 @@ BYTES_PER_CELL_UPDATE = 160  # read U^n, write U*, read U^n + 
 FALLBACK_HBM_GBS = 6650.0    # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 METRIC = "cell-updates/sec (fp64, full 2nd-order step)"
 UNIT = "cell-updates/s"
-CPU_SAMPLE_ROWS = 512        # reference / oracle CPU sample: 16384 x 512 strip of config 4
+CPU_SAMPLE_ROWS = 4096       # cpu_baseline leg of our arm: 16384 x 4096 strip of config 4
 
 
 def env_int(name, default):
@@ -157,19 +163,65 @@ def cpu_sample_case(cases, rows=CPU_SAMPLE_ROWS, n=16384):
     return cases.smooth(n, 1, ny=rows, y_extent=rows / n)
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_ram_bytes():
+    try:
+        import psutil
+        return psutil.virtual_memory().total
+    except Exception:
+        return 0
+
+
+def omp_binding():
+    return {k: os.environ.get(k) for k in ("OMP_PLACES", "OMP_PROC_BIND", "OMP_NUM_THREADS")}
+
+
 def time_reference_cpu(case, steps, warmup, threads):
-    """The reference's LagfluxSolver::heun_step on host cores (bench.cpp:70-76 timing)."""
+    """The reference's LagfluxSolver::heun_step on host cores (bench.cpp:70-76 timing:
+    steady_clock around the step loop after the warm-up steps).  The initial state
+    comes from the oracle's C generator (bit-identical to cases.initial_field)."""
     from oracle import oracle as O
-    from paper_1607_08710_b200 import cases as CS
-    f0 = CS.initial_field(case)
+    f0 = O.oracle_init_fourier(case, threads)
     r = O.RefSolver(case.grid, case.bc, case.gamma, case.params, threads=threads)
     r.set_state(f0)
+    del f0
     if warmup:
         r.heun_steps(warmup, case.cfl, case.t_final)
     t0 = time.perf_counter()
     r.heun_steps(steps, case.cfl, case.t_final)
     wall = time.perf_counter() - t0
+    del r
     return case.cells * steps / wall, wall
+
+
+def reference_case(cases, world, scaling):
+    """The grid the reference arm times: our arm's N = 1 workload (config 4, 16384^2)
+    when it fits the host (the reference holds 288 B/cell, 77 GB), else the largest
+    strip of the same generator that does; for --scaling strong the config-5 columns
+    (32768) on as many rows as fit (the whole 32768^2 grid needs 309 GB)."""
+    ram = host_ram_bytes()
+    n = 32768 if scaling == "strong" else 16384
+    rows = n
+    while rows > 512 and 300.0 * n * rows > 0.8 * ram:
+        rows //= 2
+    case = cases.smooth(n, 1, ny=rows, y_extent=rows / n)
+    if rows == n:
+        what = f"config{5 if n == 32768 else 4}-smooth {n}x{n} periodic (the full grid)"
+    else:
+        what = (f"config{5 if n == 32768 else 4} generator, {n}x{rows} periodic strip (dx = dy; "
+                f"the full {n}^2 grid needs {288 * n * n / 1e9:.0f} GB of host memory, "
+                f"this box has {ram / 1e9:.0f} GB)")
+    return case, what
 
 
 def run_reference(args):
@@ -181,23 +233,22 @@ def run_reference(args):
     from paper_1607_08710_b200 import cases as CS
     from oracle import oracle as O
     threads = os.cpu_count() or 1
-    os.environ.setdefault("OMP_PLACES", "cores")
-    os.environ.setdefault("OMP_PROC_BIND", "close")
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_lagflux.so not built"}))
         return 0
-    case = cpu_sample_case(CS)
-    steps = max(1, min(args.steps, 10))
-    value, wall = time_reference_cpu(case, steps, min(args.warmup, 1), threads)
-    sample = (f"{case.grid.nx}x{case.grid.ny} periodic strip of the config-4 generator "
-              f"(seed {case.seed}), {steps} timed heun_step calls after "
-              f"{min(args.warmup, 1)} warm-up, OpenMP {threads} threads")
+    case, what = reference_case(CS, world, args.scaling)
+    value, wall = time_reference_cpu(case, args.steps, args.warmup, threads)
+    sample = (f"{case.grid.nx}x{case.grid.ny} periodic, seed {case.seed}: {args.steps} timed "
+              f"heun_step calls after {args.warmup} warm-up ({wall:.1f} s), OpenMP {threads} "
+              f"threads on {cpu_model()}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 1),
-            "ms_per_step": wall / steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config4-smooth-16384^2 (bounded CPU strip)",
-                       "nx": case.grid.nx, "ny": case.grid.ny, "boundary": "periodic"},
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": what, "nx": case.grid.nx, "ny": case.grid.ny,
+                       "boundary": "periodic", "cfl": case.cfl, "seed": case.seed,
+                       "per_rank_share": world > 1 and args.scaling == "weak",
+                       "cpu_model": cpu_model(), "cores": threads, "omp": omp_binding()},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -205,16 +256,45 @@ def run_reference(args):
     return 0
 
 
+def fp64_roof(lib, device):
+    """lf_fp64_peak: measured fp64 thread-instruction rates of this GPU (burst and
+    sustained, DFMA / DMUL / DADD; csrc/fp64_peak.cu)."""
+    import ctypes as C
+    out = (C.c_double * 6)()
+    if lib.lf_fp64_peak(device, 60.0, 1000.0, out) != 0:
+        return None
+    keys = ["dfma_burst", "dfma_sustained", "dmul_burst", "dmul_sustained", "dadd_burst",
+            "dadd_sustained"]
+    return {k: out[i] for i, k in enumerate(keys)}
+
+
+def ncu_fp64_ops(kernel_key):
+    """fp64 arithmetic instructions (DADD + DMUL + DFMA, thread level) per cell-update of
+    the dominant kernel, from the committed ncu capture of the current build."""
+    p = os.path.join(ROOT, "profiles", "fp64_ops.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[kernel_key]
+    except Exception:
+        return None
+
+
 def run_ours(args):
     torch, dist, world, rank, local = dist_setup(args)
     from paper_1607_08710_b200 import cases as CS
     from paper_1607_08710_b200 import grid as G
+    from paper_1607_08710_b200 import native as N
     from paper_1607_08710_b200.solver import LagfluxSolver, nccl_unique_id
 
     n = args.n
-    case = CS.smooth(n, args.steps) if world == 1 else CS.smooth_weak(world, n, args.steps)
+    strong = args.scaling == "strong"
+    if strong:
+        case = CS.smooth(32768 if args.n == 16384 else args.n, args.steps)   # config 5
+    else:
+        case = CS.smooth(n, args.steps) if world == 1 else CS.smooth_weak(world, n, args.steps)
     g = case.grid
     dist_arg = None
+    nid = None
     if world > 1:
         nid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(nid, src=0)
@@ -233,7 +313,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    resolved = solver.resolved_path()   # auto: two-pass unless its scratch does not fit
+    resolved = solver.resolved_path()   # auto: the fused step at 2^27+ cells per slab
     # warm-up
     solver.advance(state, controls, args.warmup)
     barrier()
@@ -253,6 +333,33 @@ def run_ours(args):
     cells_total = g.nx * g.ny
     value = cells_total * taken / (ms_max / 1e3)
     clock_summary = clocks.summary()
+
+    # final-state digest (all ranks; interior_totals is the reference's ordered sums,
+    # chained over the ranks, so it is bit-identical for any slab count)
+    digest = {"interior_totals": [float(x).hex() for x in solver.interior_totals()],
+              "time": float(state.time).hex(), "steps": state.step}
+    if strong and world > 1:
+        # the reference's scaling_sweep check (bench.cpp:96-99,124-128): the N-rank
+        # run must equal one handle holding the whole grid, bit for bit
+        single = None
+        if rank == 0:
+            s1 = LagfluxSolver(g, case.bc, case.gamma, case.params, devices=(local,), path=args.path,
+                               math=args.math)
+            st1 = G.SolverState(field=np.zeros((4, 1, 1)))
+            s1.init_fourier(st1, case.seed)
+            s1.advance(st1, controls, args.warmup)
+            s1.advance(st1, controls, args.steps)
+            single = {"interior_totals": [float(x).hex() for x in s1.interior_totals()],
+                      "time": float(st1.time).hex(), "steps": st1.step}
+            s1.close()
+            del st1
+        barrier()
+        digest["single_handle"] = single
+        digest["equal"] = single == {k: digest[k] for k in ("interior_totals", "time", "steps")} \
+            if rank == 0 else None
+        if rank == 0 and not digest["equal"]:
+            print(json.dumps({"error": "DeterminismError: the N-rank final state differs from "
+                                       "one handle", "digest": digest}), file=sys.stderr)
 
     # dominant kernel: per-launch CUDA events around the fused step kernel
     try:
@@ -277,6 +384,29 @@ def run_ours(args):
                 "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                 "traffic_source": traffic.get("source") if traffic else None,
                 "compute": ncu_compute_bound(resolved)}
+    # the roof that binds: fp64 (measured on this GPU now, lf_fp64_peak), with the
+    # kernel's fp64 instructions per cell-update from the current build's ncu capture
+    roof = fp64_roof(N.lib(), local) if rank == 0 else None
+    ops = ncu_fp64_ops(f"{resolved}/{args.math}")
+    if roof is not None:
+        peak_ops = roof["dfma_sustained"]
+        f64 = {"bound": "fp64", "unit": "G fp64 instr/s",
+               "peak": peak_ops / 1e9,
+               "peak_source": "measured now: lf_fp64_peak, DFMA back to back for ~1 s "
+                              "(csrc/fp64_peak.cu); thread instructions, a DFMA counts once",
+               "peaks_measured_G": {k: v / 1e9 for k, v in roof.items()}}
+        if ops is not None:
+            opc = ops["fp64_ops_per_cell_update"]
+            ach = opc * cells_local / (per_launch_ms / 1e3)
+            f64.update({"achieved": ach / 1e9, "frac": ach / peak_ops,
+                        "ops_per_cell_update": opc, "ops_source": ops.get("source"),
+                        "fp64_pipe_pct_ncu": ops.get("fp64_pipe_pct"),
+                        "issue_active_pct_ncu": ops.get("issue_active_pct"),
+                        "ceiling_cell_updates_per_s": peak_ops / opc,
+                        "ceiling_hbm_frac": peak_ops / opc * BYTES_PER_CELL_UPDATE / (hbm * 1e9)})
+        roofline["fp64"] = f64
+        roofline["binding"] = ("fp64 / issue: the fp64 ceiling (fp64.ceiling_hbm_frac) is "
+                               "below the HBM roof; frac is read against it")
 
     # the same workload in the tolerance arithmetic (LF_MATH_CONTRACT), device-resident
     contract = None
@@ -296,13 +426,22 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         cvalue = cells_total * ctaken / (float(t.item()) / 1e3)
         ck_ms, _, ck_n = solver.time_steps(max(5, min(args.steps, 20)), case.cfl)
-        cach = BYTES_PER_CELL_UPDATE * cells_local / (ck_ms / max(ck_n, 1) / 1e3) / 1e9
+        ck_per = ck_ms / max(ck_n, 1)
+        cach = BYTES_PER_CELL_UPDATE * cells_local / (ck_per / 1e3) / 1e9
         contract = {"value": cvalue, "unit": UNIT, "ms_per_step": float(t.item()) / max(ctaken, 1),
-                    "roofline_frac": cach / hbm, "clocks": cclocks.summary(),
+                    "roofline_frac": cach / hbm, "kernel_ms_per_launch": ck_per,
+                    "clocks": cclocks.summary(),
                     "what": "the same steps with lf_set_math(LF_MATH_CONTRACT): FMA contraction and "
                             "reciprocal products in the same kernels; within the north-star "
                             "tolerance of the reference (relative L1 <= 1e-10 per field, dt to "
-                            "1e-12; tests/test_gpu_contract.py), not bit-identical"}
+                            "1e-12; tests/test_gpu_contract.py, tests/test_gpu_baseline_configs.py), "
+                            "not bit-identical"}
+        cops = ncu_fp64_ops(f"{resolved}/contract")
+        if roof is not None and cops is not None:
+            opc = cops["fp64_ops_per_cell_update"]
+            ach = opc * cells_local / (ck_per / 1e3)
+            contract["fp64_frac"] = ach / roof["dfma_sustained"]
+            contract["fp64_ops_per_cell_update"] = opc
         solver.set_math("exact")
         solver.init_fourier(state, case.seed)   # the e2e leg below starts from a fresh state
 
@@ -333,8 +472,11 @@ def run_ours(args):
         e2e = {"value": cells_total * k2 / (float(t.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": state_bytes / max(k2, 1),
                "d2h_bytes_per_step": (state_bytes + 48 * k2) / max(k2, 1),
+               "steps_amortised": k2,
                "what": f"upload of the state from pinned host memory, {k2} steps "
-                       f"(dt/diagnostics back to the host), download of the final state"}
+                       f"(dt/diagnostics back to the host), download of the final state; the "
+                       f"{state_bytes / 1e9:.1f} GB each way over PCIe are amortised over {k2} "
+                       f"steps, so e2e approaches value as the run gets longer"}
         del host
 
     cpu_baseline = None
@@ -343,33 +485,40 @@ def run_ours(args):
         if O.ref_available():
             threads = os.cpu_count() or 1
             cs = cpu_sample_case(CS)
-            steps = 3
+            steps = 5
             v, wall = time_reference_cpu(cs, steps, 1, threads)
             cpu_baseline = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                             "sample": f"{cs.grid.nx}x{cs.grid.ny} periodic strip of the config-4 "
                                       f"generator, {steps} heun_step calls after 1 warm-up "
-                                      f"({wall:.1f} s), OpenMP {threads} threads"}
+                                      f"({wall:.1f} s), OpenMP {threads} threads on {cpu_model()}; "
+                                      f"bench.py --impl reference times the full grid"}
 
     if rank == 0:
+        if strong:
+            workload = f"config5-smooth {g.nx}x{g.ny} periodic strong, y-slabs={world}"
+        else:
+            workload = (f"config{4 if world == 1 and g.nx < 32768 else 5}-smooth "
+                        f"{g.nx}x{g.ny} periodic{' weak' if world > 1 else ''}, y-slabs={world}")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": taken, "warmup": args.warmup, "ms_per_step": ms_max / max(taken, 1),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (seeded 8-mode Fourier flow, BASELINE config 4/5)",
-                "config": {"workload": f"config{4 if world == 1 and g.nx < 32768 else 5}-smooth "
-                                       f"{g.nx}x{g.ny} periodic, y-slabs={world}",
+                "config": {"workload": workload,
                            "nx": g.nx, "ny": g.ny, "cfl": case.cfl, "seed": case.seed,
                            "parallelism": f"y-slab x{world}", "path": args.path, "resolved_path": resolved,
                            "math": args.math,
                            "l2": "inputs larger than L2 (state %.1f GB per GPU)" % (
                                4 * 8 * g.nx * solver.local_rows()[1] / 1e9)},
                 "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clock_summary}
+                "gpu_launches": launches, "clocks": clock_summary, "digest": digest}
         if contract is not None:
             line["math_contract"] = contract
         print(json.dumps(line))
     solver.close()
     if world > 1:
         dist.destroy_process_group()
+    if strong and world > 1 and rank == 0 and not digest.get("equal"):
+        return 3
     return 0
 
 
@@ -490,10 +639,18 @@ def main():
     ap.add_argument("--no-contract", action="store_true",
                     help="skip the extra LF_MATH_CONTRACT measurement of the headline workload")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N > 1: weak = 16384 x 16384 per GPU (config 5's weak mode); strong = "
+                         "config 5's 32768^2 split over the N GPUs, with the single-handle "
+                         "determinism digest")
     ap.add_argument("--workload", choices=["smooth", "triple_point"], default="smooth",
                     help="smooth: BASELINE config 4/5 (the headline); triple_point: the "
                          "multimaterial transport (one GPU)")
     args = ap.parse_args()
+    # OpenMP binding of the reference CPU path (bench.cpp-style timing on all cores),
+    # before any library that loads libgomp (oracle/_ref, the oracle, torch)
+    os.environ.setdefault("OMP_PLACES", "cores")
+    os.environ.setdefault("OMP_PROC_BIND", "close")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

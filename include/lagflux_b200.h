@@ -61,19 +61,24 @@ enum {
 };
 
 /* Heun-step implementation for lf_heun_step / lf_advance (all give identical results):
- *   AUTO     the fastest available (TWOPASS)
+ *   AUTO     FUSED for slabs of 2^27 cells or more (Heun, no materials: the 16384^2
+ *            and 32768^2 workloads), TWOPASS below that, for time_order 1 and for
+ *            materials; FUSED also when the two-pass scratch does not fit in device
+ *            memory.  lf_resolved_path reports the choice.
  *   FUSED    one kernel per step (U^n read once, U^{n+1} written once)
  *   STAGED   the reference's phase structure, one kernel per loop (also the
- *            exact diagnosis path for every failure)
- *   TWOPASS  predictor and corrector as two warp-independent streaming kernels */
+ *            exact diagnosis path for every failure, 1D grids, euler_stage and
+ *            more than 4 materials)
+ *   TWOPASS  predictor and corrector as two warp-independent streaming kernels
+ *            (1-4 materials included) */
 enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2, LF_PATH_TWOPASS = 3 };
-/* Arithmetic of the two-pass kernels (the default path).  LF_MATH_EXACT: the
+/* Arithmetic of the fast kernels (two-pass and fused).  LF_MATH_EXACT (default): the
  * reference's operation order without contraction, bit-identical to it.
  * LF_MATH_CONTRACT: FMA contraction and quotients as products by a refined
  * reciprocal -- fewer fp64 instructions, results within the north star's
  * tolerance of the reference (relative L1 <= 1e-10 per conserved field, dt to
- * 1e-12), not bit-identical.  The stage-wise and fused kernels (and every step
- * the fast kernels flag) always compute in LF_MATH_EXACT. */
+ * 1e-12), not bit-identical.  The stage-wise kernels, the material kernels and the
+ * re-run of every step the fast kernels flag always compute in LF_MATH_EXACT. */
 enum { LF_MATH_EXACT = 0, LF_MATH_CONTRACT = 1 };
 
 typedef struct lf_desc {
@@ -149,7 +154,8 @@ int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghost
  * set every Heun step also advects the n partial densities rho*y_k, uses the
  * mixed-cell gamma of each cell (each face side its own EOS), reports a fraction
  * outside [0,1] beyond round-off as LF_ERR_FRACTION, and returns the min
- * pressure from the fresh partials; the stage-wise kernels run these steps.
+ * pressure from the fresh partials.  The two-pass material kernels run these
+ * steps for 1-4 materials in 2D, the stage-wise kernels otherwise (1D, > 4).
  * Partials: n arrays in the ghosted field layout (partials[k][j*ld + i],
  * ld >= nx + 4); interior cells are transferred. */
 int lf_set_materials(lf_handle* h, int n, const double* gammas);
@@ -247,6 +253,12 @@ int lf_selftest_box(int64_t n, uint64_t seed, int64_t* counts);
  * {cells the box accepts, of those failing a per-operation check, of those
  * whose rate or e_int differs}. */
 int lf_selftest_epilogue(int64_t n, uint64_t seed, int64_t* counts);
+/* Measured fp64 throughput of `device` (csrc/fp64_peak.cu), the fp64 roof of the
+ * step: out[6] = {DFMA burst, DFMA sustained, DMUL burst, DMUL sustained, DADD
+ * burst, DADD sustained} in fp64 thread instructions per second (a DFMA counts
+ * once).  Burst: one launch of ~burst_ms; sustained: back-to-back launches for
+ * ~sustain_ms (0: burst only). */
+int lf_fp64_peak(int device, double burst_ms, double sustain_ms, double* out);
 
 #ifdef __cplusplus
 }

@@ -10,12 +10,16 @@
 //     lagflux::b200::LagfluxSolver solver(g, bc, eos, params, threads);
 //
 // and links liblagflux_b200.so.  Residency: the GPU keeps SolverState::field
-// between steps.  With auto_sync (the default) every heun_step copies the
-// interior back to state.field, exactly like the reference; a driver that only
+// between steps.  With auto_sync (the default) state.field is authoritative,
+// exactly like the reference: every heun_step uploads it and copies the
+// interior back, so host edits between steps are seen.  A driver that only
 // reads the field at dumps calls set_auto_sync(false) and sync_to_host(state)
-// before each dump (one line in run.cpp's dump lambda) to avoid the copies.
-// MaterialCells (multimaterial runs) follow the same rule: uploaded on their
-// first step, copied back with the field.
+// before each dump (one line in run.cpp's dump lambda) to avoid the copies;
+// then the device copy is authoritative for the resident state (identified by
+// address and by the time / step the last heun_step left in it -- a different
+// SolverState, or one whose time or step was reset, is uploaded afresh), and
+// compute_dt / euler_stage / interior_totals on another field first save the
+// resident state into its host field.  MaterialCells follow the same rules.
 #pragma once
 
 #include <array>
@@ -97,8 +101,8 @@ class LagfluxSolver {
   // solver.cpp:482-487 -- `in`'s ghosts are not refilled on the host (the
   // device fills its own copy); `out`'s interior receives the stage.
   void euler_stage(CellField& in, double dt, CellField& out, std::int64_t step = -1) {
+    evict();
     upload(in);
-    resident_ = nullptr;
     check(lf_euler_stage(h_, dt, step));
     download(out);
   }
@@ -109,11 +113,14 @@ class LagfluxSolver {
     if (n_mat_ == 0) materials = nullptr;  // solver.cpp:490
     if (n_mat_ > 0 && materials == nullptr)
       throw ConfigError("multimaterial step needs material storage");
-    if (resident_ != &state) {
+    if (auto_sync_ || !is_resident(state)) {
+      evict();
       upload(state.field);
       resident_ = &state;
+      resident_time_ = state.time;
+      resident_step_ = state.step;
     }
-    if (materials != nullptr && resident_mat_ != materials) {
+    if (materials != nullptr && (auto_sync_ || resident_mat_ != materials)) {
       check(lf_upload_partials(h_, partial_ptrs(*materials).p, grid_.nxt()));
       resident_mat_ = materials;
     }
@@ -126,6 +133,8 @@ class LagfluxSolver {
     }
     state.time = o.time;
     state.step = o.step;
+    resident_time_ = o.time;
+    resident_step_ = o.step;
     state.diagnostics.push_back({o.step, o.time, o.dt, o.min_rho, o.min_p});
     if (auto_sync_) {
       download(state.field);
@@ -137,8 +146,8 @@ class LagfluxSolver {
   // solver.cpp:434-480
   double compute_dt(const CellField& field, const TimeControls& controls, double time,
                     double limit_time) const {
+    evict();
     upload(field);
-    resident_ = nullptr;
     double dt = 0.0;
     check(lf_compute_dt(h_, controls.cfl, time, limit_time, &dt));
     return dt;
@@ -147,9 +156,9 @@ class LagfluxSolver {
   // interior_totals(grid, state.field) (grid.cpp:122-133), summed on the device in
   // the reference's order: the resident copy of `state`, else its host field
   std::array<double, 4> interior_totals(const SolverState& state) const {
-    if (resident_ != &state) {
+    if (auto_sync_ || !is_resident(state)) {
+      evict();
       upload(state.field);
-      resident_ = nullptr;
     }
     std::array<double, 4> t{};
     check(lf_interior_totals(h_, t.data()));
@@ -167,7 +176,7 @@ class LagfluxSolver {
     check(lf_set_math(h_, contract ? LF_MATH_CONTRACT : LF_MATH_EXACT));
   }
   void sync_to_host(SolverState& state, MaterialCells* materials = nullptr) const {
-    if (resident_ != &state) throw Error("state is not resident on this solver");
+    if (!is_resident(state)) throw Error("state is not resident on this solver");
     download(state.field);
     if (materials != nullptr) {
       if (resident_mat_ != materials) throw Error("material cells are not resident on this solver");
@@ -217,12 +226,28 @@ class LagfluxSolver {
     double* p[4] = {f.comp[0].data(), f.comp[1].data(), f.comp[2].data(), f.comp[3].data()};
     check(lf_download(h_, p, grid_.nxt(), 0));
   }
+  bool is_resident(const SolverState& s) const {
+    return resident_ == &s && s.time == resident_time_ && s.step == resident_step_;
+  }
+  // the device copy is about to be replaced: without auto_sync it is the only
+  // current copy of the resident state, so save it (and its partials) first
+  void evict() const {
+    if (resident_ != nullptr && !auto_sync_ && is_resident(*resident_)) {
+      download(resident_->field);
+      if (resident_mat_ != nullptr)
+        check(lf_download_partials(h_, partial_ptrs(*resident_mat_).p, grid_.nxt()));
+    }
+    resident_ = nullptr;
+    resident_mat_ = nullptr;
+  }
 
   CartesianGrid grid_;
   int threads_;
   lf_handle* h_ = nullptr;
-  mutable const SolverState* resident_ = nullptr;
-  const MaterialCells* resident_mat_ = nullptr;
+  mutable SolverState* resident_ = nullptr;
+  mutable MaterialCells* resident_mat_ = nullptr;
+  double resident_time_ = 0.0;
+  std::int64_t resident_step_ = 0;
   int n_mat_ = 0;
   bool auto_sync_ = true;
 };

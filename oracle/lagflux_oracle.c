@@ -909,3 +909,60 @@ void lfo_fourier_tables(uint64_t seed, int nx, int ny, double x0, double y0, dou
     }
   }
 }
+
+/* The whole seeded smooth-flow initial state (cases.py initial_field, "fourier"):
+ * f_k = sum_m a (sx cy + cx sy) in mode order, normalised by max |f_k| over the
+ * interior, rho = 1 + 0.2 f1, u = 0.5 f2, v = 0.5 f3, p = 1 + 0.2 f4, then
+ * conserved_from_primitive (euler.hpp:87-97).  Bit-identical to the Python
+ * generator (every cell is independent; the maxima are order-free), so rows
+ * may be split over `threads` OpenMP threads.  Used to give the reference arm
+ * of bench.py the 16384^2 state without the Python generator's minutes. */
+void lfo_init_fourier(uint64_t seed, const lfo_grid* g, double gamma, double* const field[4],
+                      int threads) {
+  const int nx = g->nx, ny = g->ny, gx = g->gx, gy = g->gy;
+  const int64_t nxt = nx + 2 * gx;
+  double* tx = (double*)malloc(sizeof(double) * 64 * (size_t)nx);
+  double* ty = (double*)malloc(sizeof(double) * 64 * (size_t)ny);
+  double amp[32];
+  lfo_fourier_tables(seed, nx, ny, g->x0, g->y0, g->dx, g->dy, tx, ty, amp);
+  if (threads < 1) threads = 1;
+  double mx[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < 4; ++k) {
+    double m = 0.0;
+#pragma omp parallel for num_threads(threads) reduction(max : m) schedule(static)
+    for (int j = 0; j < ny; ++j) {
+      double* row = field[k] + (int64_t)(j + gy) * nxt + gx;
+      for (int i = 0; i < nx; ++i) row[i] = 0.0;
+      for (int md = 0; md < 8; ++md) {
+        const double* sx = tx + ((size_t)(k * 8 + md) * 2) * nx;
+        const double* cx = sx + nx;
+        const double* sy = ty + ((size_t)(k * 8 + md) * 2) * ny;
+        const double* cy = sy + ny;
+        const double a = amp[k * 8 + md], syj = sy[j], cyj = cy[j];
+        for (int i = 0; i < nx; ++i) row[i] = row[i] + a * (sx[i] * cyj + cx[i] * syj);
+      }
+      for (int i = 0; i < nx; ++i) {
+        const double v = fabs(row[i]);
+        if (v > m) m = v;
+      }
+    }
+    mx[k] = m;
+  }
+  const double gm1 = gamma - 1.0;
+#pragma omp parallel for num_threads(threads) schedule(static)
+  for (int j = 0; j < ny; ++j) {
+    const int64_t o = (int64_t)(j + gy) * nxt + gx;
+    for (int i = 0; i < nx; ++i) {
+      const double rho = 1.0 + 0.2 * (field[0][o + i] / mx[0]);
+      const double u = 0.5 * (field[1][o + i] / mx[1]);
+      const double v = 0.5 * (field[2][o + i] / mx[2]);
+      const double p = 1.0 + 0.2 * (field[3][o + i] / mx[3]);
+      field[0][o + i] = rho;
+      field[1][o + i] = rho * u;
+      field[2][o + i] = rho * v;
+      field[3][o + i] = p / gm1 + (0.5 * rho) * (u * u + v * v);
+    }
+  }
+  free(tx);
+  free(ty);
+}

@@ -144,6 +144,10 @@ void lfo_interior_totals(const lfo_grid* g, double* const field[4], double tot[4
 void lfo_fourier_tables(uint64_t seed, int nx, int ny, double x0, double y0, double dx,
                         double dy, double* tx /* 4*8*2*nx */, double* ty /* 4*8*2*ny */,
                         double* amp /* 4*8 */);
+/* The whole initial state into the interior of a ghosted field (rows split over
+ * `threads` OpenMP threads; bit-identical to cases.py initial_field). */
+void lfo_init_fourier(uint64_t seed, const lfo_grid* g, double gamma, double* const field[4],
+                      int threads);
 
 #ifdef __cplusplus
 }

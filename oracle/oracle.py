@@ -127,6 +127,7 @@ def oracle_lib():
     lib.lfo_interior_totals.argtypes = [C.POINTER(lfo_grid), P4, DP]
     lib.lfo_fourier_tables.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_double, C.c_double,
                                        C.c_double, C.c_double, DP, DP, DP]
+    lib.lfo_init_fourier.argtypes = [C.c_uint64, C.POINTER(lfo_grid), C.c_double, P4, C.c_int]
     return lib
 
 
@@ -332,6 +333,17 @@ def fourier_tables_oracle(seed: int, g: G.CartesianGrid):
     lib.lfo_fourier_tables(seed, g.nx, g.ny, g.x0, g.y0, g.dx, g.dy, tx.ctypes.data_as(DP),
                            ty.ctypes.data_as(DP), amp.ctypes.data_as(DP))
     return tx.reshape(4, 8, 2, g.nx), ty.reshape(4, 8, 2, g.ny), amp.reshape(4, 8)
+
+
+def oracle_init_fourier(case, threads: int = 0) -> np.ndarray:
+    """The seeded smooth-flow initial field (cases.initial_field for "fourier") from
+    the C restatement, rows over `threads` OpenMP threads (0: all cores): the reference
+    arm's 16384^2 input without the Python generator's minutes."""
+    g = case.grid
+    f = G.new_field(g)
+    oracle_lib().lfo_init_fourier(case.seed, C.byref(_cgrid(g)), case.gamma, _ptrs(f),
+                                  threads or (os.cpu_count() or 1))
+    return f
 
 
 # ---- multimat.cpp element functions (known-answer tests) -------------------

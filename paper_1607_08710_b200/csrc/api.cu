@@ -312,7 +312,10 @@ Scalars combined_scalars(lf_handle* h, int slot) {
 }
 
 // Fetch the 4 components of local cell (i, j) of `buf` on the slab owning global row jg.
-bool fetch_cell(lf_handle* h, double* SlabState::*buf, int i, int jg, double v[4]) {
+// Distributed handles: every rank reaches the error report (the failing index is
+// all-reduced), only the owner holds the cell -- the owner's bits win an all-reduce
+// max in which the other ranks contribute 0 (collective; +0.0 is all-zero bits).
+static bool fetch_local(lf_handle* h, double* SlabState::*buf, int i, int jg, double v[4]) {
   for (auto& s : h->slabs) {
     int jl = jg - s.sl.y0;
     const bool inside = jl >= 0 && jl < s.L.ny;
@@ -328,9 +331,25 @@ bool fetch_cell(lf_handle* h, double* SlabState::*buf, int i, int jg, double v[4
   return false;
 }
 
+static bool owner_bits_to_all(lf_handle* h, bool found, double* v, int n) {
+  if (!h->nccl) return found;
+  unsigned long long u[4] = {0, 0, 0, 0};
+  if (found)
+    for (int c = 0; c < n; ++c) std::memcpy(&u[c], &v[c], sizeof(double));
+  nccl_max_u64(h, u, n);
+  for (int c = 0; c < n; ++c) std::memcpy(&v[c], &u[c], sizeof(double));
+  return true;
+}
+
+bool fetch_cell(lf_handle* h, double* SlabState::*buf, int i, int jg, double v[4]) {
+  const bool found = fetch_local(h, buf, i, jg, v);
+  return owner_bits_to_all(h, found, v, 4);
+}
+
 // ---------------------------------------------------------------- error records
-// The mixed-cell gamma of cell (i, jg) in slot gslot.
+// The mixed-cell gamma of cell (i, jg) in slot gslot (collective like fetch_cell).
 bool fetch_gamma(lf_handle* h, int gslot, int i, int jg, double* v) {
+  bool found = false;
   for (auto& s : h->slabs) {
     const int jl = jg - s.sl.y0;
     const bool inside = jl >= 0 && jl < s.L.ny;
@@ -340,9 +359,10 @@ bool fetch_gamma(lf_handle* h, int gslot, int i, int jg, double* v) {
     CK(cudaSetDevice(s.device));
     CK(cudaMemcpy(v, s.GC[gslot] + s.L.origin() + (int64_t)jl * s.L.pitch + i, sizeof(double),
                   cudaMemcpyDeviceToHost));
-    return true;
+    found = true;
+    break;
   }
-  return false;
+  return owner_bits_to_all(h, found, v, 1);
 }
 
 int report_prim(lf_handle* h, double* SlabState::*buf, long long c, int64_t step, int gslot = 0) {
@@ -659,13 +679,21 @@ int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t ste
 
 bool use_fused(lf_handle* h) {
   if (h->path == LF_PATH_STAGED) return false;
+  // the fast kernels' limiter (sweby_fast, fastmath.cuh) is the reference's for
+  // beta >= 1 (make_limiter's range is [1, 2], but LagfluxSolver takes any
+  // LimiterParams): other betas run the stage-wise kernels, which evaluate
+  // sweby_limiter as written (reconstruct.hpp:24-30)
+  if (!(h->d.beta >= 1.0)) return false;
   // materials: the two-pass material kernels for up to 4 materials, else stage-wise
   if (h->mc.n > 0 && (h->mc.n > 4 || h->path == LF_PATH_FUSED || !h->partials_ready)) return false;
   // (the fused one-kernel step has no material transport: a slab beyond the
   // two-pass kernels' 32-bit offsets goes stage-wise)
-  if (h->mc.n > 0)
+  if (h->mc.n > 0) {
     for (auto& s : h->slabs)
       if (!tp_fits(s.L.pitch, s.L.ny)) return false;
+    // ... and so does one whose two-pass scratch was vetoed (device memory)
+    return fused_supported(h) && twopass_selected(h);
+  }
   return fused_supported(h);
 }
 
@@ -927,6 +955,11 @@ int lf_upload_partials(lf_handle* h, double* const* partials, int64_t ld) {
     }
     sync_all(h);
     h->partials_ready = 1;
+    // the cached CFL rate and fraction check came from the old partials (mixed-cell
+    // gamma): a new material state, as in lf_upload
+    h->tp_exact = 0;
+    h->rate_valid = false;
+    fused_invalidate(h);
     return 0;
   });
 }

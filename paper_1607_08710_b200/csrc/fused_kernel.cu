@@ -102,15 +102,6 @@ constexpr int PREFETCH = 2;
 #define LF_FUSED_EPI_BOX 1
 #endif
 #endif
-// LF_FUSED_EDGEROWS: the corrector's ghost-row images behind one block-uniform branch
-#ifndef LF_FUSED_EDGEROWS
-#define LF_FUSED_EDGEROWS 1
-#endif
-// LF_FUSED_DONTCARE: corrector lanes whose values are never kept load clamped
-// neighbours instead of selecting defaults (fewer selects in the critical warps)
-#ifndef LF_FUSED_DONTCARE
-#define LF_FUSED_DONTCARE 1
-#endif
 // LF_FUSED_DONTCARE_P: the same for the predictor's x-face operands (measured at
 // 16384^2: +0.6 % exact, -1.2 % contract)
 #ifndef LF_FUSED_DONTCARE_P
@@ -119,10 +110,6 @@ constexpr int PREFETCH = 2;
 #else
 #define LF_FUSED_DONTCARE_P 1
 #endif
-#endif
-// LF_FUSED_EDGE1: the boundary-face stores behind one block-uniform test
-#ifndef LF_FUSED_EDGE1
-#define LF_FUSED_EDGE1 1
 #endif
 #ifndef LF_MINBLOCKS
 #define LF_MINBLOCKS 2
@@ -350,17 +337,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       src_t = t + (sc - c);
       flip_u = a.bc_xhi == LF_REFLECTIVE;
     }
-    const bool has_ws = t >= 2 && t <= NC - 3 && src_t >= 2 && src_t <= NC - 3;
-#if LF_FUSED_DONTCARE
     // lanes without a W* column (t < 2, t > NC-3) feed no face or cell that is kept:
     // they read a clamped column instead of selecting a default state
     const int src_c = min(max(src_t, 2), NC - 3);
     const unsigned long long flip_bits = flip_u ? 0x8000000000000000ull : 0ull;
-#endif
     const bool dox = t >= 4 && t <= NC - 4 && c <= a.nx;  // x-faces of output cells
-#if LF_FUSED_EDGE1
     const bool x_edge_blk = x0 - 4 <= 0 || x0 - 4 + NC > a.nx - 1;   // holds column 0 or nx-1
-#endif
     for (int k = 0; k < nit; ++k) {
       const int aa = y0 - 7 + k;   // W* row consumed this iteration
       const int j = aa - 2;        // U^{n+1} row finished this iteration
@@ -371,31 +353,16 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         // -- W*(aa) with the boundary images of the reference's ghost fill of
         //    predictor_ (grid.cpp:72-114); a reflective image negates the normal
         //    velocity exactly as it negates the normal momentum
-#if LF_FUSED_DONTCARE
         {
           const double* ws = sWs + ((k + 1) & 1) * 4 * NC + src_c;
           w[0] = ws[0];
           w[1] = __longlong_as_double(__double_as_longlong(ws[NC]) ^ flip_bits);
           w[2] = ws[2 * NC];
           w[3] = ws[3 * NC];
-          (void)has_ws;
         }
-        if (false) {
-#else
-        if (has_ws) {
-#endif
-          const double* ws = sWs + ((k + 1) & 1) * 4 * NC + src_t;
-          w[0] = ws[0];
-          w[1] = ws[NC];
-          w[2] = ws[2 * NC];
-          w[3] = ws[3 * NC];
-          if (flip_u) w[1] = -w[1];
-        }
-#if LF_FUSED_EDGEROWS
         // the ghost-row images below are block-uniform and rare: one branch around them
         // instead of predicated selects on every row
         if ((bottom_edge && aa <= 1) || (top_edge && aa >= a.ny)) {
-#endif
         if (bottom_edge && aa == 0) {
           // W*(-1) = image of W*(0)
 #pragma unroll
@@ -428,9 +395,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 #pragma unroll
           for (int q = 0; q < 4; ++q) w[q] = sStash[q * NC + t];
         }
-#if LF_FUSED_EDGEROWS
         }
-#endif
         if (k >= 7) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -454,19 +419,11 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       double fc[4] = {0.0, 0.0, 0.0, 0.0};
       if (c_active && k >= 7) {
         const bool dx_ = dox && k >= 9;
-#if LF_FUSED_DONTCARE
         // a lane without a kept x-face reads its left neighbour's trace anyway (unused)
         const int tm = t > 0 ? t - 1 : t;
-#else
-        const int tm = dx_ ? t - 1 : t;
-#endif
         double mx[4];
 #pragma unroll
-#if LF_FUSED_DONTCARE
         for (int q = 0; q < 4; ++q) mx[q] = sTc[q * NC + tm];
-#else
-        for (int q = 0; q < 4; ++q) mx[q] = dx_ ? sTc[q * NC + tm] : xlo[q];
-#endif
         double fx[4], fs[4];
         bool okx = true, oky = true;  // implied by the cell box (face_fast.cuh): unused
         double psx, usx, psy, usy;
@@ -539,10 +496,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         }
         // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
         const int jg = j + a.y0g;
-#if LF_FUSED_EDGE1
         // one block-uniform test skips all four in the interior of the domain
         if (x_edge_blk || jg == 0 || jg == a.nyg - 1) {
-#endif
         if (c == 0)
           for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = sFc[q * NC + t];
         if (c == a.nx - 1)
@@ -552,9 +507,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         if (jg == a.nyg - 1)
           for (int q = 0; q < 4; ++q)
             a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fc[q];
-#if LF_FUSED_EDGE1
         }
-#endif
       }
       if (c_active && k >= 8) {
 #pragma unroll

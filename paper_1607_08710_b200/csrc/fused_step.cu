@@ -117,7 +117,8 @@ static bool use_twopass(lf_handle* h) {
       size_t free_b = 0, total_b = 0;
       FK(cudaSetDevice(s.device));
       FK(cudaMemGetInfo(&free_b, &total_b));
-      if (need + (double)(1ull << 30) > (double)free_b) h->tp_mem_ok = 0;
+      // (scratch already allocated, e.g. by the material path: nothing to veto)
+      if (need > 0.0 && need + (double)(1ull << 30) > (double)free_b) h->tp_mem_ok = 0;
     }
   }
   return h->path != LF_PATH_AUTO || h->tp_mem_ok != 0;

@@ -84,12 +84,14 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 #ifndef LF_TP_EDGE1
 #define LF_TP_EDGE1 1
 #endif
+#if LF_TP_ASYNC
 __device__ __forceinline__ void tp_cp_async8(double* sdst, const double* gsrc, bool pred) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gsrc),
                "r"(pred ? 8 : 0)
                : "memory");
 }
+#endif
 
 // EXACT = false: the plain fast path; a warp whose stencil rows hold a velocity
 // in (0, 2^-500) (shock precursors) does not compute with it but raises the

@@ -82,6 +82,7 @@ SIGNATURES = [
     ("lf_selftest_fastmath", C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
     ("lf_selftest_box", C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
     ("lf_selftest_epilogue", C.c_int, [C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]),
+    ("lf_fp64_peak", C.c_int, [C.c_int, C.c_double, C.c_double, DP]),
 ]
 
 _lib = None

@@ -154,6 +154,10 @@ class LagfluxSolver:
 
     def _ptrs(self, field):
         if not self.local_host:
+            g = self._grid
+            if field.shape != (4, g.nyt, g.nxt):
+                raise ValueError(f"field shape {field.shape} is not the grid's ghosted layout "
+                                 f"{(4, g.nyt, g.nxt)}")
             return N.field_ptrs(field)
         assert field.shape == self.local_field_shape(), (field.shape, self.local_field_shape())
         return N.biased_field_ptrs(field, self.local_rows()[0])
@@ -165,7 +169,26 @@ class LagfluxSolver:
 
     # ------------------------------------------------------------ state transfer
     def upload(self, field: np.ndarray):
+        self._evict(field)
         self._check(self._lib.lf_upload(self._h, self._ptrs(field), self._grid.nxt))
+        self._resident = None
+
+    def _evict(self, field: np.ndarray):
+        """The device copy of the resident state is about to be replaced by `field`
+        (compute_dt / euler_stage of another field, or another state): it is the only
+        current copy, so save it into the resident state's host field first; the
+        next heun_step of that state re-attaches from there.  A device-only state
+        (host field of another shape, e.g. after init_fourier for a benchmark) cannot
+        be saved: it is dropped, and stepping it again fails on the shape check."""
+        r = self._resident
+        if r is None or r.field is field:
+            return
+        try:
+            self._ptrs(r.field)
+        except (ValueError, AssertionError):
+            self._resident = None
+            return
+        self.download(r.field)
         self._resident = None
 
     def download(self, field: np.ndarray, fill_ghosts: bool = False):

@@ -85,8 +85,120 @@ def compare(name, g, single, ranks):
     return ok
 
 
+def run_err(g, bc, f0, steps, cfl, t_final, path, dist=None):
+    """(exception type, text) of a failing run (None if it does not fail)."""
+    s = S.LagfluxSolver(g, bc, path=path, dist=dist)
+    st = G.SolverState(field=f0.copy())
+    try:
+        for _ in range(steps):
+            s.heun_step(st, G.TimeControls(cfl, t_final), t_final)
+    except G.Error as e:  # noqa: PERF203
+        return type(e).__name__, str(e)
+    finally:
+        s.close()
+    return None
+
+
+def errors(ok):
+    """Failures in cells owned by a rank other than 0: every rank reports the
+    reference's exception (type, text with the cell's values) like one handle."""
+    # corrector positivity failure (CFL far beyond stability)
+    g = G.make_grid_2d(24, 16, 0.0, 1.0, 0.0, 1.0)
+    case = CS.Case("q", g, G.BoundaryCondition.uniform(G.TRANSMISSIVE), 1.4, G.SchemeParams(),
+                   4.0, CS.STEP_DRIVEN_LIMIT, 5, "quadrant")
+    f0 = CS.initial_field(case)
+    # a cell with negative energy in the upper rows: "non-positive pressure = <value>"
+    bad = CS.initial_field(CS.quadrant(24, 1))
+    bad[3, 2 + 13, 2 + 7] = -0.25
+    plan = [("positivity", case.bc, f0, case.cfl), ("bad cell", case.bc, bad, 0.45)]
+    for name, bc, f, cfl in plan:
+        for path in ("twopass", "fused", "staged"):
+            single = run_err(g, bc, f, 5, cfl, CS.STEP_DRIVEN_LIMIT, path)
+            for n in (2, 3):
+                uid = S.nccl_unique_id()
+                res = [None] * n
+
+                def worker(r):
+                    res[r] = run_err(g, bc, f, 5, cfl, CS.STEP_DRIVEN_LIMIT, path,
+                                     dist=(r, n, 0, uid))
+
+                ts = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(n)]
+                for t in ts:
+                    t.start()
+                for t in ts:
+                    t.join(300)
+                    if t.is_alive():
+                        print("HANG: a rank did not finish", flush=True)
+                        os._exit(3)
+                good = single is not None and all(x == single for x in res)
+                ok &= good
+                print(f"error {name} {path}: {'ok' if good else 'MISMATCH'} ({n} ranks) "
+                      f"{single} {'' if good else res}", flush=True)
+    return ok
+
+
+def strip5(ok, nranks=8, steps=20):
+    """BASELINE config 5's generator on a 32768 x 2048 periodic strip (dy = dx), 20
+    steps, as `nranks` y-slab ranks == one handle: every step's dt / time / min rho /
+    min p, interior_totals and each rank's rows of the final field.  Ranks download
+    only their own rows (local_host), as bench.py's ranks do."""
+    n, ny = 32768, 2048
+    case = CS.smooth(n, steps, ny=ny, y_extent=ny / n)
+    g = case.grid
+
+    def go(path, dist=None):
+        s = S.LagfluxSolver(g, case.bc, case.gamma, case.params, path=path, dist=dist)
+        st = G.SolverState(field=np.zeros((4, 1, 1)))
+        s.init_fourier(st, case.seed)
+        s.advance(st, G.TimeControls(case.cfl, case.t_final), steps)
+        tot = s.interior_totals()
+        y0, rows = s.local_rows()
+        if dist is None:
+            out = G.new_field(g)
+            s.download(out)
+            part = out[:, g.gy:g.gy + g.ny, g.gx:g.gx + g.nx]
+        else:
+            s.local_host = True
+            out = np.empty(s.local_field_shape())
+            s.download(out)
+            part = out[:, g.gy:g.gy + rows, g.gx:g.gx + g.nx]
+        s.close()
+        diag = [(d.dt, d.time, d.min_rho, d.min_p) for d in st.diagnostics]
+        return part, diag, tot, (y0, rows)
+
+    for path in ("fused", "auto"):
+        single = go(path)
+        uid = S.nccl_unique_id()
+        res = [None] * nranks
+
+        def worker(r):
+            res[r] = go(path, dist=(r, nranks, 0, uid))
+
+        ts = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(nranks)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join(600)
+            if t.is_alive():
+                print("HANG: a rank did not finish", flush=True)
+                os._exit(3)
+        good = len(single[1]) == steps
+        for part, diag, tot, (y0, rows) in res:
+            good &= bool(np.array_equal(part, single[0][:, y0:y0 + rows]))
+            good &= diag == single[1] and tot == single[2]
+        ok &= good
+        print(f"config5 strip {n}x{ny} {path}: {'ok' if good else 'MISMATCH'} ({steps} steps, "
+              f"{nranks} ranks)", flush=True)
+        del single, res
+    return ok
+
+
 def main():
     ok = True
+    if "--errors-only" in sys.argv:
+        sys.exit(0 if errors(ok) else 1)
+    if "--config5-strip" in sys.argv:
+        sys.exit(0 if strip5(ok) else 1)
     smooth = CS.smooth(64, 1, ny=48, y_extent=48 / 64)
     quad = CS.quadrant(48, 1)
     sedov = CS.sedov(40, 1)
@@ -112,6 +224,7 @@ def main():
     args = (c.grid, c.bc, c.gamma, c.params, f0, 10, c.cfl, c.t_final)
     single = run(*args, path="twopass", ms=ms, m0=m0)
     ok &= compare("triple point", c.grid, single, dist_run(2, *args, path="twopass", ms=ms, m0=m0))
+    ok = errors(ok)
     sys.exit(0 if ok else 1)
 
 

@@ -77,6 +77,21 @@ void run_pair(const char* name, const CartesianGrid& g, const BoundaryCondition&
   a.field = f0;
   b.field = f0;
   for (int s = 0; s < steps && a.time < limit; ++s) {
+    if (s == steps / 2) {
+      // a diagnostic compute_dt of another field between steps must not disturb
+      // the resident state (with or without auto_sync)
+      expect(ref.compute_dt(f0, controls, 0.0, 1e30) == gpu.compute_dt(f0, controls, 0.0, 1e30),
+             std::string(name) + ": compute_dt between steps");
+      if (auto_sync) {
+        // state.field is authoritative with auto_sync: a host edit between steps
+        // (one cell scaled by 1.5: same velocity, 1.5x pressure) must be seen
+        const std::size_t k = std::size_t(g.gy + g.ny / 2) * std::size_t(g.nxt()) + std::size_t(g.gx + g.nx / 3);
+        for (int c = 0; c < 4; ++c) {
+          a.field.comp[size_t(c)][k] *= 1.5;
+          b.field.comp[size_t(c)][k] *= 1.5;
+        }
+      }
+    }
     const double da = ref.heun_step(a, controls, limit);
     const double db = gpu.heun_step(b, controls, limit);
     if (da != db) {

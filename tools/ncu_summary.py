@@ -66,6 +66,10 @@ def full(rep, label=""):
             "warps_active_pct": _f(r, hdr, "sm__warps_active.avg.pct_of_peak_sustained_active"),
             "registers": _f(r, hdr, "launch__registers_per_thread"),
             "inst_executed": _f(r, hdr, "smsp__inst_executed.sum"),
+            # fp64 arithmetic, thread level (a DFMA counts once)
+            "fp64_thread_inst": {op: _f(r, hdr, f"sm__sass_thread_inst_executed_op_{op}_pred_on.sum")
+                                 for op in ("dadd", "dmul", "dfma")},
+            "fp64_pipe_warp_inst": _f(r, hdr, "sm__inst_executed_pipe_fp64.sum"),
             "top_stalls_pct": top,
         })
     return {"label": label, "report": rep, "kernels": out}
@@ -105,8 +109,32 @@ def launches(path, title):
     return "\n".join(lines) + "\n"
 
 
+def fp64_ops(rep, cells, key, label, out_json):
+    """Merge {key: fp64 instructions per cell-update} of the first captured kernel of
+    `rep` (one Heun step over `cells` cells) into out_json (profiles/fp64_ops.json,
+    read by bench.py for the fp64 roofline)."""
+    k = full(rep)["kernels"][0]
+    ops = sum(v for v in k["fp64_thread_inst"].values() if v)
+    try:
+        d = json.load(open(out_json))
+    except (OSError, ValueError):
+        d = {}
+    d[key] = {"kernel": k["kernel"].split("(")[0], "fp64_ops_per_cell_update": ops / cells,
+              "by_op_per_cell_update": {o: (v or 0) / cells for o, v in k["fp64_thread_inst"].items()},
+              "fp64_pipe_warp_inst_per_cell_update": (k["fp64_pipe_warp_inst"] or 0) / cells,
+              "inst_executed_per_cell_update": (k["inst_executed"] or 0) / cells,
+              "duration_ms": k["duration_ms"], "fp64_pipe_pct": k["fp64_pipe_pct"],
+              "issue_active_pct": k["issue_active_pct"], "registers": k["registers"],
+              "top_stalls_pct": k["top_stalls_pct"], "source": label}
+    json.dump(d, open(out_json, "w"), indent=1)
+    return d[key]
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "full":
+    if sys.argv[1] == "fp64ops":
+        print(json.dumps(fp64_ops(sys.argv[2], float(sys.argv[3]), sys.argv[4], sys.argv[5],
+                                  sys.argv[6]), indent=1))
+    elif sys.argv[1] == "full":
         print(json.dumps(full(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else ""), indent=1))
     else:
         print(launches(sys.argv[2], sys.argv[3]))
