@@ -715,6 +715,20 @@ int guarded(lf_handle* h, F&& f) {
 
 namespace lfb {
 void fill_all_public(lf_handle* h, double* SlabState::*buf) { fill_all(h, buf); }
+// fill_all's single-launch ghost fill without the halo exchange (the caller
+// exchanges the halos itself, e.g. overlapped with interior work); false if the
+// single-launch fill does not apply (then nothing was done)
+bool fill_local_public(lf_handle* h, double* SlabState::*buf) {
+  const int xbc[4] = {h->d.bc[0], h->d.bc[1], h->d.bc[2], h->d.bc[3]};
+  for (auto& s : h->slabs)
+    if (!(s.L.nx >= NG && (!h->dim2 || s.L.ny >= NG))) return false;
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    launch_fill_xy(s.field(s.*buf), s.L, xbc, s.sl, h->dim2, s.stream, 4, 1, 2, nullptr, 0);
+  }
+  CK(cudaGetLastError());
+  return true;
+}
 void fill_partials_public(lf_handle* h, double* SlabState::*buf) { fill_partials(h, buf); }
 void fill_state_public(lf_handle* h, double* SlabState::*ubuf, double* SlabState::*pbuf) {
   fill_all(h, ubuf, 4, 1, 2, pbuf, h->mc.n);

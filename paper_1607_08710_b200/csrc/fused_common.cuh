@@ -53,6 +53,7 @@ struct FusedArgs {
   int y0g;                        // global row of local row 0
   int nyg;                        // global rows
   int rows_per_chunk;
+  int chunk0, chunk_step;         // row chunk of block y: chunk0 + blockIdx.y * chunk_step
   double gamma, gm1, beta, dx, dy;
   double cfl, limit;
   int bc_xlo, bc_xhi, bc_ylo, bc_yhi;

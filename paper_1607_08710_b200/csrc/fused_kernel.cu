@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
   const bool is_p = threadIdx.x < NC;
   const int x0 = blockIdx.x * TXO;
   const int c = x0 - 4 + t;                      // this thread's column
-  const int y0 = blockIdx.y * a.rows_per_chunk;  // chunk output rows [y0, y1)
+  const int y0 = (a.chunk0 + (int)blockIdx.y * a.chunk_step) * a.rows_per_chunk;  // rows [y0, y1)
   const int y1 = min(y0 + a.rows_per_chunk, a.ny);
   const int nit = (y1 - y0) + 9;
   const int klastp = (y1 - y0) + 7;              // last P iteration (input row y1+3)

@@ -64,6 +64,10 @@ struct FusedState {
   // rewritten two steps later, after ev_out[b])
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fin[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  // distributed fused step: halo exchange and the slab's edge row chunks on `comm`,
+  // overlapped with the interior chunks on the slab stream
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_fill = nullptr, ev_edge = nullptr;
 };
 
 static FusedState* fstate(lf_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
@@ -150,6 +154,11 @@ static void fused_alloc(lf_handle* h, int steps) {
       FK(cudaEventCreateWithFlags(&f->ev_fin[b], cudaEventDisableTiming));
       FK(cudaEventCreateWithFlags(&f->ev_out[b], cudaEventDisableTiming));
     }
+    if (h->nccl) {
+      FK(cudaStreamCreateWithPriority(&f->comm, cudaStreamNonBlocking, hi));
+      FK(cudaEventCreateWithFlags(&f->ev_fill, cudaEventDisableTiming));
+      FK(cudaEventCreateWithFlags(&f->ev_edge, cudaEventDisableTiming));
+    }
     launch_acc_init(f->acc, s0.stream);
     fused_configure();
     fused_configure_contract();
@@ -217,6 +226,12 @@ void fused_release(lf_handle* h) {
     if (f->ev_fin[b]) cudaEventDestroy(f->ev_fin[b]);
     if (f->ev_out[b]) cudaEventDestroy(f->ev_out[b]);
   }
+  if (f->comm) {
+    cudaStreamSynchronize(f->comm);
+    cudaStreamDestroy(f->comm);
+  }
+  if (f->ev_fill) cudaEventDestroy(f->ev_fill);
+  if (f->ev_edge) cudaEventDestroy(f->ev_edge);
   delete f;
   h->fused = nullptr;
 }
@@ -268,14 +283,32 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   // bnd slot `cur` is free once the outflow sums of two steps ago have read it
   FK(cudaStreamWaitEvent(s0.stream, f->ev_out[cur], 0));
   const bool mat = h->mc.n > 0;   // (materials run on the two-pass kernels only)
-  if (mat)
-    fill_state_public(h, &SlabState::U, &SlabState::P);
-  else
-    fill_all_public(h, &SlabState::U);
+  const bool twopass = use_twopass(h);
+  // the outflow sums of a periodic axis are +0.0 without reading the faces
+  // (k_outflow), so their faces are neither cleared nor summed across ranks
+  const bool sum_x = !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC);
+  const bool sum_y = !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC);
   double* bnd = f->bnd + (size_t)cur * bnd_words(h);
-  if (h->nccl) FK(cudaMemsetAsync(bnd, 0, bnd_words(h) * sizeof(double), s0.stream));
+  // distributed one-kernel step: the halo rows travel on the comm stream while the
+  // slab's interior row chunks (which read no halo row) run on the slab stream; the
+  // two edge chunks follow the exchange on the comm stream
+  const bool overlap = h->nccl && !twopass && !mat && f->comm &&
+                       fill_local_public(h, &SlabState::U);
+  if (!overlap) {
+    if (mat)
+      fill_state_public(h, &SlabState::U, &SlabState::P);
+    else
+      fill_all_public(h, &SlabState::U);
+  }
+  if (h->nccl && (sum_x || sum_y))
+    FK(cudaMemsetAsync(bnd, 0, bnd_words(h) * sizeof(double), s0.stream));
+  if (overlap) {
+    FK(cudaEventRecord(f->ev_fill, s0.stream));
+    FK(cudaStreamWaitEvent(f->comm, f->ev_fill, 0));
+    nccl_exchange_halos(h, &SlabState::U, 4, f->comm);
+  }
   if (k0) FK(cudaEventRecord(k0, s0.stream));
-  if (use_twopass(h)) {
+  if (twopass) {
     // two passes: predictor U^n -> U*, F^n; ghosts / halos of U*; corrector.
     // time_order 1: one pass, the corrector kernels as the single forward-Euler
     // stage (input and base U^n, no Heun average; solver.cpp:510-514)
@@ -339,7 +372,7 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
     }
   }
   for (auto& s : h->slabs) {
-    if (use_twopass(h)) break;
+    if (twopass) break;
     FusedArgs a;
     a.u = s.U + s.L.origin();
     a.un = s.U2 + s.L.origin();
@@ -350,6 +383,8 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
     a.y0g = s.sl.y0;
     a.nyg = h->d.ny;
     a.rows_per_chunk = f->rows_per_chunk;
+    a.chunk0 = 0;
+    a.chunk_step = 1;
     a.gamma = h->k.gamma;
     a.gm1 = h->k.gm1;
     a.beta = h->k.beta;
@@ -366,18 +401,37 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
     a.ctl = f->ctl + cur;
     a.acc = f->acc + cur;
     a.bnd = bnd;
-    dim3 grid((h->d.nx + FUSED_TXO - 1) / FUSED_TXO,
-              (s.L.ny + f->rows_per_chunk - 1) / f->rows_per_chunk);
-    if (h->math == LF_MATH_CONTRACT)
-      launch_fused_step_contract(a, h->d.spatial_order >= 2, grid, s.stream);
-    else
-      launch_fused_step(a, h->d.spatial_order >= 2, grid, s.stream);
+    const int strips = (h->d.nx + FUSED_TXO - 1) / FUSED_TXO;
+    const int chunks = (s.L.ny + f->rows_per_chunk - 1) / f->rows_per_chunk;
+    const bool contract = h->math == LF_MATH_CONTRACT;
+    const bool muscl = h->d.spatial_order >= 2;
+    auto launch = [&](int c0, int step, int n, cudaStream_t st) {
+      if (n <= 0) return;
+      a.chunk0 = c0;
+      a.chunk_step = step;
+      if (contract)
+        launch_fused_step_contract(a, muscl, dim3(strips, n), st);
+      else
+        launch_fused_step(a, muscl, dim3(strips, n), st);
+    };
+    if (overlap && chunks >= 3) {
+      launch(1, 1, chunks - 2, s.stream);                 // interior chunks
+      launch(0, chunks - 1, 2, f->comm);                  // first and last, after the halos
+      FK(cudaEventRecord(f->ev_edge, f->comm));
+      FK(cudaStreamWaitEvent(s.stream, f->ev_edge, 0));
+    } else {
+      if (overlap) {
+        FK(cudaEventRecord(f->ev_edge, f->comm));
+        FK(cudaStreamWaitEvent(s.stream, f->ev_edge, 0));
+      }
+      launch(0, 1, chunks, s.stream);
+    }
   }
   if (k1) FK(cudaEventRecord(k1, s0.stream));
   FK(cudaGetLastError());
-  if (h->nccl) nccl_reduce_step(h, f->acc + cur, STEP_ACC_WORDS, bnd, bnd_words(h));
-  const bool sum_x = !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC);
-  const bool sum_y = !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC);
+  if (h->nccl)
+    nccl_reduce_step(h, f->acc + cur, STEP_ACC_WORDS, bnd, sum_x ? 8 * (size_t)h->d.ny : 0,
+                     bnd + 8 * (size_t)h->d.ny, sum_y ? 8 * (size_t)h->d.nx : 0);
   launch_finalize(f->ctl + cur, f->acc + cur, f->ctl + nxt, f->rec + n_in_batch, f->outflow,
                   !sum_x && !sum_y, h->d.dx, h->d.dy, cfl, limit, t_final, s0.stream);
   if (sum_x || sum_y) {

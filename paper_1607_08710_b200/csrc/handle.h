@@ -83,6 +83,7 @@ struct lf_handle {
 namespace lfb {
 // api.cu services used by the fused path
 void fill_all_public(lf_handle* h, double* SlabState::*buf);
+bool fill_local_public(lf_handle* h, double* SlabState::*buf);
 void fill_partials_public(lf_handle* h, double* SlabState::*buf);
 // conserved field and partial densities together (one fill launch per slab)
 void fill_state_public(lf_handle* h, double* SlabState::*ubuf, double* SlabState::*pbuf);

@@ -126,8 +126,9 @@ void nccl_destroy(lf_handle* h) {
 // ring (both neighbours are the same peer): A sends the bottom NG rows down and
 // receives the top halo from above; B sends the top rows up and receives the
 // bottom halo from below.  Rows are whole padded rows (x ghosts included).
-void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf, int ncomp) {
+void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf, int ncomp, cudaStream_t st) {
   SlabState& s = h->slabs[0];
+  if (!st) st = s.stream;
   const bool periodic = h->d.bc[2] == LF_PERIODIC;
   const int R = h->nranks, r = h->rank;
   const int lo = r > 0 ? r - 1 : (periodic ? R - 1 : -1);
@@ -137,13 +138,13 @@ void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf, int ncomp) {
   auto rows = [&](int c, int row) { return base + c * s.L.fstride + (int64_t)row * s.L.pitch; };
   nck(g_api.GroupStart(), "ncclGroupStart");
   for (int c = 0; c < ncomp; ++c) {  // phase A
-    if (lo >= 0) nck(g_api.Send(rows(c, 0), n, ncclFloat64, lo, h->nccl->comm, s.stream), "ncclSend");
-    if (hi >= 0) nck(g_api.Recv(rows(c, s.L.ny), n, ncclFloat64, hi, h->nccl->comm, s.stream), "ncclRecv");
+    if (lo >= 0) nck(g_api.Send(rows(c, 0), n, ncclFloat64, lo, h->nccl->comm, st), "ncclSend");
+    if (hi >= 0) nck(g_api.Recv(rows(c, s.L.ny), n, ncclFloat64, hi, h->nccl->comm, st), "ncclRecv");
   }
   for (int c = 0; c < ncomp; ++c) {  // phase B
     if (hi >= 0)
-      nck(g_api.Send(rows(c, s.L.ny - NG), n, ncclFloat64, hi, h->nccl->comm, s.stream), "ncclSend");
-    if (lo >= 0) nck(g_api.Recv(rows(c, -NG), n, ncclFloat64, lo, h->nccl->comm, s.stream), "ncclRecv");
+      nck(g_api.Send(rows(c, s.L.ny - NG), n, ncclFloat64, hi, h->nccl->comm, st), "ncclSend");
+    if (lo >= 0) nck(g_api.Recv(rows(c, -NG), n, ncclFloat64, lo, h->nccl->comm, st), "ncclRecv");
   }
   nck(g_api.GroupEnd(), "ncclGroupEnd");
 }
@@ -235,13 +236,18 @@ void nccl_gather_boundary(lf_handle* h, double* left, double* right, double* bot
 
 namespace lfb {
 
-void nccl_reduce_step(lf_handle* h, void* acc_u64, int n, double* bnd, size_t nbnd) {
+void nccl_reduce_step(lf_handle* h, void* acc_u64, int n, double* bnd_x, size_t nbnd_x,
+                      double* bnd_y, size_t nbnd_y) {
   SlabState& s = h->slabs[0];
   nck(g_api.GroupStart(), "ncclGroupStart");
   nck(g_api.AllReduce(acc_u64, acc_u64, (size_t)n, ncclUint64, ncclMax, h->nccl->comm, s.stream),
       "ncclAllReduce(step)");
-  nck(g_api.AllReduce(bnd, bnd, nbnd, ncclFloat64, ncclSum, h->nccl->comm, s.stream),
-      "ncclAllReduce(boundary)");
+  if (nbnd_x)
+    nck(g_api.AllReduce(bnd_x, bnd_x, nbnd_x, ncclFloat64, ncclSum, h->nccl->comm, s.stream),
+        "ncclAllReduce(boundary x)");
+  if (nbnd_y)
+    nck(g_api.AllReduce(bnd_y, bnd_y, nbnd_y, ncclFloat64, ncclSum, h->nccl->comm, s.stream),
+        "ncclAllReduce(boundary y)");
   nck(g_api.GroupEnd(), "ncclGroupEnd");
 }
 

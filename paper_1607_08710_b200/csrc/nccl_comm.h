@@ -14,12 +14,17 @@ namespace lfb {
 int nccl_unique_id(void* id128);
 int nccl_init(lf_handle* h, const void* id128);
 void nccl_destroy(lf_handle* h);
-void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf, int ncomp = 4);
+// halo rows of `buf` with the y-neighbours, on `st` (default: the slab stream)
+void nccl_exchange_halos(lf_handle* h, double* SlabState::*buf, int ncomp = 4,
+                         cudaStream_t st = nullptr);
 void nccl_combine_scalars(lf_handle* h, Scalars* s);
 void nccl_max_u64(lf_handle* h, unsigned long long* v, int n);
 // fused step: max-reduce n u64 step accumulators and sum-reduce the boundary
 // faces (nbnd doubles, each rank owns disjoint entries, zero elsewhere) in place
-void nccl_reduce_step(lf_handle* h, void* acc_u64, int n, double* bnd, size_t nbnd);
+// the step accumulators (max over ranks) and the boundary-face segments the outflow
+// sums need (disjoint per rank, so a sum; nbnd_x / nbnd_y = 0 skips a segment)
+void nccl_reduce_step(lf_handle* h, void* acc_u64, int n, double* bnd_x, size_t nbnd_x,
+                      double* bnd_y, size_t nbnd_y);
 // ordered chains over the ranks (interior totals): rank r-1 -> rank r, n doubles
 void nccl_recv_prev(lf_handle* h, double* d, int n);
 void nccl_send_next(lf_handle* h, const double* d, int n);

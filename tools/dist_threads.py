@@ -108,7 +108,7 @@ def errors(ok):
                    4.0, CS.STEP_DRIVEN_LIMIT, 5, "quadrant")
     f0 = CS.initial_field(case)
     # a cell with negative energy in the upper rows: "non-positive pressure = <value>"
-    bad = CS.initial_field(CS.quadrant(24, 1))
+    bad = f0.copy()
     bad[3, 2 + 13, 2 + 7] = -0.25
     plan = [("positivity", case.bc, f0, case.cfl), ("bad cell", case.bc, bad, 0.45)]
     for name, bc, f, cfl in plan:

@@ -67,7 +67,10 @@ def full(rep, label=""):
             "registers": _f(r, hdr, "launch__registers_per_thread"),
             "inst_executed": _f(r, hdr, "smsp__inst_executed.sum"),
             # fp64 arithmetic, thread level (a DFMA counts once)
-            "fp64_thread_inst": {op: _f(r, hdr, f"sm__sass_thread_inst_executed_op_{op}_pred_on.sum")
+            # (--set full carries the per-cycle rates: x the elapsed cycles of an SMSP)
+            "fp64_thread_inst": {op: (_f(r, hdr, f"smsp__sass_thread_inst_executed_op_{op}_pred_on"
+                                                 ".sum.per_cycle_elapsed") or 0.0)
+                                 * (_f(r, hdr, "smsp__cycles_elapsed.avg") or 0.0)
                                  for op in ("dadd", "dmul", "dfma")},
             "fp64_pipe_warp_inst": _f(r, hdr, "sm__inst_executed_pipe_fp64.sum"),
             "top_stalls_pct": top,
