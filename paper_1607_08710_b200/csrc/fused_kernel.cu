@@ -27,6 +27,8 @@
 //    error (kind, smallest index, text) and state semantics.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "../../include/lagflux_b200.h"
 #include "fastmath.cuh"
 #include "fused_common.cuh"
@@ -177,16 +179,29 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 
   unsigned fail = const_in_box(a.gamma, a.gm1) ? 0u : 1u;
 
+  // Row iterations k = 0 .. nit-1 run in three ranges.  The first KS and the last
+  // few (k > ksteady) see the chunk's pipeline fill / drain, the domain's y edges
+  // (ghost-row images, rows outside the slab) and the bottom / top boundary faces;
+  // they take the guarded body (G = true).  In between every guard is true, so the
+  // steady body (G = false) drops them: no default states, no row-range tests in
+  // the failure checks, no per-row predicates -- the same values, fewer instructions.
+  constexpr int KS = 10;
+  const int ksteady = (y1 - y0) + 3;   // last steady iteration (input row y1 - 1)
+
   if (is_p) {
     // ================================================================ stage 1 (P)
     double wm2[4] = {1.0, 0.0, 0.0, 1.0}, wm1[4] = {1.0, 0.0, 0.0, 1.0};
     double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fyprev[4] = {0.0, 0.0, 0.0, 0.0};
     // this thread owns x-face (t-1 | t), needed for U* up to column nx+1
     const bool dox = t >= 2 && t <= NC - 2 && c <= a.nx + 2;
-    for (int k = 0; k < nit; ++k) {
+    const bool xchk = dox && c >= 0 && c <= a.nx;          // kept x-face of the grid
+    const bool upd = t >= 2 && t <= NC - 3;                // lanes with a kept U* column
+    const int tl = t > 0 ? t - 1 : t, tr = t < NC - 1 ? t + 1 : t;   // clamped x neighbours
+    auto iter = [&](const int k, auto guard) {
+      constexpr bool G = decltype(guard)::value;
       const int r = y0 - 4 + k;
-      const bool p_active = k <= klastp;
-      if (threadIdx.x == 0 && k + PREFETCH <= klastp) {
+      const bool p_active = !G || k <= klastp;
+      if (threadIdx.x == 0 && (!G || k + PREFETCH <= klastp)) {
         // the slot's previous row (k+PREFETCH-URING) was last read before the
         // previous iteration's __syncthreads
         const int kn = k + PREFETCH, s = kn & (URING - 1);
@@ -196,19 +211,23 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           tma_row(sU + (s * 4 + q) * NC, src0 + (int64_t)kn * a.pitch + q * a.fstride, row_bytes,
                   &mbar[s]);
       }
-      double w[4] = {1.0, 0.0, 0.0, 1.0};
-      double ylo[4] = {1.0, 0.0, 0.0, 1.0}, yhi[4] = {1.0, 0.0, 0.0, 1.0};
+      double w[4], ylo[4], yhi[4];
+      if (G) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = ylo[q] = yhi[q] = (q == 0 || q == 3) ? 1.0 : 0.0;
+      }
       if (p_active) {
-        // -- U^n(r) -> W(r) (solver.cpp:145-163)
+        // -- U^n(r) -> W(r) (solver.cpp:145-163); lanes past the grid's ghost columns
+        //    (last strip) compute on don't-care values no kept result depends on
         mbar_wait(&mbar[k & (URING - 1)], (k / URING) & 1);
-        if (col_in_mem) {
+        if (!G || col_in_mem) {
           const double* u = sU + (k & (URING - 1)) * 4 * NC + t;
           const double r0 = u[0], m1 = u[NC], m2 = u[2 * NC], e3 = u[3 * NC];
           bool okw = true;  // implied by the box
           prim_fast(r0, m1, m2, e3, a.gm1, w, okw);
-          if (!cell_in_box(w) && col_interior && r >= 0 && r < a.ny) fail = 1;
+          if (!cell_in_box(w) && col_interior && (!G || (r >= 0 && r < a.ny))) fail = 1;
         }
-        if (k >= 2) {
+        if (!G || k >= 2) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             sWx[q * NC + t] = wm2[q];  // row r-2 for the x direction
@@ -217,22 +236,32 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         }
       }
       bar_named(1);
-      double xlo[4] = {1.0, 0.0, 0.0, 1.0};
-      if (p_active && k >= 2 && t >= 1 && t <= NC - 2) {
+      double xlo[4];
+      if (G) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xlo[q] = (q == 0 || q == 3) ? 1.0 : 0.0;
+      }
+      if (G ? (p_active && k >= 2 && t >= 1 && t <= NC - 2) : true) {
+        // (steady: the edge lanes use a clamped neighbour; their traces are unused)
+        const int il = G ? t - 1 : tl, ir = G ? t + 1 : tr;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           double hi;
-          cell_traces<MUSCL>(sWx[q * NC + t - 1], sWx[q * NC + t], sWx[q * NC + t + 1], a.beta,
-                             xlo[q], hi);
+          cell_traces<MUSCL>(sWx[q * NC + il], sWx[q * NC + t], sWx[q * NC + ir], a.beta, xlo[q],
+                             hi);
           sTx[q * NC + t] = hi;
         }
       }
       bar_named(1);
-      double fy[4] = {0.0, 0.0, 0.0, 0.0};
-      if (p_active && k >= 2) {
+      double fy[4];
+      if (G) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fy[q] = 0.0;
+      }
+      if (!G || (p_active && k >= 2)) {
         // x-face (t-1 | t) of row r-2 and y-face (r-2 | r-1)
 #if LF_FUSED_DONTCARE_P
-        const int tm = t > 0 ? t - 1 : t;   // lanes without a kept x-face: unused
+        const int tm = tl;   // lanes without a kept x-face: unused
 #else
         const int tm = dox ? t - 1 : t;
 #endif
@@ -259,16 +288,17 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         // a trace-positivity failure on a consumed face hands the step to the
         // stage-wise IEEE kernels (halo lanes and columns past the grid hold
         // dummy states and never count)
-        if (dox) {
-          if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && r - 2 >= 0 &&
-              r - 2 < a.ny)
-            fail = 1;
+        if (G ? (xchk && r - 2 >= 0 && r - 2 < a.ny) : xchk) {
+          if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3])) fail = 1;
+        }
+        if (!G || dox) {
+          // (steady: every lane stores; faces outside dox are never read for a kept value)
 #pragma unroll
           for (int q = 0; q < 4; ++q) sFnx[((k & 3) * 4 + q) * NC + t] = fx[q];
         }
-        if (k >= 3) {
-          if (!traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && col_interior && r - 1 >= 0 &&
-              r - 1 <= a.ny)
+        if (!G || k >= 3) {
+          if (!traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && col_interior &&
+              (!G || (r - 1 >= 0 && r - 1 <= a.ny)))
             fail = 1;
 #pragma unroll
           for (int q = 0; q < 4; ++q) sFny[((k & 3) * 4 + q) * NC + t] = fy[q];
@@ -278,8 +308,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       }
       bar_named(1);
       // -- predictor U*(r-2) (solver.cpp:283-291 with one flux set), then its
-      //    primitives W*(r-2) (build_primitives of predictor_, solver.cpp:505)
-      if (p_active && k >= 4 && t >= 2 && t <= NC - 3 && col_in_mem) {
+      //    primitives W*(r-2) (build_primitives of predictor_, solver.cpp:505);
+      //    steady: every lane (edge lanes read neighbouring smem, their W* is unused)
+      if (G ? (p_active && k >= 4 && upd && col_in_mem) : true) {
         const int row = r - 2;
         const double* ub = sU + ((k - 2) & (URING - 1)) * 4 * NC + t;
         double v[4];
@@ -296,7 +327,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         prim_fast(v[0], v[1], v[2], v[3], a.gm1, ws, okw);
 #pragma unroll
         for (int q = 0; q < 4; ++q) sWs[((k & 1) * 4 + q) * NC + t] = ws[q];
-        if (col_interior && row >= 0 && row < a.ny) {
+        if (upd && col_interior && (!G || (row >= 0 && row < a.ny))) {
           // e_int = v3 - (0.5 (v1^2 + v2^2)) / v0 > 0 (solver.cpp:300-302), tested
           // without the division: v3 v0 > K (1 + 2^-48) implies it; else flag
           // (conservative: the stage-wise re-run decides exactly)
@@ -306,7 +337,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           if (!cell_in_box(ws)) fail = 1;
         }
       }
-      if (p_active && k >= 3) {
+      if (!G || (p_active && k >= 3)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) fyprev[q] = fy[q];
       }
@@ -318,7 +349,11 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         }
       }
       __syncthreads();
-    }
+    };
+    int k = 0;
+    for (; k < KS && k < nit; ++k) iter(k, std::true_type{});
+    for (; k <= ksteady; ++k) iter(k, std::false_type{});
+    for (; k < nit; ++k) iter(k, std::true_type{});
   } else {
     // ================================================================ stage 2 (C)
     double vm2[4] = {1.0, 0.0, 0.0, 1.0}, vm1[4] = {1.0, 0.0, 0.0, 1.0};
@@ -342,13 +377,21 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
     const int src_c = min(max(src_t, 2), NC - 3);
     const unsigned long long flip_bits = flip_u ? 0x8000000000000000ull : 0ull;
     const bool dox = t >= 4 && t <= NC - 4 && c <= a.nx;  // x-faces of output cells
+    const bool xchk = dox && c >= 0;
+    const bool upd = t >= 4 && t <= NC - 5 && col_interior;   // output cells
+    const int tl = t > 0 ? t - 1 : t, tr = t < NC - 1 ? t + 1 : t;   // clamped x neighbours
     const bool x_edge_blk = x0 - 4 <= 0 || x0 - 4 + NC > a.nx - 1;   // holds column 0 or nx-1
-    for (int k = 0; k < nit; ++k) {
+    const bool dxy_box = pos_in_box(a.dx) && pos_in_box(a.dy);
+    auto iter = [&](const int k, auto guard) {
+      constexpr bool G = decltype(guard)::value;
       const int aa = y0 - 7 + k;   // W* row consumed this iteration
       const int j = aa - 2;        // U^{n+1} row finished this iteration
-      const bool c_active = k >= 5;
-      double w[4] = {1.0, 0.0, 0.0, 1.0};
-      double ylo[4] = {1.0, 0.0, 0.0, 1.0}, yhi[4] = {1.0, 0.0, 0.0, 1.0};
+      const bool c_active = !G || k >= 5;
+      double w[4], ylo[4], yhi[4];
+      if (G) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = ylo[q] = yhi[q] = (q == 0 || q == 3) ? 1.0 : 0.0;
+      }
       if (c_active) {
         // -- W*(aa) with the boundary images of the reference's ghost fill of
         //    predictor_ (grid.cpp:72-114); a reflective image negates the normal
@@ -360,43 +403,42 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           w[2] = ws[2 * NC];
           w[3] = ws[3 * NC];
         }
-        // the ghost-row images below are block-uniform and rare: one branch around them
-        // instead of predicated selects on every row
-        if ((bottom_edge && aa <= 1) || (top_edge && aa >= a.ny)) {
-        if (bottom_edge && aa == 0) {
-          // W*(-1) = image of W*(0)
+        // the ghost-row images below are block-uniform and rare (guarded iterations only)
+        if (G && ((bottom_edge && aa <= 1) || (top_edge && aa >= a.ny))) {
+          if (bottom_edge && aa == 0) {
+            // W*(-1) = image of W*(0)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) vm1[q] = w[q];
-          if (a.bc_ylo == LF_REFLECTIVE) vm1[2] = -vm1[2];
-        }
-        if (bottom_edge && aa == 1) {
-          // hi trace of ghost row -1 from W*(-2) = image(W*(1) or W*(0)), W*(-1), W*(0)
-          double g2[4];
+            for (int q = 0; q < 4; ++q) vm1[q] = w[q];
+            if (a.bc_ylo == LF_REFLECTIVE) vm1[2] = -vm1[2];
+          }
+          if (bottom_edge && aa == 1) {
+            // hi trace of ghost row -1 from W*(-2) = image(W*(1) or W*(0)), W*(-1), W*(0)
+            double g2[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) g2[q] = a.bc_ylo == LF_REFLECTIVE ? w[q] : vm1[q];
-          if (a.bc_ylo == LF_REFLECTIVE) g2[2] = -g2[2];
+            for (int q = 0; q < 4; ++q) g2[q] = a.bc_ylo == LF_REFLECTIVE ? w[q] : vm1[q];
+            if (a.bc_ylo == LF_REFLECTIVE) g2[2] = -g2[2];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            double lo;
-            cell_traces<MUSCL>(g2[q], vm2[q], vm1[q], a.beta, lo, hiprev[q]);
+            for (int q = 0; q < 4; ++q) {
+              double lo;
+              cell_traces<MUSCL>(g2[q], vm2[q], vm1[q], a.beta, lo, hiprev[q]);
+            }
+          }
+          if (top_edge && aa == a.ny) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              w[q] = vm1[q];
+              sStash[q * NC + t] = a.bc_yhi == LF_REFLECTIVE ? vm2[q] : vm1[q];
+            }
+            if (a.bc_yhi == LF_REFLECTIVE) {
+              w[2] = -w[2];
+              sStash[2 * NC + t] = -sStash[2 * NC + t];
+            }
+          } else if (top_edge && aa == a.ny + 1) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = sStash[q * NC + t];
           }
         }
-        if (top_edge && aa == a.ny) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            w[q] = vm1[q];
-            sStash[q * NC + t] = a.bc_yhi == LF_REFLECTIVE ? vm2[q] : vm1[q];
-          }
-          if (a.bc_yhi == LF_REFLECTIVE) {
-            w[2] = -w[2];
-            sStash[2 * NC + t] = -sStash[2 * NC + t];
-          }
-        } else if (top_edge && aa == a.ny + 1) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) w[q] = sStash[q * NC + t];
-        }
-        }
-        if (k >= 7) {
+        if (!G || k >= 7) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             sWc[q * NC + t] = vm2[q];  // row j = aa-2 for the x direction
@@ -405,25 +447,34 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         }
       }
       bar_named(2);
-      double xlo[4] = {1.0, 0.0, 0.0, 1.0};
-      if (c_active && k >= 9 && t >= 3 && t <= NC - 4) {
+      double xlo[4];
+      if (G) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xlo[q] = (q == 0 || q == 3) ? 1.0 : 0.0;
+      }
+      if (G ? (c_active && k >= 9 && t >= 3 && t <= NC - 4) : true) {
+        // (steady: the edge lanes use a clamped neighbour; their traces are unused)
+        const int il = G ? t - 1 : tl, ir = G ? t + 1 : tr;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           double hi;
-          cell_traces<MUSCL>(sWc[q * NC + t - 1], sWc[q * NC + t], sWc[q * NC + t + 1], a.beta,
-                             xlo[q], hi);
+          cell_traces<MUSCL>(sWc[q * NC + il], sWc[q * NC + t], sWc[q * NC + ir], a.beta, xlo[q],
+                             hi);
           sTc[q * NC + t] = hi;
         }
       }
       bar_named(2);
-      double fc[4] = {0.0, 0.0, 0.0, 0.0};
-      if (c_active && k >= 7) {
-        const bool dx_ = dox && k >= 9;
+      double fc[4];
+      if (G) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) fc[q] = 0.0;
+      }
+      if (!G || (c_active && k >= 7)) {
+        const bool dx_ = dox && (!G || k >= 9);
         // a lane without a kept x-face reads its left neighbour's trace anyway (unused)
-        const int tm = t > 0 ? t - 1 : t;
         double mx[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) mx[q] = sTc[q * NC + tm];
+        for (int q = 0; q < 4; ++q) mx[q] = sTc[q * NC + tl];
         double fx[4], fs[4];
         bool okx = true, oky = true;  // implied by the cell box (face_fast.cuh): unused
         double psx, usx, psy, usy;
@@ -437,17 +488,18 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         if (needs_mean(usy))
           face_mean<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2],
                        ylo[3], psy, usy, C, fs, oky);
-        if (dx_) {
-          if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3]) && c >= 0 && c <= a.nx && j >= 0 &&
-              j < a.ny)
-            fail = 1;
+        if (G ? (dx_ && c >= 0 && j >= 0 && j < a.ny) : xchk) {
+          if (!traces_ok(mx[0], mx[3], xlo[0], xlo[3])) fail = 1;
+        }
+        if (!G || dx_) {
+          // (steady: every lane stores; the update reads the faces of dox lanes only)
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             sFc[q * NC + t] = 0.5 * (sFnx[(((k + 1) & 3) * 4 + q) * NC + t] + fx[q]);
         }
-        if (k >= 8) {
-          if (!traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && col_interior && aa - 1 >= 0 &&
-              aa - 1 <= a.ny)
+        if (!G || k >= 8) {
+          if (!traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && col_interior &&
+              (!G || (aa - 1 >= 0 && aa - 1 <= a.ny)))
             fail = 1;
 #pragma unroll
           for (int q = 0; q < 4; ++q) fc[q] = 0.5 * (sFny[(((k + 1) & 3) * 4 + q) * NC + t] + fs[q]);
@@ -457,7 +509,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       }
       bar_named(2);
       // -- corrector U^{n+1}(j) (solver.cpp:283-291, two flux sets) + epilogue
-      if (c_active && k >= 9 && t >= 4 && t <= NC - 5 && col_interior) {
+      if (upd && (!G || (c_active && k >= 9))) {
         const double* ub = sU + ((k - 5) & (URING - 1)) * 4 * NC + t;
         const int64_t o = (int64_t)j * a.pitch + c;
         double v[4];
@@ -473,8 +525,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         bool ok = true, okr = true, rate_ok;
         double eint, rr;
 #if LF_FUSED_EPI_BOX
-        cell_epilogue_box<LF_FUSED_EPI_BOX == 2>(v, C, pos_in_box(a.dx) && pos_in_box(a.dy), eint,
-                                                 ok, rr, rate_ok, okr);
+        cell_epilogue_box<LF_FUSED_EPI_BOX == 2>(v, C, dxy_box, eint, ok, rr, rate_ok, okr);
 #else
         cell_epilogue(v, C, eint, ok, rr, rate_ok, okr);
 #endif
@@ -494,22 +545,24 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         } else {
           dtfail = 1;
         }
-        // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432)
+        // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432);
+        // one block-uniform test skips all four in the interior of the domain (the
+        // bottom / top rows only occur in guarded iterations)
         const int jg = j + a.y0g;
-        // one block-uniform test skips all four in the interior of the domain
-        if (x_edge_blk || jg == 0 || jg == a.nyg - 1) {
-        if (c == 0)
-          for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = sFc[q * NC + t];
-        if (c == a.nx - 1)
-          for (int q = 0; q < 4; ++q) a.bnd[4 * (int64_t)a.nyg + (int64_t)q * a.nyg + jg] = sFc[q * NC + t + 1];
-        if (jg == 0)
-          for (int q = 0; q < 4; ++q) a.bnd[8 * (int64_t)a.nyg + (int64_t)q * a.nx + c] = fcprev[q];
-        if (jg == a.nyg - 1)
-          for (int q = 0; q < 4; ++q)
-            a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fc[q];
+        if (x_edge_blk || (G && (jg == 0 || jg == a.nyg - 1))) {
+          if (c == 0)
+            for (int q = 0; q < 4; ++q) a.bnd[(int64_t)q * a.nyg + jg] = sFc[q * NC + t];
+          if (c == a.nx - 1)
+            for (int q = 0; q < 4; ++q)
+              a.bnd[4 * (int64_t)a.nyg + (int64_t)q * a.nyg + jg] = sFc[q * NC + t + 1];
+          if (G && jg == 0)
+            for (int q = 0; q < 4; ++q) a.bnd[8 * (int64_t)a.nyg + (int64_t)q * a.nx + c] = fcprev[q];
+          if (G && jg == a.nyg - 1)
+            for (int q = 0; q < 4; ++q)
+              a.bnd[8 * (int64_t)a.nyg + 4 * (int64_t)a.nx + (int64_t)q * a.nx + c] = fc[q];
         }
       }
-      if (c_active && k >= 8) {
+      if (!G || (c_active && k >= 8)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) fcprev[q] = fc[q];
       }
@@ -521,7 +574,11 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         }
       }
       __syncthreads();
-    }
+    };
+    int k = 0;
+    for (; k < KS && k < nit; ++k) iter(k, std::true_type{});
+    for (; k <= ksteady; ++k) iter(k, std::false_type{});
+    for (; k < nit; ++k) iter(k, std::true_type{});
     // block-level reductions (warp shuffles, then one atomic per warp)
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long r2 = __shfl_xor_sync(FULL, rate_key, o);

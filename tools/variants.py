@@ -25,10 +25,10 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # (a third element selects LF_MATH_*: 1 = contract; bit equality is checked
 # against the first variant of the same arithmetic)
 VARIANTS = {
+    "base_f": ("", 1),
     "f": ("", 1),
-    "f_nodcp": ("-DLF_FUSED_DONTCARE_P=0", 1),
+    "base_c_f": ("", 1, 1),
     "c_f": ("", 1, 1),
-    "c_f_nodcp": ("-DLF_FUSED_DONTCARE_P=0", 1, 1),
 }
 
 
@@ -71,7 +71,7 @@ def run(n=8192, steps=10):
     g = case.grid
     refs = {}
     results = {}
-    names = list(VARIANTS)
+    names = list(VARIANTS) * 2   # two rounds, interleaved: the better of each variant counts
     for name in names:
         so = os.path.join(OUT, f"{name}.so")
         if not os.path.exists(so):
@@ -100,6 +100,9 @@ def run(n=8192, steps=10):
             refs[math] = f
         else:
             same = bool(np.array_equal(g.interior(f) == g.interior(ref), np.ones_like(g.interior(f), bool)))
+        prev = results.get(name)
+        if prev is not None and prev["kernel_ms"] < per:
+            per = prev["kernel_ms"]
         results[name] = {"kernel_ms": per, "gcells_s": g.nx * g.ny / per / 1e6, "same_as_first": same}
         print(name, json.dumps(results[name]), flush=True)
     return results
