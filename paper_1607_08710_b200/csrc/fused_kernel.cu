@@ -116,6 +116,11 @@ constexpr int PREFETCH = 2;
 #ifndef LF_MINBLOCKS
 #define LF_MINBLOCKS 2
 #endif
+// LF_FUSED_UNROLL 2: the steady row loop two iterations per trip (register renaming
+// instead of the windows' moves; twice the code)
+#ifndef LF_FUSED_UNROLL
+#define LF_FUSED_UNROLL 1
+#endif
 template <bool MUSCL>
 __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(FusedArgs a) {
   extern __shared__ __align__(128) double smem[];
@@ -352,6 +357,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
     };
     int k = 0;
     for (; k < KS && k < nit; ++k) iter(k, std::true_type{});
+#if LF_FUSED_UNROLL == 2
+    for (; k + 1 <= ksteady; k += 2) {
+      iter(k, std::false_type{});
+      iter(k + 1, std::false_type{});
+    }
+#endif
     for (; k <= ksteady; ++k) iter(k, std::false_type{});
     for (; k < nit; ++k) iter(k, std::true_type{});
   } else {
@@ -577,6 +588,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
     };
     int k = 0;
     for (; k < KS && k < nit; ++k) iter(k, std::true_type{});
+#if LF_FUSED_UNROLL == 2
+    for (; k + 1 <= ksteady; k += 2) {
+      iter(k, std::false_type{});
+      iter(k + 1, std::false_type{});
+    }
+#endif
     for (; k <= ksteady; ++k) iter(k, std::false_type{});
     for (; k < nit; ++k) iter(k, std::true_type{});
     // block-level reductions (warp shuffles, then one atomic per warp)
