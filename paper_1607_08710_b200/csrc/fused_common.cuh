@@ -45,6 +45,14 @@ struct StepRec {
                      // 3 precursor velocities: re-run with the exact two-pass kernels
 };
 
+// The step's constant divisors' shared reciprocals (face_fast.cuh FK), computed once
+// per handle on the device (fused_make_fk: bit-identical to the kernel computing them)
+// and passed as launch parameters: they live in the constant bank instead of registers.
+struct FKBits {
+  double gamma, gm1, beta;
+  double rgm1_b, rgm1_y, rdx_b, rdx_y, rdy_b, rdy_y;
+};
+
 struct FusedArgs {
   const double* __restrict__ u;   // U^n, component 0 at (0, 0)
   double* __restrict__ un;        // U^{n+1}
@@ -61,9 +69,13 @@ struct FusedArgs {
   const StepCtl* ctl;
   StepAcc* acc;
   double* bnd;                    // [left 4*nyg | right 4*nyg | bottom 4*nx | top 4*nx]
+  FKBits fk;                      // make_fk(gamma, gm1, beta, dx, dy) of this build's arithmetic
 };
 
 size_t fused_smem_bytes();
+// make_fk on the device in each build's arithmetic (the contract build refines less)
+FKBits fused_make_fk(double gamma, double gm1, double beta, double dx, double dy);
+FKBits fused_make_fk_contract(double gamma, double gm1, double beta, double dx, double dy);
 void fused_configure();
 int fused_blocks_per_sm();   // resident blocks of k_fused_step (after fused_configure)
 void launch_fused_step(const FusedArgs& a, bool muscl, dim3 grid, cudaStream_t st);

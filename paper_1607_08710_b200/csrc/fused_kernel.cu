@@ -42,6 +42,7 @@
 
 #if LF_CONTRACT
 #define k_fused_step k_fused_step_contract   // distinct kernel names for ncu filters
+#define k_make_fk k_make_fk_contract
 #endif
 
 namespace lfb {
@@ -116,6 +117,29 @@ constexpr int PREFETCH = 2;
 #ifndef LF_MINBLOCKS
 #define LF_MINBLOCKS 2
 #endif
+// LF_FUSED_PRING 1: P keeps W(r) rows in a 4-row ring and takes their x slopes two
+// iterations later, without the exchange barrier of its own; LF_FUSED_CRING 1: C takes
+// the x slopes of W*(j) straight from the P -> C ring (each lane's image column), again
+// without an exchange barrier.  Measured at 16384^2 (tools/variants.py): both together
+// +5 % exact; in the contract build (more register pressure) PRING + CRING -3 % and
+// PRING alone -23 % (its shared memory admits one block per SM), so the contract
+// build keeps both exchanges.
+#ifndef LF_FUSED_PRING
+#if LF_CONTRACT
+#define LF_FUSED_PRING 0
+#else
+#define LF_FUSED_PRING 1
+#endif
+#endif
+#ifndef LF_FUSED_CRING
+#if LF_CONTRACT
+#define LF_FUSED_CRING 0
+#else
+#define LF_FUSED_CRING 1
+#endif
+#endif
+constexpr int WR_ROWS = LF_FUSED_PRING ? 4 : 1;
+constexpr int WC_ROWS = LF_FUSED_CRING ? 0 : 1;
 // LF_FUSED_UNROLL 2: the steady row loop two iterations per trip (register renaming
 // instead of the windows' moves; twice the code)
 #ifndef LF_FUSED_UNROLL
@@ -125,13 +149,14 @@ template <bool MUSCL>
 __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(FusedArgs a) {
   extern __shared__ __align__(128) double smem[];
   double* sU = smem;                   // [URING][4][NC] U^n rows (TMA destination)
-  double* sWx = sU + URING * 4 * NC;   // [4][NC]     P: W(r-2) for x slopes
-  double* sTx = sWx + 4 * NC;          // [4][NC]     P: x hi-traces
+  double* sWr = sU + URING * 4 * NC;   // [4][4][NC]  ring: W(r) rows (P: x slopes two rows on)
+                                       //             ([4][NC] W(r-2) without LF_FUSED_PRING)
+  double* sTx = sWr + WR_ROWS * 4 * NC;  // [4][NC]   P: x hi-traces
   double* sFnx = sTx + 4 * NC;         // [4][4][NC]  ring: F^n x-faces of a row
   double* sFny = sFnx + 16 * NC;       // [4][4][NC]  ring: F^n y-faces
-  double* sWs = sFny + 16 * NC;        // [2][4][NC]  W* rows (P -> C)
-  double* sWc = sWs + 8 * NC;          // [4][NC]     C: W*(j) for x slopes
-  double* sTc = sWc + 4 * NC;          // [4][NC]     C: x hi-traces
+  double* sWs = sFny + 16 * NC;        // [4][4][NC]  ring: W* rows (P -> C: y window, x slopes)
+  double* sWc = sWs + 16 * NC;         // [4][NC]     C: W*(j) for x slopes (without LF_FUSED_CRING)
+  double* sTc = sWc + WC_ROWS * 4 * NC;  // [4][NC]   C: x hi-traces
   double* sFc = sTc + 4 * NC;          // [4][NC]     C: 0.5 (F^n + F*) x-faces
   double* sStash = sFc + 4 * NC;       // [4][NC]     C: top-edge ghost image
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sStash + 4 * NC);  // [URING]
@@ -153,7 +178,15 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
   const double lam_x = dt / a.dx;
   const double lam_y = dt / a.dy;
 
-  const FK C = make_fk(a.gamma, a.gm1, a.beta, a.dx, a.dy);
+  // (from the launch parameters: the compiler may reread them from the constant bank
+  // instead of holding them in registers)
+  FK C;
+  C.gamma = a.fk.gamma;
+  C.gm1 = a.fk.gm1;
+  C.beta = a.fk.beta;
+  C.rgm1 = Recip{a.fk.rgm1_b, a.fk.rgm1_y};
+  C.rdx = Recip{a.fk.rdx_b, a.fk.rdx_y};
+  C.rdy = Recip{a.fk.rdy_b, a.fk.rdy_y};
 
   const int t = threadIdx.x & (NC - 1);
   const bool is_p = threadIdx.x < NC;
@@ -232,15 +265,25 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           prim_fast(r0, m1, m2, e3, a.gm1, w, okw);
           if (!cell_in_box(w) && col_interior && (!G || (r >= 0 && r < a.ny))) fail = 1;
         }
+#if LF_FUSED_PRING
+        // W(r) into the ring: its x slopes are taken two iterations on, after two
+        // block-wide barriers, so no barrier of its own is needed
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sWr[((k & 3) * 4 + q) * NC + t] = w[q];
+#endif
         if (!G || k >= 2) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            sWx[q * NC + t] = wm2[q];  // row r-2 for the x direction
+#if !LF_FUSED_PRING
+            sWr[q * NC + t] = wm2[q];  // row r-2 for the x direction
+#endif
             cell_traces<MUSCL>(wm2[q], wm1[q], w[q], a.beta, ylo[q], yhi[q]);  // row r-1
           }
         }
       }
+#if !LF_FUSED_PRING
       bar_named(1);
+#endif
       double xlo[4];
       if (G) {
 #pragma unroll
@@ -249,11 +292,11 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       if (G ? (p_active && k >= 2 && t >= 1 && t <= NC - 2) : true) {
         // (steady: the edge lanes use a clamped neighbour; their traces are unused)
         const int il = G ? t - 1 : tl, ir = G ? t + 1 : tr;
+        const double* wr = sWr + (LF_FUSED_PRING ? ((k - 2) & 3) * 4 * NC : 0);   // W(r-2)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           double hi;
-          cell_traces<MUSCL>(sWx[q * NC + il], sWx[q * NC + t], sWx[q * NC + ir], a.beta, xlo[q],
-                             hi);
+          cell_traces<MUSCL>(wr[q * NC + il], wr[q * NC + t], wr[q * NC + ir], a.beta, xlo[q], hi);
           sTx[q * NC + t] = hi;
         }
       }
@@ -331,7 +374,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         bool okw = true;
         prim_fast(v[0], v[1], v[2], v[3], a.gm1, ws, okw);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sWs[((k & 1) * 4 + q) * NC + t] = ws[q];
+        for (int q = 0; q < 4; ++q) sWs[((k & 3) * 4 + q) * NC + t] = ws[q];
         if (upd && col_interior && (!G || (row >= 0 && row < a.ny))) {
           // e_int = v3 - (0.5 (v1^2 + v2^2)) / v0 > 0 (solver.cpp:300-302), tested
           // without the division: v3 v0 > K (1 + 2^-48) implies it; else flag
@@ -387,10 +430,30 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
     // they read a clamped column instead of selecting a default state
     const int src_c = min(max(src_t, 2), NC - 3);
     const unsigned long long flip_bits = flip_u ? 0x8000000000000000ull : 0ull;
+    // the same for the x neighbours (lanes tl, tr): the x slopes of W*(j) are read
+    // straight from the P -> C ring, with each lane's image mapping
+    auto src_of = [&](int u, unsigned long long& fb) {
+      const int cu = x0 - 4 + u;
+      int su = u;
+      bool fu = false;
+      if (cu < 0 && a.bc_xlo != LF_PERIODIC) {
+        su = u + ((a.bc_xlo == LF_REFLECTIVE ? -cu - 1 : 0) - cu);
+        fu = a.bc_xlo == LF_REFLECTIVE;
+      } else if (cu >= a.nx && a.bc_xhi != LF_PERIODIC) {
+        su = u + ((a.bc_xhi == LF_REFLECTIVE ? 2 * a.nx - 1 - cu : a.nx - 1) - cu);
+        fu = a.bc_xhi == LF_REFLECTIVE;
+      }
+      fb = fu ? 0x8000000000000000ull : 0ull;
+      return min(max(su, 2), NC - 3);
+    };
     const bool dox = t >= 4 && t <= NC - 4 && c <= a.nx;  // x-faces of output cells
     const bool xchk = dox && c >= 0;
     const bool upd = t >= 4 && t <= NC - 5 && col_interior;   // output cells
     const int tl = t > 0 ? t - 1 : t, tr = t < NC - 1 ? t + 1 : t;   // clamped x neighbours
+    // a block holding ghost columns of a non-periodic x side (block-uniform): its lanes
+    // map to image columns; elsewhere every lane reads its own column
+    const bool x_img_blk = (x0 - 4 < 0 && a.bc_xlo != LF_PERIODIC) ||
+                           (x0 - 4 + NC > a.nx && a.bc_xhi != LF_PERIODIC);
     const bool x_edge_blk = x0 - 4 <= 0 || x0 - 4 + NC > a.nx - 1;   // holds column 0 or nx-1
     const bool dxy_box = pos_in_box(a.dx) && pos_in_box(a.dy);
     auto iter = [&](const int k, auto guard) {
@@ -408,7 +471,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         //    predictor_ (grid.cpp:72-114); a reflective image negates the normal
         //    velocity exactly as it negates the normal momentum
         {
-          const double* ws = sWs + ((k + 1) & 1) * 4 * NC + src_c;
+          const double* ws = sWs + ((k - 1) & 3) * 4 * NC + src_c;
           w[0] = ws[0];
           w[1] = __longlong_as_double(__double_as_longlong(ws[NC]) ^ flip_bits);
           w[2] = ws[2 * NC];
@@ -452,12 +515,16 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         if (!G || k >= 7) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
+#if !LF_FUSED_CRING
             sWc[q * NC + t] = vm2[q];  // row j = aa-2 for the x direction
+#endif
             cell_traces<MUSCL>(vm2[q], vm1[q], w[q], a.beta, ylo[q], yhi[q]);  // row aa-1
           }
         }
       }
+#if !LF_FUSED_CRING
       bar_named(2);
+#endif
       double xlo[4];
       if (G) {
 #pragma unroll
@@ -465,12 +532,43 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       }
       if (G ? (c_active && k >= 9 && t >= 3 && t <= NC - 4) : true) {
         // (steady: the edge lanes use a clamped neighbour; their traces are unused)
-        const int il = G ? t - 1 : tl, ir = G ? t + 1 : tr;
+        // W*(j) = W*(aa-2), written by P three iterations ago (j is an interior row
+        // here), at each lane's image column: the x slopes without an exchange barrier
+        const double* wj = sWs + ((k - 3) & 3) * 4 * NC;
+        double wl[4], w0[4], wr_[4];
+        if (!LF_FUSED_CRING) {
+          // (the exchanged W*(j) row: images applied by the lanes that stored it)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            wl[q] = sWc[q * NC + (G ? t - 1 : tl)];
+            w0[q] = sWc[q * NC + t];
+            wr_[q] = sWc[q * NC + (G ? t + 1 : tr)];
+          }
+        } else if (!x_img_blk) {
+          // (lanes outside [3, NC-4] read don't-care columns; their traces are unused)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            wl[q] = wj[q * NC + tl];
+            w0[q] = wj[q * NC + t];
+            wr_[q] = wj[q * NC + tr];
+          }
+        } else {
+          unsigned long long flip_l, flip_r;
+          const int src_l = src_of(tl, flip_l), src_r = src_of(tr, flip_r);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            wl[q] = wj[q * NC + src_l];
+            w0[q] = wj[q * NC + src_c];
+            wr_[q] = wj[q * NC + src_r];
+          }
+          wl[1] = __longlong_as_double(__double_as_longlong(wl[1]) ^ flip_l);
+          w0[1] = __longlong_as_double(__double_as_longlong(w0[1]) ^ flip_bits);
+          wr_[1] = __longlong_as_double(__double_as_longlong(wr_[1]) ^ flip_r);
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           double hi;
-          cell_traces<MUSCL>(sWc[q * NC + il], sWc[q * NC + t], sWc[q * NC + ir], a.beta, xlo[q],
-                             hi);
+          cell_traces<MUSCL>(wl[q], w0[q], wr_[q], a.beta, xlo[q], hi);
           sTc[q * NC + t] = hi;
         }
       }
@@ -753,13 +851,48 @@ __global__ void k_acc_init(StepAcc* acc) {
 
 #endif  // !LF_CONTRACT
 
+__global__ void k_make_fk(double gamma, double gm1, double beta, double dx, double dy,
+                          FKBits* out) {
+  const FK c = make_fk(gamma, gm1, beta, dx, dy);
+  FKBits b;
+  b.gamma = c.gamma;
+  b.gm1 = c.gm1;
+  b.beta = c.beta;
+  b.rgm1_b = c.rgm1.b;
+  b.rgm1_y = c.rgm1.y;
+  b.rdx_b = c.rdx.b;
+  b.rdx_y = c.rdx.y;
+  b.rdy_b = c.rdy.b;
+  b.rdy_y = c.rdy.y;
+  *out = b;
+}
+
+FKBits make_fk_host(double gamma, double gm1, double beta, double dx, double dy) {
+  FKBits* d = nullptr;
+  FKBits h{};
+  if (cudaMalloc(&d, sizeof(FKBits)) != cudaSuccess) return h;
+  count_launch();
+  k_make_fk<<<1, 1>>>(gamma, gm1, beta, dx, dy, d);
+  cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return h;
+}
+
 constexpr size_t SMEM_BYTES =
-    (size_t)(URING * 4 + 4 + 4 + 16 + 16 + 8 + 4 + 4 + 4 + 4) * NC * sizeof(double) +
+    (size_t)(URING * 4 + WR_ROWS * 4 + 4 + 16 + 16 + 16 + WC_ROWS * 4 + 4 + 4 + 4) * NC *
+        sizeof(double) +
     URING * sizeof(unsigned long long);
+// two blocks per SM (228 KB, 1 KB reserved per block): one block per SM halves the
+// resident warps of this latency-bound kernel
+static_assert(2 * (SMEM_BYTES + 1024) <= 228 * 1024, "fused step: two blocks per SM");
 
 }  // namespace
 
 #if LF_CONTRACT
+FKBits fused_make_fk_contract(double gamma, double gm1, double beta, double dx, double dy) {
+  return make_fk_host(gamma, gm1, beta, dx, dy);
+}
+
 // fused_contract.cu: the one-kernel step in the tolerance arithmetic (LF_MATH_CONTRACT)
 void fused_configure_contract() {
   cudaFuncSetAttribute(k_fused_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -776,6 +909,10 @@ void launch_fused_step_contract(const FusedArgs& a, bool muscl, dim3 grid, cudaS
     k_fused_step<false><<<grid, FUSED_THREADS, SMEM_BYTES, st>>>(a);
 }
 #else
+FKBits fused_make_fk(double gamma, double gm1, double beta, double dx, double dy) {
+  return make_fk_host(gamma, gm1, beta, dx, dy);
+}
+
 size_t fused_smem_bytes() { return SMEM_BYTES; }
 
 int fused_blocks_per_sm() {
