@@ -69,6 +69,7 @@ struct FusedState {
   cudaStream_t comm = nullptr;
   cudaEvent_t ev_fill = nullptr, ev_edge = nullptr;
   FKBits fk_exact{}, fk_contract{};   // launch-parameter constants of the fused kernels
+  bool fk_ok = false;                 // (computed on the first fused step)
 };
 
 static FusedState* fstate(lf_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
@@ -163,9 +164,6 @@ static void fused_alloc(lf_handle* h, int steps) {
     launch_acc_init(f->acc, s0.stream);
     fused_configure();
     fused_configure_contract();
-    f->fk_exact = fused_make_fk(h->k.gamma, h->k.gm1, h->k.beta, h->d.dx, h->d.dy);
-    f->fk_contract = fused_make_fk_contract(h->k.gamma, h->k.gm1, h->k.beta, h->d.dx, h->d.dy);
-    FK(cudaGetLastError());
     // chunk rows: the blocks are independent and equally long, so a step costs about
     // (waves) x (rows + 9 rows of pipeline fill); pick the chunk count that minimises
     // it (16384^2: 15 chunks = 6.94 waves instead of 13 = 6.02, i.e. 7 waves either way;
@@ -409,6 +407,12 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
     const int chunks = (s.L.ny + f->rows_per_chunk - 1) / f->rows_per_chunk;
     const bool contract = h->math == LF_MATH_CONTRACT;
     const bool muscl = h->d.spatial_order >= 2;
+    if (!f->fk_ok) {
+      f->fk_exact = fused_make_fk(h->k.gamma, h->k.gm1, h->k.beta, h->d.dx, h->d.dy);
+      f->fk_contract = fused_make_fk_contract(h->k.gamma, h->k.gm1, h->k.beta, h->d.dx, h->d.dy);
+      FK(cudaGetLastError());
+      f->fk_ok = true;
+    }
     a.fk = contract ? f->fk_contract : f->fk_exact;
     auto launch = [&](int c0, int step, int n, cudaStream_t st) {
       if (n <= 0) return;
