@@ -27,10 +27,8 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 VARIANTS = {
     "base_f": ("", 1),
     "f": ("", 1),
-    "f_c0": ("-DLF_FUSED_CRING=0", 1),
-    "base_c_f": ("", 1, 1),
+    "f_wring": ("-DLF_FUSED_WRING=1", 1),
     "c_f": ("", 1, 1),
-    "c_f_p0": ("-DLF_FUSED_PRING=0", 1, 1),
 }
 
 
