@@ -121,14 +121,20 @@ constexpr int PREFETCH = 2;
 // iterations later, without the exchange barrier of its own; LF_FUSED_CRING 1: C takes
 // the x slopes of W*(j) straight from the P -> C ring (each lane's image column), again
 // without an exchange barrier.  Measured at 16384^2 (tools/variants.py): both together
-// +5 % exact; in the contract build (more register pressure) PRING + CRING -3 % and
-// PRING alone -23 % (its shared memory admits one block per SM), so the contract
-// build keeps both exchanges.
+// +5 % exact, CRING alone +5.5 %; in the contract build (more register pressure)
+// PRING + CRING -3 %, CRING alone -6 %, PRING alone -23 % (its shared memory admits
+// one block per SM), so the contract build keeps both exchanges.
 #ifndef LF_FUSED_PRING
-#if LF_CONTRACT
 #define LF_FUSED_PRING 0
+#endif
+// LF_FUSED_TMA_SPREAD 1: the four component rows of each U^n row are copied by the
+// four P warps (one each) instead of all by warp 0
+// (measured: +1.1 % exact, -1.5 % contract: more spills there)
+#ifndef LF_FUSED_TMA_SPREAD
+#if LF_CONTRACT
+#define LF_FUSED_TMA_SPREAD 0
 #else
-#define LF_FUSED_PRING 1
+#define LF_FUSED_TMA_SPREAD 1
 #endif
 #endif
 #ifndef LF_FUSED_CRING
@@ -250,6 +256,21 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       constexpr bool G = decltype(guard)::value;
       const int r = y0 - 4 + k;
       const bool p_active = !G || k <= klastp;
+#if LF_FUSED_TMA_SPREAD
+      // lane 0 of P warp q copies component q of row k+PREFETCH (the four warps share
+      // the issue cost, so none lags at the next barrier); warp 0 also posts the
+      // expected bytes -- the transaction count may run negative until it does, and
+      // the phase cannot complete before its arrival
+      if ((threadIdx.x & 31) == 0 && (!G || k + PREFETCH <= klastp)) {
+        // the slot's previous row (k+PREFETCH-URING) was last read before the
+        // previous iteration's __syncthreads
+        const int kn = k + PREFETCH, s = kn & (URING - 1), q = threadIdx.x >> 5;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (q == 0) mbar_expect_tx(&mbar[s], 4 * row_bytes);
+        tma_row(sU + (s * 4 + q) * NC, src0 + (int64_t)kn * a.pitch + q * a.fstride, row_bytes,
+                &mbar[s]);
+      }
+#else
       if (threadIdx.x == 0 && (!G || k + PREFETCH <= klastp)) {
         // the slot's previous row (k+PREFETCH-URING) was last read before the
         // previous iteration's __syncthreads
@@ -260,6 +281,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           tma_row(sU + (s * 4 + q) * NC, src0 + (int64_t)kn * a.pitch + q * a.fstride, row_bytes,
                   &mbar[s]);
       }
+#endif
       double w[4], ylo[4], yhi[4];
       if (G) {
 #pragma unroll
