@@ -71,23 +71,24 @@ def ncu_traffic(path):
         return None
 
 
-def ncu_compute_bound(path):
-    """The path's kernels' real bound from the committed ncu --set full capture
-    (profiles/r01_ncu_16k.json): fp64-pipe and issue utilisation per kernel."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_16k.json")
-    try:
-        with open(p) as f:
-            d = json.load(f)
-        ks = d[path]["kernels"]
+def ncu_compute_bound(path, math="exact"):
+    """The path's kernels' real bound from the committed ncu --set full capture of the
+    current build (profiles/r02_ncu_16k.json; the two-pass kernels from round 1's
+    profiles/r01_ncu_16k.json): fp64-pipe and issue utilisation per kernel."""
+    for fn, key in (("r02_ncu_16k.json", f"{path}/{math}"), ("r01_ncu_16k.json", path)):
+        try:
+            with open(os.path.join(ROOT, "profiles", fn)) as f:
+                ks = json.load(f)[key]["kernels"]
+        except Exception:
+            continue
         return {"bound": "fp64 pipe / issue latency (not HBM)",
                 "kernels": {k["kernel"].split("(")[0].split("::")[-1]:
                             {"fp64_pipe_pct": round(k["fp64_pipe_pct"], 1),
                              "issue_active_pct": round(k["issue_active_pct"], 1),
                              "top_stall": max(k["top_stalls_pct"], key=k["top_stalls_pct"].get)}
                             for k in ks},
-                "source": "profiles/r01_ncu_16k.json (ncu --set full, 16384^2)"}
-    except Exception:
-        return None
+                "source": f"profiles/{fn} (ncu --set full, 16384^2)"}
+    return None
 
 
 class ClockSampler:
@@ -383,7 +384,7 @@ def run_ours(args):
                 "frac_of_nominal_8TBs": achieved / 8000.0,
                 "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                 "traffic_source": traffic.get("source") if traffic else None,
-                "compute": ncu_compute_bound(resolved)}
+                "compute": ncu_compute_bound(resolved, args.math)}
     # the roof that binds: fp64 (measured on this GPU now, lf_fp64_peak), with the
     # kernel's fp64 instructions per cell-update from the current build's ncu capture
     roof = fp64_roof(N.lib(), local) if rank == 0 else None

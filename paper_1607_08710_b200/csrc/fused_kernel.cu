@@ -117,16 +117,6 @@ constexpr int PREFETCH = 2;
 #ifndef LF_MINBLOCKS
 #define LF_MINBLOCKS 2
 #endif
-// LF_FUSED_PRING 1: P keeps W(r) rows in a 4-row ring and takes their x slopes two
-// iterations later, without the exchange barrier of its own; LF_FUSED_CRING 1: C takes
-// the x slopes of W*(j) straight from the P -> C ring (each lane's image column), again
-// without an exchange barrier.  Measured at 16384^2 (tools/variants.py): both together
-// +5 % exact, CRING alone +5.5 %; in the contract build (more register pressure)
-// PRING + CRING -3 %, CRING alone -6 %, PRING alone -23 % (its shared memory admits
-// one block per SM), so the contract build keeps both exchanges.
-#ifndef LF_FUSED_PRING
-#define LF_FUSED_PRING 0
-#endif
 // LF_FUSED_TMA_SPREAD 1: the four component rows of each U^n row are copied by the
 // four P warps (one each) instead of all by warp 0
 // (measured: +1.1 % exact, -1.5 % contract: more spills there)
@@ -137,6 +127,14 @@ constexpr int PREFETCH = 2;
 #define LF_FUSED_TMA_SPREAD 1
 #endif
 #endif
+// LF_FUSED_CRING 1: C takes the x slopes of W*(j) straight from the P -> C ring (each
+// lane's image column) instead of exchanging its W*(j) row through shared memory and a
+// barrier.  Measured at 16384^2 (tools/variants.py): +5.5 % exact, -6 % in the contract
+// build (register pressure: spills), which keeps the exchange.  (Also measured and
+// dropped: the same for P's W rows, a 4-row ring: +-0.5 % exact, -23 % contract, whose
+// shared memory then admits one block per SM; the y windows read back from the rings
+// instead of rotated in registers: -4 %; the steady loop unrolled twice: -12 %,
+// instruction cache.)
 #ifndef LF_FUSED_CRING
 #if LF_CONTRACT
 #define LF_FUSED_CRING 0
@@ -144,28 +142,13 @@ constexpr int PREFETCH = 2;
 #define LF_FUSED_CRING 1
 #endif
 #endif
-// LF_FUSED_WRING 1: the y windows (P: W(r-2), W(r-1), F^n y-face below; C: W*(aa-2),
-// W*(aa-1)) read back from the rings each row instead of rotated in registers
-// (measured: -4 % exact, 16 fewer moves but longer dependency chains)
-#ifndef LF_FUSED_WRING
-#define LF_FUSED_WRING 0
-#endif
-#define LF_PWIN (LF_FUSED_PRING && LF_FUSED_WRING)
-#define LF_CWIN (LF_FUSED_CRING && LF_FUSED_WRING)
-constexpr int WR_ROWS = LF_FUSED_PRING ? 4 : 1;
 constexpr int WC_ROWS = LF_FUSED_CRING ? 0 : 1;
-// LF_FUSED_UNROLL 2: the steady row loop two iterations per trip (register renaming
-// instead of the windows' moves; twice the code)
-#ifndef LF_FUSED_UNROLL
-#define LF_FUSED_UNROLL 1
-#endif
 template <bool MUSCL>
 __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(FusedArgs a) {
   extern __shared__ __align__(128) double smem[];
   double* sU = smem;                   // [URING][4][NC] U^n rows (TMA destination)
-  double* sWr = sU + URING * 4 * NC;   // [4][4][NC]  ring: W(r) rows (P: x slopes two rows on)
-                                       //             ([4][NC] W(r-2) without LF_FUSED_PRING)
-  double* sTx = sWr + WR_ROWS * 4 * NC;  // [4][NC]   P: x hi-traces
+  double* sWr = sU + URING * 4 * NC;   // [4][NC]     P: W(r-2) for x slopes
+  double* sTx = sWr + 4 * NC;          // [4][NC]     P: x hi-traces
   double* sFnx = sTx + 4 * NC;         // [4][4][NC]  ring: F^n x-faces of a row
   double* sFny = sFnx + 16 * NC;       // [4][4][NC]  ring: F^n y-faces
   double* sWs = sFny + 16 * NC;        // [4][4][NC]  ring: W* rows (P -> C: y window, x slopes)
@@ -242,10 +225,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 
   if (is_p) {
     // ================================================================ stage 1 (P)
-#if !LF_PWIN
     double wm2[4] = {1.0, 0.0, 0.0, 1.0}, wm1[4] = {1.0, 0.0, 0.0, 1.0};
     double fyprev[4] = {0.0, 0.0, 0.0, 0.0};
-#endif
     double hiprev[4] = {1.0, 0.0, 0.0, 1.0};
     // this thread owns x-face (t-1 | t), needed for U* up to column nx+1
     const bool dox = t >= 2 && t <= NC - 2 && c <= a.nx + 2;
@@ -298,35 +279,15 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           prim_fast(r0, m1, m2, e3, a.gm1, w, okw);
           if (!cell_in_box(w) && col_interior && (!G || (r >= 0 && r < a.ny))) fail = 1;
         }
-#if LF_FUSED_PRING
-        // W(r) into the ring: its x slopes are taken two iterations on, after two
-        // block-wide barriers, so no barrier of its own is needed
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sWr[((k & 3) * 4 + q) * NC + t] = w[q];
-#endif
         if (!G || k >= 2) {
-#if LF_PWIN
-          // the y window W(r-2), W(r-1) from this thread's own column of the ring
-          // (no register window to rotate)
-          const double* w2 = sWr + ((k - 2) & 3) * 4 * NC + t;
-          const double* w1 = sWr + ((k - 1) & 3) * 4 * NC + t;
-#endif
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-#if LF_PWIN
-            cell_traces<MUSCL>(w2[q * NC], w1[q * NC], w[q], a.beta, ylo[q], yhi[q]);  // row r-1
-#else
-#if !LF_FUSED_PRING
             sWr[q * NC + t] = wm2[q];  // row r-2 for the x direction
-#endif
             cell_traces<MUSCL>(wm2[q], wm1[q], w[q], a.beta, ylo[q], yhi[q]);  // row r-1
-#endif
           }
         }
       }
-#if !LF_FUSED_PRING
       bar_named(1);
-#endif
       double xlo[4];
       if (G) {
 #pragma unroll
@@ -335,7 +296,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
       if (G ? (p_active && k >= 2 && t >= 1 && t <= NC - 2) : true) {
         // (steady: the edge lanes use a clamped neighbour; their traces are unused)
         const int il = G ? t - 1 : tl, ir = G ? t + 1 : tr;
-        const double* wr = sWr + (LF_FUSED_PRING ? ((k - 2) & 3) * 4 * NC : 0);   // W(r-2)
+        const double* wr = sWr;   // W(r-2)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           double hi;
@@ -410,13 +371,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           const double fxl = sFnx[((k & 3) * 4 + q) * NC + t];
           const double fxr = sFnx[((k & 3) * 4 + q) * NC + t + 1];
           double val = ub[q * NC] - lam_x * (fxr - fxl);
-#if LF_PWIN
-          // F^n of the y-face below, stored by this thread in the previous iteration
-          const double fyp = sFny[(((k - 1) & 3) * 4 + q) * NC + t];
-#else
-          const double fyp = fyprev[q];
-#endif
-          val -= lam_y * (fy[q] - fyp);
+          val -= lam_y * (fy[q] - fyprev[q]);
           v[q] = val;
         }
         double ws[4];
@@ -434,7 +389,6 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           if (!cell_in_box(ws)) fail = 1;
         }
       }
-#if !LF_PWIN
       if (!G || (p_active && k >= 3)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) fyprev[q] = fy[q];
@@ -446,17 +400,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           wm1[q] = w[q];
         }
       }
-#endif
       __syncthreads();
     };
     int k = 0;
     for (; k < KS && k < nit; ++k) iter(k, std::true_type{});
-#if LF_FUSED_UNROLL == 2
-    for (; k + 1 <= ksteady; k += 2) {
-      iter(k, std::false_type{});
-      iter(k + 1, std::false_type{});
-    }
-#endif
     for (; k <= ksteady; ++k) iter(k, std::false_type{});
     for (; k < nit; ++k) iter(k, std::true_type{});
   } else {
@@ -564,33 +511,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           }
         }
         if (!G || k >= 7) {
-          // steady (with LF_FUSED_CRING): the y window W*(aa-2), W*(aa-1) from the P -> C
-          // ring at this lane's image column (interior rows: no y image), no registers
-          // to rotate
-          double m2[4], m1[4];
-          if (!G && LF_CWIN) {
-            const double* r2 = sWs + ((k - 3) & 3) * 4 * NC + src_c;
-            const double* r1 = sWs + ((k - 2) & 3) * 4 * NC + src_c;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              m2[q] = r2[q * NC];
-              m1[q] = r1[q * NC];
-            }
-            m2[1] = __longlong_as_double(__double_as_longlong(m2[1]) ^ flip_bits);
-            m1[1] = __longlong_as_double(__double_as_longlong(m1[1]) ^ flip_bits);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              m2[q] = vm2[q];
-              m1[q] = vm1[q];
-            }
-          }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
 #if !LF_FUSED_CRING
-            sWc[q * NC + t] = m2[q];  // row j = aa-2 for the x direction
+            sWc[q * NC + t] = vm2[q];  // row j = aa-2 for the x direction
 #endif
-            cell_traces<MUSCL>(m2[q], m1[q], w[q], a.beta, ylo[q], yhi[q]);  // row aa-1
+            cell_traces<MUSCL>(vm2[q], vm1[q], w[q], a.beta, ylo[q], yhi[q]);  // row aa-1
           }
         }
       }
@@ -747,7 +673,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
 #pragma unroll
         for (int q = 0; q < 4; ++q) fcprev[q] = fc[q];
       }
-      if (c_active && (G || !LF_CWIN)) {
+      if (c_active) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           vm2[q] = vm1[q];
@@ -758,28 +684,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
     };
     int k = 0;
     for (; k < KS && k < nit; ++k) iter(k, std::true_type{});
-#if LF_FUSED_UNROLL == 2
-    for (; k + 1 <= ksteady; k += 2) {
-      iter(k, std::false_type{});
-      iter(k + 1, std::false_type{});
-    }
-#endif
     for (; k <= ksteady; ++k) iter(k, std::false_type{});
-#if LF_CWIN
-    if (k > KS) {
-      // the steady body kept the y window in the ring: back into registers for the
-      // guarded iterations (rows aa-2, aa-1 of iteration k are interior rows)
-      const double* r2 = sWs + ((k - 3) & 3) * 4 * NC + src_c;
-      const double* r1 = sWs + ((k - 2) & 3) * 4 * NC + src_c;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        vm2[q] = r2[q * NC];
-        vm1[q] = r1[q * NC];
-      }
-      vm2[1] = __longlong_as_double(__double_as_longlong(vm2[1]) ^ flip_bits);
-      vm1[1] = __longlong_as_double(__double_as_longlong(vm1[1]) ^ flip_bits);
-    }
-#endif
     for (; k < nit; ++k) iter(k, std::true_type{});
     // block-level reductions (warp shuffles, then one atomic per warp)
     for (int o = 16; o > 0; o >>= 1) {
@@ -966,7 +871,7 @@ FKBits make_fk_host(double gamma, double gm1, double beta, double dx, double dy)
 }
 
 constexpr size_t SMEM_BYTES =
-    (size_t)(URING * 4 + WR_ROWS * 4 + 4 + 16 + 16 + 16 + WC_ROWS * 4 + 4 + 4 + 4) * NC *
+    (size_t)(URING * 4 + 4 + 4 + 16 + 16 + 16 + WC_ROWS * 4 + 4 + 4 + 4) * NC *
         sizeof(double) +
     URING * sizeof(unsigned long long);
 // two blocks per SM (228 KB, 1 KB reserved per block): one block per SM halves the

@@ -25,10 +25,10 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # (a third element selects LF_MATH_*: 1 = contract; bit equality is checked
 # against the first variant of the same arithmetic)
 VARIANTS = {
+    "base_f": ("", 1),
     "f": ("", 1),
-    "f_ts0": ("-DLF_FUSED_TMA_SPREAD=0", 1),
+    "base_c_f": ("", 1, 1),
     "c_f": ("", 1, 1),
-    "c_f_ts0": ("-DLF_FUSED_TMA_SPREAD=0", 1, 1),
 }
 
 
