@@ -314,7 +314,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    resolved = solver.resolved_path()   # auto: the fused step at 2^27+ cells per slab
+    resolved = solver.resolved_path()   # auto: the fused step from 2^23 cells per slab
     # warm-up
     solver.advance(state, controls, args.warmup)
     barrier()

@@ -61,8 +61,8 @@ enum {
 };
 
 /* Heun-step implementation for lf_heun_step / lf_advance (all give identical results):
- *   AUTO     FUSED for slabs of 2^27 cells or more (Heun, no materials: the 16384^2
- *            and 32768^2 workloads), TWOPASS below that, for time_order 1 and for
+ *   AUTO     FUSED for slabs of 2^23 cells or more (2^22 in LF_MATH_CONTRACT; Heun, no
+ *            materials: BASELINE configs 3-5), TWOPASS below that, for time_order 1 and for
  *            materials; FUSED also when the two-pass scratch does not fit in device
  *            memory.  lf_resolved_path reports the choice.
  *   FUSED    one kernel per step (U^n read once, U^{n+1} written once)

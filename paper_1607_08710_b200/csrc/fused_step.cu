@@ -90,17 +90,18 @@ bool fused_supported(lf_handle* h) {
   return true;
 }
 
-// the two-pass kernels unless the fused one is asked for (or the slab is too
-// large for their 32-bit offsets)
-// LF_PATH_AUTO on large slabs: the one-kernel step.  Both run the 16384^2 step at
-// ~11.7-11.9 G cell-updates/s, but the two-pass one moves 290 B per cell-update, draws
-// the board's full 1000 W and runs at whatever clock the power cap leaves (1.73-1.9 GHz
-// from box to box), while the fused one (64 B) stays at the full 1965 MHz (~775 W).
-// Below 2^27 cells per slab the two-pass kernels fill the GPU better (1024^2: one wave).
+// LF_PATH_AUTO on large slabs: the one-kernel step.  From 2^23 cells per slab it is
+// the faster one (tools/path_sweep.py, round 2: Sedov 4096^2 11.7 vs 10.9 G
+// cell-updates/s, smooth 8192^2 13.7 vs 12.1, 16384^2 14.7 vs ~12); it moves 64 B per
+// cell-update instead of 290 and stays at the full clock where the two-pass step
+// meets the board's power cap.  Below, the two-pass kernels fill the GPU better
+// (1024^2: one wave; 2048^2 about even).  In the contract arithmetic the fused step
+// already wins at 2048^2 (13.5 vs 12.4), so its threshold is 2^22.
 static bool prefer_fused(lf_handle* h) {
   if (h->path != LF_PATH_AUTO || h->d.time_order < 2 || h->mc.n > 0) return false;
+  const int64_t min_cells = (int64_t)1 << (h->math == LF_MATH_CONTRACT ? 22 : 23);
   for (auto& s : h->slabs)
-    if ((int64_t)s.L.nx * s.L.ny < ((int64_t)1 << 27)) return false;
+    if ((int64_t)s.L.nx * s.L.ny < min_cells) return false;
   return true;
 }
 

@@ -131,15 +131,15 @@ def test_config4_full_16384_equal_reference(cuda):
 
 def test_config5_strip_equal_reference(cuda):
     """The config-5 generator and column count (32768, dx = dy = 1/32768) on a
-    periodic 32768 x 2048 strip, 20 steps, on the fused step (config 5's path on one
-    GPU) and on LF_PATH_AUTO, against the reference."""
+    periodic 32768 x 2048 strip, 20 steps, on LF_PATH_AUTO (the fused step, config 5's
+    path) in both arithmetics and on the two-pass kernels, against the reference."""
     n, ny, steps = 32768, 2048, 20
     case = CS.smooth(n, steps, ny=ny, y_extent=ny / n)
     f0, gpu = gpu_runs(case, seed=case.seed)
     rf, rdiag = reference_run(case, f0)
     check(case, gpu, rf, rdiag)
-    # the one-kernel step explicitly (AUTO picks the two-pass kernels below 2^27 cells)
-    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path="fused")
+    # the two-pass kernels explicitly (AUTO takes the one-kernel step from 2^23 cells)
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path="twopass")
     st = G.SolverState(field=f0.copy())
     s.attach(st)
     assert s.advance(st, G.TimeControls(case.cfl, case.t_final, steps), steps) == steps

@@ -31,7 +31,7 @@ def test_distributed_slabs_equal_single_handle(cuda):
 def test_config5_strip_eight_ranks_equal_single_handle(cuda):
     """BASELINE config 5's generator on a 32768 x 2048 periodic strip, 20 steps, as
     8 y-slab ranks (the 8-GPU decomposition) == one handle, on the fused step and on
-    LF_PATH_AUTO (tools/dist_threads.py --config5-strip)."""
+    the two-pass kernels (tools/dist_threads.py --config5-strip)."""
     assert os.path.exists(FAKE), "tests/fake_nccl not built (make -C tests/fake_nccl)"
     env = dict(os.environ, LF_NCCL_LIB=FAKE)
     p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "dist_threads.py"),

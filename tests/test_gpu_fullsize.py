@@ -85,15 +85,17 @@ def test_large_initial_state_matches_host(cuda):
 
 
 def test_auto_path_by_size_and_device_memory(cuda):
-    """LF_PATH_AUTO: the two-pass kernels below 2^27 cells per slab, the one-kernel step
-    above (it stays at full clock under the power cap, fused_step.cu prefer_fused); at
+    """LF_PATH_AUTO: the two-pass kernels below 2^23 cells per slab (2^22 in the contract
+    arithmetic), the one-kernel step above (fused_step.cu prefer_fused); at
     BASELINE config 5's 32768^2 only the one-kernel step fits one B200 (the two-pass
     scratch is 206 GB) -- periodic boundaries conserve mass and energy over its steps."""
-    for n, want in ((8192, "twopass"), (16384, "fused")):
+    for n, math, want in ((2048, "exact", "twopass"), (4096, "exact", "fused"),
+                          (1024, "contract", "twopass"), (2048, "contract", "fused"),
+                          (16384, "exact", "fused")):
         case = CS.smooth(n, 1)
-        s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params)
+        s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, math=math)
         s.init_fourier(G.SolverState(field=None), case.seed)
-        assert s.resolved_path() == want, n
+        assert s.resolved_path() == want, (n, math)
         s.close()
     case = CS.smooth(16384, 1)
     s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path="twopass")

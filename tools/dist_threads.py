@@ -140,7 +140,8 @@ def errors(ok):
 def strip5(ok, nranks=8, steps=20):
     """BASELINE config 5's generator on a 32768 x 2048 periodic strip (dy = dx), 20
     steps, as `nranks` y-slab ranks == one handle: every step's dt / time / min rho /
-    min p, interior_totals and each rank's rows of the final field.  Ranks download
+    min p, interior_totals and each rank's rows of the final field, on the fused and
+    the two-pass kernels.  Ranks download
     only their own rows (local_host), as bench.py's ranks do."""
     n, ny = 32768, 2048
     case = CS.smooth(n, steps, ny=ny, y_extent=ny / n)
@@ -166,7 +167,7 @@ def strip5(ok, nranks=8, steps=20):
         diag = [(d.dt, d.time, d.min_rho, d.min_p) for d in st.diagnostics]
         return part, diag, tot, (y0, rows)
 
-    for path in ("fused", "auto"):
+    for path in ("fused", "twopass"):
         single = go(path)
         uid = S.nccl_unique_id()
         res = [None] * nranks
