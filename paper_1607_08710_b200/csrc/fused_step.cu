@@ -14,7 +14,10 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -70,7 +73,32 @@ struct FusedState {
   cudaEvent_t ev_fill = nullptr, ev_edge = nullptr;
   FKBits fk_exact{}, fk_contract{};   // launch-parameter constants of the fused kernels
   bool fk_ok = false;                 // (computed on the first fused step)
+  // CUDA graphs of whole step batches (lf_advance, single-slab handles without NCCL):
+  // a batch's launches are captured once per key and replayed; the key holds every
+  // value the captured launches bake in (batch length, the control-record slot and
+  // the state buffer the batch starts from, the step parameters, the path)
+  using GraphKey = std::tuple<int, int, const double*, double, double, double, int, int, int>;
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;   // kernels per replay (lf_launch_count)
+  };
+  std::map<GraphKey, Graph> graphs;
+  bool capturing = false;
 };
+
+// LF_GRAPHS=0 in the environment: enqueue every batch launch by launch (A/B)
+static bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LF_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static void drop_graphs(FusedState* f) {
+  for (auto& kv : f->graphs) cudaGraphExecDestroy(kv.second.exec);
+  f->graphs.clear();
+}
 
 static FusedState* fstate(lf_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
 
@@ -200,6 +228,7 @@ static void fused_alloc(lf_handle* h, int steps) {
     f->tp_rows_nmat = nmat;
   }
   if (steps > f->cap) {
+    drop_graphs(f);   // captured finalize launches point into the old records
     cudaFree(f->rec);
     cudaFreeHost(f->rec_host);
     f->cap = std::max(steps, 64);
@@ -235,6 +264,7 @@ void fused_release(lf_handle* h) {
   }
   if (f->ev_fill) cudaEventDestroy(f->ev_fill);
   if (f->ev_edge) cudaEventDestroy(f->ev_edge);
+  drop_graphs(f);
   delete f;
   h->fused = nullptr;
 }
@@ -276,6 +306,17 @@ static void seed_ctl(lf_handle* h, double time) {
   }
 }
 
+// The fused kernels' launch-parameter constants (one-time, synchronous: never inside
+// a graph capture).
+static void ensure_fk(lf_handle* h) {
+  FusedState* f = fstate(h);
+  if (f->fk_ok) return;
+  f->fk_exact = fused_make_fk(h->k.gamma, h->k.gm1, h->k.beta, h->d.dx, h->d.dy);
+  f->fk_contract = fused_make_fk_contract(h->k.gamma, h->k.gm1, h->k.beta, h->d.dx, h->d.dy);
+  FK(cudaGetLastError());
+  f->fk_ok = true;
+}
+
 // Enqueue one fused step on every slab.
 static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit, double t_final,
                          cudaEvent_t k0, cudaEvent_t k1) {
@@ -283,14 +324,16 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
   FusedState* f = fstate(h);
   const int cur = f->cur, nxt = cur ^ 1;
   SlabState& s0 = h->slabs[0];
-  // bnd slot `cur` is free once the outflow sums of two steps ago have read it
-  FK(cudaStreamWaitEvent(s0.stream, f->ev_out[cur], 0));
+  // bnd slot `cur` is free once the outflow sums of two steps ago have read it (the
+  // first two steps of a captured batch: waited for before the capture began)
   const bool mat = h->mc.n > 0;   // (materials run on the two-pass kernels only)
   const bool twopass = use_twopass(h);
   // the outflow sums of a periodic axis are +0.0 without reading the faces
   // (k_outflow), so their faces are neither cleared nor summed across ranks
   const bool sum_x = !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC);
   const bool sum_y = !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC);
+  if ((sum_x || sum_y) && (!f->capturing || n_in_batch >= 2))
+    FK(cudaStreamWaitEvent(s0.stream, f->ev_out[cur], 0));
   double* bnd = f->bnd + (size_t)cur * bnd_words(h);
   // distributed one-kernel step: the halo rows travel on the comm stream while the
   // slab's interior row chunks (which read no halo row) run on the slab stream; the
@@ -408,12 +451,7 @@ static void enqueue_step(lf_handle* h, int n_in_batch, double cfl, double limit,
     const int chunks = (s.L.ny + f->rows_per_chunk - 1) / f->rows_per_chunk;
     const bool contract = h->math == LF_MATH_CONTRACT;
     const bool muscl = h->d.spatial_order >= 2;
-    if (!f->fk_ok) {
-      f->fk_exact = fused_make_fk(h->k.gamma, h->k.gm1, h->k.beta, h->d.dx, h->d.dy);
-      f->fk_contract = fused_make_fk_contract(h->k.gamma, h->k.gm1, h->k.beta, h->d.dx, h->d.dy);
-      FK(cudaGetLastError());
-      f->fk_ok = true;
-    }
+    ensure_fk(h);
     a.fk = contract ? f->fk_contract : f->fk_exact;
     auto launch = [&](int c0, int step, int n, cudaStream_t st) {
       if (n <= 0) return;
@@ -476,11 +514,66 @@ static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_fin
     evs.resize(2 * (size_t)n);
     for (auto& e : evs) FK(cudaEventCreate(&e));
   }
-  for (int i = 0; i < n; ++i)
-    enqueue_step(h, i, cfl, limit, t_final, timing ? evs[2 * i] : nullptr,
-                 timing ? evs[2 * i + 1] : nullptr);
-  // the side stream's last outflow sums (in-order) before the outflow comes back
-  FK(cudaStreamWaitEvent(s0.stream, f->ev_out[f->cur ^ 1], 0));
+  const bool outsums = !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC) ||
+                       !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC);
+  if (!timing && graphs_enabled() && h->slabs.size() == 1 && !h->nccl) {
+    // CUDA graph of the whole batch: decide everything that allocates or
+    // synchronises first, then capture once per key and replay
+    const bool twopass = use_twopass(h);
+    if (!twopass) ensure_fk(h);
+    const FusedState::GraphKey key{n, f->cur, s0.U, cfl, limit, t_final, h->math, twopass ? 1 : 0,
+                                   h->tp_exact};
+    if (outsums)  // the first two steps' bnd slots: the previous batch's sums
+      for (int b = 0; b < 2; ++b) FK(cudaStreamWaitEvent(s0.stream, f->ev_out[b], 0));
+    auto it = f->graphs.find(key);
+    if (it == f->graphs.end()) {
+      const long long l0 = launch_count();
+      FK(cudaStreamBeginCapture(s0.stream, cudaStreamCaptureModeThreadLocal));
+      f->capturing = true;
+      try {
+        for (int i = 0; i < n; ++i) enqueue_step(h, i, cfl, limit, t_final, nullptr, nullptr);
+        if (outsums) FK(cudaStreamWaitEvent(s0.stream, f->ev_out[f->cur ^ 1], 0));
+      } catch (...) {
+        f->capturing = false;
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(s0.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      f->capturing = false;
+      cudaGraph_t g = nullptr;
+      FK(cudaStreamEndCapture(s0.stream, &g));
+      FusedState::Graph gr;
+      const cudaError_t e = cudaGraphInstantiate(&gr.exec, g, 0);
+      cudaGraphDestroy(g);
+      FK(e);
+      gr.launches = (int)(launch_count() - l0);
+      count_launch(-gr.launches);   // counted when they run
+      if (f->graphs.size() >= 16) drop_graphs(f);
+      it = f->graphs.emplace(key, gr).first;
+    } else {
+      // what the captured enqueue_step calls did to the handle's host state
+      for (int i = 0; i < n; ++i) {
+        std::swap(s0.U, s0.U2);
+        if (h->mc.n > 0) std::swap(s0.P, s0.P2);
+        f->cur ^= 1;
+      }
+    }
+    FK(cudaGraphLaunch(it->second.exec, s0.stream));
+    count_launch(it->second.launches);
+    // events recorded inside a capture belong to it: record them again, after the
+    // replay (which joins the side stream), for the next launch-by-launch batch
+    for (int b = 0; b < 2; ++b) {
+      FK(cudaEventRecord(f->ev_fin[b], s0.stream));
+      FK(cudaEventRecord(f->ev_out[b], s0.stream));
+    }
+  } else {
+    for (int i = 0; i < n; ++i)
+      enqueue_step(h, i, cfl, limit, t_final, timing ? evs[2 * i] : nullptr,
+                   timing ? evs[2 * i + 1] : nullptr);
+    // the side stream's last outflow sums (in-order) before the outflow comes back
+    if (outsums) FK(cudaStreamWaitEvent(s0.stream, f->ev_out[f->cur ^ 1], 0));
+  }
   FK(cudaMemcpyAsync(f->rec_host, f->rec, (size_t)n * sizeof(StepRec), cudaMemcpyDeviceToHost,
                      s0.stream));
   FK(cudaMemcpyAsync(f->outflow_host, f->outflow, 4 * sizeof(double), cudaMemcpyDeviceToHost,
