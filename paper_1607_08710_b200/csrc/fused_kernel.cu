@@ -119,13 +119,10 @@ constexpr int PREFETCH = 2;
 #endif
 // LF_FUSED_TMA_SPREAD 1: the four component rows of each U^n row are copied by the
 // four P warps (one each) instead of all by warp 0
-// (measured: +1.1 % exact, -1.5 % contract: more spills there)
+// (measured: +1.1 % exact; in the contract build -1.5 % with the maxima in registers,
+// +2.8 % with LF_FUSED_KEYSMEM)
 #ifndef LF_FUSED_TMA_SPREAD
-#if LF_CONTRACT
-#define LF_FUSED_TMA_SPREAD 0
-#else
 #define LF_FUSED_TMA_SPREAD 1
-#endif
 #endif
 // LF_FUSED_CRING 1: C takes the x slopes of W*(j) straight from the P -> C ring (each
 // lane's image column) instead of exchanging its W*(j) row through shared memory and a
@@ -143,6 +140,17 @@ constexpr int PREFETCH = 2;
 #endif
 #endif
 constexpr int WC_ROWS = LF_FUSED_CRING ? 0 : 1;
+// LF_FUSED_KEYSMEM 1: the corrector's running maxima (CFL rate, ~min rho, ~min e_int)
+// in per-thread shared-memory slots instead of six registers: the contract build's
+// spills shrink (48 -> 20 B), +3.4 % there (with TMA_SPREAD, which then pays: 18.1 G
+// cell-updates/s); -6 % in the exact build, which does not spill
+#ifndef LF_FUSED_KEYSMEM
+#if LF_CONTRACT
+#define LF_FUSED_KEYSMEM 1
+#else
+#define LF_FUSED_KEYSMEM 0
+#endif
+#endif
 template <bool MUSCL>
 __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(FusedArgs a) {
   extern __shared__ __align__(128) double smem[];
@@ -157,6 +165,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
   double* sFc = sTc + 4 * NC;          // [4][NC]     C: 0.5 (F^n + F*) x-faces
   double* sStash = sFc + 4 * NC;       // [4][NC]     C: top-edge ghost image
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sStash + 4 * NC);  // [URING]
+  unsigned long long* sKey = mbar + URING;   // [3][NC] corrector maxima (LF_FUSED_KEYSMEM)
 
   const StepCtl ctl = *a.ctl;
   if (ctl.done) return;
@@ -410,7 +419,13 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
     // ================================================================ stage 2 (C)
     double vm2[4] = {1.0, 0.0, 0.0, 1.0}, vm1[4] = {1.0, 0.0, 0.0, 1.0};
     double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fcprev[4] = {0.0, 0.0, 0.0, 0.0};
+#if LF_FUSED_KEYSMEM
+    sKey[t] = 0ull;
+    sKey[NC + t] = NINF_KEY;
+    sKey[2 * NC + t] = NINF_KEY;
+#else
     unsigned long long rate_key = 0ull, nmin_r = NINF_KEY, nmin_e = NINF_KEY;
+#endif
     unsigned dtfail = 0;
     // source column of this thread's W* value (ghost columns at non-periodic x edges)
     int src_t = t;
@@ -640,13 +655,24 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           fail = 1;
         } else {
           const unsigned long long kr = ~pos_bits(v[0]), ke = ~pos_bits(eint);
+#if LF_FUSED_KEYSMEM
+          const unsigned long long nr = sKey[NC + t], ne = sKey[2 * NC + t];
+          sKey[NC + t] = kr > nr ? kr : nr;
+          sKey[2 * NC + t] = ke > ne ? ke : ne;
+#else
           nmin_r = kr > nmin_r ? kr : nmin_r;
           nmin_e = ke > nmin_e ? ke : nmin_e;
+#endif
         }
         if (rate_ok) {
           if (rr == rr) {
             const unsigned long long b = pos_bits(rr);
+#if LF_FUSED_KEYSMEM
+            const unsigned long long rk = sKey[t];
+            sKey[t] = b > rk ? b : rk;
+#else
             rate_key = b > rate_key ? b : rate_key;
+#endif
           }
           if (!okr) fail = 1;
         } else {
@@ -687,6 +713,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
     for (; k <= ksteady; ++k) iter(k, std::false_type{});
     for (; k < nit; ++k) iter(k, std::true_type{});
     // block-level reductions (warp shuffles, then one atomic per warp)
+#if LF_FUSED_KEYSMEM
+    unsigned long long rate_key = sKey[t], nmin_r = sKey[NC + t], nmin_e = sKey[2 * NC + t];
+#endif
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long r2 = __shfl_xor_sync(FULL, rate_key, o);
       const unsigned long long a2 = __shfl_xor_sync(FULL, nmin_r, o);
@@ -873,7 +902,7 @@ FKBits make_fk_host(double gamma, double gm1, double beta, double dx, double dy)
 constexpr size_t SMEM_BYTES =
     (size_t)(URING * 4 + 4 + 4 + 16 + 16 + 16 + WC_ROWS * 4 + 4 + 4 + 4) * NC *
         sizeof(double) +
-    URING * sizeof(unsigned long long);
+    URING * sizeof(unsigned long long) + (LF_FUSED_KEYSMEM ? 3 * NC * sizeof(unsigned long long) : 0);
 // two blocks per SM (228 KB, 1 KB reserved per block): one block per SM halves the
 // resident warps of this latency-bound kernel
 static_assert(2 * (SMEM_BYTES + 1024) <= 228 * 1024, "fused step: two blocks per SM");
