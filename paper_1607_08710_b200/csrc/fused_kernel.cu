@@ -165,7 +165,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
   double* sFc = sTc + 4 * NC;          // [4][NC]     C: 0.5 (F^n + F*) x-faces
   double* sStash = sFc + 4 * NC;       // [4][NC]     C: top-edge ghost image
   unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sStash + 4 * NC);  // [URING]
-  unsigned long long* sKey = mbar + URING;   // [3][NC] corrector maxima (LF_FUSED_KEYSMEM)
+#if LF_FUSED_KEYSMEM
+  unsigned long long* sKey = mbar + URING;   // [3][NC] corrector maxima
+#endif
 
   const StepCtl ctl = *a.ctl;
   if (ctl.done) return;

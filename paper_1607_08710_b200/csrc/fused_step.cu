@@ -75,9 +75,12 @@ struct FusedState {
   bool fk_ok = false;                 // (computed on the first fused step)
   // CUDA graphs of whole step batches (lf_advance, single-slab handles without NCCL):
   // a batch's launches are captured once per key and replayed; the key holds every
-  // value the captured launches bake in (batch length, the control-record slot and
-  // the state buffer the batch starts from, the step parameters, the path)
-  using GraphKey = std::tuple<int, int, const double*, double, double, double, int, int, int>;
+  // value the captured launches bake in (batch length, the control-record slot, every
+  // state and scratch buffer as the batch starts -- euler_stage swaps U with U*, so
+  // U alone does not identify them --, the step parameters, the path)
+  using GraphKey = std::tuple<int, int, const double*, const double*, const double*,
+                              const double*, const double*, const double*, double, double,
+                              double, int, int, int>;
   struct Graph {
     cudaGraphExec_t exec = nullptr;
     int launches = 0;   // kernels per replay (lf_launch_count)
@@ -521,7 +524,8 @@ static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_fin
     // synchronises first, then capture once per key and replay
     const bool twopass = use_twopass(h);
     if (!twopass) ensure_fk(h);
-    const FusedState::GraphKey key{n, f->cur, s0.U, cfl, limit, t_final, h->math, twopass ? 1 : 0,
+    const FusedState::GraphKey key{n,        f->cur,  s0.U,  s0.U2,   s0.Us,   s0.P,     s0.P2,
+                                   s0.Ps,    cfl,     limit, t_final, h->math, twopass ? 1 : 0,
                                    h->tp_exact};
     if (outsums)  // the first two steps' bnd slots: the previous batch's sums
       for (int b = 0; b < 2; ++b) FK(cudaStreamWaitEvent(s0.stream, f->ev_out[b], 0));

@@ -380,3 +380,47 @@ def test_time_order_1_on_the_two_pass_kernels(cuda, cfg, spatial_order):
     assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4])
     assert list(st.boundary_outflow) == list(ref.boundary_outflow)
     assert per_step <= 5, per_step     # fill, pass, finalize (+ outflow sums): not stage-wise
+
+
+@pytest.mark.parametrize("path", ["twopass", "fused", "staged"])
+def test_foreign_field_between_steps_keeps_the_resident_state(cuda, path):
+    """A diagnostic compute_dt / euler_stage of another field between heun_steps must
+    not rewind the device-resident state (the mirror saves it into its host field
+    before replacing it, solver.py _evict); results as the oracle's uninterrupted run."""
+    case = CS.quadrant(48, 12)
+    f0 = CS.initial_field(case)
+    ref, rdiag = run_oracle(case, 12, field=f0)
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path=path)
+    st = G.SolverState(field=f0.copy())
+    ctl = G.TimeControls(case.cfl, case.t_final, case.max_steps)
+    other = CS.initial_field(CS.quadrant(48, 1))
+    for k in range(12):
+        s.heun_step(st, ctl, case.t_final)
+        if k == 3:
+            s.compute_dt(other, ctl, 0.0, 1e30)
+        if k == 7:
+            s.euler_stage(other.copy(), 1e-5, G.new_field(case.grid))
+    s.sync_to_host(st)
+    assert_fields_equal(case.grid.interior(st.field), case.grid.interior(ref.field), path)
+    assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4])
+
+
+def test_beta_below_one_runs_the_reference_limiter(cuda):
+    """LimiterParams beta < 1 (accepted by LagfluxSolver, outside make_limiter's range):
+    the fast kernels' limiter form holds for beta >= 1 only, so the handle runs the
+    stage-wise kernels -- bit-equal to the oracle, which evaluates sweby as written."""
+    case = CS.quadrant(40, 10)
+    params = G.SchemeParams(beta=0.5)
+    f0 = CS.initial_field(case)
+    o = O.OracleSolver(case.grid, case.bc, case.gamma, params)
+    ref = G.SolverState(field=f0.copy())
+    for _ in range(10):
+        o.heun_step(ref, case.cfl, case.t_final)
+    for path in ("auto", "fused", "twopass"):
+        s = LagfluxSolver(case.grid, case.bc, case.gamma, params, path=path)
+        assert s.resolved_path() == "staged", path
+        st = G.SolverState(field=f0.copy())
+        for _ in range(10):
+            s.heun_step(st, G.TimeControls(case.cfl, case.t_final), case.t_final)
+        s.sync_to_host(st)
+        assert_fields_equal(case.grid.interior(st.field), case.grid.interior(ref.field), path)

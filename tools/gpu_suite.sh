@@ -1,3 +1,4 @@
+# One GPU box: smoke(), the whole -m gpu suite, the default bench line (outputs in gpurun_out/r2d/)
 set -x
 O=gpurun_out/r2d; mkdir -p $O
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
