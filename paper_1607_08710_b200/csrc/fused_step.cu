@@ -519,9 +519,11 @@ static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_fin
   }
   const bool outsums = !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC) ||
                        !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC);
-  if (!timing && graphs_enabled() && h->slabs.size() == 1 && !h->nccl) {
-    // CUDA graph of the whole batch: decide everything that allocates or
-    // synchronises first, then capture once per key and replay
+  if (!timing && n >= 8 && graphs_enabled() && h->slabs.size() == 1 && !h->nccl) {
+    // CUDA graph of the whole batch (lf_advance batches; a single heun_step, whose
+    // limit time may change from call to call, stays launch by launch): decide
+    // everything that allocates or synchronises first, then capture once per key and
+    // replay
     const bool twopass = use_twopass(h);
     if (!twopass) ensure_fk(h);
     const FusedState::GraphKey key{n,        f->cur,  s0.U,  s0.U2,   s0.Us,   s0.P,     s0.P2,
