@@ -519,7 +519,12 @@ static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_fin
   }
   const bool outsums = !(h->d.bc[0] == LF_PERIODIC && h->d.bc[1] == LF_PERIODIC) ||
                        !(h->d.bc[2] == LF_PERIODIC && h->d.bc[3] == LF_PERIODIC);
-  if (!timing && n >= 8 && graphs_enabled() && h->slabs.size() == 1 && !h->nccl) {
+  // CUDA graphs pay where launch latency dominates the step: small single-material
+  // grids (tools/graph_ab.py: Sod 400x4 38 -> 33 us per step, quadrant 1024^2 125 ->
+  // 122); on the triple point (1.8M cells, 3 materials) the replay measured 9 % slower
+  // than the stream launches (the side stream's low priority is not part of a graph)
+  const bool small = (int64_t)h->d.nx * h->d.ny <= ((int64_t)1 << 20) && h->mc.n == 0;
+  if (!timing && n >= 8 && small && graphs_enabled() && h->slabs.size() == 1 && !h->nccl) {
     // CUDA graph of the whole batch (lf_advance batches; a single heun_step, whose
     // limit time may change from call to call, stays launch by launch): decide
     // everything that allocates or synchronises first, then capture once per key and
