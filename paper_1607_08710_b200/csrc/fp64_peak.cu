@@ -86,6 +86,8 @@ void measure(int blocks, double* sink, cudaEvent_t e0, cudaEvent_t e1, double bu
 // DADD sustained}, fp64 thread instructions per second on `device`.
 extern "C" int lf_fp64_peak(int device, double burst_ms, double sustain_ms, double* out) {
   if (!out || burst_ms <= 0.0 || sustain_ms < 0.0) return LF_ERR_ARGUMENT;
+  int prev = 0;
+  cudaGetDevice(&prev);
   if (cudaSetDevice(device) != cudaSuccess) return LF_ERR_DEVICE;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -102,5 +104,7 @@ extern "C" int lf_fp64_peak(int device, double burst_ms, double sustain_ms, doub
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(sink);
-  return cudaGetLastError() == cudaSuccess ? LF_OK : LF_ERR_DEVICE;
+  const bool ok = cudaGetLastError() == cudaSuccess;
+  cudaSetDevice(prev);   // the caller's current device is left as it was
+  return ok ? LF_OK : LF_ERR_DEVICE;
 }

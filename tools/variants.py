@@ -25,10 +25,10 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # (a third element selects LF_MATH_*: 1 = contract; bit equality is checked
 # against the first variant of the same arithmetic)
 VARIANTS = {
-    "c_f_ks_c1_ts": ("-DLF_FUSED_KEYSMEM=1 -DLF_FUSED_CRING=1 -DLF_FUSED_TMA_SPREAD=1", 1, 1),
-    "c_f_ks_c1_ts_dcp": ("-DLF_FUSED_KEYSMEM=1 -DLF_FUSED_CRING=1 -DLF_FUSED_TMA_SPREAD=1 -DLF_FUSED_DONTCARE_P=1", 1, 1),
-    "c_f_ks_c1_ts_box": ("-DLF_FUSED_KEYSMEM=1 -DLF_FUSED_CRING=1 -DLF_FUSED_TMA_SPREAD=1 -DLF_FUSED_EPI_BOX=1", 1, 1),
-    "c_f_ks_ts": ("-DLF_FUSED_KEYSMEM=1 -DLF_FUSED_TMA_SPREAD=1", 1, 1),
+    "base_f": ("", 1),
+    "f": ("", 1),
+    "base_c_f": ("", 1, 1),
+    "c_f": ("", 1, 1),
 }
 
 
