@@ -46,3 +46,15 @@ def test_epilogue_box_implies_fast_path_validity(cuda):
     assert accepted > n // 8
     assert check_failed == 0
     assert differ == 0
+
+
+def test_fp64_peak_measurement(cuda):
+    """lf_fp64_peak (the fp64 roof bench.py reports against): DFMA, DMUL and DADD
+    thread-instruction rates, burst and sustained, positive and consistent with one
+    fp64 instruction per lane per cycle on 64 lanes per SM (B200: ~18.5 T/s)."""
+    out = (C.c_double * 6)()
+    assert N.lib().lf_fp64_peak(0, 20.0, 100.0, out) == 0
+    rates = list(out)
+    assert all(r > 1e12 for r in rates), rates
+    assert max(rates) / min(rates) < 1.2, rates
+    assert N.lib().lf_fp64_peak(0, 0.0, 0.0, out) == N.LF_ERR_ARGUMENT
