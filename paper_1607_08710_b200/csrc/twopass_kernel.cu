@@ -59,38 +59,18 @@ __device__ __forceinline__ void shfl_down4(const double (&v)[N], double (&o)[N],
 
 // Build-time tuning knobs (tools/variants.py sweeps them):
 //   LF_TP_MINBLOCKS  resident blocks per SM requested from ptxas (register budget)
-//   LF_TP_LATELOAD   1: load the update operands after the face solves
-//   LF_TP_UNROLL     2: unroll the row loop twice (state rotation by renaming)
-//   LF_TP_ASYNC      1: update operands staged one row ahead in shared memory
-//                    (cp.async); -1 % here (the loads are already covered at
-//                    12 warps/SM), +20-32 % in the 8-warp material kernel
+//   (measured and dropped: update operands loaded after the face solves; the row
+//   loop unrolled twice, -15 %; operands staged one row ahead in shared memory with
+//   cp.async, -1 % here -- the loads are covered at 12 warps/SM -- but +20-32 % in
+//   the 8-warp material kernel, which keeps it)
 #ifndef LF_TP_MINBLOCKS
 #define LF_TP_MINBLOCKS 3
-#endif
-#ifndef LF_TP_LATELOAD
-#define LF_TP_LATELOAD 0
-#endif
-#ifndef LF_TP_UNROLL
-#define LF_TP_UNROLL 1
 #endif
 #ifndef LF_EPI_BOX
 #define LF_EPI_BOX 1
 #endif
-// LF_TP_ASYNC 1: stage the update operands one row ahead in shared memory with
-// cp.async (as twopass_mat_kernel.cu) instead of loading them into registers
-#ifndef LF_TP_ASYNC
-#define LF_TP_ASYNC 0
-#endif
 #ifndef LF_TP_EDGE1
 #define LF_TP_EDGE1 1
-#endif
-#if LF_TP_ASYNC
-__device__ __forceinline__ void tp_cp_async8(double* sdst, const double* gsrc, bool pred) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gsrc),
-               "r"(pred ? 8 : 0)
-               : "memory");
-}
 #endif
 
 // EXACT = false: the plain fast path; a warp whose stencil rows hold a velocity
@@ -160,30 +140,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
   double hiprev[4] = {1.0, 0.0, 0.0, 1.0}, fyprev[4] = {0.0, 0.0, 0.0, 0.0};
   // rows r-3 .. r-1 of this lane with a velocity in (0, 2^-500), one bit per row
   unsigned tiny_rows = 0;
-#if LF_TP_ASYNC
-  constexpr int NOP = CORR ? 12 : 4;   // base 0-3, fnx 4-7, fny 8-11
-  __shared__ double stage[TP_THREADS / 32][2][NOP][32];
-  double(*const st)[NOP][32] = stage[threadIdx.x >> 5];
-  auto issue = [&](int itn, int orow, int buf) {
-    const bool pb = itn >= 4 && col_in_mem;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) tp_cp_async8(&st[buf][q][lane], pb ? a.base + q * a.fstride + orow : a.base, pb);
-    if (CORR) {
-      const bool px = a.heun && pb && c >= 0 && c <= a.nx, py = a.heun && itn >= 3 && col_interior;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        tp_cp_async8(&st[buf][4 + q][lane], px ? a.fx + q * a.fx_stride + orow : a.fx, px);
-        tp_cp_async8(&st[buf][8 + q][lane], py ? a.fy + q * a.fy_stride + (orow + P) : a.fy, py);
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  issue(0, o_in - 2 * P, 0);
-#endif
 
-#if LF_TP_UNROLL == 2
-#pragma unroll 2
-#endif
   for (int it = 0; it < nit; ++it) {
     const int r = y0 - 2 + it;   // input row
     const int row = r - 2;       // row updated this iteration (when it >= 4)
@@ -213,13 +170,7 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
       for (int q = 0; q < 4; ++q) fny[q] = __ldg(a.fy + q * a.fy_stride + (o_row + P));
     }
     };
-#if LF_TP_ASYNC
-    (void)load_operands;
-    if (it + 1 < nit) issue(it + 1, o_row + P, (it + 1) & 1);
-    else asm volatile("cp.async.commit_group;\n" ::: "memory");
-#elif !LF_TP_LATELOAD
     load_operands();
-#endif
     // -- W(r) (solver.cpp:145-163)
     double w[4] = {1.0, 0.0, 0.0, 1.0};
     if (col_in_mem) {
@@ -276,20 +227,6 @@ __global__ void __launch_bounds__(TP_THREADS, LF_TP_MINBLOCKS) k_pass(PassArgs a
     if (needs_mean(usy))
       face_mean<1>(hiprev[0], hiprev[1], hiprev[2], hiprev[3], ylo[0], ylo[1], ylo[2], ylo[3],
                    psy, usy, C, fy, oky);
-#if LF_TP_LATELOAD && !LF_TP_ASYNC
-    load_operands();
-#endif
-#if LF_TP_ASYNC
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // this row's operands
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      base[q] = st[it & 1][q][lane];
-      if (CORR) {
-        fnx[q] = st[it & 1][4 + q][lane];
-        fny[q] = st[it & 1][8 + q][lane];
-      }
-    }
-#endif
     if (need_x && !traces_ok(xmh[0], xmh[3], xlo[0], xlo[3]) && c >= 0 && row >= 0 && row < a.ny)
       fail = 1;
     if (need_y && !traces_ok(hiprev[0], hiprev[3], ylo[0], ylo[3]) && r - 1 >= 0 && r - 1 <= a.ny)
