@@ -7,7 +7,10 @@
 
 namespace lfb {
 
-constexpr int FUSED_NC = 128;                 // columns per strip (threads per warp group)
+#ifndef LF_FUSED_NC
+#define LF_FUSED_NC 128
+#endif
+constexpr int FUSED_NC = LF_FUSED_NC;         // columns per strip (threads per warp group)
 constexpr int FUSED_TXO = FUSED_NC - 8;       // output columns per strip
 constexpr int FUSED_THREADS = 2 * FUSED_NC;   // predictor group + corrector group
 constexpr unsigned long long NINF_KEY = ~0x7ff0000000000000ull;  // ~bits(+inf)

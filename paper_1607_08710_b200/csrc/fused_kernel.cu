@@ -115,7 +115,7 @@ constexpr int PREFETCH = 2;
 #endif
 #endif
 #ifndef LF_MINBLOCKS
-#define LF_MINBLOCKS 2
+#define LF_MINBLOCKS (256 / FUSED_NC)
 #endif
 // LF_FUSED_TMA_SPREAD 1: the four component rows of each U^n row are copied by the
 // four P warps (one each) instead of all by warp 0
@@ -257,10 +257,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
         // the slot's previous row (k+PREFETCH-URING) was last read before the
         // previous iteration's __syncthreads
         const int kn = k + PREFETCH, s = kn & (URING - 1), q = threadIdx.x >> 5;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (q == 0) mbar_expect_tx(&mbar[s], 4 * row_bytes);
-        tma_row(sU + (s * 4 + q) * NC, src0 + (int64_t)kn * a.pitch + q * a.fstride, row_bytes,
-                &mbar[s]);
+        if (q < 4) {   // (NC = 256: eight predictor warps, four components)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (q == 0) mbar_expect_tx(&mbar[s], 4 * row_bytes);
+          tma_row(sU + (s * 4 + q) * NC, src0 + (int64_t)kn * a.pitch + q * a.fstride, row_bytes,
+                  &mbar[s]);
+        }
       }
 #else
       if (threadIdx.x == 0 && (!G || k + PREFETCH <= klastp)) {
@@ -907,7 +909,7 @@ constexpr size_t SMEM_BYTES =
     URING * sizeof(unsigned long long) + (LF_FUSED_KEYSMEM ? 3 * NC * sizeof(unsigned long long) : 0);
 // two blocks per SM (228 KB, 1 KB reserved per block): one block per SM halves the
 // resident warps of this latency-bound kernel
-static_assert(2 * (SMEM_BYTES + 1024) <= 228 * 1024, "fused step: two blocks per SM");
+static_assert(LF_MINBLOCKS * (SMEM_BYTES + 1024) <= 228 * 1024, "fused step: two blocks per SM");
 
 }  // namespace
 
