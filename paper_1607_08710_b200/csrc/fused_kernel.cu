@@ -1,6 +1,6 @@
 // fused_kernel.cu -- one kernel per Heun time step (LagfluxSolver::heun_step, solver.cpp:489-546).
 //
-// Design:
+// Design ("Fused one-kernel"):
 //  * A block owns a strip of NC = 128 columns (TXO = 120 output columns plus a
 //    4-column halo each side) and marches down a chunk of rows.  The whole step
 //    -- primitives, MUSCL traces, Lagrangian HLL, upwind fluxes, predictor U*,
@@ -18,6 +18,13 @@
 //    faces of a cell); x-direction neighbours go through shared memory.  Each
 //    thread solves its x-face and its y-face Riemann problems in one straight
 //    line of code, so the two dependency chains overlap.
+//  * Round 2: the row loop runs a guarded
+//    body for the pipeline fill / drain and the domain's y edges and a guard-free
+//    steady body in between (the same source, a compile-time flag); the corrector
+//    takes the x slopes of W*(j) straight from the P -> C ring (LF_FUSED_CRING,
+//    exact build); the step constants arrive as launch parameters; the four P warps
+//    share the TMA issue.  The kernel is fp64 / issue bound: 1566 instructions per
+//    cell-update, 645 of them fp64, 4 warps per scheduler at 128 registers.
 //  * fp64 arithmetic keeps the reference's evaluation order (--fmad=false);
 //    divisions and square roots use fastmath.cuh (the compiler's own IEEE fast
 //    path with shared reciprocals and one deferred range check per face), so
