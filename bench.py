@@ -45,6 +45,21 @@ UNIT = "cell-updates/s"
 CPU_SAMPLE_ROWS = 4096       # cpu_baseline leg of our arm: 16384 x 4096 strip of config 4
 
 
+# stdout carries exactly the one JSON line: everything else any library prints there
+# (NCCL's version banner, say) goes to stderr (main() moves fd 1 onto fd 2)
+_JSON_FD = None
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    sys.stdout.flush()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -151,12 +166,19 @@ def dist_setup(args):
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
-    if world > 1:
+    # LF_BENCH_DIST=1 with one process: the distributed machinery (process group, a
+    # one-rank distributed handle on the real NCCL) on a one-GPU box -- a check of
+    # the N > 1 code path where only one GPU is available
+    multi = world > 1 or os.environ.get("LF_BENCH_DIST") == "1"
+    if multi:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    return torch, dist, world, rank, local
+    return torch, dist, world, rank, local, multi
 
 
 def cpu_sample_case(cases, rows=CPU_SAMPLE_ROWS, n=16384):
@@ -235,7 +257,7 @@ def run_reference(args):
     from oracle import oracle as O
     threads = os.cpu_count() or 1
     if not O.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_lagflux.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libref_lagflux.so not built"})
         return 0
     case, what = reference_case(CS, world, args.scaling)
     value, wall = time_reference_cpu(case, args.steps, args.warmup, threads)
@@ -253,7 +275,7 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -281,7 +303,7 @@ def ncu_fp64_ops(kernel_key):
 
 
 def run_ours(args):
-    torch, dist, world, rank, local = dist_setup(args)
+    torch, dist, world, rank, local, multi = dist_setup(args)
     from paper_1607_08710_b200 import cases as CS
     from paper_1607_08710_b200 import grid as G
     from paper_1607_08710_b200 import native as N
@@ -296,7 +318,7 @@ def run_ours(args):
     g = case.grid
     dist_arg = None
     nid = None
-    if world > 1:
+    if multi:
         nid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(nid, src=0)
         dist_arg = (rank, world, local, nid[0])
@@ -310,7 +332,7 @@ def run_ours(args):
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
+        if multi:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -328,7 +350,7 @@ def run_ours(args):
     launches = solver.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if multi:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     cells_total = g.nx * g.ny
@@ -339,7 +361,7 @@ def run_ours(args):
     # chained over the ranks, so it is bit-identical for any slab count)
     digest = {"interior_totals": [float(x).hex() for x in solver.interior_totals()],
               "time": float(state.time).hex(), "steps": state.step}
-    if strong and world > 1:
+    if strong and multi:
         # the reference's scaling_sweep check (bench.cpp:96-99,124-128): the N-rank
         # run must equal one handle holding the whole grid, bit for bit
         single = None
@@ -423,7 +445,7 @@ def run_ours(args):
             ev1.record(stream)
             barrier()
         t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
-        if world > 1:
+        if multi:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         cvalue = cells_total * ctaken / (float(t.item()) / 1e3)
         ck_ms, _, ck_n = solver.time_steps(max(5, min(args.steps, 20)), case.cfl)
@@ -463,17 +485,20 @@ def run_ours(args):
         k2 = solver.advance(with_state, controls, args.steps)
         solver.sync_to_host(with_state)            # D2H of the result
         ev1.record(stream)
-        barrier()
+        torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        # on the device (the copies and steps are on this stream), max over ranks; the
+        # host wall clock of the same region is a cross-check
         e_ms = ev0.elapsed_time(ev1)
-        t = torch.tensor([max(e_ms, wall * 1e3)], dtype=torch.float64, device="cuda")
-        if world > 1:
+        barrier()
+        t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+        if multi:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         state_bytes = 4 * 8 * g.nx * rows
         e2e = {"value": cells_total * k2 / (float(t.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": state_bytes / max(k2, 1),
                "d2h_bytes_per_step": (state_bytes + 48 * k2) / max(k2, 1),
-               "steps_amortised": k2,
+               "steps_amortised": k2, "host_wall_ms": wall * 1e3,
                "what": f"upload of the state from pinned host memory, {k2} steps "
                        f"(dt/diagnostics back to the host), download of the final state; the "
                        f"{state_bytes / 1e9:.1f} GB each way over PCIe are amortised over {k2} "
@@ -514,11 +539,11 @@ def run_ours(args):
                 "gpu_launches": launches, "clocks": clock_summary, "digest": digest}
         if contract is not None:
             line["math_contract"] = contract
-        print(json.dumps(line))
+        emit(line)
     solver.close()
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
-    if strong and world > 1 and rank == 0 and not digest.get("equal"):
+    if strong and multi and rank == 0 and not digest.get("equal"):
         return 3
     return 0
 
@@ -526,7 +551,7 @@ def run_ours(args):
 def run_ours_mat(args):
     """--workload triple_point: the multimaterial partial-density transport (SURVEY.md
     §8f row 1) on cases/triple_point.case at its reference resolution, one GPU."""
-    torch, dist, world, rank, local = dist_setup(args)
+    torch, dist, world, rank, local, _ = dist_setup(args)
     from paper_1607_08710_b200 import cases as CS
     from paper_1607_08710_b200 import grid as G
     from paper_1607_08710_b200 import multimat as MM
@@ -620,7 +645,7 @@ def run_ours_mat(args):
                        "l2": "state %.2f GB (field + partials)" % ((4 + n_mat) * 8 * g.nx * g.ny / 1e9)},
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks.summary()}
-    print(json.dumps(line))
+    emit(line)
     solver.close()
     return 0
 
@@ -648,6 +673,9 @@ def main():
                     help="smooth: BASELINE config 4/5 (the headline); triple_point: the "
                          "multimaterial transport (one GPU)")
     args = ap.parse_args()
+    global _JSON_FD
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     # OpenMP binding of the reference CPU path (bench.cpp-style timing on all cores),
     # before any library that loads libgomp (oracle/_ref, the oracle, torch)
     os.environ.setdefault("OMP_PLACES", "cores")
