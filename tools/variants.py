@@ -25,10 +25,10 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # (a third element selects LF_MATH_*: 1 = contract; bit equality is checked
 # against the first variant of the same arithmetic)
 VARIANTS = {
-    "base_f": ("", 1),
     "f": ("", 1),
-    "base_c_f": ("", 1, 1),
+    "f_defer": ("-DLF_FUSED_EPI_DEFER=1", 1),
     "c_f": ("", 1, 1),
+    "c_f_defer": ("-DLF_FUSED_EPI_DEFER=1", 1, 1),
 }
 
 
@@ -44,6 +44,10 @@ def _head_tree():
 
 def build(names=None):
     os.makedirs(OUT, exist_ok=True)
+    # only the current variants travel to the GPU box (the snapshot is size-capped)
+    for fn in os.listdir(OUT):
+        if fn.split(".")[0] not in VARIANTS:
+            os.unlink(os.path.join(OUT, fn))
     head = None
     procs = []
     for name, (flags, _path, *_m) in VARIANTS.items():
