@@ -147,6 +147,7 @@ constexpr int PREFETCH = 2;
 #endif
 #endif
 constexpr int WC_ROWS = LF_FUSED_CRING ? 0 : 1;
+
 // LF_FUSED_KEYSMEM 1: the corrector's running maxima (CFL rate, ~min rho, ~min e_int)
 // in per-thread shared-memory slots instead of six registers: the contract build's
 // spills shrink (48 -> 20 B), +3.4 % there (with TMA_SPREAD, which then pays: 18.1 G
@@ -480,6 +481,44 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
                            (x0 - 4 + NC > a.nx && a.bc_xhi != LF_PERIODIC);
     const bool x_edge_blk = x0 - 4 <= 0 || x0 - 4 + NC > a.nx - 1;   // holds column 0 or nx-1
     const bool dxy_box = pos_in_box(a.dx) && pos_in_box(a.dy);
+    // positivity (solver.cpp:300-307) and the diagnostics minima and the CFL rate of
+    // U^{n+1} for the next step's dt (solver.cpp:457-469), of one updated cell
+    auto epilogue = [&](const double (&v)[4]) {
+      bool ok = true, okr = true, rate_ok;
+      double eint, rr;
+#if LF_FUSED_EPI_BOX
+      cell_epilogue_box<LF_FUSED_EPI_BOX == 2>(v, C, dxy_box, eint, ok, rr, rate_ok, okr);
+#else
+      cell_epilogue(v, C, eint, ok, rr, rate_ok, okr);
+#endif
+      if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
+        fail = 1;
+      } else {
+        const unsigned long long kr = ~pos_bits(v[0]), ke = ~pos_bits(eint);
+#if LF_FUSED_KEYSMEM
+        const unsigned long long nr = sKey[NC + t], ne = sKey[2 * NC + t];
+        sKey[NC + t] = kr > nr ? kr : nr;
+        sKey[2 * NC + t] = ke > ne ? ke : ne;
+#else
+        nmin_r = kr > nmin_r ? kr : nmin_r;
+        nmin_e = ke > nmin_e ? ke : nmin_e;
+#endif
+      }
+      if (rate_ok) {
+        if (rr == rr) {
+          const unsigned long long b = pos_bits(rr);
+#if LF_FUSED_KEYSMEM
+          const unsigned long long rk = sKey[t];
+          sKey[t] = b > rk ? b : rk;
+#else
+          rate_key = b > rate_key ? b : rate_key;
+#endif
+        }
+        if (!okr) fail = 1;
+      } else {
+        dtfail = 1;
+      }
+    };
     auto iter = [&](const int k, auto guard) {
       constexpr bool G = decltype(guard)::value;
       const int aa = y0 - 7 + k;   // W* row consumed this iteration
@@ -653,42 +692,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, LF_MINBLOCKS) k_fused_step(Fuse
           v[q] = val;
           a.un[q * a.fstride + o] = val;
         }
-        // positivity (solver.cpp:300-307) and the diagnostics minima
-        // and the CFL rate of U^{n+1} for the next step's dt (solver.cpp:457-469)
-        bool ok = true, okr = true, rate_ok;
-        double eint, rr;
-#if LF_FUSED_EPI_BOX
-        cell_epilogue_box<LF_FUSED_EPI_BOX == 2>(v, C, dxy_box, eint, ok, rr, rate_ok, okr);
-#else
-        cell_epilogue(v, C, eint, ok, rr, rate_ok, okr);
-#endif
-        if (!(v[0] > 0.0) || !(eint > 0.0) || !ok) {
-          fail = 1;
-        } else {
-          const unsigned long long kr = ~pos_bits(v[0]), ke = ~pos_bits(eint);
-#if LF_FUSED_KEYSMEM
-          const unsigned long long nr = sKey[NC + t], ne = sKey[2 * NC + t];
-          sKey[NC + t] = kr > nr ? kr : nr;
-          sKey[2 * NC + t] = ke > ne ? ke : ne;
-#else
-          nmin_r = kr > nmin_r ? kr : nmin_r;
-          nmin_e = ke > nmin_e ? ke : nmin_e;
-#endif
-        }
-        if (rate_ok) {
-          if (rr == rr) {
-            const unsigned long long b = pos_bits(rr);
-#if LF_FUSED_KEYSMEM
-            const unsigned long long rk = sKey[t];
-            sKey[t] = b > rk ? b : rk;
-#else
-            rate_key = b > rate_key ? b : rate_key;
-#endif
-          }
-          if (!okr) fail = 1;
-        } else {
-          dtfail = 1;
-        }
+        epilogue(v);
         // domain-boundary faces for accumulate_boundary_outflow (solver.cpp:406-432);
         // one block-uniform test skips all four in the interior of the domain (the
         // bottom / top rows only occur in guarded iterations)
