@@ -26,6 +26,8 @@
  *                                  solver.hpp:31-37 (batched, on the device)
  *   lf_last_error                  the exception object (what(), PositivityError fields)
  *   lf_write_field_csv             field_csv + write_text_file   csv.cpp:26-83, run.cpp:162-168
+ *   lf_write_field_csv_async /     (new) the same dump, snapshotted in stream order and
+ *   lf_wait_dumps                  copied / formatted / written on a host thread
  *   lf_set_materials               the constructor's `const MaterialSet*` (solver.cpp:61-88)
  *                                  with make_material_set's checks (multimat.cpp:7-15)
  *   lf_upload_partials /           MaterialCells::partial host <-> device
@@ -171,6 +173,19 @@ int lf_download_partials(lf_handle* h, double* const* partials, int64_t ld);
  * text) and writes nothing.  A distributed handle writes its own rows only. */
 int lf_write_field_csv(lf_handle* h, const char* path, uint64_t digest, double time,
                        int threads);
+
+/* lf_write_field_csv without the wait: the columns of the current state are derived
+ * into a device snapshot in stream order (later steps do not change the dump), and a
+ * host thread copies them back (on a stream of its own), checks the fractions and
+ * formats / writes the file while the caller keeps stepping.  Same bytes as
+ * lf_write_field_csv at the same state.  Errors found at this call (null path,
+ * missing material storage) return here; the dump's own (LF_ERR_FRACTION, I/O) are
+ * returned by lf_wait_dumps, which joins every pending dump of the handle (first
+ * error wins).  lf_destroy waits for pending dumps.  The snapshot holds
+ * (5 + materials) x interior doubles of device memory until its copy ends. */
+int lf_write_field_csv_async(lf_handle* h, const char* path, uint64_t digest, double time,
+                             int threads);
+int lf_wait_dumps(lf_handle* h);
 
 /* Region initial state generated on the device (initialize_hydro, run.cpp:29-78,
  * InitKind::regions): regions = nreg x {x_min, x_max, y_min, y_max, rho, u, v, p,

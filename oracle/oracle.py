@@ -164,6 +164,8 @@ def ref_lib():
     lib.lfr_interior_totals.argtypes = [C.c_void_p, DP]
     lib.lfr_edge_flux2.argtypes = [DP, DP, C.c_double, C.c_double, C.c_double, C.c_double, DP, DP,
                                    C.c_char_p, C.c_int]
+    lib.lfr_diagnostics_csv.restype = C.c_int64
+    lib.lfr_diagnostics_csv.argtypes = [C.c_int, DP, C.c_char_p, C.c_int64]
     lib.lfr_field_csv.restype = C.c_int64
     lib.lfr_field_csv.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_char_p, C.c_int64,
                                   C.POINTER(lfo_error)]
@@ -172,6 +174,17 @@ def ref_lib():
 
 def ref_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+def ref_diagnostics_csv(diags) -> bytes:
+    """The reference's diagnostics_csv (csv.cpp:104-114) of StepDiagnostics records."""
+    lib = ref_lib()
+    rec = np.array([[d.step, d.time, d.dt, d.min_rho, d.min_p] for d in diags],
+                   dtype=np.float64).reshape(-1)
+    n = lib.lfr_diagnostics_csv(len(diags), rec.ctypes.data_as(DP), None, 0)
+    buf = C.create_string_buffer(max(n, 1))
+    lib.lfr_diagnostics_csv(len(diags), rec.ctypes.data_as(DP), buf, n)
+    return buf.raw[:n]
 
 
 class OracleSolver:

@@ -209,6 +209,22 @@ int64_t lfr_field_csv(lfr_solver* r, uint64_t digest, double time, char* buf, in
   }
 }
 
+// diagnostics_csv (csv.cpp:104-114) of n records {step, time, dt, min_rho, min_p}
+// (5 doubles each, step as a double): length, min(len, cap) bytes into buf.
+int64_t lfr_diagnostics_csv(int n, const double* rec, char* buf, int64_t cap) {
+  std::vector<StepDiagnostics> diag(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) {
+    diag[size_t(k)].step = std::int64_t(rec[5 * k]);
+    diag[size_t(k)].time = rec[5 * k + 1];
+    diag[size_t(k)].dt = rec[5 * k + 2];
+    diag[size_t(k)].min_rho = rec[5 * k + 3];
+    diag[size_t(k)].min_p = rec[5 * k + 4];
+  }
+  const std::string s = diagnostics_csv(diag);
+  if (buf) std::memcpy(buf, s.data(), size_t(std::min<int64_t>(cap, int64_t(s.size()))));
+  return int64_t(s.size());
+}
+
 void lfr_destroy(lfr_solver* r) {
   if (!r) return;
   delete r->solver;

@@ -19,6 +19,9 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <mutex>
+#include <memory>
+#include <map>
 #include <vector>
 
 #include "fused.h"
@@ -860,8 +863,11 @@ int lf_create_dist(const lf_desc* desc, int device, int rank, int nranks, const 
   return rc;
 }
 
+int lf_wait_dumps(lf_handle* h);
+
 void lf_destroy(lf_handle* h) {
   if (!h) return;
+  lf_wait_dumps(h);   // asynchronous dumps still being written
   for (auto& s : h->slabs) {
     if (s.device >= 0) cudaSetDevice(s.device);
     if (s.stream) cudaStreamSynchronize(s.stream);
@@ -1011,122 +1017,263 @@ inline void put_g17(std::string& out, double v) {
 }
 }  // namespace
 
+// A field_csv dump (csv.cpp:26-83) in two parts.  dump_derive (caller thread) derives
+// the columns on the device into a snapshot buffer, in stream order with the steps;
+// dump_finish copies them back, checks the fractions and formats / writes the file.
+// lf_write_field_csv runs both; lf_write_field_csv_async runs dump_finish on a host
+// thread, so the caller keeps stepping while the dump is copied, formatted and written.
+struct DumpJob {
+  std::string path;
+  uint64_t digest = 0;
+  double time = 0.0;
+  int threads = 0;
+  lf_desc d{};
+  int dim2 = 1, n_mat = 0, ncols = 0, rows = 0, row0 = 0;
+  struct Part {
+    int device = 0, y0 = 0, ny = 0;
+    double* dbuf = nullptr;             // ncols planes of nx * ny
+    unsigned long long* dfail = nullptr;
+    double* dcell = nullptr;            // the flagged cell's partials
+    cudaStream_t copy = nullptr;        // the dump's own stream (async: off the step stream)
+    cudaEvent_t ready = nullptr;        // the derive kernels done
+  };
+  std::vector<Part> parts;
+  int rc = 0;
+  int err_kind = 0;
+  std::string err;
+};
+
+static void dump_release(DumpJob& job);
+
+static std::unique_ptr<DumpJob> dump_derive(lf_handle* h, const char* path, uint64_t digest,
+                                            double time, int threads) {
+  auto job = std::make_unique<DumpJob>();
+  job->path = path;
+  job->digest = digest;
+  job->time = time;
+  job->threads = threads;
+  job->d = h->d;
+  job->dim2 = h->dim2;
+  job->n_mat = h->mc.n;
+  job->ncols = 5 + h->mc.n;
+  // this process's rows (a distributed handle writes its slab rows only)
+  job->row0 = h->slabs.front().sl.y0;
+  job->rows = h->slabs.back().sl.y0 + h->slabs.back().L.ny - job->row0;
+  try {
+  for (auto& s : h->slabs) {
+    CK(cudaSetDevice(s.device));
+    DumpJob::Part pt;
+    pt.device = s.device;
+    pt.y0 = s.sl.y0;
+    pt.ny = s.L.ny;
+    const size_t plane = (size_t)h->d.nx * s.L.ny;
+    // stream-ordered allocations (freed on the copy stream): neither side of the dump
+    // synchronises the device, so the steps queued behind it keep running
+    CK(cudaStreamCreateWithFlags(&pt.copy, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&pt.ready, cudaEventDisableTiming));
+    job->parts.push_back(pt);
+    DumpJob::Part& q = job->parts.back();
+    CK(cudaMallocAsync(&q.dbuf, job->ncols * plane * sizeof(double), s.stream));
+    CK(cudaMallocAsync(&q.dfail, sizeof(unsigned long long), s.stream));
+    CK(cudaMallocAsync(&q.dcell, MAX_MATERIALS * sizeof(double), s.stream));
+    CK(cudaMemsetAsync(q.dfail, 0xff, sizeof(unsigned long long), s.stream));
+    launch_csv_derive(s.field(s.U), s.field(job->n_mat ? s.P : s.U), s.L, s.sl, h->d.gamma, h->mc,
+                      q.dbuf, q.dfail, s.stream);
+    if (job->n_mat) launch_csv_failcell(s.field(s.P), job->n_mat, s.L, s.sl, q.dfail, q.dcell, s.stream);
+    CK(cudaEventRecord(q.ready, s.stream));
+    CK(cudaStreamWaitEvent(q.copy, q.ready, 0));
+  }
+  } catch (...) {
+    dump_release(*job);
+    throw;
+  }
+  return job;
+}
+
+// (safe on a partly built job: CK may have thrown in dump_derive)
+static void dump_release(DumpJob& job) {
+  for (auto& pt : job.parts) {
+    cudaSetDevice(pt.device);
+    if (pt.copy) {
+      if (pt.dbuf) cudaFreeAsync(pt.dbuf, pt.copy);
+      if (pt.dfail) cudaFreeAsync(pt.dfail, pt.copy);
+      if (pt.dcell) cudaFreeAsync(pt.dcell, pt.copy);
+      cudaStreamSynchronize(pt.copy);
+      cudaStreamDestroy(pt.copy);
+    }
+    if (pt.ready) cudaEventDestroy(pt.ready);
+    pt = DumpJob::Part{};
+  }
+  job.parts.clear();
+}
+
+// (no CUDA error can throw out of here: a host thread may run it)
+static void dump_finish(DumpJob& job) {
+  const int nx = job.d.nx, rows = job.rows, row0 = job.row0, ncols = job.ncols;
+  const int n_mat = job.n_mat;
+  auto fail_job = [&](int kind, const std::string& msg) {
+    job.rc = kind;
+    job.err_kind = kind;
+    job.err = msg;
+  };
+  std::vector<double> cols((size_t)ncols * nx * rows);
+  unsigned long long fail_host = ~0ull;
+  double cell[MAX_MATERIALS] = {0.0};
+  for (auto& pt : job.parts) {
+    const size_t plane = (size_t)nx * pt.ny;
+    unsigned long long f = ~0ull;
+    double pc[MAX_MATERIALS] = {0.0};
+    bool ok = cudaSetDevice(pt.device) == cudaSuccess;   // (the copy stream waits on ready)
+    for (int c = 0; ok && c < ncols; ++c)
+      ok = cudaMemcpyAsync(&cols[((size_t)c * rows + (pt.y0 - row0)) * nx], pt.dbuf + c * plane,
+                           plane * sizeof(double), cudaMemcpyDeviceToHost, pt.copy) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(&f, pt.dfail, sizeof f, cudaMemcpyDeviceToHost, pt.copy) == cudaSuccess;
+    if (n_mat)
+      ok = ok && cudaMemcpyAsync(pc, pt.dcell, n_mat * sizeof(double), cudaMemcpyDeviceToHost,
+                                 pt.copy) == cudaSuccess;
+    ok = ok && cudaStreamSynchronize(pt.copy) == cudaSuccess;
+    if (!ok) {
+      dump_release(job);
+      return fail_job(LF_ERR_DEVICE, std::string("field dump: ") + cudaGetErrorString(cudaGetLastError()));
+    }
+    if (f < fail_host) {
+      fail_host = f;
+      std::memcpy(cell, pc, sizeof cell);
+    }
+  }
+  dump_release(job);
+  if (fail_host != ~0ull) {
+    // clamped_fraction's message for the first failing (cell, material), csv.cpp:49
+    const int i = (int)(fail_host % (unsigned long long)nx);
+    const int jl = (int)(fail_host / (unsigned long long)nx) - row0;
+    const double rho = cols[(size_t)jl * nx + i];
+    double y = 0.0;
+    for (int k = 0; k < n_mat; ++k) {
+      y = cell[k] / rho;
+      if (!(y >= 0.0 && y <= 1.0) && (y < -1e-11 || y > 1.0 + 1e-11)) break;
+    }
+    return fail_job(LF_ERR_FRACTION, "mass fraction out of [0,1] beyond round-off = " + fmt_f(y));
+  }
+  // header and column names (csv.cpp:15-23, 33-36)
+  std::string head;
+  char hb[64];
+  std::snprintf(hb, sizeof hb, "# config %016llx time ", (unsigned long long)job.digest);
+  head += hb;
+  put_g17(head, job.time);
+  head += '\n';
+  head += job.dim2 ? "x,y,rho,u,v,p,e_internal" : "x,rho,u,p,e_internal";
+  for (int k = 1; k <= n_mat; ++k) head += ",y" + std::to_string(k);
+  head += '\n';
+  // rows formatted in parallel (row order kept), then written in order
+  int nt = job.threads > 0 ? job.threads : (int)std::thread::hardware_concurrency();
+  nt = std::max(1, std::min(nt, rows));
+  std::vector<std::string> parts((size_t)nt);
+  const size_t plane = (size_t)nx * rows;
+  const lf_desc& d = job.d;
+  const bool dim2 = job.dim2 != 0;
+  auto work = [&](int t) {
+    const int j0 = (int)((int64_t)rows * t / nt), j1 = (int)((int64_t)rows * (t + 1) / nt);
+    std::string& out = parts[(size_t)t];
+    out.reserve((size_t)(j1 - j0) * nx * (size_t)(ncols + 2) * 24);
+    for (int jl = j0; jl < j1; ++jl) {
+      const double y = d.y0 + ((jl + row0) + 0.5) * d.dy;  // CartesianGrid::yc
+      for (int i = 0; i < nx; ++i) {
+        const size_t c = (size_t)jl * nx + i;
+        put_g17(out, d.x0 + (i + 0.5) * d.dx);               // CartesianGrid::xc
+        if (dim2) {
+          out += ',';
+          put_g17(out, y);
+        }
+        out += ',';
+        put_g17(out, cols[c]);
+        out += ',';
+        put_g17(out, cols[plane + c]);
+        if (dim2) {
+          out += ',';
+          put_g17(out, cols[2 * plane + c]);
+        }
+        out += ',';
+        put_g17(out, cols[3 * plane + c]);
+        out += ',';
+        put_g17(out, cols[4 * plane + c]);
+        for (int k = 0; k < n_mat; ++k) {
+          out += ',';
+          put_g17(out, cols[(5 + k) * plane + c]);
+        }
+        out += '\n';
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  FILE* fp = std::fopen(job.path.c_str(), "wb");
+  if (!fp) return fail_job(LF_ERR_ARGUMENT, "cannot open " + job.path + " for writing");
+  bool ok = std::fwrite(head.data(), 1, head.size(), fp) == head.size();
+  for (auto& p : parts) ok = ok && std::fwrite(p.data(), 1, p.size(), fp) == p.size();
+  ok = (std::fclose(fp) == 0) && ok;
+  if (!ok) return fail_job(LF_ERR_ARGUMENT, "short write to " + job.path);
+}
+
+static int dump_check(lf_handle* h, const char* path) {
+  if (!path) return set_err(h, LF_ERR_ARGUMENT, "path is null");
+  if (h->mc.n && !h->partials_ready)
+    return set_err(h, LF_ERR_CONFIG, "multimaterial dump needs material storage");
+  return 0;
+}
+
 int lf_write_field_csv(lf_handle* h, const char* path, uint64_t digest, double time,
                        int threads) {
   LF_TRACE("lf_write_field_csv");
   return guarded(h, [&] {
-    if (!path) return set_err(h, LF_ERR_ARGUMENT, "path is null");
-    if (h->mc.n && !h->partials_ready)
-      return set_err(h, LF_ERR_CONFIG, "multimaterial dump needs material storage");
-    const int nx = h->d.nx, nyg = h->d.ny, n_mat = h->mc.n;
-    const int ncols = 5 + n_mat;
-    // this process's rows (a distributed handle writes its slab rows only)
-    const int row0 = h->slabs.front().sl.y0;
-    const int rows = h->slabs.back().sl.y0 + h->slabs.back().L.ny - row0;
-    std::vector<double> cols((size_t)ncols * nx * rows);
-    unsigned long long fail_host = ~0ull;
-    for (auto& s : h->slabs) {
-      CK(cudaSetDevice(s.device));
-      const size_t plane = (size_t)nx * s.L.ny;
-      double* dbuf = nullptr;
-      unsigned long long* dfail = nullptr;
-      CK(cudaMalloc(&dbuf, ncols * plane * sizeof(double)));
-      CK(cudaMalloc(&dfail, sizeof(unsigned long long)));
-      CK(cudaMemsetAsync(dfail, 0xff, sizeof(unsigned long long), s.stream));
-      launch_csv_derive(s.field(s.U), s.field(n_mat ? s.P : s.U), s.L, s.sl, h->d.gamma, h->mc,
-                        dbuf, dfail, s.stream);
-      unsigned long long f;
-      for (int c = 0; c < ncols; ++c)
-        CK(cudaMemcpyAsync(&cols[((size_t)c * rows + (s.sl.y0 - row0)) * nx], dbuf + c * plane,
-                           plane * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
-      CK(cudaMemcpyAsync(&f, dfail, sizeof f, cudaMemcpyDeviceToHost, s.stream));
-      CK(cudaStreamSynchronize(s.stream));
-      fail_host = std::min(fail_host, f);
-      cudaFree(dbuf);
-      cudaFree(dfail);
-    }
-    if (fail_host != ~0ull) {
-      // clamped_fraction's message for the first failing (cell, material), csv.cpp:49
-      const int i = (int)(fail_host % (unsigned long long)nx);
-      const int jl = (int)(fail_host / (unsigned long long)nx) - row0;
-      const double rho = cols[(size_t)jl * nx + i];
-      double y = 0.0;
-      for (int k = 0; k < n_mat; ++k) {
-        double pk = 0.0;
-        for (auto& s : h->slabs) {
-          const int jj = jl + row0 - s.sl.y0;
-          if (jj < 0 || jj >= s.L.ny) continue;
-          CK(cudaSetDevice(s.device));
-          CK(cudaMemcpy(&pk, s.P + s.L.origin() + k * s.L.fstride + (int64_t)jj * s.L.pitch + i,
-                        sizeof(double), cudaMemcpyDeviceToHost));
-        }
-        y = pk / rho;
-        if (!(y >= 0.0 && y <= 1.0) && (y < -1e-11 || y > 1.0 + 1e-11)) break;
-      }
-      return set_err(h, LF_ERR_FRACTION, "mass fraction out of [0,1] beyond round-off = %s",
-                     fmt_f(y).c_str());
-    }
-    // header and column names (csv.cpp:15-23, 33-36)
-    std::string head;
-    char hb[64];
-    std::snprintf(hb, sizeof hb, "# config %016llx time ", (unsigned long long)digest);
-    head += hb;
-    put_g17(head, time);
-    head += '\n';
-    head += h->dim2 ? "x,y,rho,u,v,p,e_internal" : "x,rho,u,p,e_internal";
-    for (int k = 1; k <= n_mat; ++k) head += ",y" + std::to_string(k);
-    head += '\n';
-    // rows formatted in parallel (row order kept), then written in order
-    int nt = threads > 0 ? threads : (int)std::thread::hardware_concurrency();
-    nt = std::max(1, std::min(nt, rows));
-    std::vector<std::string> parts((size_t)nt);
-    const size_t plane = (size_t)nx * rows;
-    auto work = [&](int t) {
-      const int j0 = (int)((int64_t)rows * t / nt), j1 = (int)((int64_t)rows * (t + 1) / nt);
-      std::string& out = parts[(size_t)t];
-      out.reserve((size_t)(j1 - j0) * nx * (size_t)(ncols + 2) * 24);
-      for (int jl = j0; jl < j1; ++jl) {
-        const double y = h->d.y0 + ((jl + row0) + 0.5) * h->d.dy;  // CartesianGrid::yc
-        for (int i = 0; i < nx; ++i) {
-          const size_t c = (size_t)jl * nx + i;
-          put_g17(out, h->d.x0 + (i + 0.5) * h->d.dx);               // CartesianGrid::xc
-          if (h->dim2) {
-            out += ',';
-            put_g17(out, y);
-          }
-          out += ',';
-          put_g17(out, cols[c]);
-          out += ',';
-          put_g17(out, cols[plane + c]);
-          if (h->dim2) {
-            out += ',';
-            put_g17(out, cols[2 * plane + c]);
-          }
-          out += ',';
-          put_g17(out, cols[3 * plane + c]);
-          out += ',';
-          put_g17(out, cols[4 * plane + c]);
-          for (int k = 0; k < n_mat; ++k) {
-            out += ',';
-            put_g17(out, cols[(5 + k) * plane + c]);
-          }
-          out += '\n';
-        }
-      }
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
-    work(0);
-    for (auto& th : pool) th.join();
-    FILE* fp = std::fopen(path, "wb");
-    if (!fp) return set_err(h, LF_ERR_ARGUMENT, "cannot open %s for writing", path);
-    bool ok = std::fwrite(head.data(), 1, head.size(), fp) == head.size();
-    for (auto& p : parts) ok = ok && std::fwrite(p.data(), 1, p.size(), fp) == p.size();
-    ok = (std::fclose(fp) == 0) && ok;
-    if (!ok) return set_err(h, LF_ERR_ARGUMENT, "short write to %s", path);
-    (void)nyg;
+    if (int rc = dump_check(h, path)) return rc;
+    auto job = dump_derive(h, path, digest, time, threads);
+    dump_finish(*job);
+    return job->rc ? set_err(h, job->err_kind, "%s", job->err.c_str()) : 0;
+  });
+}
+
+// Pending asynchronous dumps of a handle (joined by lf_wait_dumps / lf_destroy).
+struct AsyncDump {
+  std::unique_ptr<DumpJob> job;
+  std::thread worker;
+};
+static std::mutex g_dumps_m;
+static std::map<lf_handle*, std::vector<std::unique_ptr<AsyncDump>>> g_dumps;
+
+int lf_write_field_csv_async(lf_handle* h, const char* path, uint64_t digest, double time,
+                             int threads) {
+  LF_TRACE("lf_write_field_csv_async");
+  return guarded(h, [&] {
+    if (int rc = dump_check(h, path)) return rc;
+    auto ad = std::make_unique<AsyncDump>();
+    ad->job = dump_derive(h, path, digest, time, threads);
+    DumpJob* job = ad->job.get();
+    ad->worker = std::thread([job] { dump_finish(*job); });
+    std::lock_guard<std::mutex> lk(g_dumps_m);
+    g_dumps[h].push_back(std::move(ad));
     return 0;
   });
+}
+
+int lf_wait_dumps(lf_handle* h) {
+  LF_TRACE("lf_wait_dumps");
+  if (!h) return LF_ERR_ARGUMENT;
+  std::vector<std::unique_ptr<AsyncDump>> mine;
+  {
+    std::lock_guard<std::mutex> lk(g_dumps_m);
+    auto it = g_dumps.find(h);
+    if (it == g_dumps.end()) return 0;
+    mine = std::move(it->second);
+    g_dumps.erase(it);
+  }
+  int rc = 0;
+  for (auto& ad : mine) {
+    ad->worker.join();
+    if (ad->job->rc && !rc) rc = set_err(h, ad->job->err_kind, "%s", ad->job->err.c_str());
+  }
+  return rc;
 }
 
 int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghosts) {

@@ -150,5 +150,8 @@ void launch_interior_sums(const double* u, int64_t fstride, int pitch, int nx, i
 void launch_csv_derive(const Field& u, const Field& part, const Layout& L, const Slab& sl,
                        double gamma0, const MatConsts& mc, double* out, unsigned long long* fail,
                        cudaStream_t st);
+// the n partial densities of the cell launch_csv_derive flagged (nothing if none)
+void launch_csv_failcell(const Field& part, int n, const Layout& L, const Slab& sl,
+                         const unsigned long long* fail, double* out, cudaStream_t st);
 
 }  // namespace lfb

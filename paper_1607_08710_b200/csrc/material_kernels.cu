@@ -508,6 +508,24 @@ void launch_csv_derive(const Field& u, const Field& part, const Layout& L, const
   count_launch(), k_csv_derive<<<grd, blk, 0, st>>>(u, part, L.nx, L.ny, sl.y0, gamma0, mc, out, fail);
 }
 
+namespace {
+// the partial densities of the cell k_csv_derive flagged (its failure message needs
+// them), read in stream order so an asynchronous dump keeps the dump-time values
+__global__ void k_csv_failcell(Field part, int n, int nx, int ny, int y0,
+                               const unsigned long long* fail, double* out) {
+  const unsigned long long f = *fail;
+  if (f == ~0ull) return;
+  const int i = (int)(f % (unsigned long long)nx), jl = (int)(f / (unsigned long long)nx) - y0;
+  if (jl < 0 || jl >= ny) return;
+  for (int k = 0; k < n; ++k) out[k] = part.p[k * part.fstride + (int64_t)jl * part.pitch + i];
+}
+}  // namespace
+
+void launch_csv_failcell(const Field& part, int n, const Layout& L, const Slab& sl,
+                         const unsigned long long* fail, double* out, cudaStream_t st) {
+  count_launch(), k_csv_failcell<<<1, 1, 0, st>>>(part, n, L.nx, L.ny, sl.y0, fail, out);
+}
+
 }  // namespace lfb
 
 // ---------------------------------------------------------------- region ICs

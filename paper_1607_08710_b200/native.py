@@ -56,6 +56,8 @@ SIGNATURES = [
     ("lf_download", C.c_int, [H, P4, C.c_int64, C.c_int]),
     ("lf_set_materials", C.c_int, [H, C.c_int, C.POINTER(C.c_double)]),
     ("lf_write_field_csv", C.c_int, [H, C.c_char_p, C.c_uint64, C.c_double, C.c_int]),
+    ("lf_write_field_csv_async", C.c_int, [H, C.c_char_p, C.c_uint64, C.c_double, C.c_int]),
+    ("lf_wait_dumps", C.c_int, [H]),
     ("lf_init_regions", C.c_int, [H, C.POINTER(C.c_double), C.c_int]),
     ("lf_upload_partials", C.c_int, [H, C.c_void_p, C.c_int64]),
     ("lf_download_partials", C.c_int, [H, C.c_void_p, C.c_int64]),

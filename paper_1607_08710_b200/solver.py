@@ -233,6 +233,18 @@ class LagfluxSolver:
         material fractions) to `path`, formatted on `threads` host threads."""
         self._check(self._lib.lf_write_field_csv(self._h, path.encode(), digest, time, threads))
 
+    def write_field_csv_async(self, path: str, digest: int, time: float, threads: int = 0):
+        """write_field_csv of the current resident state without waiting: the columns
+        are snapshotted on the device in stream order and a host thread copies,
+        formats and writes them while stepping continues.  The dump's own errors
+        (fraction, I/O) come from wait_dumps()."""
+        self._check(self._lib.lf_write_field_csv_async(self._h, path.encode(), digest, time,
+                                                       threads))
+
+    def wait_dumps(self):
+        """Join every pending write_field_csv_async of this solver (first error raised)."""
+        self._check(self._lib.lf_wait_dumps(self._h))
+
     def init_regions(self, state: G.SolverState, regions, mat=None):
         """Device-side initialize_hydro for region cases (cases.Region list); with a
         material set, `mat` becomes the resident MaterialCells (download with

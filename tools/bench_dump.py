@@ -35,8 +35,32 @@ t0 = time.perf_counter()
 s.write_field_csv(p, 1, state.time)
 ours = time.perf_counter() - t0
 size = os.path.getsize(p)
+# the asynchronous dump: how long the caller is held, and 20 further steps run with
+# the dump in flight against the same 20 steps after a synchronous dump
+tc = G.TimeControls(c.cfl, c.t_final)
+
+
+def steps(n):
+    for _ in range(n):
+        s.heun_step(state, tc, c.t_final, mat)
+    s.sync_to_host(state, mat=mat)
+
+
+steps(2)
+t0 = time.perf_counter()
+s.write_field_csv(os.path.join(d, "seq.csv"), 1, state.time)
+steps(20)
+seq = time.perf_counter() - t0
+pa = os.path.join(d, "async.csv")
+t0 = time.perf_counter()
+s.write_field_csv_async(pa, 1, state.time)
+held = time.perf_counter() - t0
+steps(20)
+s.wait_dumps()
+ovl = time.perf_counter() - t0
 res = {"workload": f"triple_point {nx}x{ny}, 3 materials, after 20 steps",
-       "bytes": size, "ours_s": ours, "threads": os.cpu_count()}
+       "bytes": size, "ours_s": ours, "threads": os.cpu_count(),
+       "async_call_s": held, "dump_then_20_steps_s": seq, "async_dump_with_20_steps_s": ovl}
 if O.ref_available():
     r = O.RefSolver(c.grid, c.bc, c.gamma, c.params, materials=ms)
     r.set_state(state.field)
