@@ -657,7 +657,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=16384, help="cells per side per GPU")
-    ap.add_argument("--path", choices=["auto", "twopass", "fused", "staged"], default="auto")
+    ap.add_argument("--path", choices=["auto", "twopass", "fused", "staged", "small"], default="auto")
     ap.add_argument("--math", choices=["exact", "contract"], default="exact",
                     help="exact: bit-identical to the reference; contract: FMA contraction and "
                          "reciprocal products in the two-pass kernels (north-star tolerance)")

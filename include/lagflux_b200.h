@@ -63,17 +63,22 @@ enum {
 };
 
 /* Heun-step implementation for lf_heun_step / lf_advance (all give identical results):
- *   AUTO     FUSED for slabs of 2^23 cells or more (2^22 in LF_MATH_CONTRACT; Heun, no
- *            materials: BASELINE configs 3-5), TWOPASS below that, for time_order 1 and for
- *            materials; FUSED also when the two-pass scratch does not fit in device
- *            memory.  lf_resolved_path reports the choice.
+ *   AUTO     SMALL for one-material grids of up to 2^14 cells (2D) / 2^17 cells (1D) on
+ *            one device (BASELINE config 1, 1D runs); FUSED for slabs of 2^23 cells or more
+ *            (2^22 in LF_MATH_CONTRACT; Heun, no materials: BASELINE configs 3-5), TWOPASS
+ *            in between, for time_order 1 and for materials; FUSED also when the two-pass
+ *            scratch does not fit in device memory.  lf_resolved_path reports the choice.
  *   FUSED    one kernel per step (U^n read once, U^{n+1} written once)
  *   STAGED   the reference's phase structure, one kernel per loop (also the
- *            exact diagnosis path for every failure, 1D grids, euler_stage and
- *            more than 4 materials)
+ *            exact diagnosis path for every failure, euler_stage and more than 4
+ *            materials)
  *   TWOPASS  predictor and corrector as two warp-independent streaming kernels
- *            (1-4 materials included) */
-enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2, LF_PATH_TWOPASS = 3 };
+ *            (1-4 materials included)
+ *   SMALL    a whole lf_advance batch (up to 4096 steps) in one launch of one thread-block
+ *            cluster (up to 16 blocks): one material, one slab, nx >= 2 (and ny >= 2 in
+ *            2D), up to 2^22 cells; the stage-wise arithmetic's bits */
+enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2, LF_PATH_TWOPASS = 3,
+       LF_PATH_SMALL = 4 };
 /* Arithmetic of the fast kernels (two-pass and fused).  LF_MATH_EXACT (default): the
  * reference's operation order without contraction, bit-identical to it.
  * LF_MATH_CONTRACT: FMA contraction and quotients as products by a refined
@@ -234,7 +239,8 @@ int lf_last_error(lf_handle* h, lf_error* err);
 int lf_set_stream(lf_handle* h, void* cuda_stream);   /* NULL: the handle's own stream */
 int lf_set_path(lf_handle* h, int path);               /* LF_PATH_* */
 int lf_set_math(lf_handle* h, int math);               /* LF_MATH_* (default EXACT) */
-/* The path the next step takes: LF_PATH_TWOPASS, LF_PATH_FUSED or LF_PATH_STAGED.
+/* The path the next step takes: LF_PATH_TWOPASS, LF_PATH_FUSED, LF_PATH_STAGED or
+ * LF_PATH_SMALL.
  * LF_PATH_AUTO runs the two-pass kernels when their scratch (four more states'
  * worth) fits in device memory, else the one-kernel step (e.g. 32768^2 on one GPU). */
 int lf_resolved_path(lf_handle* h, int* path);

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "fused.h"
+#include "small.h"
 #include "handle.h"
 #include "host_util.h"
 #include "nccl_comm.h"
@@ -680,6 +681,11 @@ int staged_heun(lf_handle* h, double cfl, double time, double limit, int64_t ste
   return 0;
 }
 
+// LF_PATH_SMALL (small_step.cu): asked for, or LF_PATH_AUTO on a small grid
+bool use_small(lf_handle* h) {
+  return (h->path == LF_PATH_SMALL && small_supported(h)) || prefer_small(h);
+}
+
 bool use_fused(lf_handle* h) {
   if (h->path == LF_PATH_STAGED) return false;
   // the fast kernels' limiter (sweby_fast, fastmath.cuh) is the reference's for
@@ -874,6 +880,7 @@ void lf_destroy(lf_handle* h) {
   }
   nccl_destroy(h);
   fused_release(h);
+  small_release(h);
   for (auto& s : h->slabs) free_slab(s);
   delete h;
 }
@@ -901,7 +908,8 @@ int lf_upload(lf_handle* h, double* const field[4], int64_t ld) {
       }
     }
     sync_all(h);
-    h->tp_exact = 0;  // a new state: the plain fast kernels first
+    h->tp_exact = 0;
+    h->small_ieee = 0;  // a new state: the plain fast kernels first
     h->rate_valid = false;
     fused_invalidate(h);
     return 0;
@@ -978,6 +986,7 @@ int lf_upload_partials(lf_handle* h, double* const* partials, int64_t ld) {
     // the cached CFL rate and fraction check came from the old partials (mixed-cell
     // gamma): a new material state, as in lf_upload
     h->tp_exact = 0;
+    h->small_ieee = 0;
     h->rate_valid = false;
     fused_invalidate(h);
     return 0;
@@ -1368,7 +1377,8 @@ int lf_init_fourier(lf_handle* h, uint64_t seed) {
       cudaFree(damp[k]);
     }
     CK(cudaGetLastError());
-    h->tp_exact = 0;  // a new state: the plain fast kernels first
+    h->tp_exact = 0;
+    h->small_ieee = 0;  // a new state: the plain fast kernels first
     h->rate_valid = false;
     fused_invalidate(h);
     return 0;
@@ -1427,7 +1437,8 @@ int lf_init_regions(lf_handle* h, const double* regions, int nreg) {
                      fmt_f(x).c_str(), fmt_f(y).c_str(), hits);
     }
     if (h->mc.n) h->partials_ready = 1;
-    h->tp_exact = 0;  // a new state: the plain fast kernels first
+    h->tp_exact = 0;
+    h->small_ieee = 0;  // a new state: the plain fast kernels first
     h->rate_valid = false;
     fused_invalidate(h);
     return 0;
@@ -1561,6 +1572,7 @@ int lf_heun_step(lf_handle* h, double cfl, double time, double limit_time, int64
                  double* boundary_outflow, lf_step_out* out) {
   LF_TRACE("lf_heun_step");
   return guarded(h, [&] {
+    if (use_small(h)) return small_heun(h, cfl, time, limit_time, step, boundary_outflow, out);
     if (use_fused(h))
       return fused_heun(h, cfl, time, limit_time, step, boundary_outflow, out);
     return staged_heun(h, cfl, time, limit_time, step, boundary_outflow, out);
@@ -1571,6 +1583,8 @@ int lf_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* tim
                int64_t* step, double* outflow, lf_step_out* per_step, int* taken) {
   LF_TRACE("lf_advance");
   return guarded(h, [&] {
+    if (use_small(h))
+      return small_advance(h, nsteps, cfl, t_final, time, step, outflow, per_step, taken);
     if (use_fused(h))
       return fused_advance(h, nsteps, cfl, t_final, time, step, outflow, per_step, taken);
     // stage-wise fallback keeps the run.cpp loop on the host
@@ -1605,7 +1619,7 @@ int lf_set_stream(lf_handle* h, void* stream) {
 }
 
 int lf_set_path(lf_handle* h, int path) {
-  if (!h || path < LF_PATH_AUTO || path > LF_PATH_TWOPASS) return LF_ERR_ARGUMENT;
+  if (!h || path < LF_PATH_AUTO || path > LF_PATH_SMALL) return LF_ERR_ARGUMENT;
   h->path = path;
   return 0;
 }
@@ -1613,7 +1627,10 @@ int lf_set_path(lf_handle* h, int path) {
 int lf_resolved_path(lf_handle* h, int* path) {
   if (!h || !path) return LF_ERR_ARGUMENT;
   return guarded(h, [&] {
-    *path = !use_fused(h) ? LF_PATH_STAGED : twopass_selected(h) ? LF_PATH_TWOPASS : LF_PATH_FUSED;
+    *path = use_small(h)   ? LF_PATH_SMALL
+            : !use_fused(h) ? LF_PATH_STAGED
+            : twopass_selected(h) ? LF_PATH_TWOPASS
+                                  : LF_PATH_FUSED;
     return 0;
   });
 }
@@ -1628,6 +1645,7 @@ int lf_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, doubl
                   int* kernel_launches) {
   LF_TRACE("lf_time_steps");
   return guarded(h, [&] {
+    if (use_small(h)) return small_time_steps(h, nsteps, cfl, kernel_ms, step_ms, kernel_launches);
     if (!use_fused(h))
       return set_err(h, LF_ERR_ARGUMENT, "lf_time_steps times the fused / two-pass path");
     return fused_time_steps(h, nsteps, cfl, kernel_ms, step_ms, kernel_launches);

@@ -26,6 +26,7 @@
 #include "fused_common.cuh"
 #include "twopass.h"
 #include "nccl_comm.h"
+#include "small.h"
 #include "trace.h"
 
 namespace lfb {
@@ -280,6 +281,7 @@ int64_t fused_bytes(lf_handle* h) {
 
 void fused_invalidate(lf_handle* h) {
   if (FusedState* f = fstate(h)) f->valid = false;
+  small_invalidate(h);   // every path's cached control record
 }
 
 // The control record of the current state: its CFL rate (the compute_dt of

@@ -68,6 +68,7 @@ struct lf_handle {
   lfb::Nccl* nccl = nullptr;
   bool rate_valid = false;           // scal[0].rate_bits holds the rate of the current U
   void* fused = nullptr;             // lfb::FusedState (fused_step.cu)
+  void* small = nullptr;             // lfb::SmallState (small_step.cu)
   lf_error err{};
   // multimaterial: material table and whether partial densities were uploaded
   lfb::MatConsts mc{};
@@ -75,6 +76,9 @@ struct lf_handle {
   // the two-pass path has met shock-precursor velocities: use its exact kernels
   // until a new state is uploaded (set by a step with status 3)
   int tp_exact = 0;
+  // LF_PATH_SMALL met a cell outside the fast arithmetic's box: its IEEE kernels until
+  // a new state is uploaded
+  int small_ieee = 0;
   // LF_PATH_AUTO: -1 undecided, 1 the two-pass scratch fits in device memory, 0 it
   // does not (then the one-kernel step, which needs two states, runs instead)
   int tp_mem_ok = -1;

@@ -1,0 +1,822 @@
+// small_step.cu -- LF_PATH_SMALL: the whole step loop of a small grid in one
+// persistent thread-block cluster (1D grids and small 2D grids, one material).
+//
+// A grid of a few thousand cells cannot fill a B200: the stage-wise step is a
+// dozen launches and three host round trips (~110 us), the two-pass step five
+// launches (~34 us in a CUDA graph, BASELINE config 1), against 80-190 us of CPU
+// work per step.  Here one cluster of up to 16 blocks (one per SM, SMALL_THREADS
+// threads each) runs a batch of up to thousands of heun_step calls in one launch.
+// Each thread owns cells; a cell's stage is one straight computation: the
+// primitives of its cross stencil (ghosts read through an index map of the
+// reference's fill, so no fill phase), its four faces and its update (a face is
+// solved by both of its cells, the same bits twice; the lower one stores it for
+// the Heun average and the outflow).  A step is three cluster barriers; the
+// blocks' partial reductions go to the lead block by plain shared::cluster stores
+// (no remote atomics), which also keeps dt / time / the step records and runs the
+// ordered boundary-outflow sums; the state ping-pongs between U and U2, and data
+// another block wrote is read through L2 (ld.global.cg after the barrier's
+// release / acquire).
+//
+// Arithmetic: the fast kernels' exact arithmetic (face_fast.cuh: shared
+// reciprocals, sweby_fast, the cell box) where its proofs hold (beta >= 1, gamma - 1
+// in the constant box), else the stage-wise kernels' IEEE expressions
+// (lagflux_device.cuh) -- the reference's bits either way.  A failed check or a
+// cell outside the box ends the batch at that step with its input state intact;
+// the host re-runs it with the stage-wise kernels, which report the reference's
+// exact error (a box failure whose re-run succeeds switches the handle to the IEEE
+// arithmetic until the next upload).
+//
+// Reference: solver.cpp:489-546 (heun_step), 482-487 (time_order 1 stage),
+// 131-329 (the phases), 406-432 (outflow), 434-480 (dt); grid.cpp:72-114 (fill).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "face_fast.cuh"
+#include "fused_common.cuh"
+#include "handle.h"
+#include "reduce.cuh"
+#include "small.h"
+#include "trace.h"
+
+namespace lfb {
+
+namespace {
+
+#ifndef LF_SMALL_THREADS
+#define LF_SMALL_THREADS 256
+#endif
+constexpr int SMALL_THREADS = LF_SMALL_THREADS;
+
+struct SmallArgs {
+  double* u;    // U^n (Field origin pointers; ping-pong with u2)
+  double* u2;
+  double* us;   // U* (Heun predictor)
+  int64_t pitch, fstride;
+  double* fx[2];   // face fluxes of the two stages (FluxArr layout: [c][b][a])
+  double* fy[2];
+  int64_t fx_stride, fy_stride;
+  int nx, ny;
+  int heun;
+  int bc[4];
+  Consts k;
+  double cfl, limit, t_final;
+  StepCtl* ctl;      // in: the state's control record; out: the last state's
+  StepRec* rec;      // [nsteps]
+  double* outflow;   // [4], accumulated in place
+  int nsteps;
+};
+
+constexpr int SMALL_MAX_CTAS = 16;
+constexpr int OUT_TILE = 256;
+
+// Per block: its own partial reductions; in the lead block (rank 0) also the
+// control record and every block's partials (written there by plain
+// shared::cluster stores -- no remote atomics), and the outflow staging tile.
+struct SmallShared {
+  StepCtl ctl;
+  unsigned long long rate, min_r, min_e;   // this block's
+  int fail, dtfail;
+  unsigned long long p_rate[SMALL_MAX_CTAS], p_min_r[SMALL_MAX_CTAS], p_min_e[SMALL_MAX_CTAS];
+  int p_fail[SMALL_MAX_CTAS], p_dtfail[SMALL_MAX_CTAS];
+  double dif[OUT_TILE][9];   // [element][chain]; 9: conflict-free rows
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// the same shared-memory variable in block `rank` of the cluster
+__device__ __forceinline__ uint32_t remote(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_remote(uint32_t a, unsigned long long v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_remote(uint32_t a, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_remote_i(uint32_t a) {
+  int v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_remote_u64(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+
+template <class Op>
+__device__ __forceinline__ unsigned long long wred(unsigned long long v, Op op) {
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// The ghost fill (grid.cpp:72-114) as an index map: ghost layer l <= 2 of a side
+// reads interior cell src (n >= 2: every source of the first two layers is
+// interior), a reflective image times -1 in the normal momentum; a corner is the y
+// image of the x image (k_fill_xy's composition; a multiplication by +-1 is exact,
+// so the order does not matter).
+__device__ __forceinline__ int img(int i, int n, int lo, int hi, bool& flip) {
+  flip = false;
+  if (i < 0) {
+    const int l = -i;
+    if (lo == 0) return 0;
+    if (lo == 1) {
+      flip = true;
+      return l - 1;
+    }
+    return n - l;
+  }
+  if (i >= n) {
+    const int l = i - n + 1;
+    if (hi == 0) return n - 1;
+    if (hi == 1) {
+      flip = true;
+      return n - l;
+    }
+    return l - 1;
+  }
+  return i;
+}
+
+// build_primitives (solver.cpp:145-170) of cell (i, j) of the ghosted grid, read
+// through the ghost map; bad |= the reference's check
+template <bool DIM2, bool FAST>
+__device__ __forceinline__ void cell_prims(const SmallArgs& a, const double* f, int i, int j,
+                                           double w[4], bool& bad) {
+  bool fx, fy = false;
+  const int is = img(i, a.nx, a.bc[0], a.bc[1], fx);
+  const int js = DIM2 ? img(j, a.ny, a.bc[2], a.bc[3], fy) : 0;
+  const int64_t o = (int64_t)js * a.pitch + is;
+  const double r = __ldcg(f + o);
+  double mx = __ldcg(f + a.fstride + o), my = __ldcg(f + 2 * a.fstride + o);
+  const double e = __ldcg(f + 3 * a.fstride + o);
+  if (fx) mx = -1.0 * mx;   // sx * row[...] (grid.cpp:86-94)
+  if (fy) my = -1.0 * my;
+  if constexpr (FAST) {
+    // the fast reciprocal; the cell box implies the reference's checks and proves
+    // every division / square root of the faces this cell feeds (face_fast.cuh)
+    bool dead = true;
+    prim_fast(r, mx, my, e, a.k.gm1, w, dead);
+    if (!cell_in_box(w)) bad = true;
+  } else {
+    w[0] = 0.0;
+    w[1] = w[2] = w[3] = 0.0;
+    if (!(r > 0.0)) {
+      bad = true;
+    } else {
+      w[0] = r;
+      primitive(r, mx, my, e, a.k.gm1, w[1], w[2], w[3]);
+      bad = bad || !(w[3] > 0.0);
+    }
+  }
+}
+
+// the two faces of a cell along one axis (compute_fluxes, solver.cpp:196-239):
+// s[0..4] = the cells c-2 .. c+2; lo face (c-1 | c) and hi face (c | c+1)
+template <int AXIS, bool MUSCL, bool FAST>
+__device__ __forceinline__ void cell_faces(const SmallArgs& a, const FK& fk,
+                                           const double (&s)[5][4], double flo[4], double fhi[4],
+                                           bool& bad) {
+  double m_lo[4], p_lo[4], m_hi[4], p_hi[4];
+  if constexpr (FAST) {
+    // the fast kernels' traces (sweby_fast: beta >= 1) and face solves (face_fast.cuh)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double lo;
+      cell_traces<MUSCL>(s[0][c], s[1][c], s[2][c], fk.beta, lo, m_lo[c]);
+      cell_traces<MUSCL>(s[1][c], s[2][c], s[3][c], fk.beta, p_lo[c], m_hi[c]);
+      double hi;
+      cell_traces<MUSCL>(s[2][c], s[3][c], s[4][c], fk.beta, p_hi[c], hi);
+    }
+    if (!traces_ok(m_lo[0], m_lo[3], p_lo[0], p_lo[3]) ||
+        !traces_ok(m_hi[0], m_hi[3], p_hi[0], p_hi[3]))
+      bad = true;
+    bool dead = true;
+    double ps0, us0, ps1, us1;
+    face_fast<AXIS>(m_lo[0], m_lo[1], m_lo[2], m_lo[3], p_lo[0], p_lo[1], p_lo[2], p_lo[3], fk, flo,
+                    dead, ps0, us0);
+    face_fast<AXIS>(m_hi[0], m_hi[1], m_hi[2], m_hi[3], p_hi[0], p_hi[1], p_hi[2], p_hi[3], fk, fhi,
+                    dead, ps1, us1);
+    if (needs_mean(us0))
+      face_mean<AXIS>(m_lo[0], m_lo[1], m_lo[2], m_lo[3], p_lo[0], p_lo[1], p_lo[2], p_lo[3], ps0,
+                      us0, fk, flo, dead);
+    if (needs_mean(us1))
+      face_mean<AXIS>(m_hi[0], m_hi[1], m_hi[2], m_hi[3], p_hi[0], p_hi[1], p_hi[2], p_hi[3], ps1,
+                      us1, fk, fhi, dead);
+  } else {
+  #pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (MUSCL) {
+        // muscl_face_trace (reconstruct.hpp:44-49): each cell's limited slope serves
+        // both of its faces
+        const double s1 = slope3(s[0][c], s[1][c], s[2][c], a.k.beta);
+        const double s2 = slope3(s[1][c], s[2][c], s[3][c], a.k.beta);
+        const double s3 = slope3(s[2][c], s[3][c], s[4][c], a.k.beta);
+        m_lo[c] = s[1][c] + 0.5 * s1;
+        p_lo[c] = s[2][c] - 0.5 * s2;
+        m_hi[c] = s[2][c] + 0.5 * s2;
+        p_hi[c] = s[3][c] - 0.5 * s3;
+      } else {
+        m_lo[c] = s[1][c];
+        p_lo[c] = s[2][c];
+        m_hi[c] = s[2][c];
+        p_hi[c] = s[3][c];
+      }
+      flo[c] = fhi[c] = 0.0;
+    }
+    if (traces_ok(m_lo[0], m_lo[3], p_lo[0], p_lo[3]))
+      face_flux<AXIS>(m_lo[0], m_lo[1], m_lo[2], m_lo[3], p_lo[0], p_lo[1], p_lo[2], p_lo[3], a.k, flo);
+    else
+      bad = true;
+    if (traces_ok(m_hi[0], m_hi[3], p_hi[0], p_hi[3]))
+      face_flux<AXIS>(m_hi[0], m_hi[1], m_hi[2], m_hi[3], p_hi[0], p_hi[1], p_hi[2], p_hi[3], a.k, fhi);
+    else
+      bad = true;
+  }
+}
+
+// One stage for interior cell (i, j): primitives of its cross stencil, its four
+// faces, apply_update (solver.cpp:272-308).  Stage 1 (!TWO) stores its faces (a
+// cell owns its low faces, the last cell of a row / column the high one too);
+// stage 2 stores its own and reads stage 1's for F = 0.5 (F^n + F*).
+template <bool DIM2, bool MUSCL, bool FAST, bool TWO>
+__device__ __forceinline__ void cell_stage(const SmallArgs& a, const FK& fk, const double* in,
+                                           const double* base, int i, int j, double lam_x,
+                                           double lam_y, double vals[4], bool& bad) {
+  double fxl[4], fxr[4], fyb[4], fyt[4];
+  {
+    double s[5][4];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) cell_prims<DIM2, FAST>(a, in, i - 2 + d, j, s[d], bad);
+    cell_faces<0, MUSCL, FAST>(a, fk, s, fxl, fxr, bad);
+  }
+  if (DIM2) {
+    double s[5][4];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) cell_prims<DIM2, FAST>(a, in, i, j - 2 + d, s[d], bad);
+    cell_faces<1, MUSCL, FAST>(a, fk, s, fyb, fyt, bad);
+  }
+  const int k = TWO ? 1 : 0;
+  const int64_t ox = (int64_t)j * a.pitch + i;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double* fx = a.fx[k] + c * a.fx_stride;
+    __stcg(fx + ox, fxl[c]);
+    if (i == a.nx - 1) __stcg(fx + ox + 1, fxr[c]);
+    if (DIM2) {
+      double* fy = a.fy[k] + c * a.fy_stride;
+      __stcg(fy + ox, fyb[c]);
+      if (j == a.ny - 1) __stcg(fy + ox + a.pitch, fyt[c]);
+    }
+  }
+  const int64_t o = (int64_t)j * a.pitch + i;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double l = fxl[c], r = fxr[c];
+    if (TWO) {
+      const double* fa = a.fx[0] + c * a.fx_stride;
+      l = 0.5 * (__ldcg(fa + ox) + l);
+      r = 0.5 * (__ldcg(fa + ox + 1) + r);
+    }
+    double val = __ldcg(base + c * a.fstride + o) - lam_x * (r - l);
+    if (DIM2) {
+      double b = fyb[c], t = fyt[c];
+      if (TWO) {
+        const double* fa = a.fy[0] + c * a.fy_stride;
+        b = 0.5 * (__ldcg(fa + ox) + b);
+        t = 0.5 * (__ldcg(fa + ox + a.pitch) + t);
+      }
+      val -= lam_y * (t - b);
+    }
+    vals[c] = val;
+  }
+}
+
+template <bool DIM2, bool MUSCL, bool FAST>
+__global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_run(SmallArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ SmallShared sh;
+  const int tid = threadIdx.x;
+  const uint32_t rank = cluster.block_rank(), nblk = cluster.num_blocks();
+  const bool lead = rank == 0;
+  const int gtid = (int)rank * SMALL_THREADS + tid;
+  const int gthreads = (int)nblk * SMALL_THREADS;
+  // the lead block's control record and partial slots, as shared::cluster addresses
+  const uint32_t r_ctl = remote(&sh.ctl, 0);
+  const uint32_t r_rate = remote(&sh.p_rate[rank], 0), r_min_r = remote(&sh.p_min_r[rank], 0),
+                 r_min_e = remote(&sh.p_min_e[rank], 0), r_fail = remote(&sh.p_fail[rank], 0),
+                 r_dtfail = remote(&sh.p_dtfail[rank], 0);
+  if (lead && tid == 0) sh.ctl = *a.ctl;
+  const FK fk = make_fk(a.k.gamma, a.k.gm1, a.k.beta, a.k.dx, a.k.dy);
+  double* u = a.u;
+  double* u2 = a.u2;
+  const MaxOp mx;
+  const MinOp mn;
+  const int ncell = a.nx * a.ny;
+  int n = 0;
+  for (; n < a.nsteps; ++n) {
+    if (tid == 0) {
+      sh.rate = 0ull;
+      sh.min_r = sh.min_e = 0x7ff0000000000000ull;
+      sh.fail = sh.dtfail = 0;
+    }
+    // (releases the lead's control record of this step and the local resets)
+    cluster.sync();
+    StepCtl c;
+    {
+      unsigned long long w[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) w[q] = ld_remote_u64(r_ctl + 8 * q);
+      memcpy(&c, w, sizeof c);
+    }
+    if (c.done) break;
+    // compute_dt's tail (solver.cpp:471-479) from the rate of the input state
+    const double rate = __longlong_as_double((long long)c.rate_bits);
+    double dt = a.cfl / rate;
+    if (c.time + dt > a.limit) dt = a.limit - c.time;
+    if (c.dtfail || !(dt > 0.0)) break;
+    const double lam_x = dt / a.k.dx;  // solver.cpp:262-263
+    const double lam_y = dt / a.k.dy;
+    bool bad = false, dtbad = false;
+    unsigned long long mr = 0x7ff0000000000000ull, me = 0x7ff0000000000000ull, rk = 0ull;
+    // the last stage's cell: positivity (solver.cpp:300-307), minima, and the next
+    // step's CFL rate (solver.cpp:449-470) of the new value
+    auto finish = [&](const double v[4]) {
+      const double eint = internal_energy(v[0], v[1], v[2], v[3]);
+      if (!(v[0] > 0.0) || !(eint > 0.0)) {
+        bad = true;
+      } else {
+        const unsigned long long r = pos_bits(v[0]), e = pos_bits(eint);
+        mr = r < mr ? r : mr;
+        me = e < me ? e : me;
+      }
+      double rr;
+      if (cfl_rate<DIM2>(v[0], v[1], v[2], v[3], a.k, rr)) {
+        if (rr == rr) {
+          const unsigned long long b = pos_bits(rr);
+          rk = b > rk ? b : rk;
+        }
+      } else {
+        dtbad = true;
+      }
+    };
+    // stage 1: U^n -> U* (or U^{n+1} when time_order = 1)
+    for (int t = gtid; t < ncell; t += gthreads) {
+      const int i = t % a.nx, j = t / a.nx;
+      double v[4];
+      cell_stage<DIM2, MUSCL, FAST, false>(a, fk, u, u, i, j, lam_x, lam_y, v, bad);
+      const int64_t o = (int64_t)j * a.pitch + i;
+      double* out = a.heun ? a.us : u2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) __stcg(out + q * a.fstride + o, v[q]);
+      if (a.heun) {
+        const double eint = internal_energy(v[0], v[1], v[2], v[3]);
+        if (!(v[0] > 0.0) || !(eint > 0.0)) bad = true;
+      } else {
+        finish(v);
+      }
+    }
+    if (a.heun) {
+      __threadfence();
+      cluster.sync();
+      // stage 2: U* -> U^{n+1} from U^n with 0.5 (F^n + F*)
+      for (int t = gtid; t < ncell; t += gthreads) {
+        const int i = t % a.nx, j = t / a.nx;
+        double v[4];
+        cell_stage<DIM2, MUSCL, FAST, true>(a, fk, a.us, u, i, j, lam_x, lam_y, v, bad);
+        const int64_t o = (int64_t)j * a.pitch + i;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) __stcg(u2 + q * a.fstride + o, v[q]);
+        finish(v);
+      }
+    }
+    // block partials (warp shuffles, then the block's own shared atomics), then one
+    // plain store of each into the lead block's slot for this block
+    rk = wred(rk, mx);
+    mr = wred(mr, mn);
+    me = wred(me, mn);
+    const bool wbad = __any_sync(0xffffffffu, bad), wdt = __any_sync(0xffffffffu, dtbad);
+    if ((tid & 31) == 0) {
+      if (rk) atomicMax(&sh.rate, rk);
+      if (mr != 0x7ff0000000000000ull) atomicMin(&sh.min_r, mr);
+      if (me != 0x7ff0000000000000ull) atomicMin(&sh.min_e, me);
+      if (wbad) sh.fail = 1;
+      if (wdt) sh.dtfail = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      st_remote(r_rate, sh.rate);
+      st_remote(r_min_r, sh.min_r);
+      st_remote(r_min_e, sh.min_e);
+      st_remote(r_fail, sh.fail);
+      st_remote(r_dtfail, sh.dtfail);
+    }
+    __threadfence();
+    cluster.sync();
+    // every block reads the failure flags (uniform decision, no extra barrier)
+    int fail = 0;
+    for (uint32_t b = 0; b < nblk; ++b) fail |= ld_remote_i(remote(&sh.p_fail[b], 0));
+    if (fail) break;   // the host re-runs this step stage-wise
+    if (lead) {
+      // accumulate_boundary_outflow (solver.cpp:406-432): the boundary-face
+      // differences (Heun-averaged as k_gather_boundary) staged a tile at a time by
+      // the whole block, then summed in order by lanes 0-3 (x, over the rows) and
+      // 4-7 (y, over the columns) of warp 0
+      const int ex = a.ny, ey = DIM2 ? a.nx : 0;
+      const int len = ex > ey ? ex : ey;
+      double s = 0.0;
+      for (int base = 0; base < len; base += OUT_TILE) {
+#pragma unroll
+        for (int k = tid; k < 8 * OUT_TILE; k += SMALL_THREADS) {
+          const int ch = k / OUT_TILE, e = base + k % OUT_TILE, q = ch & 3;
+          double d = 0.0;
+          if (ch < 4 && e < ex) {
+            const double* fa = a.fx[0] + q * a.fx_stride + (int64_t)e * a.pitch;
+            const double* fb = a.fx[1] + q * a.fx_stride + (int64_t)e * a.pitch;
+            const double left = a.heun ? 0.5 * (__ldcg(fa) + __ldcg(fb)) : __ldcg(fa);
+            const double right =
+                a.heun ? 0.5 * (__ldcg(fa + a.nx) + __ldcg(fb + a.nx)) : __ldcg(fa + a.nx);
+            d = right - left;
+          } else if (ch >= 4 && e < ey) {
+            const double* fa = a.fy[0] + q * a.fy_stride + e;
+            const double* fb = a.fy[1] + q * a.fy_stride + e;
+            const int64_t tp = (int64_t)a.ny * a.pitch;
+            const double bot = a.heun ? 0.5 * (__ldcg(fa) + __ldcg(fb)) : __ldcg(fa);
+            const double top = a.heun ? 0.5 * (__ldcg(fa + tp) + __ldcg(fb + tp)) : __ldcg(fa + tp);
+            d = top - bot;
+          }
+          sh.dif[k % OUT_TILE][ch] = d;
+        }
+        __syncthreads();
+        if (tid < 8) {
+          const int m = min(OUT_TILE, (tid < 4 ? ex : ey) - base);
+          for (int e = 0; e < m; ++e) s += sh.dif[e][tid];
+        }
+        __syncthreads();
+      }
+      if (tid < 8) {
+        const int q = tid & 3;
+        const double ax = dt * (DIM2 ? a.k.dy : 1.0), ay = dt * a.k.dx;
+        if (tid < 4) a.outflow[q] += ax * s;
+        __syncwarp(0xffu);
+        if (DIM2 && tid >= 4) a.outflow[q] += ay * s;
+      }
+      if (tid == 0) {
+        unsigned long long rt = 0ull, m_r = 0x7ff0000000000000ull, m_e = 0x7ff0000000000000ull;
+        int dtf = 0;
+        for (uint32_t b = 0; b < nblk; ++b) {
+          rt = sh.p_rate[b] > rt ? sh.p_rate[b] : rt;
+          m_r = sh.p_min_r[b] < m_r ? sh.p_min_r[b] : m_r;
+          m_e = sh.p_min_e[b] < m_e ? sh.p_min_e[b] : m_e;
+          dtf |= sh.p_dtfail[b];
+        }
+        StepRec r;
+        r.dt = dt;
+        r.hits = c.time + dt >= a.limit;
+        r.time = r.hits ? a.limit : c.time + dt;
+        r.min_rho = __longlong_as_double((long long)m_r);
+        r.min_eint = __longlong_as_double((long long)m_e);
+        r.min_p_mat = __longlong_as_double(0x7ff0000000000000ll);
+        r.status = 0;
+        a.rec[n] = r;
+        StepCtl nx_;
+        nx_.time = r.time;
+        nx_.rate_bits = rt;
+        nx_.dtfail = dtf;
+        nx_.done = !(r.time < a.t_final);
+        sh.ctl = nx_;
+      }
+    }
+    double* t = u;
+    u = u2;
+    u2 = t;
+  }
+  // the step that stopped the batch: 1 failed (the host re-runs it stage-wise),
+  // 2 skipped (limit reached); later steps skipped
+  if (lead && tid == 0) {
+    for (int k = n; k < a.nsteps; ++k) {
+      StepRec r{};
+      r.status = (k == n && !sh.ctl.done) ? 1 : 2;
+      r.time = sh.ctl.time;
+      a.rec[k] = r;
+    }
+    *a.ctl = sh.ctl;
+  }
+  cluster.sync();   // no block leaves while another may still address its shared memory
+}
+
+// LF_SMALL_FAST=0 in the environment: the IEEE expressions throughout (A/B)
+bool small_fast_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LF_SMALL_FAST");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// One cluster of up to 16 blocks (the non-portable maximum; fewer where the device
+// cannot co-schedule them), each block on its own SM.
+template <bool DIM2, bool MUSCL>
+cudaError_t launch_small(const SmallArgs& a, int want, bool fast, cudaStream_t st) {
+  auto kern = fast ? k_small_run<DIM2, MUSCL, true> : k_small_run<DIM2, MUSCL, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(SMALL_THREADS);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncta = std::max(want, 1);
+  cfg.gridDim = dim3(ncta);
+  at[0].val.clusterDim.x = ncta;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  int maxc = 0;
+  if (cudaOccupancyMaxPotentialClusterSize(&maxc, kern, &cfg) == cudaSuccess && maxc >= 1 &&
+      ncta > maxc) {
+    ncta = maxc;
+    cfg.gridDim = dim3(ncta);
+    at[0].val.clusterDim.x = ncta;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+}  // namespace
+
+// ================================================================= host driver
+
+struct SmallState {
+  StepCtl* ctl = nullptr;        // device [1]
+  StepCtl* ctl_host = nullptr;   // pinned [1]
+  StepRec* rec = nullptr;        // device [cap]
+  StepRec* rec_host = nullptr;   // pinned [cap]
+  double* outflow = nullptr;     // device [4]
+  double* outflow_host = nullptr;
+  int cap = 0;
+  bool valid = false;            // ctl holds the rate of the current U
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+namespace {
+
+struct SmallFail : std::runtime_error {
+  explicit SmallFail(const std::string& w) : std::runtime_error(w) {}
+};
+#define SK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) throw SmallFail(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+SmallState* sstate(lf_handle* h) { return reinterpret_cast<SmallState*>(h->small); }
+
+void small_alloc(lf_handle* h, int steps) {
+  SlabState& s = h->slabs[0];
+  SK(cudaSetDevice(s.device));
+  alloc_staged_public(h);
+  SmallState* m = sstate(h);
+  if (!m) {
+    m = new SmallState;
+    h->small = m;
+    SK(cudaMalloc(&m->ctl, sizeof(StepCtl)));
+    SK(cudaHostAlloc(&m->ctl_host, sizeof(StepCtl), cudaHostAllocDefault));
+    SK(cudaMalloc(&m->outflow, 4 * sizeof(double)));
+    SK(cudaHostAlloc(&m->outflow_host, 4 * sizeof(double), cudaHostAllocDefault));
+    SK(cudaEventCreate(&m->e0));
+    SK(cudaEventCreate(&m->e1));
+  }
+  if (steps > m->cap) {
+    cudaFree(m->rec);
+    cudaFreeHost(m->rec_host);
+    m->cap = std::max(steps, 256);
+    SK(cudaMalloc(&m->rec, (size_t)m->cap * sizeof(StepRec)));
+    SK(cudaHostAlloc(&m->rec_host, (size_t)m->cap * sizeof(StepRec), cudaHostAllocDefault));
+  }
+}
+
+// Run up to n steps from `time` in one launch; returns the completed count and
+// the index of a failed step (-1 if none).  U holds the state after them.
+int run_small(lf_handle* h, int n, double cfl, double limit, double t_final, double time,
+              double* outflow, int* failed_at, float* ms) {
+  LF_TRACE("small-grid step batch");
+  SmallState* m = sstate(h);
+  SlabState& s = h->slabs[0];
+  if (!m->valid) {
+    const Scalars sc = rate_of_current(h);
+    m->ctl_host->rate_bits = sc.rate_bits;
+    m->ctl_host->dtfail = sc.fail_dt != LLONG_MAX;
+    m->valid = true;
+  } else {
+    SK(cudaMemcpyAsync(m->ctl_host, m->ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost, s.stream));
+    SK(cudaStreamSynchronize(s.stream));
+  }
+  m->ctl_host->time = time;
+  m->ctl_host->done = 0;
+  SK(cudaMemcpyAsync(m->ctl, m->ctl_host, sizeof(StepCtl), cudaMemcpyHostToDevice, s.stream));
+  double o[4] = {0, 0, 0, 0};
+  if (outflow) std::memcpy(o, outflow, sizeof o);
+  std::memcpy(m->outflow_host, o, sizeof o);
+  SK(cudaMemcpyAsync(m->outflow, m->outflow_host, sizeof o, cudaMemcpyHostToDevice, s.stream));
+  SmallArgs a;
+  a.u = s.U + s.L.origin();
+  a.u2 = s.U2 + s.L.origin();
+  a.us = s.Us + s.L.origin();
+  a.pitch = s.L.pitch;
+  a.fstride = s.L.fstride;
+  for (int k = 0; k < 2; ++k) {
+    a.fx[k] = s.FX[k];
+    a.fy[k] = s.FY[k];
+  }
+  a.fx_stride = s.fx_stride;
+  a.fy_stride = s.fy_stride;
+  a.nx = s.L.nx;
+  a.ny = s.L.ny;
+  a.heun = h->d.time_order >= 2;
+  for (int q = 0; q < 4; ++q) a.bc[q] = h->d.bc[q];
+  a.k = h->k;
+  a.cfl = cfl;
+  a.limit = limit;
+  a.t_final = t_final;
+  a.ctl = m->ctl;
+  a.rec = m->rec;
+  a.outflow = m->outflow;
+  a.nsteps = n;
+  const bool muscl = h->d.spatial_order >= 2;
+  if (ms) SK(cudaEventRecord(m->e0, s.stream));
+  count_launch();
+  const int64_t cells = (int64_t)a.nx * a.ny;
+  const int want = (int)std::min<int64_t>((cells + SMALL_THREADS - 1) / SMALL_THREADS, SMALL_MAX_CTAS);
+  cudaError_t le;
+  // the fast exact arithmetic where its proofs hold (beta >= 1 for sweby_fast, gamma - 1
+  // in the constant box); a cell outside the cell box flags the step (stage-wise re-run)
+  const bool fast = small_fast_enabled() && !h->small_ieee && h->d.beta >= 1.0 && h->k.gm1 >= 0x1p-14 &&
+                    h->k.gm1 < 0x1p6 && h->k.gamma < 0x1p7;
+  if (h->dim2)
+    le = muscl ? launch_small<true, true>(a, want, fast, s.stream)
+               : launch_small<true, false>(a, want, fast, s.stream);
+  else
+    le = muscl ? launch_small<false, true>(a, want, fast, s.stream)
+               : launch_small<false, false>(a, want, fast, s.stream);
+  SK(le);
+  SK(cudaGetLastError());
+  if (ms) SK(cudaEventRecord(m->e1, s.stream));
+  SK(cudaMemcpyAsync(m->rec_host, m->rec, (size_t)n * sizeof(StepRec), cudaMemcpyDeviceToHost,
+                     s.stream));
+  SK(cudaMemcpyAsync(m->outflow_host, m->outflow, 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                     s.stream));
+  SK(cudaStreamSynchronize(s.stream));
+  if (ms) SK(cudaEventElapsedTime(ms, m->e0, m->e1));
+  int done = 0;
+  *failed_at = -1;
+  for (int i = 0; i < n; ++i) {
+    if (m->rec_host[i].status == 0) {
+      ++done;
+      continue;
+    }
+    if (m->rec_host[i].status == 1) *failed_at = i;
+    break;
+  }
+  if (done & 1) std::swap(s.U, s.U2);   // the kernel ping-pongs U and U2 once per step
+  fused_invalidate(h);   // (also clears m->valid)
+  m->valid = *failed_at < 0;
+  h->rate_valid = false;
+  if (outflow) std::memcpy(outflow, m->outflow_host, 4 * sizeof(double));
+  return done;
+}
+
+void to_out(const StepRec& r, int64_t step, double gm1, lf_step_out* o) {
+  o->dt = r.dt;
+  o->hits_limit = r.hits;
+  o->time = r.time;
+  o->step = step;
+  o->min_rho = r.min_rho;
+  o->min_p = gm1 * r.min_eint;
+}
+
+}  // namespace
+
+// LF_PATH_SMALL: one material, one slab on one device (no NCCL), and a grid small
+// enough for one block (AUTO: up to SMALL_AUTO_CELLS cells, measured by
+// tools/small_sweep.py against the two-pass / stage-wise paths).
+bool small_supported(lf_handle* h) {
+  if (h->mc.n > 0 || h->slabs.size() != 1 || h->nccl) return false;
+  // (the kernel reads ghosts through an index map whose sources are interior cells)
+  if (h->d.nx < 2 || (h->dim2 && h->d.ny < 2)) return false;
+  return (int64_t)h->d.nx * h->d.ny <= SMALL_MAX_CELLS;
+}
+
+bool prefer_small(lf_handle* h) {
+  return h->path == LF_PATH_AUTO && small_supported(h) &&
+         (int64_t)h->d.nx * h->d.ny <= (h->dim2 ? SMALL_AUTO_CELLS_2D : SMALL_AUTO_CELLS_1D);
+}
+
+void small_invalidate(lf_handle* h) {
+  if (SmallState* m = sstate(h)) m->valid = false;
+}
+
+void small_release(lf_handle* h) {
+  SmallState* m = sstate(h);
+  if (!m) return;
+  cudaFree(m->ctl);
+  cudaFreeHost(m->ctl_host);
+  cudaFree(m->rec);
+  cudaFreeHost(m->rec_host);
+  cudaFree(m->outflow);
+  cudaFreeHost(m->outflow_host);
+  if (m->e0) cudaEventDestroy(m->e0);
+  if (m->e1) cudaEventDestroy(m->e1);
+  delete m;
+  h->small = nullptr;
+}
+
+int small_heun(lf_handle* h, double cfl, double time, double limit, int64_t step,
+               double* outflow, lf_step_out* out) {
+  small_alloc(h, 1);
+  int failed_at;
+  double acc[4] = {0, 0, 0, 0};
+  if (outflow) std::memcpy(acc, outflow, sizeof acc);
+  if (run_small(h, 1, cfl, limit, limit, time, acc, &failed_at, nullptr) == 1) {
+    if (outflow) std::memcpy(outflow, acc, sizeof acc);
+    if (out) to_out(sstate(h)->rec_host[0], step + 1, h->d.gamma - 1.0, out);
+    return 0;
+  }
+  // a check failed: the stage-wise kernels reproduce the reference's error
+  small_invalidate(h);
+  fused_invalidate(h);
+  const int rc = staged_heun_public(h, cfl, time, limit, step, outflow, out);
+  if (rc == 0) h->small_ieee = 1;   // the fast arithmetic's box failed, not the step
+  return rc;
+}
+
+int small_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* time,
+                  int64_t* step, double* outflow, lf_step_out* per_step, int* taken) {
+  if (taken) *taken = 0;
+  int k = 0;
+  while (k < nsteps && *time < t_final) {
+    const int batch = std::min(nsteps - k, SMALL_BATCH);
+    small_alloc(h, batch);
+    SmallState* m = sstate(h);
+    int failed_at;
+    const int done = run_small(h, batch, cfl, t_final, t_final, *time, outflow, &failed_at, nullptr);
+    for (int i = 0; i < done; ++i) {
+      *step += 1;
+      if (per_step) to_out(m->rec_host[i], *step, h->d.gamma - 1.0, &per_step[k + i]);
+      *time = m->rec_host[i].time;
+    }
+    k += done;
+    if (taken) *taken = k;
+    if (failed_at >= 0) {
+      small_invalidate(h);
+      fused_invalidate(h);
+      lf_step_out o;
+      const int rc = staged_heun_public(h, cfl, *time, t_final, *step, outflow, &o);
+      if (rc) return rc;
+      h->small_ieee = 1;   // the fast arithmetic's box failed, not the step
+      *step = o.step;
+      *time = o.time;
+      if (per_step) per_step[k] = o;
+      ++k;
+      if (taken) *taken = k;
+      continue;
+    }
+    if (done < batch) break;  // reached t_final
+  }
+  return 0;
+}
+
+int small_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
+                     int* launches) {
+  small_alloc(h, nsteps);
+  SmallState* m = sstate(h);
+  SlabState& s = h->slabs[0];
+  double t0 = 0.0;
+  if (m->valid) {
+    SK(cudaMemcpy(m->ctl_host, m->ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost));
+    t0 = m->ctl_host->time;
+  }
+  const double big = 1.7976931348623157e308;
+  SK(cudaEventRecord(m->e0, s.stream));
+  int failed_at;
+  float ms = 0.f;
+  const int done = run_small(h, nsteps, cfl, big, big, t0, nullptr, &failed_at, &ms);
+  *kernel_ms = ms;
+  *step_ms = ms;
+  *launches = 1;
+  (void)done;
+  return failed_at >= 0 ? LF_ERR_DEVICE : 0;
+}
+
+}  // namespace lfb

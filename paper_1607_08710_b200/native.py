@@ -17,7 +17,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "lagflux_b200.h")
 LF_OK, LF_ERR_CONFIG, LF_ERR_DT_STATE, LF_ERR_DT_NONPOS = 0, 1, 2, 3
 LF_ERR_PRIMITIVE, LF_ERR_TRACE, LF_ERR_POSITIVITY, LF_ERR_DEVICE, LF_ERR_ARGUMENT = 4, 5, 6, 7, 8
 LF_ERR_FRACTION = 9
-LF_PATH_AUTO, LF_PATH_FUSED, LF_PATH_STAGED, LF_PATH_TWOPASS = 0, 1, 2, 3
+LF_PATH_AUTO, LF_PATH_FUSED, LF_PATH_STAGED, LF_PATH_TWOPASS, LF_PATH_SMALL = 0, 1, 2, 3, 4
 LF_MATH_EXACT, LF_MATH_CONTRACT = 0, 1
 
 

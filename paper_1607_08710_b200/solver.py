@@ -44,8 +44,8 @@ class LagfluxSolver:
 
     devices: one entry per y-slab driven from this process (repeats allowed).
     dist:    (rank, nranks, device, nccl_id_bytes) for one-process-per-GPU slabs.
-    path:    "auto" | "twopass" | "fused" | "staged" (Heun step implementation;
-             all produce identical results).
+    path:    "auto" | "twopass" | "fused" | "staged" | "small" (Heun step
+             implementation; all produce identical results).
     materials: a multimat.MaterialSet (the constructor's `const MaterialSet*`,
              solver.cpp:61-88); heun_step then takes the MaterialCells."""
 
@@ -120,7 +120,7 @@ class LagfluxSolver:
 
     def set_path(self, path: str):
         code = {"auto": N.LF_PATH_AUTO, "fused": N.LF_PATH_FUSED, "staged": N.LF_PATH_STAGED,
-                "twopass": N.LF_PATH_TWOPASS}[path]
+                "twopass": N.LF_PATH_TWOPASS, "small": N.LF_PATH_SMALL}[path]
         self._check(self._lib.lf_set_path(self._h, code))
 
     def set_math(self, math: str):
@@ -132,11 +132,11 @@ class LagfluxSolver:
         self.math = math
 
     def resolved_path(self) -> str:
-        """The path the next step takes ('twopass', 'fused' or 'staged')."""
+        """The path the next step takes ('twopass', 'fused', 'staged' or 'small')."""
         p = C.c_int()
         self._check(self._lib.lf_resolved_path(self._h, C.byref(p)))
         return {N.LF_PATH_TWOPASS: "twopass", N.LF_PATH_FUSED: "fused",
-                N.LF_PATH_STAGED: "staged"}[p.value]
+                N.LF_PATH_STAGED: "staged", N.LF_PATH_SMALL: "small"}[p.value]
 
     def set_stream(self, stream_ptr: Optional[int]):
         self._check(self._lib.lf_set_stream(self._h, stream_ptr))

@@ -1,0 +1,131 @@
+"""LF_PATH_SMALL (csrc/small_step.cu): the step loop of a small grid in one thread-block
+cluster, against the oracle bit for bit.
+
+The golden / error / random suites already run the path (test_gpu_parity.PATHS, and
+LF_PATH_AUTO picks it for the small random grids); here: the AUTO choice, every
+cluster size from one block to sixteen and past them (strided cells), every boundary
+pair, both orders in space and time, 1D, step limits inside a batch, and the sticky
+switch to the IEEE arithmetic after a cell leaves the fast arithmetic's box.
+"""
+import numpy as np
+import pytest
+
+from paper_1607_08710_b200 import cases as CS
+from paper_1607_08710_b200 import grid as G
+from paper_1607_08710_b200 import multimat as MM
+from paper_1607_08710_b200.solver import LagfluxSolver
+from helpers import assert_fields_equal, diag_array, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(case, steps, path="small", advance=True, field=None):
+    s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, path=path)
+    assert s.resolved_path() == path
+    st = G.SolverState(field=CS.initial_field(case) if field is None else np.array(field))
+    ctl = G.TimeControls(case.cfl, case.t_final, steps)
+    if advance:
+        s.attach(st)
+        while st.step < steps and st.time < case.t_final:
+            if s.advance(st, ctl, steps - st.step) == 0:
+                break
+    else:
+        while st.step < steps and st.time < case.t_final:
+            s.heun_step(st, ctl, case.t_final)
+    s.sync_to_host(st)
+    s.close()
+    return st
+
+
+def _check(case, steps, st, what):
+    ref, rdiag = run_oracle(case, steps)
+    g = case.grid
+    assert_fields_equal(g.interior(st.field), g.interior(ref.field), what)
+    assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4]), what
+    assert np.array_equal(np.array(st.boundary_outflow), np.array(ref.boundary_outflow)), what
+
+
+def test_auto_picks_the_small_path_where_it_is_faster(cuda):
+    def resolved(case, **kw):
+        s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, **kw)
+        p = s.resolved_path()
+        s.close()
+        return p
+    assert resolved(CS.sod()) == "small"                      # BASELINE config 1
+    assert resolved(CS.quadrant(128, 1)) == "small"
+    assert resolved(CS.quadrant(256, 1)) == "twopass"
+    g1 = G.make_grid_1d(100_000, 0.0, 1.0)
+    assert resolved(CS.Case("s", g1, G.BoundaryCondition(), 1.4, G.SchemeParams(), 0.5, 0.2,
+                            G.INT64_MAX, "riemann_x")) == "small"
+    assert resolved(CS.quadrant(64, 1), devices=(0, 0)) == "twopass"   # y-slabs
+    tp = CS.triple_point(64, 28, 1)
+    s = LagfluxSolver(tp.grid, tp.bc, tp.gamma, tp.params,
+                      materials=MM.make_material_set(tp.material_gammas))
+    assert s.resolved_path() != "small"                      # materials: not on this path
+    s.close()
+
+
+# cells per grid: 1 block (256 threads) .. 16 blocks .. beyond (strided cells)
+@pytest.mark.parametrize("nx,ny", [(12, 9), (40, 13), (64, 56), (128, 32), (160, 40), (300, 37)])
+def test_cluster_sizes_equal_oracle(cuda, nx, ny):
+    g = G.make_grid_2d(nx, ny, 0.0, 1.0, 0.0, ny / nx)
+    case = CS.Case("q", g, G.BoundaryCondition(G.REFLECTIVE, G.TRANSMISSIVE, G.TRANSMISSIVE,
+                                               G.REFLECTIVE), 1.4, G.SchemeParams(), 0.45,
+                   CS.STEP_DRIVEN_LIMIT, 12, "quadrant")
+    st = _run(case, 12)
+    _check(case, 12, st, f"{nx}x{ny}")
+
+
+BCS = [(G.TRANSMISSIVE, G.TRANSMISSIVE), (G.REFLECTIVE, G.REFLECTIVE),
+       (G.TRANSMISSIVE, G.REFLECTIVE), (G.PERIODIC, G.PERIODIC)]
+
+
+@pytest.mark.parametrize("xb", BCS)
+@pytest.mark.parametrize("yb", BCS)
+def test_boundary_pairs(cuda, xb, yb):
+    g = G.make_grid_2d(23, 17, 0.0, 1.0, 0.0, 0.8)
+    case = CS.Case("q", g, G.BoundaryCondition(xb[0], xb[1], yb[0], yb[1]), 1.4,
+                   G.SchemeParams(beta=1.5), 0.4, CS.STEP_DRIVEN_LIMIT, 10, "quadrant")
+    _check(case, 10, _run(case, 10), f"{xb} {yb}")
+
+
+@pytest.mark.parametrize("space,time", [(1, 1), (1, 2), (2, 1), (2, 2)])
+@pytest.mark.parametrize("dim", [1, 2])
+def test_orders_and_dimensions(cuda, space, time, dim):
+    if dim == 1:
+        g = G.make_grid_1d(333, 0.0, 1.0)
+        case = CS.Case("s", g, G.BoundaryCondition(G.REFLECTIVE, G.TRANSMISSIVE), 1.4,
+                       G.SchemeParams(spatial_order=space, time_order=time), 0.5, 0.2,
+                       G.INT64_MAX, "riemann_x")
+        steps = 10_000
+    else:
+        case = CS.quadrant(48, 25)
+        case = CS.Case(case.name, case.grid, case.bc, case.gamma,
+                       G.SchemeParams(spatial_order=space, time_order=time), case.cfl,
+                       case.t_final, 25, "quadrant")
+        steps = 25
+    _check(case, steps, _run(case, steps), f"dim {dim} order {space}/{time}")
+
+
+def test_heun_step_calls_and_limits_inside_a_batch(cuda):
+    """Single heun_step calls; lf_advance batches that end at t_final mid-batch and at a
+    step count -- the same records as the oracle."""
+    case = CS.sod()
+    _check(case, 10**6, _run(case, 10**6, advance=False), "heun_step")
+    _check(case, 10**6, _run(case, 10**6, advance=True), "advance to t_final")
+    _check(case, 77, _run(case, 77, advance=True), "advance 77 steps")
+
+
+def test_out_of_box_cell_switches_to_ieee_and_stays_exact(cuda):
+    """A region of density / pressure 1e-35 (outside the fast arithmetic's box): the first
+    step flags, the stage-wise kernels re-run it, the handle continues with the IEEE
+    arithmetic -- every step equal to the oracle."""
+    base = CS.quadrant(48, 6)
+    g = base.grid
+    f = CS.initial_field(base)
+    f[:, g.gy + 20:g.gy + 24, g.gx + 20:g.gx + 24] *= 1e-35
+    ref, rdiag = run_oracle(base, 6, field=f)
+    for advance in (False, True):
+        st = _run(base, 6, advance=advance, field=f)
+        assert_fields_equal(g.interior(st.field), g.interior(ref.field), f"advance={advance}")
+        assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4])
