@@ -16,6 +16,7 @@ constexpr int64_t SMALL_MAX_CELLS = (int64_t)1 << 22;
 constexpr int64_t SMALL_AUTO_CELLS_1D = (int64_t)1 << 17;
 constexpr int64_t SMALL_AUTO_CELLS_2D = (int64_t)1 << 14;
 constexpr int SMALL_BATCH = 4096;   // steps per launch of lf_advance
+constexpr int SMALL_MAX_PERIMETER = 1280;   // 2D: nx + ny (boundary faces in shared memory)
 
 bool small_supported(lf_handle* h);
 bool prefer_small(lf_handle* h);

@@ -50,7 +50,7 @@ namespace lfb {
 namespace {
 
 #ifndef LF_SMALL_THREADS
-#define LF_SMALL_THREADS 256
+#define LF_SMALL_THREADS 224   // + one outflow warp: 8 warps, 2 per scheduler
 #endif
 constexpr int SMALL_THREADS = LF_SMALL_THREADS;
 
@@ -61,6 +61,7 @@ struct SmallArgs {
   int64_t pitch, fstride;
   double* fx[2];   // face fluxes of the two stages (FluxArr layout: [c][b][a])
   double* fy[2];
+  int ob;          // doubles per boundary-face block (outflow sums; see k_small_run)
   int64_t fx_stride, fy_stride;
   int nx, ny;
   int heun;
@@ -74,7 +75,6 @@ struct SmallArgs {
 };
 
 constexpr int SMALL_MAX_CTAS = 16;
-constexpr int OUT_TILE = 256;
 
 // Per block: its own partial reductions; in the lead block (rank 0) also the
 // control record and every block's partials (written there by plain
@@ -83,9 +83,9 @@ struct SmallShared {
   StepCtl ctl;
   unsigned long long rate, min_r, min_e;   // this block's
   int fail, dtfail;
+  // p_fail: every block's failure flag, in every block; the other p_*: in the lead
   unsigned long long p_rate[SMALL_MAX_CTAS], p_min_r[SMALL_MAX_CTAS], p_min_e[SMALL_MAX_CTAS];
   int p_fail[SMALL_MAX_CTAS], p_dtfail[SMALL_MAX_CTAS];
-  double dif[OUT_TILE][9];   // [element][chain]; 9: conflict-free rows
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -100,13 +100,11 @@ __device__ __forceinline__ uint32_t remote(const void* p, uint32_t rank) {
 __device__ __forceinline__ void st_remote(uint32_t a, unsigned long long v) {
   asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_remote_d(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 __device__ __forceinline__ void st_remote(uint32_t a, int v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_remote_i(uint32_t a) {
-  int v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
 }
 __device__ __forceinline__ unsigned long long ld_remote_u64(uint32_t a) {
   unsigned long long v;
@@ -251,8 +249,25 @@ __device__ __forceinline__ void cell_faces(const SmallArgs& a, const FK& fk,
 // stage 2 stores its own and reads stage 1's for F = 0.5 (F^n + F*).
 template <bool DIM2, bool MUSCL, bool FAST, bool TWO>
 __device__ __forceinline__ void cell_stage(const SmallArgs& a, const FK& fk, const double* in,
-                                           const double* base, int i, int j, double lam_x,
-                                           double lam_y, double vals[4], bool& bad) {
+                                           const double* base, int i, int j, uint32_t rb,
+                                           double lam_x, double lam_y, double vals[4], bool& bad) {
+  const int64_t o = (int64_t)j * a.pitch + i;   // (cells and low faces share offsets)
+  // the operands that do not depend on this stage's faces, loaded first
+  double u0[4], fnl[4], fnr[4], fnb[4], fnt[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    u0[c] = __ldcg(base + c * a.fstride + o);
+    if (TWO) {
+      const double* fa = a.fx[0] + c * a.fx_stride;
+      fnl[c] = __ldcg(fa + o);
+      fnr[c] = __ldcg(fa + o + 1);
+      if (DIM2) {
+        const double* fb = a.fy[0] + c * a.fy_stride;
+        fnb[c] = __ldcg(fb + o);
+        fnt[c] = __ldcg(fb + o + a.pitch);
+      }
+    }
+  }
   double fxl[4], fxr[4], fyb[4], fyt[4];
   {
     double s[5][4];
@@ -267,47 +282,87 @@ __device__ __forceinline__ void cell_stage(const SmallArgs& a, const FK& fk, con
     cell_faces<1, MUSCL, FAST>(a, fk, s, fyb, fyt, bad);
   }
   const int k = TWO ? 1 : 0;
-  const int64_t ox = (int64_t)j * a.pitch + i;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     double* fx = a.fx[k] + c * a.fx_stride;
-    __stcg(fx + ox, fxl[c]);
-    if (i == a.nx - 1) __stcg(fx + ox + 1, fxr[c]);
+    __stcg(fx + o, fxl[c]);
+    if (i == a.nx - 1) __stcg(fx + o + 1, fxr[c]);
     if (DIM2) {
       double* fy = a.fy[k] + c * a.fy_stride;
-      __stcg(fy + ox, fyb[c]);
-      if (j == a.ny - 1) __stcg(fy + ox + a.pitch, fyt[c]);
+      __stcg(fy + o, fyb[c]);
+      if (j == a.ny - 1) __stcg(fy + o + a.pitch, fyt[c]);
     }
   }
-  const int64_t o = (int64_t)j * a.pitch + i;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     double l = fxl[c], r = fxr[c];
     if (TWO) {
-      const double* fa = a.fx[0] + c * a.fx_stride;
-      l = 0.5 * (__ldcg(fa + ox) + l);
-      r = 0.5 * (__ldcg(fa + ox + 1) + r);
+      l = 0.5 * (fnl[c] + l);
+      r = 0.5 * (fnr[c] + r);
     }
-    double val = __ldcg(base + c * a.fstride + o) - lam_x * (r - l);
+    double val = u0[c] - lam_x * (r - l);
     if (DIM2) {
       double b = fyb[c], t = fyt[c];
       if (TWO) {
-        const double* fa = a.fy[0] + c * a.fy_stride;
-        b = 0.5 * (__ldcg(fa + ox) + b);
-        t = 0.5 * (__ldcg(fa + ox + a.pitch) + t);
+        b = 0.5 * (fnb[c] + b);
+        t = 0.5 * (fnt[c] + t);
       }
       val -= lam_y * (t - b);
+      // the step's domain-boundary faces (Heun-averaged as k_gather_boundary) into the
+      // lead block's boundary block: [left 4 ny | right 4 ny | bottom 4 nx | top 4 nx]
+      if (rb) {
+        if (j == 0) st_remote_d(rb + 8u * (8 * a.ny + c * a.nx + i), b);
+        if (j == a.ny - 1) st_remote_d(rb + 8u * (8 * a.ny + 4 * a.nx + c * a.nx + i), t);
+      }
+    }
+    if (rb) {
+      if (i == 0) st_remote_d(rb + 8u * (c * a.ny + j), l);
+      if (i == a.nx - 1) st_remote_d(rb + 8u * (4 * a.ny + c * a.ny + j), r);
     }
     vals[c] = val;
   }
 }
 
+// accumulate_boundary_outflow (solver.cpp:406-432) of a completed step, by lanes 0-3
+// (x: s += right - left over the rows in order) and 4-7 (y: s += top - bottom over the
+// columns) of one warp, from the step's boundary block in shared memory; then
+// outflow += dt dy s_x, += dt dx s_y.
+template <bool DIM2>
+__device__ void outflow_sums(const SmallArgs& a, const double* sb, double dt) {
+  const int lane = threadIdx.x & 31;
+  if (lane < 8) {
+    const int q = lane & 3;
+    double s = 0.0;
+    if (lane < 4) {
+      const double* L = sb + q * a.ny;
+      const double* R = L + 4 * a.ny;
+#pragma unroll 8
+      for (int j = 0; j < a.ny; ++j) s += R[j] - L[j];
+    } else if (DIM2) {
+      const double* B = sb + 8 * a.ny + q * a.nx;
+      const double* T = B + 4 * a.nx;
+#pragma unroll 8
+      for (int i = 0; i < a.nx; ++i) s += T[i] - B[i];
+    }
+    const double ax = dt * (DIM2 ? a.k.dy : 1.0), ay = dt * a.k.dx;
+    if (lane < 4) a.outflow[q] += ax * s;
+    __syncwarp(0xffu);
+    if (DIM2 && lane >= 4) a.outflow[q] += ay * s;
+  }
+  __syncwarp();
+}
+
 template <bool DIM2, bool MUSCL, bool FAST>
-__global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_run(SmallArgs a) {
+__global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ SmallShared sh;
+  // two boundary blocks (step parity): a step's boundary faces, stored by the cells
+  // that own them in its last stage, summed by the lead's outflow warp during the
+  // next step's first stage
+  extern __shared__ double sbnd[];
   const int tid = threadIdx.x;
+  const bool cellw = tid < SMALL_THREADS;   // cell warps; the last warp sums the outflow
   const uint32_t rank = cluster.block_rank(), nblk = cluster.num_blocks();
   const bool lead = rank == 0;
   const int gtid = (int)rank * SMALL_THREADS + tid;
@@ -315,8 +370,7 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_run(SmallArgs a) {
   // the lead block's control record and partial slots, as shared::cluster addresses
   const uint32_t r_ctl = remote(&sh.ctl, 0);
   const uint32_t r_rate = remote(&sh.p_rate[rank], 0), r_min_r = remote(&sh.p_min_r[rank], 0),
-                 r_min_e = remote(&sh.p_min_e[rank], 0), r_fail = remote(&sh.p_fail[rank], 0),
-                 r_dtfail = remote(&sh.p_dtfail[rank], 0);
+                 r_min_e = remote(&sh.p_min_e[rank], 0), r_dtfail = remote(&sh.p_dtfail[rank], 0);
   if (lead && tid == 0) sh.ctl = *a.ctl;
   const FK fk = make_fk(a.k.gamma, a.k.gm1, a.k.beta, a.k.dx, a.k.dy);
   double* u = a.u;
@@ -324,6 +378,8 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_run(SmallArgs a) {
   const MaxOp mx;
   const MinOp mn;
   const int ncell = a.nx * a.ny;
+  int pend = -1, pend_par = 0;   // (lead outflow warp) a completed step whose sums are due
+  double pend_dt = 0.0;
   int n = 0;
   for (; n < a.nsteps; ++n) {
     if (tid == 0) {
@@ -331,7 +387,8 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_run(SmallArgs a) {
       sh.min_r = sh.min_e = 0x7ff0000000000000ull;
       sh.fail = sh.dtfail = 0;
     }
-    // (releases the lead's control record of this step and the local resets)
+    // (releases the lead's control record of this step, the local resets and every
+    // global store of the previous step: barrier.cluster arrive.release / wait.acquire)
     cluster.sync();
     StepCtl c;
     {
@@ -348,6 +405,7 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_run(SmallArgs a) {
     if (c.dtfail || !(dt > 0.0)) break;
     const double lam_x = dt / a.k.dx;  // solver.cpp:262-263
     const double lam_y = dt / a.k.dy;
+    const uint32_t rb = remote(sbnd + (n & 1) * a.ob, 0);
     bool bad = false, dtbad = false;
     unsigned long long mr = 0x7ff0000000000000ull, me = 0x7ff0000000000000ull, rk = 0ull;
     // the last stage's cell: positivity (solver.cpp:300-307), minima, and the next
@@ -371,38 +429,47 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_run(SmallArgs a) {
         dtbad = true;
       }
     };
-    // stage 1: U^n -> U* (or U^{n+1} when time_order = 1)
-    for (int t = gtid; t < ncell; t += gthreads) {
-      const int i = t % a.nx, j = t / a.nx;
-      double v[4];
-      cell_stage<DIM2, MUSCL, FAST, false>(a, fk, u, u, i, j, lam_x, lam_y, v, bad);
-      const int64_t o = (int64_t)j * a.pitch + i;
-      double* out = a.heun ? a.us : u2;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) __stcg(out + q * a.fstride + o, v[q]);
-      if (a.heun) {
-        const double eint = internal_energy(v[0], v[1], v[2], v[3]);
-        if (!(v[0] > 0.0) || !(eint > 0.0)) bad = true;
-      } else {
-        finish(v);
-      }
-    }
-    if (a.heun) {
-      __threadfence();
-      cluster.sync();
-      // stage 2: U* -> U^{n+1} from U^n with 0.5 (F^n + F*)
+    if (cellw) {
+      // stage 1: U^n -> U* (or U^{n+1} when time_order = 1)
       for (int t = gtid; t < ncell; t += gthreads) {
         const int i = t % a.nx, j = t / a.nx;
         double v[4];
-        cell_stage<DIM2, MUSCL, FAST, true>(a, fk, a.us, u, i, j, lam_x, lam_y, v, bad);
+        cell_stage<DIM2, MUSCL, FAST, false>(a, fk, u, u, i, j, a.heun ? 0u : rb, lam_x, lam_y, v,
+                                             bad);
         const int64_t o = (int64_t)j * a.pitch + i;
+        double* out = a.heun ? a.us : u2;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) __stcg(u2 + q * a.fstride + o, v[q]);
-        finish(v);
+        for (int q = 0; q < 4; ++q) __stcg(out + q * a.fstride + o, v[q]);
+        if (a.heun) {
+          const double eint = internal_energy(v[0], v[1], v[2], v[3]);
+          if (!(v[0] > 0.0) || !(eint > 0.0)) bad = true;
+        } else {
+          finish(v);
+        }
+      }
+    } else if (lead && pend >= 0) {
+      // the previous step's outflow sums, off the critical path
+      outflow_sums<DIM2>(a, sbnd + pend_par * a.ob, pend_dt);
+      pend = -1;
+    }
+    if (a.heun) {
+      cluster.sync();
+      // stage 2: U* -> U^{n+1} from U^n with 0.5 (F^n + F*)
+      if (cellw) {
+        for (int t = gtid; t < ncell; t += gthreads) {
+          const int i = t % a.nx, j = t / a.nx;
+          double v[4];
+          cell_stage<DIM2, MUSCL, FAST, true>(a, fk, a.us, u, i, j, rb, lam_x, lam_y, v, bad);
+          const int64_t o = (int64_t)j * a.pitch + i;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) __stcg(u2 + q * a.fstride + o, v[q]);
+          finish(v);
+        }
       }
     }
-    // block partials (warp shuffles, then the block's own shared atomics), then one
-    // plain store of each into the lead block's slot for this block
+    // block partials (warp shuffles, then the block's own shared atomics), then plain
+    // stores into the lead block's slot for this block; the failure flag into every
+    // block's slot (each decides alone, after one barrier)
     rk = wred(rk, mx);
     mr = wred(mr, mn);
     me = wred(me, mn);
@@ -419,89 +486,46 @@ __global__ void __launch_bounds__(SMALL_THREADS, 1) k_small_run(SmallArgs a) {
       st_remote(r_rate, sh.rate);
       st_remote(r_min_r, sh.min_r);
       st_remote(r_min_e, sh.min_e);
-      st_remote(r_fail, sh.fail);
       st_remote(r_dtfail, sh.dtfail);
+      for (uint32_t b = 0; b < nblk; ++b) st_remote(remote(&sh.p_fail[rank], b), sh.fail);
     }
-    __threadfence();
     cluster.sync();
-    // every block reads the failure flags (uniform decision, no extra barrier)
     int fail = 0;
-    for (uint32_t b = 0; b < nblk; ++b) fail |= ld_remote_i(remote(&sh.p_fail[b], 0));
+    for (uint32_t b = 0; b < nblk; ++b) fail |= sh.p_fail[b];
     if (fail) break;   // the host re-runs this step stage-wise
-    if (lead) {
-      // accumulate_boundary_outflow (solver.cpp:406-432): the boundary-face
-      // differences (Heun-averaged as k_gather_boundary) staged a tile at a time by
-      // the whole block, then summed in order by lanes 0-3 (x, over the rows) and
-      // 4-7 (y, over the columns) of warp 0
-      const int ex = a.ny, ey = DIM2 ? a.nx : 0;
-      const int len = ex > ey ? ex : ey;
-      double s = 0.0;
-      for (int base = 0; base < len; base += OUT_TILE) {
-#pragma unroll
-        for (int k = tid; k < 8 * OUT_TILE; k += SMALL_THREADS) {
-          const int ch = k / OUT_TILE, e = base + k % OUT_TILE, q = ch & 3;
-          double d = 0.0;
-          if (ch < 4 && e < ex) {
-            const double* fa = a.fx[0] + q * a.fx_stride + (int64_t)e * a.pitch;
-            const double* fb = a.fx[1] + q * a.fx_stride + (int64_t)e * a.pitch;
-            const double left = a.heun ? 0.5 * (__ldcg(fa) + __ldcg(fb)) : __ldcg(fa);
-            const double right =
-                a.heun ? 0.5 * (__ldcg(fa + a.nx) + __ldcg(fb + a.nx)) : __ldcg(fa + a.nx);
-            d = right - left;
-          } else if (ch >= 4 && e < ey) {
-            const double* fa = a.fy[0] + q * a.fy_stride + e;
-            const double* fb = a.fy[1] + q * a.fy_stride + e;
-            const int64_t tp = (int64_t)a.ny * a.pitch;
-            const double bot = a.heun ? 0.5 * (__ldcg(fa) + __ldcg(fb)) : __ldcg(fa);
-            const double top = a.heun ? 0.5 * (__ldcg(fa + tp) + __ldcg(fb + tp)) : __ldcg(fa + tp);
-            d = top - bot;
-          }
-          sh.dif[k % OUT_TILE][ch] = d;
-        }
-        __syncthreads();
-        if (tid < 8) {
-          const int m = min(OUT_TILE, (tid < 4 ? ex : ey) - base);
-          for (int e = 0; e < m; ++e) s += sh.dif[e][tid];
-        }
-        __syncthreads();
+    if (lead && tid == 0) {
+      unsigned long long rt = 0ull, m_r = 0x7ff0000000000000ull, m_e = 0x7ff0000000000000ull;
+      int dtf = 0;
+      for (uint32_t b = 0; b < nblk; ++b) {
+        rt = sh.p_rate[b] > rt ? sh.p_rate[b] : rt;
+        m_r = sh.p_min_r[b] < m_r ? sh.p_min_r[b] : m_r;
+        m_e = sh.p_min_e[b] < m_e ? sh.p_min_e[b] : m_e;
+        dtf |= sh.p_dtfail[b];
       }
-      if (tid < 8) {
-        const int q = tid & 3;
-        const double ax = dt * (DIM2 ? a.k.dy : 1.0), ay = dt * a.k.dx;
-        if (tid < 4) a.outflow[q] += ax * s;
-        __syncwarp(0xffu);
-        if (DIM2 && tid >= 4) a.outflow[q] += ay * s;
-      }
-      if (tid == 0) {
-        unsigned long long rt = 0ull, m_r = 0x7ff0000000000000ull, m_e = 0x7ff0000000000000ull;
-        int dtf = 0;
-        for (uint32_t b = 0; b < nblk; ++b) {
-          rt = sh.p_rate[b] > rt ? sh.p_rate[b] : rt;
-          m_r = sh.p_min_r[b] < m_r ? sh.p_min_r[b] : m_r;
-          m_e = sh.p_min_e[b] < m_e ? sh.p_min_e[b] : m_e;
-          dtf |= sh.p_dtfail[b];
-        }
-        StepRec r;
-        r.dt = dt;
-        r.hits = c.time + dt >= a.limit;
-        r.time = r.hits ? a.limit : c.time + dt;
-        r.min_rho = __longlong_as_double((long long)m_r);
-        r.min_eint = __longlong_as_double((long long)m_e);
-        r.min_p_mat = __longlong_as_double(0x7ff0000000000000ll);
-        r.status = 0;
-        a.rec[n] = r;
-        StepCtl nx_;
-        nx_.time = r.time;
-        nx_.rate_bits = rt;
-        nx_.dtfail = dtf;
-        nx_.done = !(r.time < a.t_final);
-        sh.ctl = nx_;
-      }
+      StepRec r;
+      r.dt = dt;
+      r.hits = c.time + dt >= a.limit;
+      r.time = r.hits ? a.limit : c.time + dt;
+      r.min_rho = __longlong_as_double((long long)m_r);
+      r.min_eint = __longlong_as_double((long long)m_e);
+      r.min_p_mat = __longlong_as_double(0x7ff0000000000000ll);
+      r.status = 0;
+      a.rec[n] = r;
+      StepCtl nx_;
+      nx_.time = r.time;
+      nx_.rate_bits = rt;
+      nx_.dtfail = dtf;
+      nx_.done = !(r.time < a.t_final);
+      sh.ctl = nx_;
     }
+    pend = n;
+    pend_par = n & 1;
+    pend_dt = dt;
     double* t = u;
     u = u2;
     u2 = t;
   }
+  if (lead && !cellw && pend >= 0) outflow_sums<DIM2>(a, sbnd + pend_par * a.ob, pend_dt);
   // the step that stopped the batch: 1 failed (the host re-runs it stage-wise),
   // 2 skipped (limit reached); later steps skipped
   if (lead && tid == 0) {
@@ -532,8 +556,12 @@ cudaError_t launch_small(const SmallArgs& a, int want, bool fast, cudaStream_t s
   auto kern = fast ? k_small_run<DIM2, MUSCL, true> : k_small_run<DIM2, MUSCL, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
+  const size_t smem = 2 * (size_t)a.ob * sizeof(double);
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(SMALL_THREADS);
+  cfg.blockDim = dim3(SMALL_THREADS + 32);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -644,6 +672,7 @@ int run_small(lf_handle* h, int n, double cfl, double limit, double t_final, dou
   a.fy_stride = s.fy_stride;
   a.nx = s.L.nx;
   a.ny = s.L.ny;
+  a.ob = 8 * a.ny + (h->dim2 ? 8 * a.nx : 0);
   a.heun = h->d.time_order >= 2;
   for (int q = 0; q < 4; ++q) a.bc[q] = h->d.bc[q];
   a.k = h->k;
@@ -715,6 +744,8 @@ bool small_supported(lf_handle* h) {
   if (h->mc.n > 0 || h->slabs.size() != 1 || h->nccl) return false;
   // (the kernel reads ghosts through an index map whose sources are interior cells)
   if (h->d.nx < 2 || (h->dim2 && h->d.ny < 2)) return false;
+  // the boundary faces of two steps in the lead block's shared memory (160 KB)
+  if (h->dim2 && h->d.nx + h->d.ny > SMALL_MAX_PERIMETER) return false;
   return (int64_t)h->d.nx * h->d.ny <= SMALL_MAX_CELLS;
 }
 
