@@ -694,7 +694,8 @@ bool use_fused(lf_handle* h) {
   // sweby_limiter as written (reconstruct.hpp:24-30)
   if (!(h->d.beta >= 1.0)) return false;
   // materials: the two-pass material kernels for up to 4 materials, else stage-wise
-  if (h->mc.n > 0 && (h->mc.n > 4 || h->path == LF_PATH_FUSED || !h->partials_ready)) return false;
+  if (h->mc.n > 0 && (h->mc.n > TP_MAX_MATERIALS || h->path == LF_PATH_FUSED || !h->partials_ready))
+    return false;
   // (the fused one-kernel step has no material transport: a slab beyond the
   // two-pass kernels' 32-bit offsets goes stage-wise)
   if (h->mc.n > 0) {
@@ -941,7 +942,7 @@ int lf_set_materials(lf_handle* h, int n, const double* gammas) {
       CK(cudaMemsetAsync(s.P, 0, kb, s.stream));
       CK(cudaMemsetAsync(s.Ps, 0, kb, s.stream));
       CK(cudaMemsetAsync(s.P2, 0, kb, s.stream));
-      if (n <= 4) {  // the two-pass material kernels' stage-a fluxes
+      if (n <= TP_MAX_MATERIALS) {  // the two-pass material kernels' stage-a fluxes
         CK(cudaMalloc(&s.MFX, (size_t)n * s.fx_stride * sizeof(double)));
         CK(cudaMalloc(&s.MFY, (size_t)n * s.fy_stride * sizeof(double)));
         CK(cudaMemsetAsync(s.MFX, 0, (size_t)n * s.fx_stride * sizeof(double), s.stream));

@@ -224,7 +224,7 @@ static void fused_alloc(lf_handle* h, int steps) {
     f->sms = sms;
   }
   // two-pass chunking follows the resident warps of the kernel in use
-  const int nmat = std::min(h->mc.n, 4);
+  const int nmat = std::min(h->mc.n, TP_MAX_MATERIALS);
   if (f->tp_rows_nmat != nmat) {
     int ny_local = 0;
     for (auto& s : h->slabs) ny_local = std::max(ny_local, s.L.ny);

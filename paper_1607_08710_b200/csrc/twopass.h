@@ -13,6 +13,7 @@ namespace lfb {
 #define LF_TP_THREADS 128
 #endif
 constexpr int TP_THREADS = LF_TP_THREADS;   // independent warps per block x 32
+constexpr int TP_MAX_MATERIALS = 8;   // the two-pass material kernels (more: stage-wise)
 
 struct PassArgs {
   const double* x;      // stage input, ghost-filled: U^n (predictor) or U* (corrector)

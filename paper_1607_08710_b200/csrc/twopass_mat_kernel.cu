@@ -67,13 +67,14 @@ constexpr int TXW = LANES - 4;
 __device__ __forceinline__ double shup(double v) { return __shfl_up_sync(FULL, v, 1); }
 __device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(FULL, v, 1); }
 
+
 struct MatK {
   int n;
-  double gamma[4];
+  double gamma[TP_MAX_MATERIALS];
 };
 
 struct MatR {
-  Recip rg[4];   // 1 / (gamma_k - 1.0), shared by every cell
+  Recip rg[TP_MAX_MATERIALS];   // 1 / (gamma_k - 1.0), shared by every cell
 };
 
 // fill_all_ghosts' closure for one cell (solver.cpp:100-121) from the raw
@@ -263,8 +264,10 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
 #if LF_MAT_ASYNC
   // [warp][buffer][operand][lane]: bse 0-3, pbs 4.., fnx, fny, max_, may_
   constexpr int NOP = CORR ? 12 + 3 * K : 4 + K;
-  __shared__ double stage[TP_THREADS / 32][2][NOP][32];
-  double(*const st)[NOP][32] = stage[threadIdx.x >> 5];
+  // (dynamic: 5-8 materials need more than the 48 KB of static shared memory)
+  extern __shared__ __align__(16) double stage_dyn[];
+  double(*const st)[NOP][32] =
+      reinterpret_cast<double(*)[NOP][32]>(stage_dyn + (threadIdx.x >> 5) * 2 * NOP * 32);
   auto issue = [&](int itn, int orow, int buf) {
     const bool pu = itn >= 4 && upd;
 #pragma unroll
@@ -622,29 +625,65 @@ __global__ void __launch_bounds__(TP_THREADS, 2) k_pass_mat(PassArgs a, MatPassA
   }
 }
 
+// the corrector / predictor's operand staging (LF_MAT_ASYNC): [warp][buffer][operand][lane]
+constexpr size_t stage_bytes(bool corr, int k) {
+  return LF_MAT_ASYNC ? sizeof(double) * (TP_THREADS / 32) * 2 * (corr ? 12 + 3 * k : 4 + k) * 32
+                      : 0;
+}
+
+template <bool CORR, bool MUSCL, int K>
+void launch_one(const PassArgs& a, const MatPassArgs& m, const MatK& mk, unsigned blocks,
+                cudaStream_t st) {
+  constexpr size_t smem = stage_bytes(CORR, K);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_pass_mat<CORR, MUSCL, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  launch_chain(k_pass_mat<CORR, MUSCL, K>, dim3(blocks), dim3(TP_THREADS), smem, st, a, m, mk);
+}
+
 template <bool CORR, bool MUSCL>
 void launch_k(const PassArgs& a, const MatPassArgs& m, const MatK& mk, unsigned blocks,
               cudaStream_t st) {
   switch (mk.n) {
-    case 1: launch_chain(k_pass_mat<CORR, MUSCL, 1>, dim3(blocks), dim3(TP_THREADS), 0, st, a, m, mk); break;
-    case 2: launch_chain(k_pass_mat<CORR, MUSCL, 2>, dim3(blocks), dim3(TP_THREADS), 0, st, a, m, mk); break;
-    case 3: launch_chain(k_pass_mat<CORR, MUSCL, 3>, dim3(blocks), dim3(TP_THREADS), 0, st, a, m, mk); break;
-    default: launch_chain(k_pass_mat<CORR, MUSCL, 4>, dim3(blocks), dim3(TP_THREADS), 0, st, a, m, mk); break;
+    case 1: launch_one<CORR, MUSCL, 1>(a, m, mk, blocks, st); break;
+    case 2: launch_one<CORR, MUSCL, 2>(a, m, mk, blocks, st); break;
+    case 3: launch_one<CORR, MUSCL, 3>(a, m, mk, blocks, st); break;
+    case 4: launch_one<CORR, MUSCL, 4>(a, m, mk, blocks, st); break;
+    case 5: launch_one<CORR, MUSCL, 5>(a, m, mk, blocks, st); break;
+    case 6: launch_one<CORR, MUSCL, 6>(a, m, mk, blocks, st); break;
+    case 7: launch_one<CORR, MUSCL, 7>(a, m, mk, blocks, st); break;
+    default: launch_one<CORR, MUSCL, 8>(a, m, mk, blocks, st); break;
   }
+}
+
+template <int K>
+int resident_blocks() {
+  constexpr size_t smem = stage_bytes(true, K);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_pass_mat<true, true, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, K>, TP_THREADS,
+                                                    smem) != cudaSuccess)
+    b = 0;
+  return b;
 }
 
 }  // namespace
 
 int tp_resident_warps_mat(int nmat) {
   int b = 0;
-  cudaError_t e;
   switch (nmat) {
-    case 1: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, 1>, TP_THREADS, 0); break;
-    case 2: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, 2>, TP_THREADS, 0); break;
-    case 3: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, 3>, TP_THREADS, 0); break;
-    default: e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pass_mat<true, true, 4>, TP_THREADS, 0);
+    case 1: b = resident_blocks<1>(); break;
+    case 2: b = resident_blocks<2>(); break;
+    case 3: b = resident_blocks<3>(); break;
+    case 4: b = resident_blocks<4>(); break;
+    case 5: b = resident_blocks<5>(); break;
+    case 6: b = resident_blocks<6>(); break;
+    case 7: b = resident_blocks<7>(); break;
+    default: b = resident_blocks<8>();
   }
-  if (e != cudaSuccess || b < 1) b = 2;
+  if (b < 1) b = 2;
   return b * (TP_THREADS / 32);
 }
 
@@ -652,7 +691,7 @@ void launch_pass_mat(const PassArgs& a, const MatPassArgs& m, const MatConsts& m
                      bool muscl, cudaStream_t st) {
   MatK mk{};
   mk.n = mc.n;
-  for (int k = 0; k < 4; ++k) mk.gamma[k] = k < mc.n ? mc.gamma[k] : 1.5;
+  for (int k = 0; k < TP_MAX_MATERIALS; ++k) mk.gamma[k] = k < mc.n ? mc.gamma[k] : 1.5;
   const int warps = a.strips * ((a.ny + a.rows_per_chunk - 1) / a.rows_per_chunk);
   const unsigned blocks = (unsigned)((warps + TP_THREADS / 32 - 1) / (TP_THREADS / 32));
   count_launch();

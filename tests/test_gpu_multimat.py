@@ -179,3 +179,71 @@ def test_device_region_init_errors(cuda):
         CS.regions_field(CS.MatCase(c.name, c.grid, c.bc, c.gamma, c.material_gammas, tuple(bad),
                                     c.params, c.cfl, c.t_final, c.max_steps))
     assert str(e1.value) == str(e2.value)
+
+
+def _many_materials_case(n_mat, space=2, time=2):
+    """n_mat materials in a 4 x 2 tiling of regions (two reuse a material when n_mat < 8),
+    shearing contacts and pressure jumps -- mixed cells of up to four materials appear
+    within a few steps."""
+    g = G.make_grid_2d(64, 40, 0.0, 1.0, 0.0, 0.625)
+    rng = np.random.default_rng(5_000 + n_mat)
+    gammas = tuple(float(x) for x in rng.uniform(1.2, 2.2, n_mat))
+    regions = []
+    for a in range(4):
+        for b in range(2):
+            m = (2 * a + b) % n_mat + 1
+            regions.append(CS.Region(a / 4, (a + 1) / 4, b * 0.3125, (b + 1) * 0.3125,
+                                     float(rng.uniform(0.3, 2.0)), float(rng.uniform(-0.6, 0.6)),
+                                     float(rng.uniform(-0.6, 0.6)), float(rng.uniform(0.2, 2.0)), m))
+    return CS.MatCase(f"mm_{n_mat}mat", g, G.BoundaryCondition(G.REFLECTIVE, G.TRANSMISSIVE,
+                                                                G.PERIODIC, G.PERIODIC),
+                      1.4, gammas, tuple(regions), G.SchemeParams(spatial_order=space, time_order=time),
+                      0.4, 1e30, 12)
+
+
+@pytest.mark.parametrize("n_mat", [5, 6, 7, 8])
+@pytest.mark.parametrize("devices", [(0,), (0, 0)])
+def test_five_to_eight_materials_on_the_two_pass_kernels(cuda, n_mat, devices):
+    """More than four materials run the two-pass material kernels (up to 8; more go
+    stage-wise) with the oracle's bits."""
+    c = _many_materials_case(n_mat)
+    f0, m0 = CS.regions_field(c)
+    s = LagfluxSolver(c.grid, c.bc, c.gamma, c.params,
+                      materials=MM.make_material_set(c.material_gammas), devices=devices)
+    st = G.SolverState(field=f0.copy())
+    s.heun_step(st, G.TimeControls(c.cfl, c.t_final), c.t_final,
+                MM.MaterialCells(c.grid, n_mat, m0.partial.copy()))
+    assert s.resolved_path() == "twopass"   # (once the partial densities are resident)
+    s.close()
+    ref, rmat = run_oracle_mat(c)
+    for use_advance in (False, True):
+        state, mat = run_gpu_mat(c, devices=devices, use_advance=use_advance)
+        g = c.grid
+        what = f"{n_mat} materials, {len(devices)} slab(s), advance={use_advance}"
+        assert_fields_equal(g.interior(state.field), g.interior(ref.field), what)
+        assert_fields_equal(g.interior(mat.partial), g.interior(rmat.partial), what + "/partials")
+        assert np.array_equal(diag_array(state)[:, :4], diag_array(ref)[:, :4]), what
+        assert np.array_equal(np.array(state.boundary_outflow), np.array(ref.boundary_outflow))
+
+
+@pytest.mark.parametrize("space,time", [(1, 2), (2, 1)])
+def test_eight_materials_other_orders(cuda, space, time):
+    c = _many_materials_case(8, space, time)
+    ref, rmat = run_oracle_mat(c)
+    state, mat = run_gpu_mat(c, use_advance=True)
+    g = c.grid
+    assert_fields_equal(g.interior(state.field), g.interior(ref.field), f"{space}/{time}")
+    assert_fields_equal(g.interior(mat.partial), g.interior(rmat.partial), f"{space}/{time}")
+
+
+def test_nine_materials_go_stage_wise(cuda):
+    c = _many_materials_case(8)
+    c = CS.MatCase(c.name, c.grid, c.bc, c.gamma, c.material_gammas + (1.6,), c.regions, c.params,
+                   c.cfl, c.t_final, 3)
+    f0, m0 = CS.regions_field(c)
+    s = LagfluxSolver(c.grid, c.bc, c.gamma, c.params,
+                      materials=MM.make_material_set(c.material_gammas))
+    st = G.SolverState(field=f0.copy())
+    s.heun_step(st, G.TimeControls(c.cfl, c.t_final), c.t_final, MM.MaterialCells(c.grid, 9, m0.partial.copy()))
+    assert s.resolved_path() == "staged"
+    s.close()
