@@ -70,10 +70,10 @@ enum {
  *            scratch does not fit in device memory.  lf_resolved_path reports the choice.
  *   FUSED    one kernel per step (U^n read once, U^{n+1} written once)
  *   STAGED   the reference's phase structure, one kernel per loop (also the
- *            exact diagnosis path for every failure, euler_stage and more than 4
- *            materials)
+ *            exact diagnosis path for every failure, euler_stage, 1D grids with
+ *            materials and more than 8 materials)
  *   TWOPASS  predictor and corrector as two warp-independent streaming kernels
- *            (1-4 materials included)
+ *            (1-8 materials included)
  *   SMALL    a whole lf_advance batch (up to 4096 steps) in one launch of one thread-block
  *            cluster (up to 16 blocks): one material, one slab, nx >= 2 (and ny >= 2 in
  *            2D), up to 2^22 cells; the stage-wise arithmetic's bits */
@@ -162,7 +162,7 @@ int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghost
  * mixed-cell gamma of each cell (each face side its own EOS), reports a fraction
  * outside [0,1] beyond round-off as LF_ERR_FRACTION, and returns the min
  * pressure from the fresh partials.  The two-pass material kernels run these
- * steps for 1-4 materials in 2D, the stage-wise kernels otherwise (1D, > 4).
+ * steps for 1-8 materials in 2D, the stage-wise kernels otherwise (1D, > 8).
  * Partials: n arrays in the ghosted field layout (partials[k][j*ld + i],
  * ld >= nx + 4); interior cells are transferred. */
 int lf_set_materials(lf_handle* h, int n, const double* gammas);

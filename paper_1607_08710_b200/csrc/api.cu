@@ -693,7 +693,7 @@ bool use_fused(lf_handle* h) {
   // LimiterParams): other betas run the stage-wise kernels, which evaluate
   // sweby_limiter as written (reconstruct.hpp:24-30)
   if (!(h->d.beta >= 1.0)) return false;
-  // materials: the two-pass material kernels for up to 4 materials, else stage-wise
+  // materials: the two-pass material kernels for up to 8 materials, else stage-wise
   if (h->mc.n > 0 && (h->mc.n > TP_MAX_MATERIALS || h->path == LF_PATH_FUSED || !h->partials_ready))
     return false;
   // (the fused one-kernel step has no material transport: a slab beyond the
