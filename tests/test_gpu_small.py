@@ -65,7 +65,7 @@ def test_auto_picks_the_small_path_where_it_is_faster(cuda):
     s.close()
 
 
-# cells per grid: 1 block (256 threads) .. 16 blocks .. beyond (strided cells)
+# cells per grid: 1 block (224 cell threads) .. 16 blocks .. beyond (strided cells)
 @pytest.mark.parametrize("nx,ny", [(12, 9), (40, 13), (64, 56), (128, 32), (160, 40), (300, 37)])
 def test_cluster_sizes_equal_oracle(cuda, nx, ny):
     g = G.make_grid_2d(nx, ny, 0.0, 1.0, 0.0, ny / nx)
@@ -129,3 +129,26 @@ def test_out_of_box_cell_switches_to_ieee_and_stays_exact(cuda):
         st = _run(base, 6, advance=advance, field=f)
         assert_fields_equal(g.interior(st.field), g.interior(ref.field), f"advance={advance}")
         assert np.array_equal(diag_array(st)[:, :4], rdiag[:, :4])
+
+
+@pytest.mark.parametrize("nx,ny", [(2, 2), (2, 3), (3, 2), (3, 5), (5, 3)])
+@pytest.mark.parametrize("bc", [(G.REFLECTIVE, G.PERIODIC), (G.PERIODIC, G.TRANSMISSIVE),
+                                (G.TRANSMISSIVE, G.REFLECTIVE)])
+def test_tiny_grids_ghost_map(cuda, nx, ny, bc):
+    """Grids of 2-5 cells per axis: every ghost of the first two layers maps to an
+    interior cell (periodic wrap, reflective images of the far cells)."""
+    xb = (bc[0], bc[0])
+    yb = (bc[1], bc[1]) if bc[1] == G.PERIODIC else (bc[1], G.TRANSMISSIVE)
+    g = G.make_grid_2d(nx, ny, 0.0, 1.0, 0.0, 1.0)
+    case = CS.Case("q", g, G.BoundaryCondition(xb[0], xb[1], yb[0], yb[1]), 1.4, G.SchemeParams(),
+                   0.3, CS.STEP_DRIVEN_LIMIT, 8, "quadrant")
+    _check(case, 8, _run(case, 8), f"{nx}x{ny} {bc}")
+
+
+@pytest.mark.parametrize("nx", [2, 3])
+@pytest.mark.parametrize("bc", [G.TRANSMISSIVE, G.REFLECTIVE, G.PERIODIC])
+def test_tiny_1d_grids(cuda, nx, bc):
+    g = G.make_grid_1d(nx, 0.0, 1.0)
+    case = CS.Case("s", g, G.BoundaryCondition(bc, bc), 1.4, G.SchemeParams(), 0.3,
+                   CS.STEP_DRIVEN_LIMIT, 8, "riemann_x")
+    _check(case, 8, _run(case, 8), f"1D {nx} {bc}")
