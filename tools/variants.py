@@ -26,9 +26,7 @@ CSRC = os.path.join(ROOT, "paper_1607_08710_b200", "csrc")
 # against the first variant of the same arithmetic)
 VARIANTS = {
     "f": ("", 1),
-    "f_defer": ("-DLF_FUSED_EPI_DEFER=1", 1),
-    "c_f": ("", 1, 1),
-    "c_f_defer": ("-DLF_FUSED_EPI_DEFER=1", 1, 1),
+    "f_intmm": ("-DLF_INTMINMAX=1", 1),
 }
 
 
