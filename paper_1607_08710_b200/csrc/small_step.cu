@@ -10,10 +10,11 @@
 // primitives of its cross stencil (ghosts read through an index map of the
 // reference's fill, so no fill phase), its four faces and its update (a face is
 // solved by both of its cells, the same bits twice; the lower one stores it for
-// the Heun average and the outflow).  A step is three cluster barriers; the
-// blocks' partial reductions go to the lead block by plain shared::cluster stores
-// (no remote atomics), which also keeps dt / time / the step records and runs the
-// ordered boundary-outflow sums; the state ping-pongs between U and U2, and data
+// the Heun average and the outflow).  A Heun step is two cluster barriers: the
+// blocks' partial reductions are broadcast to every block by plain shared::cluster
+// stores (no remote atomics) and every block derives the next dt / time itself; the
+// lead block writes the step records and runs the ordered boundary-outflow sums;
+// the state ping-pongs between U and U2, and data
 // another block wrote is read through L2 (ld.global.cg after the barrier's
 // release / acquire).
 //
@@ -80,12 +81,14 @@ constexpr int SMALL_MAX_CTAS = 16;
 // control record and every block's partials (written there by plain
 // shared::cluster stores -- no remote atomics), and the outflow staging tile.
 struct SmallShared {
-  StepCtl ctl;
-  unsigned long long rate, min_r, min_e;   // this block's
-  int fail, dtfail;
-  // p_fail: every block's failure flag, in every block; the other p_*: in the lead
-  unsigned long long p_rate[SMALL_MAX_CTAS], p_min_r[SMALL_MAX_CTAS], p_min_e[SMALL_MAX_CTAS];
-  int p_fail[SMALL_MAX_CTAS], p_dtfail[SMALL_MAX_CTAS];
+  StepCtl ctl;                             // this block's copy (every block computes it)
+  unsigned long long rate, min_r, min_e;   // this block's partials
+  int fail, dtfail, stop;
+  // every block's partials, in every block, by step parity (a fast block's next step
+  // must not overwrite a slot a slow block has not read)
+  unsigned long long p_rate[2][SMALL_MAX_CTAS], p_min_r[2][SMALL_MAX_CTAS],
+      p_min_e[2][SMALL_MAX_CTAS];
+  int p_fail[2][SMALL_MAX_CTAS], p_dtfail[2][SMALL_MAX_CTAS];
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -105,11 +108,6 @@ __device__ __forceinline__ void st_remote_d(uint32_t a, double v) {
 }
 __device__ __forceinline__ void st_remote(uint32_t a, int v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_remote_u64(uint32_t a) {
-  unsigned long long v;
-  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
-  return v;
 }
 
 template <class Op>
@@ -367,11 +365,7 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
   const bool lead = rank == 0;
   const int gtid = (int)rank * SMALL_THREADS + tid;
   const int gthreads = (int)nblk * SMALL_THREADS;
-  // the lead block's control record and partial slots, as shared::cluster addresses
-  const uint32_t r_ctl = remote(&sh.ctl, 0);
-  const uint32_t r_rate = remote(&sh.p_rate[rank], 0), r_min_r = remote(&sh.p_min_r[rank], 0),
-                 r_min_e = remote(&sh.p_min_e[rank], 0), r_dtfail = remote(&sh.p_dtfail[rank], 0);
-  if (lead && tid == 0) sh.ctl = *a.ctl;
+  if (tid == 0) sh.ctl = *a.ctl;
   const FK fk = make_fk(a.k.gamma, a.k.gm1, a.k.beta, a.k.dx, a.k.dy);
   double* u = a.u;
   double* u2 = a.u2;
@@ -387,16 +381,8 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       sh.min_r = sh.min_e = 0x7ff0000000000000ull;
       sh.fail = sh.dtfail = 0;
     }
-    // (releases the lead's control record of this step, the local resets and every
-    // global store of the previous step: barrier.cluster arrive.release / wait.acquire)
-    cluster.sync();
-    StepCtl c;
-    {
-      unsigned long long w[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) w[q] = ld_remote_u64(r_ctl + 8 * q);
-      memcpy(&c, w, sizeof c);
-    }
+    __syncthreads();   // (this block's control record of the step, the resets)
+    const StepCtl c = sh.ctl;
     if (c.done) break;
     // compute_dt's tail (solver.cpp:471-479) from the rate of the input state
     const double rate = __longlong_as_double((long long)c.rate_bits);
@@ -405,7 +391,8 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
     if (c.dtfail || !(dt > 0.0)) break;
     const double lam_x = dt / a.k.dx;  // solver.cpp:262-263
     const double lam_y = dt / a.k.dy;
-    const uint32_t rb = remote(sbnd + (n & 1) * a.ob, 0);
+    const int par = n & 1;
+    const uint32_t rb = remote(sbnd + par * a.ob, 0);
     bool bad = false, dtbad = false;
     unsigned long long mr = 0x7ff0000000000000ull, me = 0x7ff0000000000000ull, rk = 0ull;
     // the last stage's cell: positivity (solver.cpp:300-307), minima, and the next
@@ -453,6 +440,7 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       pend = -1;
     }
     if (a.heun) {
+      // (releases U* and the stage-1 faces: barrier.cluster arrive.release / wait.acquire)
       cluster.sync();
       // stage 2: U* -> U^{n+1} from U^n with 0.5 (F^n + F*)
       if (cellw) {
@@ -467,9 +455,9 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
         }
       }
     }
-    // block partials (warp shuffles, then the block's own shared atomics), then plain
-    // stores into the lead block's slot for this block; the failure flag into every
-    // block's slot (each decides alone, after one barrier)
+    // block partials (warp shuffles, then the block's own shared atomics), broadcast by
+    // plain shared::cluster stores into every block's slot for this block: after one
+    // barrier every block reduces them itself (no second barrier for a control record)
     rk = wred(rk, mx);
     mr = wred(mr, mn);
     me = wred(me, mn);
@@ -482,44 +470,48 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       if (wdt) sh.dtfail = 1;
     }
     __syncthreads();
-    if (tid == 0) {
-      st_remote(r_rate, sh.rate);
-      st_remote(r_min_r, sh.min_r);
-      st_remote(r_min_e, sh.min_e);
-      st_remote(r_dtfail, sh.dtfail);
-      for (uint32_t b = 0; b < nblk; ++b) st_remote(remote(&sh.p_fail[rank], b), sh.fail);
+    if (tid < nblk) {   // one thread per destination block
+      st_remote(remote(&sh.p_rate[par][rank], tid), sh.rate);
+      st_remote(remote(&sh.p_min_r[par][rank], tid), sh.min_r);
+      st_remote(remote(&sh.p_min_e[par][rank], tid), sh.min_e);
+      st_remote(remote(&sh.p_fail[par][rank], tid), sh.fail);
+      st_remote(remote(&sh.p_dtfail[par][rank], tid), sh.dtfail);
     }
+    // (releases U^{n+1}, the boundary faces and the partials)
     cluster.sync();
-    int fail = 0;
-    for (uint32_t b = 0; b < nblk; ++b) fail |= sh.p_fail[b];
-    if (fail) break;   // the host re-runs this step stage-wise
-    if (lead && tid == 0) {
+    if (tid == 0) {
       unsigned long long rt = 0ull, m_r = 0x7ff0000000000000ull, m_e = 0x7ff0000000000000ull;
-      int dtf = 0;
+      int fail = 0, dtf = 0;
       for (uint32_t b = 0; b < nblk; ++b) {
-        rt = sh.p_rate[b] > rt ? sh.p_rate[b] : rt;
-        m_r = sh.p_min_r[b] < m_r ? sh.p_min_r[b] : m_r;
-        m_e = sh.p_min_e[b] < m_e ? sh.p_min_e[b] : m_e;
-        dtf |= sh.p_dtfail[b];
+        rt = sh.p_rate[par][b] > rt ? sh.p_rate[par][b] : rt;
+        m_r = sh.p_min_r[par][b] < m_r ? sh.p_min_r[par][b] : m_r;
+        m_e = sh.p_min_e[par][b] < m_e ? sh.p_min_e[par][b] : m_e;
+        fail |= sh.p_fail[par][b];
+        dtf |= sh.p_dtfail[par][b];
       }
-      StepRec r;
-      r.dt = dt;
-      r.hits = c.time + dt >= a.limit;
-      r.time = r.hits ? a.limit : c.time + dt;
-      r.min_rho = __longlong_as_double((long long)m_r);
-      r.min_eint = __longlong_as_double((long long)m_e);
-      r.min_p_mat = __longlong_as_double(0x7ff0000000000000ll);
-      r.status = 0;
-      a.rec[n] = r;
-      StepCtl nx_;
-      nx_.time = r.time;
-      nx_.rate_bits = rt;
-      nx_.dtfail = dtf;
-      nx_.done = !(r.time < a.t_final);
-      sh.ctl = nx_;
+      sh.stop = fail;
+      if (!fail) {
+        StepRec r;
+        r.dt = dt;
+        r.hits = c.time + dt >= a.limit;
+        r.time = r.hits ? a.limit : c.time + dt;
+        r.min_rho = __longlong_as_double((long long)m_r);
+        r.min_eint = __longlong_as_double((long long)m_e);
+        r.min_p_mat = __longlong_as_double(0x7ff0000000000000ll);
+        r.status = 0;
+        if (lead) a.rec[n] = r;
+        StepCtl nx_;
+        nx_.time = r.time;
+        nx_.rate_bits = rt;
+        nx_.dtfail = dtf;
+        nx_.done = !(r.time < a.t_final);
+        sh.ctl = nx_;
+      }
     }
+    __syncthreads();
+    if (sh.stop) break;   // the host re-runs this step stage-wise
     pend = n;
-    pend_par = n & 1;
+    pend_par = par;
     pend_dt = dt;
     double* t = u;
     u = u2;
