@@ -571,7 +571,16 @@ cudaError_t launch_small(const SmallArgs& a, int want, bool fast, cudaStream_t s
     cfg.gridDim = dim3(ncta);
     at[0].val.clusterDim.x = ncta;
   }
-  return cudaLaunchKernelEx(&cfg, kern, a);
+  // (a device shared with other work may not co-schedule the whole cluster at launch
+  // time: halve it until it fits -- the kernel strides its cells over any block count)
+  for (;;) {
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+    if (e != cudaErrorClusterOutOfResources || ncta == 1) return e;
+    (void)cudaGetLastError();
+    ncta = (ncta + 1) / 2;
+    cfg.gridDim = dim3(ncta);
+    at[0].val.clusterDim.x = ncta;
+  }
 }
 
 }  // namespace
