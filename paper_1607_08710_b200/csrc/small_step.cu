@@ -575,7 +575,8 @@ cudaError_t launch_small(const SmallArgs& a, int want, bool fast, cudaStream_t s
   // time: halve it until it fits -- the kernel strides its cells over any block count)
   for (;;) {
     e = cudaLaunchKernelEx(&cfg, kern, a);
-    if (e != cudaErrorClusterOutOfResources || ncta == 1) return e;
+    if ((e != cudaErrorInvalidClusterSize && e != cudaErrorLaunchOutOfResources) || ncta == 1)
+      return e;
     (void)cudaGetLastError();
     ncta = (ncta + 1) / 2;
     cfg.gridDim = dim3(ncta);
