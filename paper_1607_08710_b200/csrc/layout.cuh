@@ -45,6 +45,34 @@ struct Layout {
   __host__ __device__ int64_t off(int i, int j) const { return (int64_t)j * pitch + i; }
 };
 
+// The ghost fill (grid.cpp:72-114) as an index map: ghost layer l of a side of n
+// cells reads cell src of the same row / column (n >= l: every source is interior);
+// flip: a reflective image, times -1 in the normal momentum.  A corner is the y image
+// of the x image (k_fill_xy's composition; multiplying by -1 is exact, so the order
+// of the two does not matter).  bc: 0 transmissive, 1 reflective, 2 periodic.
+__host__ __device__ inline int ghost_src(int i, int n, int lo, int hi, bool& flip) {
+  flip = false;
+  if (i < 0) {
+    const int l = -i;
+    if (lo == 0) return 0;
+    if (lo == 1) {
+      flip = true;
+      return l - 1;
+    }
+    return n - l;
+  }
+  if (i >= n) {
+    const int l = i - n + 1;
+    if (hi == 0) return n - 1;
+    if (hi == 1) {
+      flip = true;
+      return n - l;
+    }
+    return l - 1;
+  }
+  return i;
+}
+
 // A field: pointer to (component 0, i = 0, j = 0) plus the layout strides.
 struct Field {
   double* p;

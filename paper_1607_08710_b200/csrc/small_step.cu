@@ -116,42 +116,15 @@ __device__ __forceinline__ unsigned long long wred(unsigned long long v, Op op) 
   return v;
 }
 
-// The ghost fill (grid.cpp:72-114) as an index map: ghost layer l <= 2 of a side
-// reads interior cell src (n >= 2: every source of the first two layers is
-// interior), a reflective image times -1 in the normal momentum; a corner is the y
-// image of the x image (k_fill_xy's composition; a multiplication by +-1 is exact,
-// so the order does not matter).
-__device__ __forceinline__ int img(int i, int n, int lo, int hi, bool& flip) {
-  flip = false;
-  if (i < 0) {
-    const int l = -i;
-    if (lo == 0) return 0;
-    if (lo == 1) {
-      flip = true;
-      return l - 1;
-    }
-    return n - l;
-  }
-  if (i >= n) {
-    const int l = i - n + 1;
-    if (hi == 0) return n - 1;
-    if (hi == 1) {
-      flip = true;
-      return n - l;
-    }
-    return l - 1;
-  }
-  return i;
-}
-
 // build_primitives (solver.cpp:145-170) of cell (i, j) of the ghosted grid, read
 // through the ghost map; bad |= the reference's check
 template <bool DIM2, bool FAST>
 __device__ __forceinline__ void cell_prims(const SmallArgs& a, const double* f, int i, int j,
                                            double w[4], bool& bad) {
   bool fx, fy = false;
-  const int is = img(i, a.nx, a.bc[0], a.bc[1], fx);
-  const int js = DIM2 ? img(j, a.ny, a.bc[2], a.bc[3], fy) : 0;
+  // (the ghost fill as an index map, layout.cuh: no fill phase)
+  const int is = ghost_src(i, a.nx, a.bc[0], a.bc[1], fx);
+  const int js = DIM2 ? ghost_src(j, a.ny, a.bc[2], a.bc[3], fy) : 0;
   const int64_t o = (int64_t)js * a.pitch + is;
   const double r = __ldcg(f + o);
   double mx = __ldcg(f + a.fstride + o), my = __ldcg(f + 2 * a.fstride + o);
