@@ -63,8 +63,8 @@ enum {
 };
 
 /* Heun-step implementation for lf_heun_step / lf_advance (all give identical results):
- *   AUTO     SMALL for one-material grids of up to 2^14 cells (2D) / 2^17 cells (1D) on
- *            one device (BASELINE config 1, 1D runs); FUSED for slabs of 2^23 cells or more
+ *   AUTO     SMALL for one-material grids of up to 2^17 cells in 2D and every 1D grid (up
+ *            to 2^22 cells) on one device (BASELINE config 1); FUSED for slabs of 2^23 cells or more
  *            (2^22 in LF_MATH_CONTRACT; Heun, no materials: BASELINE configs 3-5), TWOPASS
  *            in between, for time_order 1 and for materials; FUSED also when the two-pass
  *            scratch does not fit in device memory.  lf_resolved_path reports the choice.
@@ -75,8 +75,9 @@ enum {
  *   TWOPASS  predictor and corrector as two warp-independent streaming kernels
  *            (1-8 materials included)
  *   SMALL    a whole lf_advance batch (up to 4096 steps) in one launch of one thread-block
- *            cluster (up to 16 blocks): one material, one slab, nx >= 2 (and ny >= 2 in
- *            2D), up to 2^22 cells; the stage-wise arithmetic's bits */
+ *            cluster (up to 16 blocks), or of one cooperative grid beyond 16 x 224 cells
+ *            (batches of 256 steps): one material, one slab, nx >= 2 (and ny >= 2 in 2D),
+ *            up to 2^22 cells; the reference's bits */
 enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2, LF_PATH_TWOPASS = 3,
        LF_PATH_SMALL = 4 };
 /* Arithmetic of the fast kernels (two-pass and fused).  LF_MATH_EXACT (default): the

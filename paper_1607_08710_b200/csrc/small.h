@@ -8,15 +8,19 @@
 
 namespace lfb {
 
-// LF_PATH_SMALL accepts grids up to this size (one cluster of at most 16 blocks;
-// beyond it the other paths are faster by far); LF_PATH_AUTO takes it up to the
-// measured crossovers (tools/small_sweep.py, profiles/r02_small_sweep.json: 2D 128^2
-// 56 vs 62 us per step on the two-pass kernels, 256^2 196 vs 63; 1D 65536 cells 97 us).
+// LF_PATH_SMALL accepts grids up to this size; LF_PATH_AUTO takes it up to the measured
+// crossovers (tools/small_sweep.py, profiles/r02_small_sweep.json): in 2D against the
+// two-pass kernels (2^17 cells: 51 vs 64 us per step; 512^2: 95 vs 74), in 1D always
+// (the stage-wise kernels: 2.4 ms per step at 2^18 cells against 52 us).  Up to one
+// cluster's worth of cells (16 x 224) the path runs as one thread-block cluster, beyond
+// it as a cooperative grid of one block per SM (small_step.cu).
 constexpr int64_t SMALL_MAX_CELLS = (int64_t)1 << 22;
-constexpr int64_t SMALL_AUTO_CELLS_1D = (int64_t)1 << 17;
-constexpr int64_t SMALL_AUTO_CELLS_2D = (int64_t)1 << 14;
+constexpr int64_t SMALL_AUTO_CELLS_1D = SMALL_MAX_CELLS;
+constexpr int64_t SMALL_AUTO_CELLS_2D = (int64_t)1 << 17;
 constexpr int SMALL_BATCH = 4096;   // steps per launch of lf_advance
-constexpr int SMALL_MAX_PERIMETER = 1280;   // 2D: nx + ny (boundary faces in shared memory)
+constexpr int SMALL_GRID_BATCH = 256;   // grid mode (its boundary-face history per step)
+constexpr int SMALL_MAX_PERIMETER = 1280;   // cluster mode, 2D: nx + ny (boundary faces
+                                            // of two steps in shared memory, 160 KB)
 
 bool small_supported(lf_handle* h);
 bool prefer_small(lf_handle* h);

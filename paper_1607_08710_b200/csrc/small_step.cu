@@ -1,5 +1,6 @@
 // small_step.cu -- LF_PATH_SMALL: the whole step loop of a small grid in one
-// persistent thread-block cluster (1D grids and small 2D grids, one material).
+// persistent thread-block cluster (1D grids and small 2D grids, one material), or --
+// beyond one cluster's worth of cells -- one persistent cooperative grid.
 //
 // A grid of a few thousand cells cannot fill a B200: the stage-wise step is a
 // dozen launches and three host round trips (~110 us), the two-pass step five
@@ -26,6 +27,12 @@
 // the host re-runs it with the stage-wise kernels, which report the reference's
 // exact error (a box failure whose re-run succeeds switches the handle to the IEEE
 // arithmetic until the next upload).
+//
+// Grid mode (more than 16 x 224 cells, or a perimeter whose boundary faces do not fit
+// in shared memory): a cooperative launch of up to one block per SM, grid barriers
+// instead of cluster barriers, the block partials through global memory (every block
+// combines them), and every step's boundary faces into a history buffer whose ordered
+// outflow sums run after the batch (k_small_sums, then k_small_accum in step order).
 //
 // Reference: solver.cpp:489-546 (heun_step), 482-487 (time_order 1 stage),
 // 131-329 (the phases), 406-432 (outflow), 434-480 (dt); grid.cpp:72-114 (fill).
@@ -73,9 +80,14 @@ struct SmallArgs {
   StepRec* rec;      // [nsteps]
   double* outflow;   // [4], accumulated in place
   int nsteps;
+  // grid mode (a cooperative grid of up to one block per SM, beyond one cluster):
+  unsigned long long* gpart;   // [2 parities][5 fields][SMALL_MAX_GRID] block partials
+  double* bhist;               // [nsteps][ob] every step's boundary faces (summed after
+                               // the kernel, k_small_sums / k_small_accum)
 };
 
-constexpr int SMALL_MAX_CTAS = 16;
+constexpr int SMALL_MAX_CTAS = 16;     // one cluster (non-portable maximum)
+constexpr int SMALL_MAX_GRID = 1024;   // grid mode: blocks (one per SM in practice)
 
 // Per block: its own partial reductions; in the lead block (rank 0) also the
 // control record and every block's partials (written there by plain
@@ -84,6 +96,8 @@ struct SmallShared {
   StepCtl ctl;                             // this block's copy (every block computes it)
   unsigned long long rate, min_r, min_e;   // this block's partials
   int fail, dtfail, stop;
+  unsigned long long g_rate, g_min_r, g_min_e;   // grid mode: the combined partials
+  int g_fail, g_dtfail;
   // every block's partials, in every block, by step parity (a fast block's next step
   // must not overwrite a slot a slow block has not read)
   unsigned long long p_rate[2][SMALL_MAX_CTAS], p_min_r[2][SMALL_MAX_CTAS],
@@ -221,7 +235,17 @@ __device__ __forceinline__ void cell_faces(const SmallArgs& a, const FK& fk,
 template <bool DIM2, bool MUSCL, bool FAST, bool TWO>
 __device__ __forceinline__ void cell_stage(const SmallArgs& a, const FK& fk, const double* in,
                                            const double* base, int i, int j, uint32_t rb,
-                                           double lam_x, double lam_y, double vals[4], bool& bad) {
+                                           double* gb, double lam_x, double lam_y, double vals[4],
+                                           bool& bad) {
+  // the step's domain-boundary faces (Heun-averaged as k_gather_boundary) into its
+  // boundary block [left 4 ny | right 4 ny | bottom 4 nx | top 4 nx]: the lead block's
+  // shared memory (cluster) or the step's slot of the history (grid)
+  auto put = [&](int idx, double v) {
+    if (rb)
+      st_remote_d(rb + 8u * idx, v);
+    else
+      __stcg(gb + idx, v);
+  };
   const int64_t o = (int64_t)j * a.pitch + i;   // (cells and low faces share offsets)
   // the operands that do not depend on this stage's faces, loaded first
   double u0[4], fnl[4], fnr[4], fnb[4], fnt[4];
@@ -279,16 +303,14 @@ __device__ __forceinline__ void cell_stage(const SmallArgs& a, const FK& fk, con
         t = 0.5 * (fnt[c] + t);
       }
       val -= lam_y * (t - b);
-      // the step's domain-boundary faces (Heun-averaged as k_gather_boundary) into the
-      // lead block's boundary block: [left 4 ny | right 4 ny | bottom 4 nx | top 4 nx]
-      if (rb) {
-        if (j == 0) st_remote_d(rb + 8u * (8 * a.ny + c * a.nx + i), b);
-        if (j == a.ny - 1) st_remote_d(rb + 8u * (8 * a.ny + 4 * a.nx + c * a.nx + i), t);
+      if (rb || gb) {
+        if (j == 0) put(8 * a.ny + c * a.nx + i, b);
+        if (j == a.ny - 1) put(8 * a.ny + 4 * a.nx + c * a.nx + i, t);
       }
     }
-    if (rb) {
-      if (i == 0) st_remote_d(rb + 8u * (c * a.ny + j), l);
-      if (i == a.nx - 1) st_remote_d(rb + 8u * (4 * a.ny + c * a.ny + j), r);
+    if (rb || gb) {
+      if (i == 0) put(c * a.ny + j, l);
+      if (i == a.nx - 1) put(4 * a.ny + c * a.ny + j, r);
     }
     vals[c] = val;
   }
@@ -323,18 +345,26 @@ __device__ void outflow_sums(const SmallArgs& a, const double* sb, double dt) {
   __syncwarp();
 }
 
-template <bool DIM2, bool MUSCL, bool FAST>
+template <bool DIM2, bool MUSCL, bool FAST, bool GRID>
 __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a) {
   namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
   __shared__ SmallShared sh;
+  // GRID: a cooperative grid (one block per SM) synchronised by grid barriers; else one
+  // cluster synchronised by barrier.cluster (both release / acquire the global stores)
+  auto sync_all = [&]() {
+    if constexpr (GRID)
+      cg::this_grid().sync();
+    else
+      cg::this_cluster().sync();
+  };
   // two boundary blocks (step parity): a step's boundary faces, stored by the cells
   // that own them in its last stage, summed by the lead's outflow warp during the
   // next step's first stage
   extern __shared__ double sbnd[];
   const int tid = threadIdx.x;
   const bool cellw = tid < SMALL_THREADS;   // cell warps; the last warp sums the outflow
-  const uint32_t rank = cluster.block_rank(), nblk = cluster.num_blocks();
+  const uint32_t rank = GRID ? blockIdx.x : cg::this_cluster().block_rank();
+  const uint32_t nblk = GRID ? gridDim.x : cg::this_cluster().num_blocks();
   const bool lead = rank == 0;
   const int gtid = (int)rank * SMALL_THREADS + tid;
   const int gthreads = (int)nblk * SMALL_THREADS;
@@ -353,6 +383,9 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       sh.rate = 0ull;
       sh.min_r = sh.min_e = 0x7ff0000000000000ull;
       sh.fail = sh.dtfail = 0;
+      sh.g_rate = 0ull;
+      sh.g_min_r = sh.g_min_e = 0x7ff0000000000000ull;
+      sh.g_fail = sh.g_dtfail = 0;
     }
     __syncthreads();   // (this block's control record of the step, the resets)
     const StepCtl c = sh.ctl;
@@ -365,7 +398,8 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
     const double lam_x = dt / a.k.dx;  // solver.cpp:262-263
     const double lam_y = dt / a.k.dy;
     const int par = n & 1;
-    const uint32_t rb = remote(sbnd + par * a.ob, 0);
+    const uint32_t rb = GRID ? 0u : remote(sbnd + par * a.ob, 0);
+    double* const gb = GRID ? a.bhist + (int64_t)n * a.ob : nullptr;
     bool bad = false, dtbad = false;
     unsigned long long mr = 0x7ff0000000000000ull, me = 0x7ff0000000000000ull, rk = 0ull;
     // the last stage's cell: positivity (solver.cpp:300-307), minima, and the next
@@ -394,8 +428,8 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       for (int t = gtid; t < ncell; t += gthreads) {
         const int i = t % a.nx, j = t / a.nx;
         double v[4];
-        cell_stage<DIM2, MUSCL, FAST, false>(a, fk, u, u, i, j, a.heun ? 0u : rb, lam_x, lam_y, v,
-                                             bad);
+        cell_stage<DIM2, MUSCL, FAST, false>(a, fk, u, u, i, j, a.heun ? 0u : rb,
+                                             a.heun ? nullptr : gb, lam_x, lam_y, v, bad);
         const int64_t o = (int64_t)j * a.pitch + i;
         double* out = a.heun ? a.us : u2;
 #pragma unroll
@@ -407,20 +441,20 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
           finish(v);
         }
       }
-    } else if (lead && pend >= 0) {
+    } else if (!GRID && lead && pend >= 0) {
       // the previous step's outflow sums, off the critical path
       outflow_sums<DIM2>(a, sbnd + pend_par * a.ob, pend_dt);
       pend = -1;
     }
     if (a.heun) {
-      // (releases U* and the stage-1 faces: barrier.cluster arrive.release / wait.acquire)
-      cluster.sync();
+      // (releases U* and the stage-1 faces)
+      sync_all();
       // stage 2: U* -> U^{n+1} from U^n with 0.5 (F^n + F*)
       if (cellw) {
         for (int t = gtid; t < ncell; t += gthreads) {
           const int i = t % a.nx, j = t / a.nx;
           double v[4];
-          cell_stage<DIM2, MUSCL, FAST, true>(a, fk, a.us, u, i, j, rb, lam_x, lam_y, v, bad);
+          cell_stage<DIM2, MUSCL, FAST, true>(a, fk, a.us, u, i, j, rb, gb, lam_x, lam_y, v, bad);
           const int64_t o = (int64_t)j * a.pitch + i;
 #pragma unroll
           for (int q = 0; q < 4; ++q) __stcg(u2 + q * a.fstride + o, v[q]);
@@ -443,7 +477,16 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       if (wdt) sh.dtfail = 1;
     }
     __syncthreads();
-    if (tid < nblk) {   // one thread per destination block
+    unsigned long long* const gp = GRID ? a.gpart + par * 5 * SMALL_MAX_GRID : nullptr;
+    if constexpr (GRID) {
+      if (tid == 0) {
+        __stcg(gp + rank, sh.rate);
+        __stcg(gp + SMALL_MAX_GRID + rank, sh.min_r);
+        __stcg(gp + 2 * SMALL_MAX_GRID + rank, sh.min_e);
+        __stcg(gp + 3 * SMALL_MAX_GRID + rank, (unsigned long long)sh.fail);
+        __stcg(gp + 4 * SMALL_MAX_GRID + rank, (unsigned long long)sh.dtfail);
+      }
+    } else if (tid < nblk) {   // one thread per destination block
       st_remote(remote(&sh.p_rate[par][rank], tid), sh.rate);
       st_remote(remote(&sh.p_min_r[par][rank], tid), sh.min_r);
       st_remote(remote(&sh.p_min_e[par][rank], tid), sh.min_e);
@@ -451,16 +494,51 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       st_remote(remote(&sh.p_dtfail[par][rank], tid), sh.dtfail);
     }
     // (releases U^{n+1}, the boundary faces and the partials)
-    cluster.sync();
+    sync_all();
+    if constexpr (GRID) {
+      // every block combines all blocks' partials (one slot per thread, then warps)
+      unsigned long long vr = 0ull, vm = 0x7ff0000000000000ull, ve = 0x7ff0000000000000ull;
+      int vf = 0, vd = 0;
+      for (uint32_t b = tid; b < nblk; b += blockDim.x) {
+        const unsigned long long r_ = __ldcg(gp + b), m_ = __ldcg(gp + SMALL_MAX_GRID + b);
+        const unsigned long long e_ = __ldcg(gp + 2 * SMALL_MAX_GRID + b);
+        vr = r_ > vr ? r_ : vr;
+        vm = m_ < vm ? m_ : vm;
+        ve = e_ < ve ? e_ : ve;
+        vf |= (int)__ldcg(gp + 3 * SMALL_MAX_GRID + b);
+        vd |= (int)__ldcg(gp + 4 * SMALL_MAX_GRID + b);
+      }
+      vr = wred(vr, mx);
+      vm = wred(vm, mn);
+      ve = wred(ve, mn);
+      vf = __any_sync(0xffffffffu, vf);
+      vd = __any_sync(0xffffffffu, vd);
+      if ((tid & 31) == 0) {
+        if (vr) atomicMax(&sh.g_rate, vr);
+        if (vm != 0x7ff0000000000000ull) atomicMin(&sh.g_min_r, vm);
+        if (ve != 0x7ff0000000000000ull) atomicMin(&sh.g_min_e, ve);
+        if (vf) sh.g_fail = 1;
+        if (vd) sh.g_dtfail = 1;
+      }
+      __syncthreads();
+    }
     if (tid == 0) {
       unsigned long long rt = 0ull, m_r = 0x7ff0000000000000ull, m_e = 0x7ff0000000000000ull;
       int fail = 0, dtf = 0;
-      for (uint32_t b = 0; b < nblk; ++b) {
-        rt = sh.p_rate[par][b] > rt ? sh.p_rate[par][b] : rt;
-        m_r = sh.p_min_r[par][b] < m_r ? sh.p_min_r[par][b] : m_r;
-        m_e = sh.p_min_e[par][b] < m_e ? sh.p_min_e[par][b] : m_e;
-        fail |= sh.p_fail[par][b];
-        dtf |= sh.p_dtfail[par][b];
+      if constexpr (GRID) {
+        rt = sh.g_rate;
+        m_r = sh.g_min_r;
+        m_e = sh.g_min_e;
+        fail = sh.g_fail;
+        dtf = sh.g_dtfail;
+      } else {
+        for (uint32_t b = 0; b < nblk; ++b) {
+          rt = sh.p_rate[par][b] > rt ? sh.p_rate[par][b] : rt;
+          m_r = sh.p_min_r[par][b] < m_r ? sh.p_min_r[par][b] : m_r;
+          m_e = sh.p_min_e[par][b] < m_e ? sh.p_min_e[par][b] : m_e;
+          fail |= sh.p_fail[par][b];
+          dtf |= sh.p_dtfail[par][b];
+        }
       }
       sh.stop = fail;
       if (!fail) {
@@ -490,7 +568,7 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
     u = u2;
     u2 = t;
   }
-  if (lead && !cellw && pend >= 0) outflow_sums<DIM2>(a, sbnd + pend_par * a.ob, pend_dt);
+  if (!GRID && lead && !cellw && pend >= 0) outflow_sums<DIM2>(a, sbnd + pend_par * a.ob, pend_dt);
   // the step that stopped the batch: 1 failed (the host re-runs it stage-wise),
   // 2 skipped (limit reached); later steps skipped
   if (lead && tid == 0) {
@@ -502,7 +580,47 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
     }
     *a.ctl = sh.ctl;
   }
-  cluster.sync();   // no block leaves while another may still address its shared memory
+  if constexpr (!GRID)
+    cg::this_cluster().sync();   // no block leaves while another may still address its shared memory
+}
+
+// Grid mode's outflow (solver.cpp:406-432), after the kernel: k_small_sums forms each
+// completed step's ordered sums (one thread per step and chain: lanes of chains 0-3 sum
+// right - left over the rows in order, 4-7 top - bottom over the columns), k_small_accum
+// adds them to the outflow step by step in order (acc += dt dy s_x, += dt dx s_y).
+__global__ void k_small_sums(const StepRec* __restrict__ rec, const double* __restrict__ bhist,
+                             int nsteps, int ob, int nx, int ny, int dim2, double* sums) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = t >> 3, ch = t & 7;
+  if (n >= nsteps || rec[n].status != 0) return;
+  const double* sb = bhist + (int64_t)n * ob;
+  const int q = ch & 3;
+  double s = 0.0;
+  if (ch < 4) {
+    const double* L = sb + q * ny;
+    const double* R = L + 4 * ny;
+#pragma unroll 8
+    for (int j = 0; j < ny; ++j) s += R[j] - L[j];
+  } else if (dim2) {
+    const double* B = sb + 8 * ny + q * nx;
+    const double* T = B + 4 * nx;
+#pragma unroll 8
+    for (int i = 0; i < nx; ++i) s += T[i] - B[i];
+  }
+  sums[t] = s;
+}
+
+__global__ void k_small_accum(const StepRec* __restrict__ rec, const double* __restrict__ sums,
+                              int nsteps, int dim2, double dx, double dy, double* outflow) {
+  const int q = threadIdx.x;
+  if (q >= 4) return;
+  double acc = outflow[q];
+  for (int n = 0; n < nsteps && rec[n].status == 0; ++n) {
+    const double ax = rec[n].dt * (dim2 ? dy : 1.0), ay = rec[n].dt * dx;
+    acc += ax * sums[8 * n + q];
+    if (dim2) acc += ay * sums[8 * n + 4 + q];
+  }
+  outflow[q] = acc;
 }
 
 // LF_SMALL_FAST=0 in the environment: the IEEE expressions throughout (A/B)
@@ -515,24 +633,38 @@ bool small_fast_enabled() {
 }
 
 // One cluster of up to 16 blocks (the non-portable maximum; fewer where the device
-// cannot co-schedule them), each block on its own SM.
+// cannot co-schedule them), each block on its own SM -- or, in grid mode, a cooperative
+// grid of up to one block per SM (every block co-resident, grid barriers).
 template <bool DIM2, bool MUSCL>
-cudaError_t launch_small(const SmallArgs& a, int want, bool fast, cudaStream_t st) {
-  auto kern = fast ? k_small_run<DIM2, MUSCL, true> : k_small_run<DIM2, MUSCL, false>;
+cudaError_t launch_small(const SmallArgs& a, int want, bool fast, bool grid, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(SMALL_THREADS + 32);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (grid) {
+    auto kern = fast ? k_small_run<DIM2, MUSCL, true, true> : k_small_run<DIM2, MUSCL, false, true>;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, SMALL_THREADS + 32, 0);
+    if (e != cudaSuccess) return e;
+    const int nb = std::max(1, std::min({want, sms * std::max(per, 1), SMALL_MAX_GRID}));
+    cfg.gridDim = dim3(nb);
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+  }
+  auto kern = fast ? k_small_run<DIM2, MUSCL, true, false> : k_small_run<DIM2, MUSCL, false, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   const size_t smem = 2 * (size_t)a.ob * sizeof(double);
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(SMALL_THREADS + 32);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  int ncta = std::max(want, 1);
+  int ncta = std::max(1, std::min(want, SMALL_MAX_CTAS));
   cfg.gridDim = dim3(ncta);
   at[0].val.clusterDim.x = ncta;
   at[0].val.clusterDim.y = 1;
@@ -557,6 +689,19 @@ cudaError_t launch_small(const SmallArgs& a, int want, bool fast, cudaStream_t s
   }
 }
 
+// grid mode beyond one cluster's worth of cells, and whenever the boundary faces of two
+// steps do not fit in the lead block's shared memory (LF_SMALL_GRID=0 / 1 in the
+// environment: never / always where possible, for A/B)
+bool use_grid_mode(const lf_handle* h) {
+  static const int force = [] {
+    const char* e = std::getenv("LF_SMALL_GRID");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  if (h->dim2 && h->d.nx + h->d.ny > SMALL_MAX_PERIMETER) return true;
+  if (force >= 0) return force == 1;
+  return (int64_t)h->d.nx * h->d.ny > (int64_t)SMALL_MAX_CTAS * SMALL_THREADS;
+}
+
 }  // namespace
 
 // ================================================================= host driver
@@ -571,6 +716,10 @@ struct SmallState {
   int cap = 0;
   bool valid = false;            // ctl holds the rate of the current U
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // grid mode: block partials, the boundary-face history and per-step sums of a batch
+  unsigned long long* gpart = nullptr;   // device [2][5][SMALL_MAX_GRID]
+  double* bhist = nullptr;               // device [SMALL_GRID_BATCH][ob]
+  double* sums = nullptr;                // device [SMALL_GRID_BATCH][8]
 };
 
 namespace {
@@ -600,6 +749,12 @@ void small_alloc(lf_handle* h, int steps) {
     SK(cudaHostAlloc(&m->outflow_host, 4 * sizeof(double), cudaHostAllocDefault));
     SK(cudaEventCreate(&m->e0));
     SK(cudaEventCreate(&m->e1));
+  }
+  if (!m->gpart && use_grid_mode(h)) {
+    const int64_t ob = 8 * (int64_t)s.L.ny + (h->dim2 ? 8 * (int64_t)s.L.nx : 0);
+    SK(cudaMalloc(&m->gpart, 2 * 5 * SMALL_MAX_GRID * sizeof(unsigned long long)));
+    SK(cudaMalloc(&m->bhist, (size_t)SMALL_GRID_BATCH * ob * sizeof(double)));
+    SK(cudaMalloc(&m->sums, (size_t)SMALL_GRID_BATCH * 8 * sizeof(double)));
   }
   if (steps > m->cap) {
     cudaFree(m->rec);
@@ -658,23 +813,34 @@ int run_small(lf_handle* h, int n, double cfl, double limit, double t_final, dou
   a.rec = m->rec;
   a.outflow = m->outflow;
   a.nsteps = n;
+  const bool grid = use_grid_mode(h);
+  a.gpart = m->gpart;
+  a.bhist = m->bhist;
   const bool muscl = h->d.spatial_order >= 2;
   if (ms) SK(cudaEventRecord(m->e0, s.stream));
   count_launch();
   const int64_t cells = (int64_t)a.nx * a.ny;
-  const int want = (int)std::min<int64_t>((cells + SMALL_THREADS - 1) / SMALL_THREADS, SMALL_MAX_CTAS);
+  const int want = (int)std::min<int64_t>((cells + SMALL_THREADS - 1) / SMALL_THREADS, SMALL_MAX_GRID);
   cudaError_t le;
   // the fast exact arithmetic where its proofs hold (beta >= 1 for sweby_fast, gamma - 1
   // in the constant box); a cell outside the cell box flags the step (stage-wise re-run)
   const bool fast = small_fast_enabled() && !h->small_ieee && h->d.beta >= 1.0 && h->k.gm1 >= 0x1p-14 &&
                     h->k.gm1 < 0x1p6 && h->k.gamma < 0x1p7;
   if (h->dim2)
-    le = muscl ? launch_small<true, true>(a, want, fast, s.stream)
-               : launch_small<true, false>(a, want, fast, s.stream);
+    le = muscl ? launch_small<true, true>(a, want, fast, grid, s.stream)
+               : launch_small<true, false>(a, want, fast, grid, s.stream);
   else
-    le = muscl ? launch_small<false, true>(a, want, fast, s.stream)
-               : launch_small<false, false>(a, want, fast, s.stream);
+    le = muscl ? launch_small<false, true>(a, want, fast, grid, s.stream)
+               : launch_small<false, false>(a, want, fast, grid, s.stream);
   SK(le);
+  if (grid) {   // the batch's boundary-outflow sums, in step order
+    count_launch(2);
+    k_small_sums<<<(8 * n + 255) / 256, 256, 0, s.stream>>>(m->rec, m->bhist, n, a.ob, a.nx,
+                                                           a.ny, h->dim2, m->sums);
+    k_small_accum<<<1, 32, 0, s.stream>>>(m->rec, m->sums, n, h->dim2, h->d.dx, h->d.dy,
+                                          m->outflow);
+    SK(cudaGetLastError());
+  }
   SK(cudaGetLastError());
   if (ms) SK(cudaEventRecord(m->e1, s.stream));
   SK(cudaMemcpyAsync(m->rec_host, m->rec, (size_t)n * sizeof(StepRec), cudaMemcpyDeviceToHost,
@@ -719,8 +885,6 @@ bool small_supported(lf_handle* h) {
   if (h->mc.n > 0 || h->slabs.size() != 1 || h->nccl) return false;
   // (the kernel reads ghosts through an index map whose sources are interior cells)
   if (h->d.nx < 2 || (h->dim2 && h->d.ny < 2)) return false;
-  // the boundary faces of two steps in the lead block's shared memory (160 KB)
-  if (h->dim2 && h->d.nx + h->d.ny > SMALL_MAX_PERIMETER) return false;
   return (int64_t)h->d.nx * h->d.ny <= SMALL_MAX_CELLS;
 }
 
@@ -744,6 +908,9 @@ void small_release(lf_handle* h) {
   cudaFreeHost(m->outflow_host);
   if (m->e0) cudaEventDestroy(m->e0);
   if (m->e1) cudaEventDestroy(m->e1);
+  cudaFree(m->gpart);
+  cudaFree(m->bhist);
+  cudaFree(m->sums);
   delete m;
   h->small = nullptr;
 }
@@ -772,7 +939,7 @@ int small_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* 
   if (taken) *taken = 0;
   int k = 0;
   while (k < nsteps && *time < t_final) {
-    const int batch = std::min(nsteps - k, SMALL_BATCH);
+    const int batch = std::min(nsteps - k, use_grid_mode(h) ? SMALL_GRID_BATCH : SMALL_BATCH);
     small_alloc(h, batch);
     SmallState* m = sstate(h);
     int failed_at;
@@ -805,24 +972,32 @@ int small_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* 
 
 int small_time_steps(lf_handle* h, int nsteps, double cfl, double* kernel_ms, double* step_ms,
                      int* launches) {
-  small_alloc(h, nsteps);
+  const int per = use_grid_mode(h) ? SMALL_GRID_BATCH : SMALL_BATCH;
+  small_alloc(h, std::min(nsteps, per));
   SmallState* m = sstate(h);
-  SlabState& s = h->slabs[0];
   double t0 = 0.0;
   if (m->valid) {
     SK(cudaMemcpy(m->ctl_host, m->ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost));
     t0 = m->ctl_host->time;
   }
   const double big = 1.7976931348623157e308;
-  SK(cudaEventRecord(m->e0, s.stream));
-  int failed_at;
-  float ms = 0.f;
-  const int done = run_small(h, nsteps, cfl, big, big, t0, nullptr, &failed_at, &ms);
-  *kernel_ms = ms;
-  *step_ms = ms;
-  *launches = 1;
-  (void)done;
-  return failed_at >= 0 ? LF_ERR_DEVICE : 0;
+  double total = 0.0;
+  int k = 0, nl = 0;
+  while (k < nsteps) {
+    int failed_at;
+    float ms = 0.f;
+    const int n = std::min(nsteps - k, per);
+    const int done = run_small(h, n, cfl, big, big, t0, nullptr, &failed_at, &ms);
+    total += ms;
+    ++nl;
+    if (failed_at >= 0) return LF_ERR_DEVICE;
+    t0 = m->rec_host[done - 1].time;
+    k += done;
+  }
+  *kernel_ms = total;
+  *step_ms = total;
+  *launches = nl;
+  return 0;
 }
 
 }  // namespace lfb

@@ -1,5 +1,6 @@
 """LF_PATH_SMALL (csrc/small_step.cu): the step loop of a small grid in one thread-block
-cluster, against the oracle bit for bit.
+cluster (or, beyond one cluster's worth of cells, one cooperative grid), against the
+oracle bit for bit.
 
 The golden / error / random suites already run the path (test_gpu_parity.PATHS, and
 LF_PATH_AUTO picks it for the small random grids); here: the AUTO choice, every
@@ -53,7 +54,8 @@ def test_auto_picks_the_small_path_where_it_is_faster(cuda):
         return p
     assert resolved(CS.sod()) == "small"                      # BASELINE config 1
     assert resolved(CS.quadrant(128, 1)) == "small"
-    assert resolved(CS.quadrant(256, 1)) == "twopass"
+    assert resolved(CS.quadrant(256, 1)) == "small"                # (grid mode)
+    assert resolved(CS.quadrant(512, 1)) == "twopass"
     g1 = G.make_grid_1d(100_000, 0.0, 1.0)
     assert resolved(CS.Case("s", g1, G.BoundaryCondition(), 1.4, G.SchemeParams(), 0.5, 0.2,
                             G.INT64_MAX, "riemann_x")) == "small"
@@ -152,3 +154,25 @@ def test_tiny_1d_grids(cuda, nx, bc):
     case = CS.Case("s", g, G.BoundaryCondition(bc, bc), 1.4, G.SchemeParams(), 0.3,
                    CS.STEP_DRIVEN_LIMIT, 8, "riemann_x")
     _check(case, 8, _run(case, 8), f"1D {nx} {bc}")
+
+
+@pytest.mark.parametrize("nx,ny", [(256, 256), (1400, 2), (3, 1500), (400, 300)])
+def test_grid_mode_equals_oracle(cuda, nx, ny):
+    """The cooperative-grid mode: beyond one cluster's worth of cells, and for any grid
+    whose boundary faces do not fit in shared memory (perimeter > 1280); its outflow is
+    summed after each batch (k_small_sums / k_small_accum)."""
+    g = G.make_grid_2d(nx, ny, 0.0, 1.0, 0.0, 1.0)
+    case = CS.Case("q", g, G.BoundaryCondition(G.REFLECTIVE, G.TRANSMISSIVE, G.TRANSMISSIVE,
+                                               G.REFLECTIVE), 1.4, G.SchemeParams(), 0.4,
+                   CS.STEP_DRIVEN_LIMIT, 9, "quadrant")
+    _check(case, 9, _run(case, 9), f"{nx}x{ny}")
+
+
+def test_grid_mode_batches_and_1d(cuda):
+    """More steps than one grid-mode batch (256), and a 1D grid of 2^16 cells."""
+    case = CS.quadrant(96, 300)   # (9 216 cells: grid mode)
+    _check(case, 300, _run(case, 300), "300 steps")
+    g = G.make_grid_1d(1 << 16, 0.0, 1.0)
+    c1 = CS.Case("s", g, G.BoundaryCondition(G.REFLECTIVE, G.TRANSMISSIVE), 1.4, G.SchemeParams(),
+                 0.5, 0.2, 40, "riemann_x")
+    _check(c1, 40, _run(c1, 40), "1D 65536")

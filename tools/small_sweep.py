@@ -35,7 +35,7 @@ def cases():
     out = [("config1_sod_400x4", CS.sod())]
     for n in (100, 1000, 10000, 65536):
         out.append((f"sod1d_{n}", sod1d(n)))
-    for n in (32, 64, 128, 256):
+    for n in (32, 64, 128, 256, 512):
         c = CS.quadrant(n, 200)
         out.append((f"quadrant_{n}", c))
     return out
@@ -81,7 +81,7 @@ def main():
     res = {}
     for name, case in cases():
         row, ref_field = {}, None
-        for path in ("small", "twopass", "staged"):
+        for path in ("small", "twopass", "staged") if "--small-only" not in sys.argv else ("small",):
             if path == "staged" and case.grid.nx * case.grid.ny > 20000:
                 continue
             r = time_path(case, path)
@@ -92,6 +92,10 @@ def main():
                 ref_field = field
             row[path]["same_bits_as_small"] = bool(np.array_equal(field, ref_field))
         steps = row["small"]["steps"]
+        if "--small-only" in sys.argv:
+            res[name] = row
+            print(name, json.dumps(row), flush=True)
+            continue
         try:
             for th in (1, os.cpu_count() or 1):
                 rr, rf = time_reference(case, steps, th)
