@@ -17,6 +17,11 @@ namespace lfb {
 constexpr int64_t SMALL_MAX_CELLS = (int64_t)1 << 22;
 constexpr int64_t SMALL_AUTO_CELLS_1D = SMALL_MAX_CELLS;
 constexpr int64_t SMALL_AUTO_CELLS_2D = (int64_t)1 << 17;
+// with materials (the IEEE closures of every stencil cell): 2D to 2^15 cells
+// (tools/small_mat_sweep.py: the triple point at 70x30 / 256x110 84 us per step against
+// 107 / 110 on the two-pass material kernels, 512x220 296 vs 111); 1D always (a 400-cell
+// contact: 27 vs 160 us stage-wise)
+constexpr int64_t SMALL_AUTO_CELLS_2D_MAT = (int64_t)1 << 15;
 constexpr int SMALL_BATCH = 4096;   // steps per launch of lf_advance
 constexpr int SMALL_GRID_BATCH = 256;   // grid mode (its boundary-face history per step)
 constexpr int SMALL_MAX_PERIMETER = 1280;   // cluster mode, 2D: nx + ny (boundary faces

@@ -80,28 +80,41 @@ struct SmallArgs {
   StepRec* rec;      // [nsteps]
   double* outflow;   // [4], accumulated in place
   int nsteps;
+  // multimaterial (MAT kernels): partial densities (Layout of the field, nmat components)
+  // of U^n, U* and U^{n+1}, the stage-1 closure's fractions of every interior cell and
+  // the stage-1 faces' u* (the corrector's stage-a material fluxes are rebuilt from them)
+  int nmat;
+  double gam[8];
+  double* p;
+  double* p2;
+  double* ps;
+  double* y0;
+  double* usx0;
+  double* usy0;
   // grid mode (a cooperative grid of up to one block per SM, beyond one cluster):
-  unsigned long long* gpart;   // [2 parities][5 fields][SMALL_MAX_GRID] block partials
+  unsigned long long* gpart;   // [2 parities][6 fields][SMALL_MAX_GRID] block partials
   double* bhist;               // [nsteps][ob] every step's boundary faces (summed after
                                // the kernel, k_small_sums / k_small_accum)
 };
 
 constexpr int SMALL_MAX_CTAS = 16;     // one cluster (non-portable maximum)
 constexpr int SMALL_MAX_GRID = 1024;   // grid mode: blocks (one per SM in practice)
+constexpr int SMALL_MAX_MAT = 8;       // materials on this path (more: the stage-wise kernels)
+constexpr int SMALL_NPART = 6;         // reduced fields: rate, min rho, min e, fail, dtfail, min p
 
 // Per block: its own partial reductions; in the lead block (rank 0) also the
 // control record and every block's partials (written there by plain
 // shared::cluster stores -- no remote atomics), and the outflow staging tile.
 struct SmallShared {
   StepCtl ctl;                             // this block's copy (every block computes it)
-  unsigned long long rate, min_r, min_e;   // this block's partials
+  unsigned long long rate, min_r, min_e, min_pk;   // this block's partials
   int fail, dtfail, stop;
-  unsigned long long g_rate, g_min_r, g_min_e;   // grid mode: the combined partials
+  unsigned long long g_rate, g_min_r, g_min_e, g_min_pk;   // grid mode: the combined partials
   int g_fail, g_dtfail;
   // every block's partials, in every block, by step parity (a fast block's next step
   // must not overwrite a slot a slow block has not read)
   unsigned long long p_rate[2][SMALL_MAX_CTAS], p_min_r[2][SMALL_MAX_CTAS],
-      p_min_e[2][SMALL_MAX_CTAS];
+      p_min_e[2][SMALL_MAX_CTAS], p_min_pk[2][SMALL_MAX_CTAS];
   int p_fail[2][SMALL_MAX_CTAS], p_dtfail[2][SMALL_MAX_CTAS];
 };
 
@@ -316,6 +329,324 @@ __device__ __forceinline__ void cell_stage(const SmallArgs& a, const FK& fk, con
   }
 }
 
+// ---------------------------------------------------------------- multimaterial
+// (MAT kernels; the stage-wise kernels' IEEE expressions, material_kernels.cu)
+
+// order-preserving key of a non-NaN double (unsigned compare == IEEE compare)
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// fill_all_ghosts' closure (solver.cpp:100-121): the clamped fractions of a cell's
+// partials and its mixed-cell gamma; bad: a fraction beyond round-off
+template <int KM>
+__device__ __forceinline__ double closure(const SmallArgs& a, const double* pk, int64_t o, double r,
+                                          double y[KM], bool& bad) {
+  double ysum = 0.0, gp = 0.0;
+  int pure = -1;
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    if (k >= a.nmat) break;
+    const double raw = __ldcg(pk + k * a.fstride + o) / r;
+    double yk = raw;
+    if (yk < 0.0 || yk > 1.0) {
+      if (raw < -1e-11 || raw > 1.0 + 1e-11) {
+        bad = true;
+        yk = 0.0;
+      } else {
+        yk = raw < 0.0 ? 0.0 : 1.0;
+      }
+    }
+    y[k] = yk;
+    if (yk == 1.0) pure = k;
+    ysum += yk / (a.gam[k] - 1.0);
+  }
+#pragma unroll
+  for (int k = 0; k < KM; ++k)
+    if (k < a.nmat && pure == k) gp = a.gam[k];
+  return pure >= 0 ? gp : 1.0 + 1.0 / ysum;
+}
+
+// a stencil cell (i, j) read through the ghost map (partials: even parity): its closure
+// and its primitives with that gamma (build_primitives, solver.cpp:145-163)
+template <bool DIM2, int KM>
+__device__ __forceinline__ void mat_cell(const SmallArgs& a, const double* f, const double* pk,
+                                         int i, int j, double w[4], double& g, double y[KM],
+                                         bool& bad) {
+  bool fx, fy = false;
+  const int is = ghost_src(i, a.nx, a.bc[0], a.bc[1], fx);
+  const int js = DIM2 ? ghost_src(j, a.ny, a.bc[2], a.bc[3], fy) : 0;
+  const int64_t o = (int64_t)js * a.pitch + is;
+  const double r = __ldcg(f + o);
+  double mx = __ldcg(f + a.fstride + o), my = __ldcg(f + 2 * a.fstride + o);
+  const double e = __ldcg(f + 3 * a.fstride + o);
+  if (fx) mx = -1.0 * mx;
+  if (fy) my = -1.0 * my;
+  g = closure<KM>(a, pk, o, r, y, bad);
+  w[0] = w[1] = w[2] = w[3] = 0.0;
+  if (!(r > 0.0)) {
+    bad = true;
+  } else {
+    w[0] = r;
+    primitive(r, mx, my, e, g - 1.0, w[1], w[2], w[3]);
+    if (!(w[3] > 0.0)) bad = true;
+  }
+}
+
+// the fractions a stage-1 closure stored for cell (i, j) (ghosts: the source cell's)
+template <bool DIM2, int KM>
+__device__ __forceinline__ void stored_fractions(const SmallArgs& a, int i, int j, double y[KM]) {
+  bool f;
+  const int is = ghost_src(i, a.nx, a.bc[0], a.bc[1], f);
+  const int js = DIM2 ? ghost_src(j, a.ny, a.bc[2], a.bc[3], f) : 0;
+  const int64_t o = (int64_t)js * a.pitch + is;
+#pragma unroll
+  for (int k = 0; k < KM; ++k)
+    if (k < a.nmat) y[k] = __ldcg(a.y0 + k * a.fstride + o);
+}
+
+// lagrangian_hll + contact_flux with each side's own EOS (solver.cpp:228-238)
+template <int AXIS>
+__device__ __forceinline__ void face_g(const double wm[4], const double wp[4], double el,
+                                       double er, double f[4], double& us) {
+  const double ul = AXIS == 0 ? wm[1] : wm[2];
+  const double ur = AXIS == 0 ? wp[1] : wp[2];
+  const double cl = sqrt(el * wm[3] / wm[0]);
+  const double cr = sqrt(er * wp[3] / wp[0]);
+  const double cmax = smax(cl, cr);
+  const double rho_sum = wm[0] + wp[0];
+  const double ps =
+      (wp[0] * wm[3] + wm[0] * wp[3]) / rho_sum - (wm[0] * wp[0] / rho_sum) * cmax * (ur - ul);
+  us = (wm[0] * ul + wp[0] * ur) / rho_sum - (wp[3] - wm[3]) / (cmax * rho_sum);
+  double a0, a1, a2, a3;
+  if (us > 0.0) {
+    a0 = wm[0];
+    a1 = wm[0] * wm[1];
+    a2 = wm[0] * wm[2];
+    a3 = wm[3] / (el - 1.0) + 0.5 * wm[0] * (wm[1] * wm[1] + wm[2] * wm[2]);
+  } else if (us < 0.0) {
+    a0 = wp[0];
+    a1 = wp[0] * wp[1];
+    a2 = wp[0] * wp[2];
+    a3 = wp[3] / (er - 1.0) + 0.5 * wp[0] * (wp[1] * wp[1] + wp[2] * wp[2]);
+  } else {
+    const double m1 = wm[0] * wm[1], m2 = wm[0] * wm[2];
+    const double m3 = wm[3] / (el - 1.0) + 0.5 * wm[0] * (wm[1] * wm[1] + wm[2] * wm[2]);
+    const double p1 = wp[0] * wp[1], p2 = wp[0] * wp[2];
+    const double p3 = wp[3] / (er - 1.0) + 0.5 * wp[0] * (wp[1] * wp[1] + wp[2] * wp[2]);
+    a0 = 0.5 * (wm[0] + wp[0]);
+    a1 = 0.5 * (m1 + p1);
+    a2 = 0.5 * (m2 + p2);
+    a3 = 0.5 * (m3 + p3);
+  }
+  f[0] = a0 * us;
+  f[1] = AXIS == 0 ? a1 * us + ps : a1 * us;
+  f[2] = AXIS == 1 ? a2 * us + ps : a2 * us;
+  f[3] = a3 * us + ps * us;
+}
+
+// edge_material_flux (solver.cpp:345-357) added to acc as gather does (acc += w t)
+template <int KM>
+__device__ __forceinline__ void add_mat_flux(const SmallArgs& a, double mass, double us,
+                                             const double ylo[KM], const double yhi[KM], double w,
+                                             double acc[KM]) {
+  double rest = mass;
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    if (k >= a.nmat) break;
+    double fk;
+    if (k < a.nmat - 1) {
+      fk = us == 0.0 ? 0.0 : mass * (us > 0.0 ? ylo[k] : yhi[k]);
+      rest -= fk;
+    } else {
+      fk = us == 0.0 ? 0.0 : rest;
+    }
+    acc[k] += w * fk;
+  }
+}
+
+// The two faces of a cell along one axis with the cells' own EOS; traces as cell_faces
+template <int AXIS, bool MUSCL>
+__device__ __forceinline__ void mat_faces(const SmallArgs& a, const double (&s)[5][4],
+                                          const double (&g)[5], double flo[4], double fhi[4],
+                                          double& uslo, double& ushi, bool& bad) {
+  double m_lo[4], p_lo[4], m_hi[4], p_hi[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (MUSCL) {
+      const double s1 = slope3(s[0][c], s[1][c], s[2][c], a.k.beta);
+      const double s2 = slope3(s[1][c], s[2][c], s[3][c], a.k.beta);
+      const double s3 = slope3(s[2][c], s[3][c], s[4][c], a.k.beta);
+      m_lo[c] = s[1][c] + 0.5 * s1;
+      p_lo[c] = s[2][c] - 0.5 * s2;
+      m_hi[c] = s[2][c] + 0.5 * s2;
+      p_hi[c] = s[3][c] - 0.5 * s3;
+    } else {
+      m_lo[c] = s[1][c];
+      p_lo[c] = s[2][c];
+      m_hi[c] = s[2][c];
+      p_hi[c] = s[3][c];
+    }
+    flo[c] = fhi[c] = 0.0;
+  }
+  uslo = ushi = 0.0;
+  if (traces_ok(m_lo[0], m_lo[3], p_lo[0], p_lo[3]))
+    face_g<AXIS>(m_lo, p_lo, g[1], g[2], flo, uslo);
+  else
+    bad = true;
+  if (traces_ok(m_hi[0], m_hi[3], p_hi[0], p_hi[3]))
+    face_g<AXIS>(m_hi, p_hi, g[2], g[3], fhi, ushi);
+  else
+    bad = true;
+}
+
+// One multimaterial stage for interior cell (i, j): closures and primitives of the cross
+// stencil, the four faces with per-side EOS, apply_update (solver.cpp:272-308) and
+// update_partials (solver.cpp:331-404).  Stage 1 (!TWO) stores its faces, their u* and
+// this cell's fractions (the corrector's stage-a material fluxes); stage 2 rebuilds
+// those and accumulates as gather does: (0 + 0.5 a) + 0.5 b.
+template <bool DIM2, bool MUSCL, bool TWO, int KM>
+__device__ __forceinline__ void cell_stage_mat(const SmallArgs& a, const double* in,
+                                               const double* pin, const double* base,
+                                               const double* pbase, int i, int j, uint32_t rb,
+                                               double* gb, double lam_x, double lam_y,
+                                               double vals[4], double pv[KM],
+                                               bool& bad) {
+  auto put = [&](int idx, double v) {
+    if (rb)
+      st_remote_d(rb + 8u * idx, v);
+    else
+      __stcg(gb + idx, v);
+  };
+  const int64_t o = (int64_t)j * a.pitch + i;
+  double u0[4], fnl[4], fnr[4], fnb[4], fnt[4];
+  double usl0 = 0.0, usr0 = 0.0, usb0 = 0.0, ust0 = 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    u0[c] = __ldcg(base + c * a.fstride + o);
+    if (TWO) {
+      const double* fa = a.fx[0] + c * a.fx_stride;
+      fnl[c] = __ldcg(fa + o);
+      fnr[c] = __ldcg(fa + o + 1);
+      if (DIM2) {
+        const double* fb = a.fy[0] + c * a.fy_stride;
+        fnb[c] = __ldcg(fb + o);
+        fnt[c] = __ldcg(fb + o + a.pitch);
+      }
+    }
+  }
+  if (TWO) {
+    usl0 = __ldcg(a.usx0 + o);
+    usr0 = __ldcg(a.usx0 + o + 1);
+    if (DIM2) {
+      usb0 = __ldcg(a.usy0 + o);
+      ust0 = __ldcg(a.usy0 + o + a.pitch);
+    }
+  }
+  // partial-flux accumulators of the four faces
+  double ml[KM], mr[KM], mb[KM], mt[KM];
+#pragma unroll
+  for (int k = 0; k < KM; ++k) ml[k] = mr[k] = mb[k] = mt[k] = 0.0;
+  const double w = TWO ? 0.5 : 1.0;
+  double ymid[KM];   // this cell's fractions (this stage's closure)
+  double fxl[4], fxr[4], fyb[4], fyt[4], usl, usr, usb = 0.0, ust = 0.0;
+  {
+    double s[5][4], g[5], yl[KM], yr[KM], yd[KM];
+    mat_cell<DIM2, KM>(a, in, pin, i - 2, j, s[0], g[0], yd, bad);
+    mat_cell<DIM2, KM>(a, in, pin, i - 1, j, s[1], g[1], yl, bad);
+    mat_cell<DIM2, KM>(a, in, pin, i, j, s[2], g[2], ymid, bad);
+    mat_cell<DIM2, KM>(a, in, pin, i + 1, j, s[3], g[3], yr, bad);
+    mat_cell<DIM2, KM>(a, in, pin, i + 2, j, s[4], g[4], yd, bad);
+    mat_faces<0, MUSCL>(a, s, g, fxl, fxr, usl, usr, bad);
+    if (TWO) {   // stage a: the stage-1 faces with the stage-1 fractions
+      double y0l[KM], y0m[KM], y0r[KM];
+      stored_fractions<DIM2, KM>(a, i - 1, j, y0l);
+      stored_fractions<DIM2, KM>(a, i, j, y0m);
+      stored_fractions<DIM2, KM>(a, i + 1, j, y0r);
+      add_mat_flux<KM>(a, fnl[0], usl0, y0l, y0m, w, ml);
+      add_mat_flux<KM>(a, fnr[0], usr0, y0m, y0r, w, mr);
+    }
+    add_mat_flux<KM>(a, fxl[0], usl, yl, ymid, w, ml);
+    add_mat_flux<KM>(a, fxr[0], usr, ymid, yr, w, mr);
+  }
+  if (DIM2) {
+    double s[5][4], g[5], yb[KM], yt[KM], yd[KM];
+    mat_cell<DIM2, KM>(a, in, pin, i, j - 2, s[0], g[0], yd, bad);
+    mat_cell<DIM2, KM>(a, in, pin, i, j - 1, s[1], g[1], yb, bad);
+    mat_cell<DIM2, KM>(a, in, pin, i, j, s[2], g[2], yd, bad);
+    mat_cell<DIM2, KM>(a, in, pin, i, j + 1, s[3], g[3], yt, bad);
+    mat_cell<DIM2, KM>(a, in, pin, i, j + 2, s[4], g[4], yd, bad);
+    mat_faces<1, MUSCL>(a, s, g, fyb, fyt, usb, ust, bad);
+    if (TWO) {
+      double y0b[KM], y0m[KM], y0t[KM];
+      stored_fractions<DIM2, KM>(a, i, j - 1, y0b);
+      stored_fractions<DIM2, KM>(a, i, j, y0m);
+      stored_fractions<DIM2, KM>(a, i, j + 1, y0t);
+      add_mat_flux<KM>(a, fnb[0], usb0, y0b, y0m, w, mb);
+      add_mat_flux<KM>(a, fnt[0], ust0, y0m, y0t, w, mt);
+    }
+    add_mat_flux<KM>(a, fyb[0], usb, yb, ymid, w, mb);
+    add_mat_flux<KM>(a, fyt[0], ust, ymid, yt, w, mt);
+  }
+  const int k = TWO ? 1 : 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double* fx = a.fx[k] + c * a.fx_stride;
+    __stcg(fx + o, fxl[c]);
+    if (i == a.nx - 1) __stcg(fx + o + 1, fxr[c]);
+    if (DIM2) {
+      double* fy = a.fy[k] + c * a.fy_stride;
+      __stcg(fy + o, fyb[c]);
+      if (j == a.ny - 1) __stcg(fy + o + a.pitch, fyt[c]);
+    }
+  }
+  if (!TWO) {   // the corrector's stage-a inputs: u* of the faces, this cell's fractions
+    __stcg(a.usx0 + o, usl);
+    if (i == a.nx - 1) __stcg(a.usx0 + o + 1, usr);
+    if (DIM2) {
+      __stcg(a.usy0 + o, usb);
+      if (j == a.ny - 1) __stcg(a.usy0 + o + a.pitch, ust);
+    }
+#pragma unroll
+    for (int kk = 0; kk < KM; ++kk)
+      if (kk < a.nmat) __stcg(a.y0 + kk * a.fstride + o, ymid[kk]);
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double l = fxl[c], r = fxr[c];
+    if (TWO) {
+      l = 0.5 * (fnl[c] + l);
+      r = 0.5 * (fnr[c] + r);
+    }
+    double val = u0[c] - lam_x * (r - l);
+    if (DIM2) {
+      double b = fyb[c], t = fyt[c];
+      if (TWO) {
+        b = 0.5 * (fnb[c] + b);
+        t = 0.5 * (fnt[c] + t);
+      }
+      val -= lam_y * (t - b);
+      if (rb || gb) {
+        if (j == 0) put(8 * a.ny + c * a.nx + i, b);
+        if (j == a.ny - 1) put(8 * a.ny + 4 * a.nx + c * a.nx + i, t);
+      }
+    }
+    if (rb || gb) {
+      if (i == 0) put(c * a.ny + j, l);
+      if (i == a.nx - 1) put(4 * a.ny + c * a.ny + j, r);
+    }
+    vals[c] = val;
+  }
+#pragma unroll
+  for (int kk = 0; kk < KM; ++kk) {
+    if (kk >= a.nmat) break;
+    double val = __ldcg(pbase + kk * a.fstride + o) - lam_x * (mr[kk] - ml[kk]);
+    if (DIM2) val -= lam_y * (mt[kk] - mb[kk]);
+    pv[kk] = val;
+  }
+}
+
 // accumulate_boundary_outflow (solver.cpp:406-432) of a completed step, by lanes 0-3
 // (x: s += right - left over the rows in order) and 4-7 (y: s += top - bottom over the
 // columns) of one warp, from the step's boundary block in shared memory; then
@@ -345,8 +676,11 @@ __device__ void outflow_sums(const SmallArgs& a, const double* sb, double dt) {
   __syncwarp();
 }
 
-template <bool DIM2, bool MUSCL, bool FAST, bool GRID>
+template <bool DIM2, bool MUSCL, bool FAST, bool GRID, int KM>
 __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a) {
+  // KM: 0 one material; else the material kernels' array bound (nmat <= KM)
+  constexpr bool MAT = KM > 0;
+  constexpr int KA = KM > 0 ? KM : 1;
   namespace cg = cooperative_groups;
   __shared__ SmallShared sh;
   // GRID: a cooperative grid (one block per SM) synchronised by grid barriers; else one
@@ -372,6 +706,8 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
   const FK fk = make_fk(a.k.gamma, a.k.gm1, a.k.beta, a.k.dx, a.k.dy);
   double* u = a.u;
   double* u2 = a.u2;
+  double* pk = a.p;     // (MAT) partial densities of U^n / U^{n+1}
+  double* pk2 = a.p2;
   const MaxOp mx;
   const MinOp mn;
   const int ncell = a.nx * a.ny;
@@ -383,8 +719,10 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       sh.rate = 0ull;
       sh.min_r = sh.min_e = 0x7ff0000000000000ull;
       sh.fail = sh.dtfail = 0;
+      sh.min_pk = ~0ull;
       sh.g_rate = 0ull;
       sh.g_min_r = sh.g_min_e = 0x7ff0000000000000ull;
+      sh.g_min_pk = ~0ull;
       sh.g_fail = sh.g_dtfail = 0;
     }
     __syncthreads();   // (this block's control record of the step, the resets)
@@ -402,6 +740,7 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
     double* const gb = GRID ? a.bhist + (int64_t)n * a.ob : nullptr;
     bool bad = false, dtbad = false;
     unsigned long long mr = 0x7ff0000000000000ull, me = 0x7ff0000000000000ull, rk = 0ull;
+    unsigned long long mpk = ~0ull;   // (MAT) min p (order key)
     // the last stage's cell: positivity (solver.cpp:300-307), minima, and the next
     // step's CFL rate (solver.cpp:449-470) of the new value
     auto finish = [&](const double v[4]) {
@@ -423,7 +762,90 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
         dtbad = true;
       }
     };
-    if (cellw) {
+    // (MAT) the last stage's cell: positivity and min rho as above; min p from the fresh
+    // partials (solver.cpp:522-538); the next step's CFL rate with the mixed-cell gamma of
+    // the next fill's closure (solver.cpp:449-470 with gamma_[0]; a fraction beyond
+    // round-off there fails the next step)
+    auto finish_mat = [&](const double v[4], const double pv[KA]) {
+      const double eint = internal_energy(v[0], v[1], v[2], v[3]);
+      if (!(v[0] > 0.0) || !(eint > 0.0)) {
+        bad = true;
+      } else {
+        const unsigned long long r = pos_bits(v[0]), e = pos_bits(eint);
+        mr = r < mr ? r : mr;
+        me = e < me ? e : me;
+      }
+      const double r = v[0];
+      double sm = 0.0, ysum = 0.0, gp = 0.0;
+      int pure = -1;
+      bool fbad = false;
+#pragma unroll
+      for (int k = 0; k < KA; ++k) {
+        if (k >= a.nmat) break;
+        sm += (pv[k] / r) / (a.gam[k] - 1.0);
+        const double raw = pv[k] / r;
+        double yk = raw;
+        if (yk < 0.0 || yk > 1.0) {
+          if (raw < -1e-11 || raw > 1.0 + 1e-11) {
+            fbad = true;
+            yk = 0.0;
+          } else {
+            yk = raw < 0.0 ? 0.0 : 1.0;
+          }
+        }
+        if (yk == 1.0) pure = k;
+        ysum += yk / (a.gam[k] - 1.0);
+      }
+      const double x = (v[3] - 0.5 * (v[1] * v[1] + v[2] * v[2]) / r) / sm;
+      if (x == x) {
+        const unsigned long long key = order_key(x);
+        mpk = key < mpk ? key : mpk;
+      }
+#pragma unroll
+      for (int k = 0; k < KA; ++k)
+        if (k < a.nmat && pure == k) gp = a.gam[k];
+      const double g = pure >= 0 ? gp : 1.0 + 1.0 / ysum;
+      bool ok = !fbad && r > 0.0;
+      if (ok) {
+        const double inv = 1.0 / r;
+        const double uu = v[1] * inv, vv = v[2] * inv;
+        const double p = (g - 1.0) * (v[3] - 0.5 * (v[1] * v[1] + v[2] * v[2]) * inv);
+        ok = p > 0.0;
+        if (ok) {
+          const double cs = sqrt(g * p * inv);
+          double rr = (fabs(uu) + cs) / a.k.dx;
+          if (DIM2) rr += (fabs(vv) + cs) / a.k.dy;
+          if (rr == rr) {
+            const unsigned long long b = pos_bits(rr);
+            rk = b > rk ? b : rk;
+          }
+        }
+      }
+      if (!ok) dtbad = true;
+    };
+    if (MAT && cellw) {
+      // stage 1: (U^n, P^n) -> (U*, P*) (or the next state when time_order = 1)
+      for (int t = gtid; t < ncell; t += gthreads) {
+        const int i = t % a.nx, j = t / a.nx;
+        double v[4], pv[KA];
+        cell_stage_mat<DIM2, MUSCL, false, KA>(a, u, pk, u, pk, i, j, a.heun ? 0u : rb,
+                                           a.heun ? nullptr : gb, lam_x, lam_y, v, pv, bad);
+        const int64_t o = (int64_t)j * a.pitch + i;
+        double* out = a.heun ? a.us : u2;
+        double* pout = a.heun ? a.ps : pk2;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) __stcg(out + q * a.fstride + o, v[q]);
+#pragma unroll
+        for (int q = 0; q < KA; ++q)
+          if (q < a.nmat) __stcg(pout + q * a.fstride + o, pv[q]);
+        if (a.heun) {
+          const double eint = internal_energy(v[0], v[1], v[2], v[3]);
+          if (!(v[0] > 0.0) || !(eint > 0.0)) bad = true;
+        } else {
+          finish_mat(v, pv);
+        }
+      }
+    } else if (cellw) {
       // stage 1: U^n -> U* (or U^{n+1} when time_order = 1)
       for (int t = gtid; t < ncell; t += gthreads) {
         const int i = t % a.nx, j = t / a.nx;
@@ -450,7 +872,21 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       // (releases U* and the stage-1 faces)
       sync_all();
       // stage 2: U* -> U^{n+1} from U^n with 0.5 (F^n + F*)
-      if (cellw) {
+      if (MAT && cellw) {
+        for (int t = gtid; t < ncell; t += gthreads) {
+          const int i = t % a.nx, j = t / a.nx;
+          double v[4], pv[KA];
+          cell_stage_mat<DIM2, MUSCL, true, KA>(a, a.us, a.ps, u, pk, i, j, rb, gb, lam_x, lam_y, v,
+                                            pv, bad);
+          const int64_t o = (int64_t)j * a.pitch + i;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) __stcg(u2 + q * a.fstride + o, v[q]);
+#pragma unroll
+          for (int q = 0; q < KA; ++q)
+            if (q < a.nmat) __stcg(pk2 + q * a.fstride + o, pv[q]);
+          finish_mat(v, pv);
+        }
+      } else if (cellw) {
         for (int t = gtid; t < ncell; t += gthreads) {
           const int i = t % a.nx, j = t / a.nx;
           double v[4];
@@ -468,16 +904,18 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
     rk = wred(rk, mx);
     mr = wred(mr, mn);
     me = wred(me, mn);
+    if (MAT) mpk = wred(mpk, mn);
     const bool wbad = __any_sync(0xffffffffu, bad), wdt = __any_sync(0xffffffffu, dtbad);
     if ((tid & 31) == 0) {
       if (rk) atomicMax(&sh.rate, rk);
       if (mr != 0x7ff0000000000000ull) atomicMin(&sh.min_r, mr);
       if (me != 0x7ff0000000000000ull) atomicMin(&sh.min_e, me);
+      if (MAT && mpk != ~0ull) atomicMin(&sh.min_pk, mpk);
       if (wbad) sh.fail = 1;
       if (wdt) sh.dtfail = 1;
     }
     __syncthreads();
-    unsigned long long* const gp = GRID ? a.gpart + par * 5 * SMALL_MAX_GRID : nullptr;
+    unsigned long long* const gp = GRID ? a.gpart + par * SMALL_NPART * SMALL_MAX_GRID : nullptr;
     if constexpr (GRID) {
       if (tid == 0) {
         __stcg(gp + rank, sh.rate);
@@ -485,6 +923,7 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
         __stcg(gp + 2 * SMALL_MAX_GRID + rank, sh.min_e);
         __stcg(gp + 3 * SMALL_MAX_GRID + rank, (unsigned long long)sh.fail);
         __stcg(gp + 4 * SMALL_MAX_GRID + rank, (unsigned long long)sh.dtfail);
+        __stcg(gp + 5 * SMALL_MAX_GRID + rank, sh.min_pk);
       }
     } else if (tid < nblk) {   // one thread per destination block
       st_remote(remote(&sh.p_rate[par][rank], tid), sh.rate);
@@ -492,12 +931,14 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
       st_remote(remote(&sh.p_min_e[par][rank], tid), sh.min_e);
       st_remote(remote(&sh.p_fail[par][rank], tid), sh.fail);
       st_remote(remote(&sh.p_dtfail[par][rank], tid), sh.dtfail);
+      st_remote(remote(&sh.p_min_pk[par][rank], tid), sh.min_pk);
     }
     // (releases U^{n+1}, the boundary faces and the partials)
     sync_all();
     if constexpr (GRID) {
       // every block combines all blocks' partials (one slot per thread, then warps)
       unsigned long long vr = 0ull, vm = 0x7ff0000000000000ull, ve = 0x7ff0000000000000ull;
+      unsigned long long vp = ~0ull;
       int vf = 0, vd = 0;
       for (uint32_t b = tid; b < nblk; b += blockDim.x) {
         const unsigned long long r_ = __ldcg(gp + b), m_ = __ldcg(gp + SMALL_MAX_GRID + b);
@@ -507,7 +948,10 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
         ve = e_ < ve ? e_ : ve;
         vf |= (int)__ldcg(gp + 3 * SMALL_MAX_GRID + b);
         vd |= (int)__ldcg(gp + 4 * SMALL_MAX_GRID + b);
+        const unsigned long long p_ = __ldcg(gp + 5 * SMALL_MAX_GRID + b);
+        vp = p_ < vp ? p_ : vp;
       }
+      vp = wred(vp, mn);
       vr = wred(vr, mx);
       vm = wred(vm, mn);
       ve = wred(ve, mn);
@@ -517,6 +961,7 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
         if (vr) atomicMax(&sh.g_rate, vr);
         if (vm != 0x7ff0000000000000ull) atomicMin(&sh.g_min_r, vm);
         if (ve != 0x7ff0000000000000ull) atomicMin(&sh.g_min_e, ve);
+        if (vp != ~0ull) atomicMin(&sh.g_min_pk, vp);
         if (vf) sh.g_fail = 1;
         if (vd) sh.g_dtfail = 1;
       }
@@ -524,11 +969,13 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
     }
     if (tid == 0) {
       unsigned long long rt = 0ull, m_r = 0x7ff0000000000000ull, m_e = 0x7ff0000000000000ull;
+      unsigned long long m_p = ~0ull;
       int fail = 0, dtf = 0;
       if constexpr (GRID) {
         rt = sh.g_rate;
         m_r = sh.g_min_r;
         m_e = sh.g_min_e;
+        m_p = sh.g_min_pk;
         fail = sh.g_fail;
         dtf = sh.g_dtfail;
       } else {
@@ -536,6 +983,7 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
           rt = sh.p_rate[par][b] > rt ? sh.p_rate[par][b] : rt;
           m_r = sh.p_min_r[par][b] < m_r ? sh.p_min_r[par][b] : m_r;
           m_e = sh.p_min_e[par][b] < m_e ? sh.p_min_e[par][b] : m_e;
+          m_p = sh.p_min_pk[par][b] < m_p ? sh.p_min_pk[par][b] : m_p;
           fail |= sh.p_fail[par][b];
           dtf |= sh.p_dtfail[par][b];
         }
@@ -548,7 +996,10 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
         r.time = r.hits ? a.limit : c.time + dt;
         r.min_rho = __longlong_as_double((long long)m_r);
         r.min_eint = __longlong_as_double((long long)m_e);
-        r.min_p_mat = __longlong_as_double(0x7ff0000000000000ll);
+        // (MAT) min p decoded from its order key; +inf (min_p's initial value) if none
+        r.min_p_mat = m_p == ~0ull ? __longlong_as_double(0x7ff0000000000000ll)
+                      : __longlong_as_double(
+                            (long long)((m_p >> 63) ? (m_p & 0x7fffffffffffffffull) : ~m_p));
         r.status = 0;
         if (lead) a.rec[n] = r;
         StepCtl nx_;
@@ -567,6 +1018,9 @@ __global__ void __launch_bounds__(SMALL_THREADS + 32, 1) k_small_run(SmallArgs a
     double* t = u;
     u = u2;
     u2 = t;
+    t = pk;
+    pk = pk2;
+    pk2 = t;
   }
   if (!GRID && lead && !cellw && pend >= 0) outflow_sums<DIM2>(a, sbnd + pend_par * a.ob, pend_dt);
   // the step that stopped the batch: 1 failed (the host re-runs it stage-wise),
@@ -636,7 +1090,23 @@ bool small_fast_enabled() {
 // cannot co-schedule them), each block on its own SM -- or, in grid mode, a cooperative
 // grid of up to one block per SM (every block co-resident, grid barriers).
 template <bool DIM2, bool MUSCL>
-cudaError_t launch_small(const SmallArgs& a, int want, bool fast, bool grid, cudaStream_t st) {
+cudaError_t launch_small(const SmallArgs& a, int want, bool fast, bool grid, bool mat,
+                         cudaStream_t st) {
+  // (the material kernels: the IEEE arithmetic only)
+  // (array bounds of 4 or 8 materials: registers for the common 2-4)
+  auto pick = [&](bool g) {
+    if (mat && a.nmat <= 4)
+      return g ? k_small_run<DIM2, MUSCL, false, true, 4>
+               : k_small_run<DIM2, MUSCL, false, false, 4>;
+    if (mat)
+      return g ? k_small_run<DIM2, MUSCL, false, true, 8>
+               : k_small_run<DIM2, MUSCL, false, false, 8>;
+    if (fast)
+      return g ? k_small_run<DIM2, MUSCL, true, true, 0>
+               : k_small_run<DIM2, MUSCL, true, false, 0>;
+    return g ? k_small_run<DIM2, MUSCL, false, true, 0>
+             : k_small_run<DIM2, MUSCL, false, false, 0>;
+  };
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(SMALL_THREADS + 32);
   cfg.stream = st;
@@ -644,7 +1114,7 @@ cudaError_t launch_small(const SmallArgs& a, int want, bool fast, bool grid, cud
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (grid) {
-    auto kern = fast ? k_small_run<DIM2, MUSCL, true, true> : k_small_run<DIM2, MUSCL, false, true>;
+    auto kern = pick(true);
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -656,7 +1126,7 @@ cudaError_t launch_small(const SmallArgs& a, int want, bool fast, bool grid, cud
     at[0].val.cooperative = 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
   }
-  auto kern = fast ? k_small_run<DIM2, MUSCL, true, false> : k_small_run<DIM2, MUSCL, false, false>;
+  auto kern = pick(false);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   const size_t smem = 2 * (size_t)a.ob * sizeof(double);
@@ -752,7 +1222,7 @@ void small_alloc(lf_handle* h, int steps) {
   }
   if (!m->gpart && use_grid_mode(h)) {
     const int64_t ob = 8 * (int64_t)s.L.ny + (h->dim2 ? 8 * (int64_t)s.L.nx : 0);
-    SK(cudaMalloc(&m->gpart, 2 * 5 * SMALL_MAX_GRID * sizeof(unsigned long long)));
+    SK(cudaMalloc(&m->gpart, 2 * SMALL_NPART * SMALL_MAX_GRID * sizeof(unsigned long long)));
     SK(cudaMalloc(&m->bhist, (size_t)SMALL_GRID_BATCH * ob * sizeof(double)));
     SK(cudaMalloc(&m->sums, (size_t)SMALL_GRID_BATCH * 8 * sizeof(double)));
   }
@@ -775,7 +1245,7 @@ int run_small(lf_handle* h, int n, double cfl, double limit, double t_final, dou
   if (!m->valid) {
     const Scalars sc = rate_of_current(h);
     m->ctl_host->rate_bits = sc.rate_bits;
-    m->ctl_host->dtfail = sc.fail_dt != LLONG_MAX;
+    m->ctl_host->dtfail = sc.fail_dt != LLONG_MAX || sc.fail_frac != LLONG_MAX;
     m->valid = true;
   } else {
     SK(cudaMemcpyAsync(m->ctl_host, m->ctl, sizeof(StepCtl), cudaMemcpyDeviceToHost, s.stream));
@@ -816,6 +1286,15 @@ int run_small(lf_handle* h, int n, double cfl, double limit, double t_final, dou
   const bool grid = use_grid_mode(h);
   a.gpart = m->gpart;
   a.bhist = m->bhist;
+  const bool mat = h->mc.n > 0;
+  a.nmat = h->mc.n;
+  for (int k = 0; k < 8; ++k) a.gam[k] = k < h->mc.n ? h->mc.gamma[k] : 1.5;
+  a.p = mat ? s.P + s.L.origin() : nullptr;
+  a.p2 = mat ? s.P2 + s.L.origin() : nullptr;
+  a.ps = mat ? s.Ps + s.L.origin() : nullptr;
+  a.y0 = mat ? s.Y[0] + s.L.origin() : nullptr;
+  a.usx0 = mat ? s.USX[0] : nullptr;
+  a.usy0 = mat ? s.USY[0] : nullptr;
   const bool muscl = h->d.spatial_order >= 2;
   if (ms) SK(cudaEventRecord(m->e0, s.stream));
   count_launch();
@@ -824,14 +1303,14 @@ int run_small(lf_handle* h, int n, double cfl, double limit, double t_final, dou
   cudaError_t le;
   // the fast exact arithmetic where its proofs hold (beta >= 1 for sweby_fast, gamma - 1
   // in the constant box); a cell outside the cell box flags the step (stage-wise re-run)
-  const bool fast = small_fast_enabled() && !h->small_ieee && h->d.beta >= 1.0 && h->k.gm1 >= 0x1p-14 &&
+  const bool fast = !mat && small_fast_enabled() && !h->small_ieee && h->d.beta >= 1.0 && h->k.gm1 >= 0x1p-14 &&
                     h->k.gm1 < 0x1p6 && h->k.gamma < 0x1p7;
   if (h->dim2)
-    le = muscl ? launch_small<true, true>(a, want, fast, grid, s.stream)
-               : launch_small<true, false>(a, want, fast, grid, s.stream);
+    le = muscl ? launch_small<true, true>(a, want, fast, grid, mat, s.stream)
+               : launch_small<true, false>(a, want, fast, grid, mat, s.stream);
   else
-    le = muscl ? launch_small<false, true>(a, want, fast, grid, s.stream)
-               : launch_small<false, false>(a, want, fast, grid, s.stream);
+    le = muscl ? launch_small<false, true>(a, want, fast, grid, mat, s.stream)
+               : launch_small<false, false>(a, want, fast, grid, mat, s.stream);
   SK(le);
   if (grid) {   // the batch's boundary-outflow sums, in step order
     count_launch(2);
@@ -859,7 +1338,10 @@ int run_small(lf_handle* h, int n, double cfl, double limit, double t_final, dou
     if (m->rec_host[i].status == 1) *failed_at = i;
     break;
   }
-  if (done & 1) std::swap(s.U, s.U2);   // the kernel ping-pongs U and U2 once per step
+  if (done & 1) {   // the kernel ping-pongs U and U2 (and the partials) once per step
+    std::swap(s.U, s.U2);
+    if (mat) std::swap(s.P, s.P2);
+  }
   fused_invalidate(h);   // (also clears m->valid)
   m->valid = *failed_at < 0;
   h->rate_valid = false;
@@ -867,30 +1349,34 @@ int run_small(lf_handle* h, int n, double cfl, double limit, double t_final, dou
   return done;
 }
 
-void to_out(const StepRec& r, int64_t step, double gm1, lf_step_out* o) {
+void to_out(const StepRec& r, int64_t step, double gm1, lf_step_out* o, bool mat) {
   o->dt = r.dt;
   o->hits_limit = r.hits;
   o->time = r.time;
   o->step = step;
   o->min_rho = r.min_rho;
-  o->min_p = gm1 * r.min_eint;
+  o->min_p = mat ? r.min_p_mat : gm1 * r.min_eint;
 }
 
 }  // namespace
 
-// LF_PATH_SMALL: one material, one slab on one device (no NCCL), and a grid small
-// enough for one block (AUTO: up to SMALL_AUTO_CELLS cells, measured by
-// tools/small_sweep.py against the two-pass / stage-wise paths).
+// LF_PATH_SMALL: up to 8 materials (partials resident), one slab on one device (no
+// NCCL), up to SMALL_MAX_CELLS cells (AUTO: the crossovers in small.h, measured by
+// tools/small_sweep.py and tools/small_mat_sweep.py).
 bool small_supported(lf_handle* h) {
-  if (h->mc.n > 0 || h->slabs.size() != 1 || h->nccl) return false;
+  if (h->mc.n > SMALL_MAX_MAT || (h->mc.n > 0 && !h->partials_ready) || h->slabs.size() != 1 ||
+      h->nccl)
+    return false;
   // (the kernel reads ghosts through an index map whose sources are interior cells)
   if (h->d.nx < 2 || (h->dim2 && h->d.ny < 2)) return false;
   return (int64_t)h->d.nx * h->d.ny <= SMALL_MAX_CELLS;
 }
 
 bool prefer_small(lf_handle* h) {
-  return h->path == LF_PATH_AUTO && small_supported(h) &&
-         (int64_t)h->d.nx * h->d.ny <= (h->dim2 ? SMALL_AUTO_CELLS_2D : SMALL_AUTO_CELLS_1D);
+  const int64_t lim = !h->dim2        ? SMALL_AUTO_CELLS_1D
+                      : h->mc.n > 0 ? SMALL_AUTO_CELLS_2D_MAT
+                                    : SMALL_AUTO_CELLS_2D;
+  return h->path == LF_PATH_AUTO && small_supported(h) && (int64_t)h->d.nx * h->d.ny <= lim;
 }
 
 void small_invalidate(lf_handle* h) {
@@ -923,7 +1409,7 @@ int small_heun(lf_handle* h, double cfl, double time, double limit, int64_t step
   if (outflow) std::memcpy(acc, outflow, sizeof acc);
   if (run_small(h, 1, cfl, limit, limit, time, acc, &failed_at, nullptr) == 1) {
     if (outflow) std::memcpy(outflow, acc, sizeof acc);
-    if (out) to_out(sstate(h)->rec_host[0], step + 1, h->d.gamma - 1.0, out);
+    if (out) to_out(sstate(h)->rec_host[0], step + 1, h->d.gamma - 1.0, out, h->mc.n > 0);
     return 0;
   }
   // a check failed: the stage-wise kernels reproduce the reference's error
@@ -946,7 +1432,7 @@ int small_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* 
     const int done = run_small(h, batch, cfl, t_final, t_final, *time, outflow, &failed_at, nullptr);
     for (int i = 0; i < done; ++i) {
       *step += 1;
-      if (per_step) to_out(m->rec_host[i], *step, h->d.gamma - 1.0, &per_step[k + i]);
+      if (per_step) to_out(m->rec_host[i], *step, h->d.gamma - 1.0, &per_step[k + i], h->mc.n > 0);
       *time = m->rec_host[i].time;
     }
     k += done;

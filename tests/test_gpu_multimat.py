@@ -209,7 +209,8 @@ def test_five_to_eight_materials_on_the_two_pass_kernels(cuda, n_mat, devices):
     c = _many_materials_case(n_mat)
     f0, m0 = CS.regions_field(c)
     s = LagfluxSolver(c.grid, c.bc, c.gamma, c.params,
-                      materials=MM.make_material_set(c.material_gammas), devices=devices)
+                      materials=MM.make_material_set(c.material_gammas), devices=devices,
+                      path="twopass")
     st = G.SolverState(field=f0.copy())
     s.heun_step(st, G.TimeControls(c.cfl, c.t_final), c.t_final,
                 MM.MaterialCells(c.grid, n_mat, m0.partial.copy()))
@@ -217,7 +218,7 @@ def test_five_to_eight_materials_on_the_two_pass_kernels(cuda, n_mat, devices):
     s.close()
     ref, rmat = run_oracle_mat(c)
     for use_advance in (False, True):
-        state, mat = run_gpu_mat(c, devices=devices, use_advance=use_advance)
+        state, mat = run_gpu_mat(c, devices=devices, use_advance=use_advance, path="twopass")
         g = c.grid
         what = f"{n_mat} materials, {len(devices)} slab(s), advance={use_advance}"
         assert_fields_equal(g.interior(state.field), g.interior(ref.field), what)

@@ -60,11 +60,16 @@ def test_auto_picks_the_small_path_where_it_is_faster(cuda):
     assert resolved(CS.Case("s", g1, G.BoundaryCondition(), 1.4, G.SchemeParams(), 0.5, 0.2,
                             G.INT64_MAX, "riemann_x")) == "small"
     assert resolved(CS.quadrant(64, 1), devices=(0, 0)) == "twopass"   # y-slabs
-    tp = CS.triple_point(64, 28, 1)
-    s = LagfluxSolver(tp.grid, tp.bc, tp.gamma, tp.params,
-                      materials=MM.make_material_set(tp.material_gammas))
-    assert s.resolved_path() != "small"                      # materials: not on this path
-    s.close()
+    # materials (once the partial densities are resident): up to 2^15 cells in 2D
+    for (nx, ny), want in (((64, 28), "small"), ((256, 200), "twopass")):
+        tp = CS.triple_point(nx, ny, 1)
+        f0, m0 = CS.regions_field(tp)
+        s = LagfluxSolver(tp.grid, tp.bc, tp.gamma, tp.params,
+                          materials=MM.make_material_set(tp.material_gammas))
+        s.heun_step(G.SolverState(field=f0.copy()), G.TimeControls(tp.cfl, tp.t_final),
+                    tp.t_final, MM.MaterialCells(tp.grid, len(tp.material_gammas), m0.partial.copy()))
+        assert s.resolved_path() == want, (nx, ny)
+        s.close()
 
 
 # cells per grid: 1 block (224 cell threads) .. 16 blocks .. beyond (strided cells)
@@ -176,3 +181,39 @@ def test_grid_mode_batches_and_1d(cuda):
     c1 = CS.Case("s", g, G.BoundaryCondition(G.REFLECTIVE, G.TRANSMISSIVE), 1.4, G.SchemeParams(),
                  0.5, 0.2, 40, "riemann_x")
     _check(c1, 40, _run(c1, 40), "1D 65536")
+
+
+# ---------------------------------------------------------------- multimaterial
+from test_oracle_multimat import MAT_CASES, run_oracle_mat  # noqa: E402
+from test_gpu_multimat import run_gpu_mat, _many_materials_case  # noqa: E402
+
+
+@pytest.mark.parametrize("name", list(MAT_CASES))
+@pytest.mark.parametrize("advance", [False, True])
+def test_materials_golden_cases_on_the_small_path(cuda, name, advance):
+    """The multimaterial goldens (1D contacts, triple point 70x30, four-material quadrant,
+    first order) on the small path: field, partials, records, outflow equal the oracle."""
+    c = MAT_CASES[name]
+    ref, rmat = run_oracle_mat(c)
+    state, mat = run_gpu_mat(c, use_advance=advance, path="small")
+    g = c.grid
+    assert_fields_equal(g.interior(state.field), g.interior(ref.field), name)
+    assert_fields_equal(g.interior(mat.partial), g.interior(rmat.partial), name + "/partials")
+    assert np.array_equal(diag_array(state)[:, :4], diag_array(ref)[:, :4]), name
+    assert np.array_equal(np.array(state.boundary_outflow), np.array(ref.boundary_outflow))
+
+
+@pytest.mark.parametrize("n_mat", [2, 5, 8])
+@pytest.mark.parametrize("mode", ["auto", "grid"])
+def test_many_materials_on_the_small_path(cuda, n_mat, mode):
+    c = _many_materials_case(n_mat)
+    if mode == "grid":   # a grid larger than one cluster's worth of cells
+        c = CS.MatCase(c.name, G.make_grid_2d(96, 60, 0.0, 1.0, 0.0, 0.625), c.bc, c.gamma,
+                       c.material_gammas, c.regions, c.params, c.cfl, c.t_final, 6)
+    ref, rmat = run_oracle_mat(c)
+    state, mat = run_gpu_mat(c, use_advance=True, path="small")
+    g = c.grid
+    assert_fields_equal(g.interior(state.field), g.interior(ref.field), f"{n_mat} {mode}")
+    assert_fields_equal(g.interior(mat.partial), g.interior(rmat.partial), f"{n_mat} {mode}")
+    assert np.array_equal(diag_array(state)[:, :4], diag_array(ref)[:, :4])
+    assert np.array_equal(np.array(state.boundary_outflow), np.array(ref.boundary_outflow))
