@@ -63,21 +63,21 @@ enum {
 };
 
 /* Heun-step implementation for lf_heun_step / lf_advance (all give identical results):
- *   AUTO     SMALL for one-material grids of up to 2^17 cells in 2D and every 1D grid (up
- *            to 2^22 cells) on one device (BASELINE config 1); FUSED for slabs of 2^23 cells or more
+ *   AUTO     SMALL for grids of up to 2^17 cells in 2D (2^15 with materials) and every 1D
+ *            grid (up to 2^22 cells) on one device (BASELINE config 1); FUSED for slabs of 2^23 cells or more
  *            (2^22 in LF_MATH_CONTRACT; Heun, no materials: BASELINE configs 3-5), TWOPASS
  *            in between, for time_order 1 and for materials; FUSED also when the two-pass
  *            scratch does not fit in device memory.  lf_resolved_path reports the choice.
  *   FUSED    one kernel per step (U^n read once, U^{n+1} written once)
  *   STAGED   the reference's phase structure, one kernel per loop (also the
- *            exact diagnosis path for every failure, euler_stage, 1D grids with
- *            materials and more than 8 materials)
+ *            exact diagnosis path for every failure, euler_stage and more than 8
+ *            materials)
  *   TWOPASS  predictor and corrector as two warp-independent streaming kernels
  *            (1-8 materials included)
  *   SMALL    a whole lf_advance batch (up to 4096 steps) in one launch of one thread-block
  *            cluster (up to 16 blocks), or of one cooperative grid beyond 16 x 224 cells
- *            (batches of 256 steps): one material, one slab, nx >= 2 (and ny >= 2 in 2D),
- *            up to 2^22 cells; the reference's bits */
+ *            (batches of 256 steps): up to 8 materials, one slab, nx >= 2 (and ny >= 2
+ *            in 2D), up to 2^22 cells; the reference's bits */
 enum { LF_PATH_AUTO = 0, LF_PATH_FUSED = 1, LF_PATH_STAGED = 2, LF_PATH_TWOPASS = 3,
        LF_PATH_SMALL = 4 };
 /* Arithmetic of the fast kernels (two-pass and fused).  LF_MATH_EXACT (default): the
@@ -163,7 +163,8 @@ int lf_download(lf_handle* h, double* const field[4], int64_t ld, int fill_ghost
  * mixed-cell gamma of each cell (each face side its own EOS), reports a fraction
  * outside [0,1] beyond round-off as LF_ERR_FRACTION, and returns the min
  * pressure from the fresh partials.  The two-pass material kernels run these
- * steps for 1-8 materials in 2D, the stage-wise kernels otherwise (1D, > 8).
+ * steps for 1-8 materials in 2D, the small-grid path for 1D and small 2D grids, the
+ * stage-wise kernels for more than 8.
  * Partials: n arrays in the ghosted field layout (partials[k][j*ld + i],
  * ld >= nx + 4); interior cells are transferred. */
 int lf_set_materials(lf_handle* h, int n, const double* gammas);
