@@ -43,11 +43,14 @@ def run_gpu_mat(c, devices=(0,), field=None, partial=None, steps=None, use_advan
     return state, mat
 
 
+@pytest.mark.parametrize("path", ["auto", "twopass", "staged"])
 @pytest.mark.parametrize("name", list(MAT_CASES))
-def test_multimaterial_golden_bitwise(cuda, name):
+def test_multimaterial_golden_bitwise(cuda, name, path):
+    """(auto: the small-grid path on these grids; twopass: the two-pass material kernels
+    in 2D, the stage-wise kernels in 1D, where the two-pass kernels do not run)"""
     c = MAT_CASES[name]
     gold = load_golden(name)
-    state, mat = run_gpu_mat(c)
+    state, mat = run_gpu_mat(c, path=path)
     g = c.grid
     assert_fields_equal(g.interior(state.field), gold["final"], name)
     assert_fields_equal(g.interior(mat.partial), gold["final_partial"], name + "/partials")
