@@ -6,6 +6,12 @@
 namespace lfb {
 
 bool fused_supported(lf_handle* h);
+// LF_PATH_AUTO resolves to the one-kernel step (fused_step.cu); below this many cells
+// per slab the small-grid path (small.h) or the two-pass kernels are faster
+// (tools/chunk_sweep.py: 256^2 38 us per step against 28 on the small-grid path,
+// 320^2 42 against 48)
+constexpr int64_t FUSED_AUTO_MIN_CELLS = (int64_t)5 << 14;
+bool prefer_fused(lf_handle* h);
 int fused_heun(lf_handle* h, double cfl, double time, double limit, int64_t step,
                double* outflow, lf_step_out* out);
 int fused_advance(lf_handle* h, int nsteps, double cfl, double t_final, double* time,

@@ -122,18 +122,30 @@ bool fused_supported(lf_handle* h) {
   return true;
 }
 
-// LF_PATH_AUTO on large slabs: the one-kernel step.  From 2^23 cells per slab it is
-// the faster one (tools/path_sweep.py, round 2: Sedov 4096^2 11.7 vs 10.9 G
-// cell-updates/s, smooth 8192^2 13.7 vs 12.1, 16384^2 14.7 vs ~12); it moves 64 B per
-// cell-update instead of 290 and stays at the full clock where the two-pass step
-// meets the board's power cap.  Below, the two-pass kernels fill the GPU better
-// (1024^2: one wave; 2048^2 about even).  In the contract arithmetic the fused step
-// already wins at 2048^2 (13.5 vs 12.4), so its threshold is 2^22.
-static bool prefer_fused(lf_handle* h) {
-  if (h->path != LF_PATH_AUTO || h->d.time_order < 2 || h->mc.n > 0) return false;
-  const int64_t min_cells = (int64_t)1 << (h->math == LF_MATH_CONTRACT ? 22 : 23);
-  for (auto& s : h->slabs)
-    if ((int64_t)s.L.nx * s.L.ny < min_cells) return false;
+// LF_PATH_AUTO, one material, Heun: the one-kernel step on every 2D slab past the
+// small-grid path's range.  From 2^23 cells per slab (2^22 in the contract arithmetic)
+// it is clearly the faster one (tools/path_sweep.py, round 2: Sedov 4096^2 11.7 vs 10.9
+// G cell-updates/s, smooth 8192^2 13.7 vs 12.1, 16384^2 14.7 vs ~12): it moves 64 B per
+// cell-update instead of 290 and stays at the full clock where the two-pass step meets
+// the board's power cap.  Below that, with row chunks as short as the cost model in
+// fused_alloc likes (a 1024^2 step is one wave of 288 blocks of 32 rows), it is ahead
+// of or level with the two-pass kernels down to 320^2 (tools/chunk_sweep.py,
+// profiles/r02_chunk_sweep.json: 512^2 4.3 vs 3.0 G/s, 768^2 6.2 vs 5.5, quadrant
+// 1024^2 8.1 vs 7.8, smooth 1024^2 7.9 vs 8.3, 2048^2 10.5 vs 10.6; in the contract
+// arithmetic ahead everywhere), and it needs no U* / F^n scratch.  Narrow grids, whose
+// last 120-column strip would be mostly empty, stay on the two-pass kernels' 28-column
+// warp strips.
+bool prefer_fused(lf_handle* h) {
+  if (h->path != LF_PATH_AUTO || !h->dim2 || h->d.time_order < 2 || h->mc.n > 0) return false;
+  if (!(h->d.beta >= 1.0)) return false;   // (stage-wise: api.cu use_fused)
+  const int64_t big = (int64_t)1 << (h->math == LF_MATH_CONTRACT ? 22 : 23);
+  const int strips = (h->d.nx + FUSED_TXO - 1) / FUSED_TXO;
+  const bool wide = 5 * (int64_t)h->d.nx >= 4 * (int64_t)strips * FUSED_TXO;   // >= 80 % full
+  for (auto& s : h->slabs) {
+    const int64_t cells = (int64_t)s.L.nx * s.L.ny;
+    if (cells >= big) continue;
+    if (!(wide && cells > FUSED_AUTO_MIN_CELLS)) return false;
+  }
   return true;
 }
 
@@ -210,9 +222,11 @@ static void fused_alloc(lf_handle* h, int steps) {
     const int64_t nslab = (int64_t)h->slabs.size();   // in-process slabs share the device
     int best_rows = std::max(ny_local, 1);
     int64_t best_cost = INT64_MAX;
+    int min_rows = 4;
+    if (const char* e = getenv("LF_FUSED_MIN_ROWS")) min_rows = std::max(1, atoi(e));
     for (int chunks = 1; chunks <= 512; ++chunks) {
       const int rows = (ny_local + chunks - 1) / chunks;
-      if (rows < 64 && chunks > 1) break;
+      if (rows < min_rows && chunks > 1) break;
       const int64_t blocks = nslab * strips * ((ny_local + rows - 1) / rows);
       const int64_t cost = ((blocks + cap - 1) / cap) * (rows + 9);
       if (cost < best_cost) {

@@ -47,6 +47,7 @@
 #include <string>
 
 #include "face_fast.cuh"
+#include "fused.h"
 #include "fused_common.cuh"
 #include "handle.h"
 #include "reduce.cuh"
@@ -1376,7 +1377,11 @@ bool prefer_small(lf_handle* h) {
   const int64_t lim = !h->dim2        ? SMALL_AUTO_CELLS_1D
                       : h->mc.n > 0 ? SMALL_AUTO_CELLS_2D_MAT
                                     : SMALL_AUTO_CELLS_2D;
-  return h->path == LF_PATH_AUTO && small_supported(h) && (int64_t)h->d.nx * h->d.ny <= lim;
+  if (!(h->path == LF_PATH_AUTO && small_supported(h) && (int64_t)h->d.nx * h->d.ny <= lim))
+    return false;
+  // the top of the 2D range (5 * 2^14 .. 2^17 cells) goes to the one-kernel step where
+  // that applies (fused.h FUSED_AUTO_MIN_CELLS); narrow grids stay here
+  return !(prefer_fused(h) && fused_supported(h));
 }
 
 void small_invalidate(lf_handle* h) {

@@ -85,14 +85,17 @@ def test_large_initial_state_matches_host(cuda):
 
 
 def test_auto_path_by_size_and_device_memory(cuda):
-    """LF_PATH_AUTO: the two-pass kernels below 2^23 cells per slab (2^22 in the contract
-    arithmetic), the one-kernel step above (fused_step.cu prefer_fused); at
+    """LF_PATH_AUTO: the one-kernel step on every 2D slab past the small-grid path's range
+    whose 120-column strips are at least 80 % full, the two-pass kernels on narrower ones
+    below 2^23 cells per slab (2^22 in the contract arithmetic; fused_step.cu prefer_fused); at
     BASELINE config 5's 32768^2 only the one-kernel step fits one B200 (the two-pass
     scratch is 206 GB) -- periodic boundaries conserve mass and energy over its steps."""
-    for n, math, want in ((2048, "exact", "twopass"), (4096, "exact", "fused"),
-                          (1024, "contract", "twopass"), (2048, "contract", "fused"),
-                          (16384, "exact", "fused")):
-        case = CS.smooth(n, 1)
+    for n, ny, math, want in ((2048, 2048, "exact", "fused"), (4096, 4096, "exact", "fused"),
+                              (1024, 1024, "contract", "fused"), (512, 512, "exact", "fused"),
+                              (130, 4096, "exact", "twopass"), (130, 32768, "exact", "twopass"),
+                              (130, 65536, "exact", "fused"), (130, 32768, "contract", "fused"),
+                              (16384, 16384, "exact", "fused")):
+        case = CS.smooth(n, 1, ny=ny)
         s = LagfluxSolver(case.grid, case.bc, case.gamma, case.params, math=math)
         s.init_fourier(G.SolverState(field=None), case.seed)
         assert s.resolved_path() == want, (n, math)

@@ -55,7 +55,14 @@ def test_auto_picks_the_small_path_where_it_is_faster(cuda):
     assert resolved(CS.sod()) == "small"                      # BASELINE config 1
     assert resolved(CS.quadrant(128, 1)) == "small"
     assert resolved(CS.quadrant(256, 1)) == "small"                # (grid mode)
-    assert resolved(CS.quadrant(512, 1)) == "twopass"
+    assert resolved(CS.quadrant(320, 1)) == "fused"               # (from 5 * 2^14 cells)
+    assert resolved(CS.quadrant(512, 1)) == "fused"
+    q512 = CS.quadrant(512, 1)
+    assert resolved(CS.Case("q", q512.grid, q512.bc, 1.4, G.SchemeParams(time_order=1), 0.45, 1e300,
+                            1, "quadrant")) == "twopass"           # (the fused step is Heun)
+    narrow = G.make_grid_2d(130, 800, 0.0, 1.0, 0.0, 1.0)         # a mostly empty second strip
+    assert resolved(CS.Case("n", narrow, G.BoundaryCondition(), 1.4, G.SchemeParams(), 0.5, 0.2,
+                            G.INT64_MAX, "quadrant")) == "small"
     g1 = G.make_grid_1d(100_000, 0.0, 1.0)
     assert resolved(CS.Case("s", g1, G.BoundaryCondition(), 1.4, G.SchemeParams(), 0.5, 0.2,
                             G.INT64_MAX, "riemann_x")) == "small"
