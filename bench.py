@@ -336,7 +336,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    resolved = solver.resolved_path()   # auto: the fused step from 2^23 cells per slab
+    resolved = solver.resolved_path()   # auto: the fused one-kernel step on this grid
     # warm-up
     solver.advance(state, controls, args.warmup)
     barrier()

@@ -64,9 +64,11 @@ enum {
 
 /* Heun-step implementation for lf_heun_step / lf_advance (all give identical results):
  *   AUTO     SMALL for grids of up to 2^17 cells in 2D (2^15 with materials) and every 1D
- *            grid (up to 2^22 cells) on one device (BASELINE config 1); FUSED for slabs of 2^23 cells or more
- *            (2^22 in LF_MATH_CONTRACT; Heun, no materials: BASELINE configs 3-5), TWOPASS
- *            in between, for time_order 1 and for materials; FUSED also when the two-pass
+ *            grid (up to 2^22 cells) on one device (BASELINE config 1); FUSED for every
+ *            larger 2D slab (Heun, no materials: BASELINE configs 2-5) -- always from 2^23
+ *            cells (2^22 in LF_MATH_CONTRACT), and below that from 5 * 2^14 cells when nx
+ *            fills its 120-column strips to 80 % or more; TWOPASS for narrow mid-size
+ *            grids, for time_order 1 and for materials; FUSED also when the two-pass
  *            scratch does not fit in device memory.  lf_resolved_path reports the choice.
  *   FUSED    one kernel per step (U^n read once, U^{n+1} written once)
  *   STAGED   the reference's phase structure, one kernel per loop (also the
