@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <tuple>
 #include <stdexcept>
 #include <string>
@@ -78,7 +79,12 @@ struct FusedState {
   // a batch's launches are captured once per key and replayed; the key holds every
   // value the captured launches bake in (batch length, the control-record slot, every
   // state and scratch buffer as the batch starts -- euler_stage swaps U with U*, so
-  // U alone does not identify them --, the step parameters, the path)
+  // U alone does not identify them --, the step parameters, the path).  Capturing and
+  // instantiating costs ~8 us per kernel node against ~1 us saved per replayed node
+  // (tools/graph_sweep.py; quadrant 1024^2, 200 steps from cold: 31.9 ms with every
+  // batch captured at first sight, 25.6 ms launch by launch), so a batch runs launch by
+  // launch the first time its key is seen and is captured when the key comes back --
+  // only runs long enough to repeat a batch pay for graphs, and only they build them
   using GraphKey = std::tuple<int, int, const double*, const double*, const double*,
                               const double*, const double*, const double*, double, double,
                               double, int, int, int>;
@@ -87,21 +93,24 @@ struct FusedState {
     int launches = 0;   // kernels per replay (lf_launch_count)
   };
   std::map<GraphKey, Graph> graphs;
+  std::set<GraphKey> seen;   // keys that ran launch by launch once
   bool capturing = false;
 };
 
-// LF_GRAPHS=0 in the environment: enqueue every batch launch by launch (A/B)
-static bool graphs_enabled() {
-  static const bool on = [] {
+// LF_GRAPHS in the environment: 0 = enqueue every batch launch by launch (A/B),
+// 2 = capture a batch the first time its key is seen, 1 / unset = the second time
+static int graphs_mode() {
+  static const int mode = [] {
     const char* e = std::getenv("LF_GRAPHS");
-    return !(e && e[0] == '0');
+    return e && e[0] == '0' ? 0 : (e && e[0] == '2' ? 2 : 1);
   }();
-  return on;
+  return mode;
 }
 
 static void drop_graphs(FusedState* f) {
   for (auto& kv : f->graphs) cudaGraphExecDestroy(kv.second.exec);
   f->graphs.clear();
+  f->seen.clear();
 }
 
 static FusedState* fstate(lf_handle* h) { return reinterpret_cast<FusedState*>(h->fused); }
@@ -540,16 +549,25 @@ static int run_batch(lf_handle* h, int n, double cfl, double limit, double t_fin
   // 122); on the triple point (1.8M cells, 3 materials) the replay measured 9 % slower
   // than the stream launches (the side stream's low priority is not part of a graph)
   const bool small = (int64_t)h->d.nx * h->d.ny <= ((int64_t)1 << 20) && h->mc.n == 0;
-  if (!timing && n >= 8 && small && graphs_enabled() && h->slabs.size() == 1 && !h->nccl) {
+  bool graph = !timing && n >= 8 && small && graphs_mode() != 0 && h->slabs.size() == 1 && !h->nccl;
+  FusedState::GraphKey key{};
+  if (graph) {
+    key = FusedState::GraphKey{n,        f->cur,  s0.U,  s0.U2,   s0.Us,   s0.P,     s0.P2,
+                               s0.Ps,    cfl,     limit, t_final, h->math, use_twopass(h) ? 1 : 0,
+                               h->tp_exact};
+    if (graphs_mode() == 1 && !f->graphs.count(key) && !f->seen.count(key)) {
+      if (f->seen.size() >= 64) f->seen.clear();
+      f->seen.insert(key);   // first sight: launch by launch
+      graph = false;
+    }
+  }
+  if (graph) {
     // CUDA graph of the whole batch (lf_advance batches; a single heun_step, whose
     // limit time may change from call to call, stays launch by launch): decide
     // everything that allocates or synchronises first, then capture once per key and
     // replay
     const bool twopass = use_twopass(h);
     if (!twopass) ensure_fk(h);
-    const FusedState::GraphKey key{n,        f->cur,  s0.U,  s0.U2,   s0.Us,   s0.P,     s0.P2,
-                                   s0.Ps,    cfl,     limit, t_final, h->math, twopass ? 1 : 0,
-                                   h->tp_exact};
     if (outsums)  // the first two steps' bnd slots: the previous batch's sums
       for (int b = 0; b < 2; ++b) FK(cudaStreamWaitEvent(s0.stream, f->ev_out[b], 0));
     auto it = f->graphs.find(key);
