@@ -25,6 +25,7 @@
 #include <array>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "lagflux/error.hpp"
 #include "lagflux/multimat.hpp"
@@ -142,6 +143,73 @@ class LagfluxSolver {
     }
     return o.dt;
   }
+
+  // The run.cpp:180-210 loop between two dump events, on the device (lf_advance): up
+  // to max_count heun_steps while state.time < limit_time, each with the reference's
+  // dt clipping against limit_time; dt, time and the diagnostics stay on the device
+  // and come back once per batch.  state.time / step / diagnostics / boundary_outflow
+  // are updated as by that many heun_step calls; state.field follows the residency
+  // rules above (auto_sync: uploaded before and copied back after the batch).
+  // Returns the steps taken; a failing step throws the reference's exception after
+  // the completed steps were recorded.
+  std::int64_t advance(SolverState& state, const TimeControls& controls, double limit_time,
+                       std::int64_t max_count, MaterialCells* materials = nullptr) {
+    if (n_mat_ == 0) materials = nullptr;
+    if (n_mat_ > 0 && materials == nullptr)
+      throw ConfigError("multimaterial step needs material storage");
+    if (auto_sync_ || !is_resident(state)) {
+      evict();
+      upload(state.field);
+      resident_ = &state;
+      resident_time_ = state.time;
+      resident_step_ = state.step;
+    }
+    if (materials != nullptr && (auto_sync_ || resident_mat_ != materials)) {
+      check(lf_upload_partials(h_, partial_ptrs(*materials).p, grid_.nxt()));
+      resident_mat_ = materials;
+    }
+    const double t_end = limit_time < controls.t_final ? limit_time : controls.t_final;
+    std::int64_t done = 0;
+    std::vector<lf_step_out> rec;
+    int rc = 0;
+    while (rc == 0 && done < max_count && state.time < t_end && state.step < controls.max_steps) {
+      std::int64_t chunk = max_count - done;
+      if (chunk > controls.max_steps - state.step) chunk = controls.max_steps - state.step;
+      if (chunk > 4096) chunk = 4096;
+      rec.resize(std::size_t(chunk));
+      int taken = 0;
+      double time = state.time;
+      std::int64_t step = state.step;
+      rc = lf_advance(h_, int(chunk), controls.cfl, t_end, &time, &step,
+                      state.boundary_outflow.data(), rec.data(), &taken);
+      for (int k = 0; k < taken; ++k)
+        state.diagnostics.push_back(
+            {rec[std::size_t(k)].step, rec[std::size_t(k)].time, rec[std::size_t(k)].dt,
+             rec[std::size_t(k)].min_rho, rec[std::size_t(k)].min_p});
+      state.time = time;
+      state.step = step;
+      resident_time_ = time;
+      resident_step_ = step;
+      done += taken;
+      if (taken < chunk) break;  // reached t_end (or failed: rc)
+    }
+    if (auto_sync_ || rc) {
+      download(state.field);  // a corrector failure leaves its output, as in the reference
+      if (materials != nullptr) lf_download_partials(h_, partial_ptrs(*materials).p, grid_.nxt());
+    }
+    check(rc);
+    return done;
+  }
+
+  // field_csv + write_text_file of the resident state (csv.cpp:26-83, run.cpp:162-168),
+  // derived and formatted from the device copy, byte-identical; with wait = false a
+  // host thread writes the file while the caller keeps stepping (wait_dumps joins)
+  void write_field_csv(const std::string& path, std::uint64_t digest, double time,
+                       bool wait = true) {
+    check(wait ? lf_write_field_csv(h_, path.c_str(), digest, time, threads_)
+               : lf_write_field_csv_async(h_, path.c_str(), digest, time, threads_));
+  }
+  void wait_dumps() { check(lf_wait_dumps(h_)); }
 
   // solver.cpp:434-480
   double compute_dt(const CellField& field, const TimeControls& controls, double time,

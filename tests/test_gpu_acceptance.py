@@ -21,6 +21,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF_DIR = os.path.join(ROOT, "oracle", "_ref")
 B200 = os.path.join(REF_DIR, "acceptance_b200")
+RESIDENT = os.path.join(REF_DIR, "acceptance_b200_resident")
 REF = os.path.join(REF_DIR, "acceptance_ref")
 CASES = os.path.join(REF_DIR, "cases")
 
@@ -47,14 +48,30 @@ def _criteria(stdout):
     return res
 
 
-def test_reference_acceptance_program_on_the_gpu_path(cuda, tmp_path):
-    for p in (B200, REF, CASES):
+_REF_RUN = {}
+
+
+def _reference_run(tmp_path_factory):
+    """The CPU program's output, run once per session."""
+    if not _REF_RUN:
+        d = tmp_path_factory.mktemp("acceptance_ref")
+        _REF_RUN["dir"] = d
+        _REF_RUN["res"] = _run(REF, d)
+    return _REF_RUN["dir"], _REF_RUN["res"]
+
+
+@pytest.mark.parametrize("exe", [B200, RESIDENT], ids=["solver_swapped", "driver_swapped"])
+def test_reference_acceptance_program_on_the_gpu_path(cuda, tmp_path, tmp_path_factory, exe):
+    """solver_swapped: the reference's run.cpp loop stepping the GPU solver (state.field
+    copied both ways every step).  driver_swapped: acceptance.cpp's run_hydro_case calls
+    also go to lagflux::b200::run_hydro_case (include/lagflux_b200_run.hpp): the state
+    stays on the device between dump events and the dumps are written from it."""
+    for p in (exe, REF, CASES):
         assert os.path.exists(p), f"{p} not built (make -C oracle acceptance)"
-    db, dr = tmp_path / "b200", tmp_path / "ref"
+    db = tmp_path / "b200"
     db.mkdir()
-    dr.mkdir()
-    rc_b, out_b, err_b = _run(B200, db)
-    rc_r, out_r, err_r = _run(REF, dr)
+    rc_b, out_b, err_b = _run(exe, db)
+    dr, (rc_r, out_r, err_r) = _reference_run(tmp_path_factory)
     print(out_b)
     cb, cr = _criteria(out_b), _criteria(out_r)
     assert sorted(cb) == list(range(1, 13)), out_b + err_b
