@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <utility>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -261,6 +262,53 @@ int main() {
       eb = e.what();
     }
     expect(!ea.empty() && ea == eb, "PositivityError text: '" + ea + "' vs '" + eb + "'");
+  }
+  {
+    // advance() (the run.cpp:180-210 loop on the device) against heun_step calls of the
+    // reference: dump-style limit times hit exactly, then a CFL far past stability so
+    // that a step fails -- same exception text, same completed steps and diagnostics
+    const CartesianGrid g = make_grid_2d(96, 40, 0.0, 1.0, 0.0, 0.5);
+    const BoundaryCondition bc{BcKind::transmissive, BcKind::reflective, BcKind::reflective,
+                               BcKind::transmissive};
+    for (int auto_sync = 0; auto_sync < 2; ++auto_sync) {
+      LagfluxSolver ref(g, bc, eos, SchemeParams{}, 2);
+      b200::LagfluxSolver gpu(g, bc, eos, SchemeParams{}, 2);
+      gpu.set_auto_sync(auto_sync != 0);
+      SolverState a, b;
+      a.field = sod_field(g, eos);
+      b.field = a.field;
+      const TimeControls controls{0.45, 0.05, 1 << 30};
+      const double limits[3] = {0.0125, 0.03, 0.05};
+      for (double limit : limits) {
+        while (a.time < limit) ref.heun_step(a, controls, limit);
+        gpu.advance(b, controls, limit, std::numeric_limits<std::int64_t>::max());
+        expect(a.time == b.time && a.step == b.step, "advance: time / step at a limit");
+      }
+      if (!auto_sync) gpu.sync_to_host(b);
+      expect(same_interior(g, a.field, b.field), "advance: field");
+      expect(a.diagnostics.size() == b.diagnostics.size(), "advance: diagnostics count");
+      for (std::size_t k = 0; k < a.diagnostics.size() && k < b.diagnostics.size(); ++k)
+        if (a.diagnostics[k].dt != b.diagnostics[k].dt || a.diagnostics[k].min_p != b.diagnostics[k].min_p)
+          expect(false, "advance: diagnostics " + std::to_string(k));
+      expect(a.boundary_outflow == b.boundary_outflow, "advance: boundary outflow");
+      const TimeControls wild{40.0, 1e30, 1 << 30};
+      std::string ea, eb;
+      try {
+        for (int k = 0; k < 50; ++k) ref.heun_step(a, wild, 1e30);
+      } catch (const Error& e) {
+        ea = e.what();
+      }
+      try {
+        gpu.advance(b, wild, 1e30, 50);
+      } catch (const Error& e) {
+        eb = e.what();
+      }
+      expect(!ea.empty() && ea == eb, "advance: error text '" + ea + "' vs '" + eb + "'");
+      expect(a.step == b.step && a.time == b.time && a.diagnostics.size() == b.diagnostics.size(),
+             "advance: completed steps before the failure");
+      std::printf("advance (auto_sync %d): %lld steps, three limit times and a failing batch compared\n",
+                  auto_sync, static_cast<long long>(a.step));
+    }
   }
   run_multimaterial(70, 30, 40, true);
   run_multimaterial(70, 30, 40, false);
