@@ -28,10 +28,33 @@ CASES = os.path.join(REF_DIR, "cases")
 pytestmark = pytest.mark.gpu
 
 
-def _run(exe, cwd):
+@pytest.fixture(scope="module")
+def runs(cuda, tmp_path_factory):
+    """{exe: (cwd, returncode, stdout, stderr)}: the three programs run side by side
+    (two on the GPU, the CPU reference on the host cores), once per session."""
+    for p in (B200, RESIDENT, REF, CASES):
+        assert os.path.exists(p), f"{p} not built (make -C oracle acceptance)"
     env = dict(os.environ, LAGFLUX_CASE_DIR=CASES)
-    out = subprocess.run([exe], cwd=cwd, env=env, capture_output=True, text=True, timeout=1500)
-    return out.returncode, out.stdout, out.stderr
+    # criterion 1 also asks each Sod run for < 5 s of wall clock, and the program's first
+    # run pays the process's CUDA start-up: page the driver and the library in first
+    # (a fresh box loads them from a cold image), so that the timing sees a warm start
+    warm = os.path.join(REF_DIR, "dropin_check")
+    if os.path.exists(warm):
+        subprocess.run([warm], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=900)
+    procs = {}
+    for exe in (B200, RESIDENT, REF):
+        cwd = tmp_path_factory.mktemp(os.path.basename(exe))
+        procs[exe] = (cwd, subprocess.Popen([exe], cwd=cwd, env=env, stdout=subprocess.PIPE,
+                                            stderr=subprocess.PIPE, text=True))
+    res = {}
+    for exe, (cwd, p) in procs.items():
+        try:
+            out, err = p.communicate(timeout=1500)
+        except subprocess.TimeoutExpired:
+            p.kill()
+            out, err = p.communicate()
+        res[exe] = (cwd, p.returncode, out, err)
+    return res
 
 
 def _criteria(stdout):
@@ -48,30 +71,14 @@ def _criteria(stdout):
     return res
 
 
-_REF_RUN = {}
-
-
-def _reference_run(tmp_path_factory):
-    """The CPU program's output, run once per session."""
-    if not _REF_RUN:
-        d = tmp_path_factory.mktemp("acceptance_ref")
-        _REF_RUN["dir"] = d
-        _REF_RUN["res"] = _run(REF, d)
-    return _REF_RUN["dir"], _REF_RUN["res"]
-
-
 @pytest.mark.parametrize("exe", [B200, RESIDENT], ids=["solver_swapped", "driver_swapped"])
-def test_reference_acceptance_program_on_the_gpu_path(cuda, tmp_path, tmp_path_factory, exe):
+def test_reference_acceptance_program_on_the_gpu_path(cuda, runs, exe):
     """solver_swapped: the reference's run.cpp loop stepping the GPU solver (state.field
     copied both ways every step).  driver_swapped: acceptance.cpp's run_hydro_case calls
     also go to lagflux::b200::run_hydro_case (include/lagflux_b200_run.hpp): the state
     stays on the device between dump events and the dumps are written from it."""
-    for p in (exe, REF, CASES):
-        assert os.path.exists(p), f"{p} not built (make -C oracle acceptance)"
-    db = tmp_path / "b200"
-    db.mkdir()
-    rc_b, out_b, err_b = _run(exe, db)
-    dr, (rc_r, out_r, err_r) = _reference_run(tmp_path_factory)
+    db, rc_b, out_b, err_b = runs[exe]
+    dr, rc_r, out_r, err_r = runs[REF]
     print(out_b)
     cb, cr = _criteria(out_b), _criteria(out_r)
     assert sorted(cb) == list(range(1, 13)), out_b + err_b
