@@ -87,3 +87,18 @@ def test_biased_field_pointers_address_the_local_rows():
         for r in (0, rows - 1):
             assert addr + ((y0 + 2 + r) * nxt + 2) * 8 == local[c, 2 + r, 2:].ctypes.data
     assert N.biased_field_ptrs(local, 0)[1][0] == N.field_ptrs(local)[1][0]
+
+
+def test_cpp_adapter_headers_compile_against_the_reference_headers(tmp_path):
+    """include/lagflux_b200.hpp and include/lagflux_b200_run.hpp are compiled inside the
+    reference's build: they must parse against its headers (only where the reference
+    tree is present: this container, not the GPU box)."""
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("reference tree absent")
+    src = tmp_path / "use.cpp"
+    src.write_text('#include "lagflux_b200_run.hpp"\n'
+                   "lagflux::HydroRun go(const lagflux::CaseConfig& c) {\n"
+                   "  return lagflux::b200::run_hydro_case(c, false);\n}\n")
+    subprocess.run(["/usr/bin/g++", "-std=gnu++20", "-fsyntax-only", "-Wall", "-Wextra", "-I", ref_inc,
+                    "-I", os.path.join(ROOT, "include"), str(src)], check=True)
