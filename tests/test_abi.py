@@ -6,6 +6,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 from paper_1607_08710_b200 import native as N
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
