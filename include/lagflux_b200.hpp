@@ -195,7 +195,10 @@ class LagfluxSolver {
     }
     if (auto_sync_ || rc) {
       download(state.field);  // a corrector failure leaves its output, as in the reference
-      if (materials != nullptr) lf_download_partials(h_, partial_ptrs(*materials).p, grid_.nxt());
+      if (materials != nullptr) {
+        const int rp = lf_download_partials(h_, partial_ptrs(*materials).p, grid_.nxt());
+        if (rc == 0) check(rp);   // (after a failing step its error is the one reported)
+      }
     }
     check(rc);
     return done;
