@@ -104,16 +104,24 @@ inline HydroRun run_hydro_case(const CaseConfig& c, bool write_outputs, int devi
     throw;
   }
 
-  run.summary.steps = run.state.step;
-  run.summary.final_time = run.state.time;
-  run.summary.truncated_by_max_steps = run.state.time < c.t_final;
-  run.summary.min_rho = std::numeric_limits<double>::infinity();
-  run.summary.min_p = std::numeric_limits<double>::infinity();
-  for (const StepDiagnostics& d : run.state.diagnostics) {
-    run.summary.min_rho = std::min(run.summary.min_rho, d.min_rho);
-    run.summary.min_p = std::min(run.summary.min_p, d.min_p);
+  // RunSummary (run.hpp:14-25): counts, whether max_steps cut the run short, and the
+  // minima over every step's diagnostics (0 when no step ran)
+  RunSummary& sum = run.summary;
+  const std::vector<StepDiagnostics>& diag = run.state.diagnostics;
+  sum.steps = run.state.step;
+  sum.final_time = run.state.time;
+  sum.truncated_by_max_steps = sum.final_time < c.t_final;
+  if (diag.empty()) {
+    sum.min_rho = sum.min_p = 0.0;
+  } else {
+    double lo_rho = std::numeric_limits<double>::infinity(), lo_p = lo_rho;
+    for (const StepDiagnostics& d : diag) {
+      if (d.min_rho < lo_rho) lo_rho = d.min_rho;
+      if (d.min_p < lo_p) lo_p = d.min_p;
+    }
+    sum.min_rho = lo_rho;
+    sum.min_p = lo_p;
   }
-  if (run.state.diagnostics.empty()) run.summary.min_rho = run.summary.min_p = 0.0;
 
   if (run.summary.truncated_by_max_steps) dump(run.state.time);
   solver.wait_dumps();
